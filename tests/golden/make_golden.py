@@ -1,0 +1,210 @@
+"""Generate the golden fixtures by running the UNMODIFIED reference.
+
+Run in the build container only (it imports ``/root/reference/pkg/src``
+read-only; nothing at test time needs the reference):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+Each instance is run through the reference's public API exactly as
+``cli._build_stage`` / ``_factorize_stage`` do (cli.py:188-305) and the
+results are frozen as ``tests/golden/<name>.npz``.  Large float arrays are
+stored as sketches (projections on fixed Gaussian vectors) to keep the
+fixtures small; integer structure (perm, kNN, skeleton indices, ranks, row
+counts) is stored in full so the bit-exact claims are checked in full.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, str(HERE.parents[1]))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import hikersolve as hk  # noqa: E402  (the reference, read-only)
+from hikersolve.data import PointSet  # noqa: E402
+
+from paper_1701_02324_b200 import workloads  # noqa: E402
+
+
+def sketch_vec(tag, node, n):
+    return np.random.default_rng([tag, node]).standard_normal(n)
+
+
+def coords_digest(x):
+    return hashlib.sha256(np.ascontiguousarray(x, dtype=np.float64).tobytes()).hexdigest()
+
+
+def run_instance(name, coords, kernel, leaf, tau, max_rank, samples, mode, seed,
+                 kappa=None, nrhs=2, store_coords=True, hybrid=False):
+    t0 = time.time()
+    ps = PointSet(coords)
+    tree = hk.build_tree(ps, leaf, seed=seed)
+    knn = hk.knn_bruteforce(tree.points, kappa) if mode == "knn_augmented" else None
+    cfg = hk.SkeletonConfig(tau=tau, max_rank=max_rank, samples=samples,
+                            sample_mode=mode, seed=seed)
+    skels = hk.build_skeletons(tree, kernel, cfg, knn=knn, threads=8)
+    op = hk.build_operator(tree, skels, kernel)
+    lam = kernel.regularization
+    f = hk.factorize(op, lam, threads=8)
+    n = tree.n
+    rng = np.random.default_rng([seed, 1000])
+    b = rng.standard_normal((n, nrhs))
+    x = hk.solve_multi(f, b, in_tree_order=True)
+    w = np.random.default_rng([seed, 78]).standard_normal(n)
+    u = hk.hmatvec(op, w, lam)
+
+    nn = len(tree.nodes)
+    ranks = np.full(nn, -1, dtype=np.int64)
+    rows_count = np.full(nn, -1, dtype=np.int64)
+    skel_idx, skel_off = [], [0]
+    interp_sk, theta_sk = [], []
+    interp_fro = np.zeros(nn)
+    theta_fro = np.zeros(nn)
+    z_cond = np.zeros(nn)
+    for nd in tree.nodes:
+        i = nd.index
+        fac = f.factors[i]
+        if nd.level > 0:
+            s = skels[i]
+            ranks[i] = s.rank
+            skel_idx.append(np.asarray(s.indices, dtype=np.int64))
+            interp_sk.append(s.interp @ sketch_vec(77, i, s.interp.shape[1]))
+            interp_fro[i] = np.linalg.norm(s.interp)
+            rows_count[i] = hk.skeleton.sample_rows(
+                tree, nd, samples, mode, seed, knn=knn).size
+            theta_sk.append(fac.theta @ sketch_vec(78, i, fac.theta.shape[1]))
+            theta_fro[i] = np.linalg.norm(fac.theta)
+        else:
+            skel_idx.append(np.zeros(0, dtype=np.int64))
+        skel_off.append(skel_off[-1] + skel_idx[-1].size)
+        if not nd.is_leaf:
+            z_cond[i] = fac.z_cond
+    out = {
+        "perm": np.asarray(tree.perm, dtype=np.int64),
+        "split_value": np.array([nd.split_value if nd.split_value is not None else np.nan
+                                 for nd in tree.nodes]),
+        "ranks": ranks,
+        "rows_count": rows_count,
+        "skel_idx": np.concatenate(skel_idx),
+        "skel_off": np.asarray(skel_off, dtype=np.int64),
+        "interp_sketch": np.concatenate(interp_sk) if interp_sk else np.zeros(0),
+        "interp_fro": interp_fro,
+        "theta_sketch": np.concatenate(theta_sk) if theta_sk else np.zeros(0),
+        "theta_fro": theta_fro,
+        "z_cond": z_cond,
+        "x": x,
+        "u": u,
+        "coords_sha256": np.array(coords_digest(coords)),
+    }
+    if knn is not None:
+        out["knn"] = np.asarray(knn, dtype=np.int64)
+    if store_coords:
+        out["coords"] = np.asarray(coords, dtype=np.float64)
+    if hybrid:
+        xb, rep = hk.hybrid_solve(op, f, b[:, 0], tol=1e-10, restart=50,
+                                  operator_mode="compressed")
+        out["hybrid_x"] = xb
+        out["hybrid_iterations"] = np.array(rep.iterations)
+        out["hybrid_final_residual"] = np.array(rep.final_residual)
+    meta = {"name": name, "family": kernel.family, "h": kernel.h,
+            "degree": kernel.degree, "shift": kernel.shift, "lam": lam,
+            "leaf": leaf, "tau": tau, "max_rank": max_rank, "samples": samples,
+            "mode": mode, "seed": seed, "kappa": kappa, "nrhs": nrhs, "n": n,
+            "d": int(coords.shape[1]), "depth": tree.depth,
+            "seconds": round(time.time() - t0, 2)}
+    out["meta"] = np.array(json.dumps(meta))
+    np.savez_compressed(HERE / f"{name}.npz", **out)
+    print(name, meta["seconds"], "s; ranks", sorted(set(ranks.tolist())))
+
+
+def workload_instance(key, n, nrhs=2, store_coords=False, hybrid=False):
+    w = workloads.CONFIGS[key].scaled(n)
+    coords = workloads.points(w, 0)
+    kern = hk.KernelSpec("gaussian", h=w.h, regularization=w.lam)
+    run_instance(f"{key.lower()}_n{n}", coords, kern, w.leaf_size, w.tau,
+                 w.max_rank, w.samples, "knn_augmented", 0, kappa=w.kappa,
+                 nrhs=nrhs, store_coords=store_coords, hybrid=hybrid)
+
+
+def main(which):
+    if "frozen" in which:
+        ps = hk.generate("uniform_cube", 1024, 3, d=3)
+        kern = hk.KernelSpec("gaussian", h=0.3, regularization=1e-2)
+        run_instance("frozen_n1024", ps.coords, kern, 256, 1e-7, 384, 256,
+                     "exact", 3, hybrid=True)
+    if "tiny" in which:
+        ps = hk.generate("uniform_cube", 10, 0, d=2)
+        run_instance("tiny_n10", ps.coords, hk.KernelSpec("gaussian", h=0.5),
+                     5, 1e-7, 64, 256, "exact", 0)
+        ps = hk.generate("uniform_cube", 128, 3, d=2)
+        run_instance("rank0_n128", ps.coords,
+                     hk.KernelSpec("gaussian", h=1e-9, regularization=1e-1),
+                     32, 1e-4, 8, 256, "exact", 0)
+    if "families" in which:
+        base = hk.generate("uniform_cube", 1024, 11, d=3)
+        run_instance("laplace_n1024", base.coords * 2.0,
+                     hk.KernelSpec("laplace3d", regularization=1e-1), 128, 1e-8,
+                     64, 256, "uniform", 11)
+        run_instance("poly_n1024", base.coords * 0.05,
+                     hk.KernelSpec("polynomial", degree=2, shift=0.02,
+                                   regularization=1e-3), 128, 1e-8, 64, 256,
+                     "uniform", 11)
+        run_instance("gauss_uniform_n2000", hk.generate("uniform_cube", 2000, 5, d=4).coords,
+                     hk.KernelSpec("gaussian", h=0.4, regularization=1e-2), 100, 1e-6,
+                     48, 96, "uniform", 5)
+    if "c1" in which:
+        workload_instance("C1", 4096, nrhs=4, store_coords=True, hybrid=True)
+    if "c2" in which:
+        workload_instance("C2", 8192)
+    if "c3" in which:
+        workload_instance("C3", 8192)
+    if "c4" in which:
+        workload_instance("C4", 8192)
+    if "c5" in which:
+        workload_instance("C5", 2048, hybrid=True)
+    if "knn_small" in which:
+        rng = np.random.default_rng(0)
+        pts = rng.random((200, 3))
+        np.savez_compressed(HERE / "knn_n200.npz", coords=pts,
+                            knn=hk.knn_bruteforce(PointSet(pts), 5))
+    if "gmres" in which:
+        ps = hk.generate("uniform_cube", 512, 3, d=3)
+        kern = hk.KernelSpec("gaussian", h=0.5, regularization=1e-6)
+        tree = hk.build_tree(ps, 512, seed=3)
+        from hikersolve import oracle as ref_oracle
+        dense = ref_oracle.dense_kernel_matrix(kern, tree.points, 1e-6)
+        b = np.random.default_rng([3, 41]).standard_normal(512)
+        x, rep = hk.gmres(lambda v: dense @ v, lambda v: v, b, tol=1e-8,
+                          max_iter=500, restart=50)
+        np.savez_compressed(HERE / "gmres_n512.npz", x=x,
+                            iterations=np.array(rep.iterations),
+                            converged=np.array(rep.converged),
+                            final_residual=np.array(rep.final_residual),
+                            residuals=np.array(rep.residuals))
+    if "qr" in which:
+        rng = np.random.default_rng(1)
+        cases = {}
+        for t in range(12):
+            m, n = int(rng.integers(5, 60)), int(rng.integers(5, 60))
+            u, _ = np.linalg.qr(rng.standard_normal((m, min(m, n))))
+            v, _ = np.linalg.qr(rng.standard_normal((n, min(m, n))))
+            a = (u * 0.6 ** np.arange(min(m, n))) @ v.T
+            tol, mr = [1e-3, 1e-8, 1e-12][t % 3], int(rng.integers(1, 40))
+            cols, p = hk.interpolative_decomposition(a, tol, mr)
+            cases[f"a{t}"] = a
+            cases[f"cols{t}"] = np.asarray(cols, dtype=np.int64)
+            cases[f"p{t}"] = p
+            cases[f"tol{t}"] = np.array([tol, mr])
+        np.savez_compressed(HERE / "id_cases.npz", **cases)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:] or ["frozen", "tiny", "families", "c1", "c2", "c3", "c4",
+                          "c5", "knn_small", "qr", "gmres"])
