@@ -1,0 +1,172 @@
+/* libhks -- C ABI of the B200-native hierarchical kernel factorize / solve.
+ *
+ * This is the drop-in boundary for the north-star path of the reference
+ * package `hikersolve` (arXiv 1701.02324).  The reference has no FFI: its
+ * boundary is the Python API re-exported in pkg/src/hikersolve/__init__.py:12-75.
+ * Every entry point below replaces the numerical core of one of those
+ * functions (cited per function); the Python package
+ * `paper_1701_02324_b200` keeps the reference's names, argument meaning and
+ * exceptions on top of this ABI, and INTEGRATION.md shows the ctypes binding
+ * a maintainer of the reference would add.
+ *
+ * Conventions
+ *  - all pointers are DEVICE pointers unless a parameter says "host";
+ *  - matrices are column-major with an explicit leading dimension;
+ *  - points are row-major (n x d) float64 in tree order;
+ *  - every call is stream-ordered on `stream` (a cudaStream_t, NULL = legacy
+ *    default stream) and returns HKS_OK or an error code; the thread-local
+ *    message of the last failure is hks_last_error();
+ *  - no call allocates persistent device memory except hks_plan_create,
+ *    which owns its descriptor tables and level workspaces until
+ *    hks_plan_destroy.
+ */
+#ifndef HKS_H_
+#define HKS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HKS_ABI_VERSION 1
+
+enum hks_status {
+  HKS_OK = 0,
+  HKS_ERR_INVALID = 1,          /* ValueError in the reference */
+  HKS_ERR_CUDA = 2,             /* CUDA runtime failure */
+  HKS_ERR_SINGULAR = 3,         /* SingularMatrixError, linalg.py:163-168 */
+  HKS_ERR_REDUCED_SINGULAR = 4, /* FactorizationError, solver.py:99-105 */
+  HKS_ERR_SKELETON = 5,         /* RuntimeError, skeleton.py:166-169 */
+  HKS_ERR_NOT_SUPPORTED = 6
+};
+
+enum hks_family { HKS_GAUSSIAN = 0, HKS_LAPLACE3D = 1, HKS_POLYNOMIAL = 2 };
+
+/* KernelSpec, kernels.py:23-48 */
+typedef struct hks_kernel {
+  int32_t family;
+  int32_t degree;
+  double h;
+  double shift;
+  double regularization;
+} hks_kernel;
+
+/* Flat per-node buffers of a factorization layout (see hks_layout). */
+enum hks_buffer {
+  HKS_BUF_INTERP = 0,   /* double: r x c interpolation matrix P (Skeleton.interp), ld r */
+  HKS_BUF_SKEL = 1,     /* int64:  r skeleton indices (Skeleton.indices) */
+  HKS_BUF_THETA = 2,    /* double: r x r theta (NodeFactor.theta), ld r */
+  HKS_BUF_LEAF_LU = 3,  /* double: m x m LU of K_aa + lam I (NodeFactor.diag_lu.lu), ld m */
+  HKS_BUF_LEAF_PIV = 4, /* int32:  m pivots, 0-based (NodeFactor.diag_lu.piv) */
+  HKS_BUF_PHI = 5,      /* double: m x r phi, ld m */
+  HKS_BUF_Z_LU = 6,     /* double: R x R LU of Z, ld R */
+  HKS_BUF_Z_PIV = 7,    /* int32:  R pivots, 0-based */
+  HKS_BUF_PUSH = 8,     /* double: R x r child_push, ld R */
+  HKS_BUF_COUP = 9,     /* double: r_left x r_right coupling K(q_l, q_r), ld r_left */
+  HKS_BUF_STATS = 10,   /* per node: double anorm[nnodes], double rcond[nnodes] (dgecon),
+                           int32 info[nnodes] (first zero pivot) -- 3 * nnodes doubles */
+  HKS_NBUF = 11
+};
+
+typedef struct hks_plan hks_plan;
+
+const char* hks_last_error(void);
+int hks_abi_version(void);
+
+/* Storage layout of a complete tree with n points, `depth` levels below the
+ * root and rank cap `max_rank` (leaf ranks <= min(max_rank, leaf size),
+ * internal ranks <= min(max_rank, r_left + r_right)).  Host outputs:
+ * sizes[HKS_NBUF] element counts; offsets[b * nnodes + i] element offset of
+ * node i in buffer b (-1 if node i has no such array).  `offsets` may be NULL.
+ * Node ranges follow tree.py:100-121 (left child takes ceil(size / 2)). */
+int hks_layout(int64_t n, int64_t depth, int64_t max_rank, int64_t* sizes, int64_t* offsets);
+
+/* eval_block, kernels.py:64-105: out = K(X[rows], X[cols]) + diag * [i == j].
+ * rows/cols: device int64 index lists, or NULL for the ranges
+ * [row0, row0 + nrows) / [col0, col0 + ncols).  row_major selects out[i*ldo + j]
+ * instead of out[i + j*ldo]. */
+int hks_eval_block(const double* X, int64_t d, const hks_kernel* kern, const int64_t* rows,
+                   int64_t row0, int64_t nrows, const int64_t* cols, int64_t col0, int64_t ncols,
+                   double* out, int64_t ldo, int32_t row_major, double diag, void* stream);
+
+/* Fused kernel summation U = beta U + K(X[rows], X[cols]) W (+ diag * W when
+ * rows and cols are the same range) without forming K -- the "never
+ * materialise K" path of treecode.py:99-101, krylov.py:176-185 (dense_oracle)
+ * and the sampled residual checks.  W: ncols x k (ldw), U: nrows x k (ldu). */
+int hks_kernel_sum(const double* X, int64_t d, const hks_kernel* kern, const int64_t* rows,
+                   int64_t row0, int64_t nrows, const int64_t* cols, int64_t col0, int64_t ncols,
+                   const double* W, int64_t ldw, int64_t k, double* U, int64_t ldu, double beta,
+                   double diag, void* stream);
+
+/* factor_dense, linalg.py:151-169: in-place LU with partial pivoting of an
+ * n x n matrix; piv 0-based (scipy lu_factor); *info_host = 0 or the 1-based
+ * step of the first exactly-zero pivot. */
+int hks_lu_factor(double* A, int64_t n, int64_t lda, int32_t* piv, int32_t* info_host, void* stream);
+
+/* solve_dense, linalg.py:172-179: B := A^-1 B in place (nrhs columns). */
+int hks_lu_solve(const double* LU, const int32_t* piv, int64_t n, int64_t lda, double* B,
+                 int64_t ldb, int64_t nrhs, void* stream);
+
+/* pivoted_qr + interpolative_decomposition, linalg.py:43-136, for one
+ * m x n matrix A (column-major, lda; overwritten).  Outputs (device):
+ * pivots[n] int64, interp[max_rank x n] (ld = rank), host *rank_host. */
+int hks_interp_decomp(double* A, int64_t m, int64_t n, int64_t lda, double tol, int64_t max_rank,
+                      int64_t* pivots, double* interp, int64_t* rank_host, void* stream);
+
+/* ----- plan: the level program of one compressed operator ----------------
+ * A plan holds the tree layout, the skeleton ranks and the uploaded
+ * descriptor programs of build_operator / factorize / solve / hmatvec /
+ * upward_pass.  It owns no factor storage: every call receives
+ * `buffers[HKS_NBUF]`, the device base pointers of the flat per-node arrays
+ * of hks_layout (entries a call does not touch may be NULL), so one plan
+ * serves any number of factorizations (e.g. different lambda) of the same
+ * operator.  X: n x d tree-ordered points (device, must outlive the plan);
+ * ranks_host[nnodes] the skeleton ranks (root ignored).  Calls on one plan
+ * must be ordered on one stream (plan-owned workspaces). */
+int hks_plan_create(hks_plan** plan, const double* X, int64_t n, int64_t d, int64_t depth,
+                    int64_t max_rank, const int64_t* ranks_host, const hks_kernel* kern);
+int hks_plan_destroy(hks_plan* plan);
+
+/* build_operator, treecode.py:41-62: the sibling couplings K(q_l, q_r) from
+ * HKS_BUF_SKEL into HKS_BUF_COUP.  Leaf blocks are never stored (they are
+ * re-evaluated inside factorize and the fused hmatvec; hks_leaf_block gives
+ * the HierarchicalOperator.leaf_blocks diagnostic view). */
+int hks_build_operator(hks_plan* plan, void* const* buffers, void* stream);
+int hks_leaf_block(hks_plan* plan, int64_t leaf, double* out, void* stream);
+
+/* factorize, solver.py:111-186.  Reads INTERP, COUP; writes THETA, LEAF_LU,
+ * LEAF_PIV, PHI, Z_LU, Z_PIV, PUSH, STATS.  with_cond: run the dgecon
+ * estimate of every Z (NodeFactor.z_cond).  On an exactly-zero pivot returns
+ * HKS_ERR_SINGULAR (leaf, linalg.py:163-168) or HKS_ERR_REDUCED_SINGULAR
+ * (Z, solver.py:99-105) with the failing heap index in *bad_node_host. */
+int hks_factorize(hks_plan* plan, void* const* buffers, double lam, int32_t with_cond,
+                  int64_t* bad_node_host, void* stream);
+
+/* z_cond (1 / dgecon rcond; 0 for leaves) and info per node, host outputs. */
+int hks_factor_stats(hks_plan* plan, void* const* buffers, double* z_cond_host, int32_t* info_host,
+                     void* stream);
+
+/* solve / solve_multi, solver.py:189-270: x = (Ktilde + lam I)^-1 b for k
+ * right-hand sides in tree order; b, x: n x k column-major (ld n); x may
+ * alias b. */
+int hks_solve(hks_plan* plan, void* const* buffers, const double* b, double* x, int64_t k,
+              void* stream);
+
+/* hmatvec, treecode.py:92-128: u = (Ktilde + lam I) w, n x k (ld n), u != w. */
+int hks_hmatvec(hks_plan* plan, void* const* buffers, const double* w, double* u, int64_t k,
+                double lam, void* stream);
+
+/* upward_pass, treecode.py:65-89 (k columns): skeleton weights of every
+ * non-root node written into `out`; node i's r_i x k block starts at
+ * out + offsets[i] with leading dimension lds[i] (hks_upward_offsets). */
+int hks_upward_offsets(hks_plan* plan, int64_t k, int64_t* offsets_host, int64_t* lds_host,
+                       int64_t* total_host);
+int hks_upward(hks_plan* plan, void* const* buffers, const double* w, int64_t k, double* out,
+               void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HKS_H_ */

@@ -1,0 +1,125 @@
+// C-ABI entry points that are not plan-bound: error plumbing, single-block
+// kernel evaluation / summation and the dense LU wrappers used by the
+// reference-named factor_dense / solve_dense / eval_block.
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "hks_internal.h"
+
+namespace hks {
+
+static thread_local char g_err[1024] = "";
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+// Small device-side descriptor upload for one-off launches.
+template <class D>
+static cudaError_t one_desc(const D& h, D** d, cudaStream_t s) {
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(d), sizeof(D), s);
+  if (e != cudaSuccess) return e;
+  return cudaMemcpyAsync(*d, &h, sizeof(D), cudaMemcpyHostToDevice, s);
+}
+
+}  // namespace hks
+
+using namespace hks;
+
+static inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+extern "C" const char* hks_last_error(void) { return g_err; }
+extern "C" int hks_abi_version(void) { return HKS_ABI_VERSION; }
+
+static int check_kernel(const hks_kernel* k, int64_t d) {
+  if (!k) return set_error(HKS_ERR_INVALID, "null kernel");
+  if (k->family == HKS_GAUSSIAN && !(k->h > 0)) return set_error(HKS_ERR_INVALID, "gaussian bandwidth h must be positive");
+  if (k->family == HKS_LAPLACE3D && d != 3) return set_error(HKS_ERR_INVALID, "laplace3d kernel requires 3-d points");
+  if (k->family < 0 || k->family > 2) return set_error(HKS_ERR_INVALID, "unknown kernel family %d", k->family);
+  return HKS_OK;
+}
+
+extern "C" int hks_eval_block(const double* X, int64_t d, const hks_kernel* kern, const int64_t* rows, int64_t row0,
+                              int64_t nrows, const int64_t* cols, int64_t col0, int64_t ncols, double* out,
+                              int64_t ldo, int32_t row_major, double diag, void* stream) {
+  int rc = check_kernel(kern, d);
+  if (rc) return rc;
+  if (nrows == 0 || ncols == 0) return HKS_OK;
+  cudaStream_t s = as_stream(stream);
+  EvalDesc h{rows ? abs_ref(rows) : kNull, cols ? abs_ref(cols) : kNull, row0, col0, (int)nrows, (int)ncols,
+             abs_ref(out), (int)ldo, diag != 0.0};
+  Bases b{};
+  b.lam = diag;
+  EvalDesc* dd = nullptr;
+  cudaError_t e = one_desc(h, &dd, s);
+  if (e == cudaSuccess)
+    e = launch_eval_batched(X, (int)d, make_kernel_params(kern), b, dd, 1, (int)nrows, (int)ncols, row_major != 0, s);
+  if (dd) cudaFreeAsync(dd, s);
+  if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_eval_block: %s", cudaGetErrorString(e));
+  return HKS_OK;
+}
+
+extern "C" int hks_kernel_sum(const double* X, int64_t d, const hks_kernel* kern, const int64_t* rows, int64_t row0,
+                              int64_t nrows, const int64_t* cols, int64_t col0, int64_t ncols, const double* W,
+                              int64_t ldw, int64_t k, double* U, int64_t ldu, double beta, double diag,
+                              void* stream) {
+  int rc = check_kernel(kern, d);
+  if (rc) return rc;
+  if (nrows == 0 || k == 0) return HKS_OK;
+  cudaStream_t s = as_stream(stream);
+  SumDesc h{rows ? abs_ref(rows) : kNull, cols ? abs_ref(cols) : kNull, row0, col0, (int)nrows, (int)ncols, (int)k,
+            abs_ref(W), (int)ldw, abs_ref(U), (int)ldu, beta, diag != 0.0};
+  Bases b{};
+  b.lam = diag;
+  SumDesc* dd = nullptr;
+  cudaError_t e = one_desc(h, &dd, s);
+  if (e == cudaSuccess) e = launch_ksum_batched(X, (int)d, make_kernel_params(kern), b, dd, 1, (int)nrows, s);
+  if (dd) cudaFreeAsync(dd, s);
+  if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_kernel_sum: %s", cudaGetErrorString(e));
+  return HKS_OK;
+}
+
+extern "C" int hks_lu_factor(double* A, int64_t n, int64_t lda, int32_t* piv, int32_t* info_host, void* stream) {
+  if (n < 0 || lda < n) return set_error(HKS_ERR_INVALID, "hks_lu_factor: bad dims");
+  if (n == 0) {
+    if (info_host) *info_host = 0;
+    return HKS_OK;
+  }
+  cudaStream_t s = as_stream(stream);
+  int* dinfo = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&dinfo), sizeof(int), s);
+  LuDesc h{abs_ref(A), abs_ref(piv), abs_ref(dinfo), kNull, kNull, (int)n, (int)lda};
+  Bases b{};
+  LuDesc* dd = nullptr;
+  if (e == cudaSuccess) e = one_desc(h, &dd, s);
+  if (e == cudaSuccess) e = launch_getrf_batched(b, dd, 1, (int)n, s);
+  int info = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost, s);
+  if (dd) cudaFreeAsync(dd, s);
+  if (dinfo) cudaFreeAsync(dinfo, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_lu_factor: %s", cudaGetErrorString(e));
+  if (info_host) *info_host = info;
+  if (info) return set_error(HKS_ERR_SINGULAR, "singular matrix: zero pivot at elimination step %d", info - 1);
+  return HKS_OK;
+}
+
+extern "C" int hks_lu_solve(const double* LU, const int32_t* piv, int64_t n, int64_t lda, double* B, int64_t ldb,
+                            int64_t nrhs, void* stream) {
+  if (n < 0 || lda < n || ldb < n || nrhs < 0) return set_error(HKS_ERR_INVALID, "hks_lu_solve: bad dims");
+  if (n == 0 || nrhs == 0) return HKS_OK;
+  cudaStream_t s = as_stream(stream);
+  LuSolveDesc h{abs_ref(LU), abs_ref(piv), abs_ref(B), (int)n, (int)nrhs, (int)lda, (int)ldb};
+  Bases b{};
+  LuSolveDesc* dd = nullptr;
+  cudaError_t e = one_desc(h, &dd, s);
+  if (e == cudaSuccess) e = launch_getrs_batched(b, dd, 1, (int)n, (int)nrhs, s);
+  if (dd) cudaFreeAsync(dd, s);
+  if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_lu_solve: %s", cudaGetErrorString(e));
+  return HKS_OK;
+}

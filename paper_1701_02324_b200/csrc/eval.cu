@@ -1,0 +1,243 @@
+// Kernel-block evaluation and fused kernel summation (FP64, sm_100a).
+//
+// eval_block (kernels.py:64-105) as a batched tile kernel: squared distances
+// in the diff form sum_k (x_k - y_k)^2 accumulated in index order, so
+// K(X, Y) == K(Y, X)^T bit for bit and K(x, x) == 1 exactly
+// (tests/test_kernels.py:7-9, 69-81); gaussian exp(sq / (-2 h^2)) with a
+// true division (kernels.py:95); laplace 1/(4 pi r), r == 0 -> 0
+// (kernels.py:96-101); polynomial (x.y + c)^p (kernels.py:102-104).
+//
+// ksum: U = K(X_rows, X_cols) W (+ lam W) without ever writing K to memory
+// -- each 64x64 kernel tile is built in shared memory and consumed at once
+// (hmatvec's leaf level, treecode.py:99-101; sampled residual checks).
+#include "common.cuh"
+#include "hks_internal.h"
+
+namespace hks {
+
+KernelParams make_kernel_params(const hks_kernel* k) {
+  KernelParams p;
+  p.family = k->family;
+  p.h = k->h;
+  p.neg2h2 = -2.0 * (k->h * k->h);
+  p.degree = k->degree;
+  p.shift = k->shift;
+  return p;
+}
+
+namespace {
+
+constexpr int TM = 64, TN = 64, DC = 32, XS = DC + 1;
+
+__device__ __forceinline__ double kernel_value(const KernelParams& kp, double acc) {
+  if (kp.family == HKS_GAUSSIAN) return exp(acc / kp.neg2h2);
+  if (kp.family == HKS_LAPLACE3D) return acc == 0.0 ? 0.0 : 1.0 / ((4.0 * 3.141592653589793) * sqrt(acc));
+  const double t = acc + kp.shift;
+  if (kp.degree == 1) return t;
+  if (kp.degree == 2) return t * t;
+  return pow(t, (double)kp.degree);
+}
+
+__device__ __forceinline__ int64_t row_id(const int64_t* ids, int64_t base, int i) {
+  return ids ? ids[i] : base + i;
+}
+
+// Accumulates the 16 pair terms of one thread: its row `lr` (against 16
+// columns cbase..cbase+15) or its column (against 16 rows), depending on
+// the caller's mapping; stage = shared X tiles for one d-chunk.
+template <bool POLY>
+__device__ __forceinline__ void accumulate16(const double* xa, const double* xb16, int xb_stride,
+                                             int dc, double (&acc)[16]) {
+  for (int k = 0; k < dc; ++k) {
+    const double a = xa[k];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const double b = xb16[q * xb_stride + k];
+      if (POLY) {
+        acc[q] = fma(a, b, acc[q]);
+      } else {
+        const double df = a - b;
+        acc[q] = fma(df, df, acc[q]);
+      }
+    }
+  }
+}
+
+// Stage rows [r0, r0+TM) of the row set and [c0, c0+TN) of the column set
+// for dims [k0, k0+dc) into shared memory.
+__device__ __forceinline__ void stage(const double* X, int d, const int64_t* rows, int64_t row0,
+                                      int m, int r0, const int64_t* cols, int64_t col0, int n,
+                                      int c0, int k0, int dc, double* Xr, double* Xc) {
+  for (int e = threadIdx.x; e < TM * dc; e += blockDim.x) {
+    const int i = e / dc, k = e % dc;
+    Xr[i * XS + k] = (r0 + i < m) ? X[row_id(rows, row0, r0 + i) * d + k0 + k] : 0.0;
+  }
+  for (int e = threadIdx.x; e < TN * dc; e += blockDim.x) {
+    const int j = e / dc, k = e % dc;
+    Xc[j * XS + k] = (c0 + j < n) ? X[row_id(cols, col0, c0 + j) * d + k0 + k] : 0.0;
+  }
+}
+
+template <bool ROW_MAJOR>
+__global__ void __launch_bounds__(256) eval_kernel(const double* __restrict__ X, int d, KernelParams kp,
+                                                   const Bases bases,
+                                                   const EvalDesc* __restrict__ descs, int tiles_n) {
+  const EvalDesc e = descs[blockIdx.y];
+  const int64_t* erows = e.rows == kNull ? nullptr : at<const int64_t>(bases, e.rows);
+  const int64_t* ecols = e.cols == kNull ? nullptr : at<const int64_t>(bases, e.cols);
+  double* eout = at<double>(bases, e.out);
+  const double ediag = e.diag ? bases.lam : 0.0;
+  const int r0 = (blockIdx.x / tiles_n) * TM, c0 = (blockIdx.x % tiles_n) * TN;
+  if (r0 >= e.m || c0 >= e.n) return;
+  __shared__ double Xr[TM * XS];
+  __shared__ double Xc[TN * XS];
+  const int t = threadIdx.x;
+  // ROW_MAJOR: thread owns one column and 16 rows (coalesced row-major store);
+  // else one row and 16 columns (coalesced column-major store)
+  const int own = t & 63, grp = (t >> 6) * 16;
+  double acc[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+  const bool poly = kp.family == HKS_POLYNOMIAL;
+  for (int k0 = 0; k0 < d; k0 += DC) {
+    const int dc = min(DC, d - k0);
+    stage(X, d, erows, e.row0, e.m, r0, ecols, e.col0, e.n, c0, k0, dc, Xr, Xc);
+    __syncthreads();
+    const double* mine = ROW_MAJOR ? Xc + own * XS : Xr + own * XS;
+    const double* other = ROW_MAJOR ? Xr + grp * XS : Xc + grp * XS;
+    // keep the subtraction order (x_row - x_col) fixed in both mappings
+    if (poly) {
+      accumulate16<true>(mine, other, XS, dc, acc);
+    } else if (ROW_MAJOR) {
+      for (int k = 0; k < dc; ++k) {
+        const double b = mine[k];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const double df = other[q * XS + k] - b;
+          acc[q] = fma(df, df, acc[q]);
+        }
+      }
+    } else {
+      accumulate16<false>(mine, other, XS, dc, acc);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int i = ROW_MAJOR ? r0 + grp + q : r0 + own;
+    const int j = ROW_MAJOR ? c0 + own : c0 + grp + q;
+    if (i < e.m && j < e.n) {
+      double v = kernel_value(kp, acc[q]);
+      if (i == j) v += ediag;
+      if (ROW_MAJOR)
+        eout[(size_t)i * e.ldo + j] = v;
+      else
+        eout[i + (size_t)j * e.ldo] = v;
+    }
+  }
+}
+
+constexpr int KC = 16;  // right-hand sides per pass
+
+__global__ void __launch_bounds__(256) ksum_kernel(const double* __restrict__ X, int d, KernelParams kp,
+                                                   const Bases bases,
+                                                   const SumDesc* __restrict__ descs) {
+  const SumDesc s = descs[blockIdx.y];
+  const int64_t* srows = s.rows == kNull ? nullptr : at<const int64_t>(bases, s.rows);
+  const int64_t* scols = s.cols == kNull ? nullptr : at<const int64_t>(bases, s.cols);
+  const double* sW = at<const double>(bases, s.W);
+  double* sU = at<double>(bases, s.U);
+  const double sdiag = s.diag ? bases.lam : 0.0;
+  const int r0 = blockIdx.x * TM;
+  if (r0 >= s.m) return;
+  // Kt (the 64x64 kernel tile) reuses the staging area once the d-loop is done
+  __shared__ double stage_area[(TM + TN) * XS];
+  __shared__ double Ws[TN * KC];
+  double* Xr = stage_area;
+  double* Xc = stage_area + TM * XS;
+  double* Kt = stage_area;
+  static_assert(TM * (TN + 1) <= (TM + TN) * XS, "kernel tile must fit the staging area");
+  const int t = threadIdx.x;
+  const int own = t & 63, grp = (t >> 6) * 16;
+  const int kq = (t >> 6) * 4;  // 4 right-hand sides per thread in the product
+  const bool poly = kp.family == HKS_POLYNOMIAL;
+  for (int kb = 0; kb < s.k; kb += KC) {
+    const int kc = min(KC, s.k - kb);
+    double out[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int c0 = 0; c0 < s.n; c0 += TN) {
+      double acc[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+      for (int k0 = 0; k0 < d; k0 += DC) {
+        const int dc = min(DC, d - k0);
+        stage(X, d, srows, s.row0, s.m, r0, scols, s.col0, s.n, c0, k0, dc, Xr, Xc);
+        __syncthreads();
+        if (poly)
+          accumulate16<true>(Xr + own * XS, Xc + grp * XS, XS, dc, acc);
+        else
+          accumulate16<false>(Xr + own * XS, Xc + grp * XS, XS, dc, acc);
+        __syncthreads();
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int j = c0 + grp + q;
+        Kt[own * (TN + 1) + grp + q] = (r0 + own < s.m && j < s.n) ? kernel_value(kp, acc[q]) : 0.0;
+      }
+      for (int e2 = t; e2 < TN * KC; e2 += blockDim.x) {
+        const int j = e2 / KC, c = e2 % KC;
+        Ws[e2] = (c0 + j < s.n && c < kc) ? sW[(c0 + j) + (size_t)(kb + c) * s.ldw] : 0.0;
+      }
+      __syncthreads();
+      for (int j = 0; j < TN; ++j) {
+        const double kv = Kt[own * (TN + 1) + j];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) out[q] = fma(kv, Ws[j * KC + kq + q], out[q]);
+      }
+      __syncthreads();
+    }
+    const int i = r0 + own;
+    if (i < s.m) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = kq + q;
+        if (c >= kc) continue;
+        double* u = sU + i + (size_t)(kb + c) * s.ldu;
+        double v = out[q];
+        if (s.diag) v += sdiag * sW[i + (size_t)(kb + c) * s.ldw];
+        if (s.beta != 0.0) v += s.beta * *u;
+        *u = v;
+      }
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_eval_batched(const double* X, int d, KernelParams kp, const Bases& bases,
+                                const EvalDesc* d_descs, int count, int max_m, int max_n, bool row_major,
+                                      cudaStream_t stream) {
+  if (count <= 0 || max_m <= 0 || max_n <= 0) return cudaSuccess;
+  const int tm = (max_m + TM - 1) / TM, tn = (max_n + TN - 1) / TN;
+  for (int first = 0; first < count; first += 65535) {
+    const int cnt = count - first < 65535 ? count - first : 65535;
+    dim3 grid(tm * tn, cnt);
+    if (row_major)
+      eval_kernel<true><<<grid, 256, 0, stream>>>(X, d, kp, bases, d_descs + first, tn);
+    else
+      eval_kernel<false><<<grid, 256, 0, stream>>>(X, d, kp, bases, d_descs + first, tn);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ksum_batched(const double* X, int d, KernelParams kp, const Bases& bases,
+                                const SumDesc* d_descs, int count, int max_m, cudaStream_t stream) {
+  if (count <= 0 || max_m <= 0) return cudaSuccess;
+  for (int first = 0; first < count; first += 65535) {
+    const int cnt = count - first < 65535 ? count - first : 65535;
+    dim3 grid((max_m + TM - 1) / TM, cnt);
+    ksum_kernel<<<grid, 256, 0, stream>>>(X, d, kp, bases, d_descs + first);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace hks

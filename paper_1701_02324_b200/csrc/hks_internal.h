@@ -1,0 +1,74 @@
+// Internal (C++) interface between the kernel translation units and the C-ABI.
+#pragma once
+
+#include <cstdarg>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/hks.h"
+#include "common.cuh"
+
+namespace hks {
+
+// Records a thread-local error message (read back through hks_last_error)
+// and returns `code` so call sites can `return set_error(...)`.
+int set_error(int code, const char* fmt, ...);
+
+cudaError_t launch_gemm_batched(const Bases& bases, const GemmDesc* d_descs, int count, int max_m,
+                                int max_n, cudaStream_t stream);
+cudaError_t launch_copy_batched(const Bases& bases, const CopyDesc* d_descs, int count, int max_elems,
+                                cudaStream_t stream);
+cudaError_t launch_getrf_batched(const Bases& bases, const LuDesc* d_descs, int count, int max_n,
+                                 cudaStream_t stream);
+cudaError_t launch_getrs_batched(const Bases& bases, const LuSolveDesc* d_descs, int count, int max_n,
+                                 int max_nrhs, cudaStream_t stream);
+cudaError_t launch_gecon_batched(const Bases& bases, const LuDesc* d_descs, int count, int max_n,
+                                 cudaStream_t stream);
+
+// Kernel-block evaluation (K1/K2/K3).  Rows/cols are either explicit global
+// (tree-order) index lists or contiguous ranges starting at row0/col0.
+struct EvalDesc {
+  Ref rows;  // int64 index list, or kNull for the range row0 + [0, m)
+  Ref cols;
+  int64_t row0, col0;
+  int m, n;
+  Ref out;
+  int ldo;
+  int diag;  // add Bases::lam where the local row index equals the local column index
+};
+
+struct KernelParams {
+  int family;     // HKS_GAUSSIAN / HKS_LAPLACE3D / HKS_POLYNOMIAL
+  double h;       // gaussian bandwidth
+  double neg2h2;  // -2 h^2, formed as in kernels.py:95
+  int degree;
+  double shift;
+};
+
+KernelParams make_kernel_params(const hks_kernel* k);
+
+cudaError_t launch_eval_batched(const double* X, int d, KernelParams kp, const Bases& bases,
+                                const EvalDesc* d_descs, int count, int max_m, int max_n, bool row_major,
+                                cudaStream_t stream);
+
+// U[i,:] = beta*U[i,:] + sum_j K(x_rows[i], x_cols[j]) W[j,:] + diag * W[i,:]
+// (the diag term only when rows and cols are the same range), never
+// materialising K: the fused kernel-summation used by hmatvec's leaf level
+// and by the sampled accuracy checks.
+struct SumDesc {
+  Ref rows;
+  Ref cols;
+  int64_t row0, col0;
+  int m, n, k;
+  Ref W;
+  int ldw;
+  Ref U;
+  int ldu;
+  double beta;
+  int diag;  // add Bases::lam * W (rows == cols ranges only)
+};
+
+cudaError_t launch_ksum_batched(const double* X, int d, KernelParams kp, const Bases& bases,
+                                const SumDesc* d_descs, int count, int max_m, cudaStream_t stream);
+
+}  // namespace hks

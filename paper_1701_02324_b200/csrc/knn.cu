@@ -1,0 +1,174 @@
+// Exact brute-force kNN (tree.py:163-188) on the FP64 DMMA path.
+//
+// d^2 = (|x|^2 + |y|^2) - 2 x.y in the reference's GEMM form, self excluded,
+// neighbours ordered by (d^2, index) -- the lexsort of tree.py:181-187.  A
+// CTA owns 64 queries and streams all points in 64-wide tiles; the dot
+// products of a tile are 8x8x4 DMMA fragments staged through shared memory,
+// and each warp keeps the running top-k of 16 queries in registers (lane j =
+// j-th best), inserting with a ballot when a candidate beats the k-th.
+#include <cfloat>
+
+#include "hks_internal.h"
+
+namespace hks {
+namespace {
+
+constexpr int QB = 64, CB = 64, DCH = 32, DS = DCH + 4;  // DS: smem row stride
+constexpr int KT = 128;
+
+__global__ void sqnorm_kernel(const double* __restrict__ X, int64_t n, int d, double* __restrict__ sq) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const double* x = X + (size_t)p * d;
+    double s = 0.0;
+    for (int k = 0; k < d; ++k) s = fma(x[k], x[k], s);
+    sq[p] = s;
+  }
+}
+
+__device__ __forceinline__ bool lex_less(double a, int ia, double b, int ib) {
+  return a < b || (a == b && ia < ib);
+}
+
+__global__ void __launch_bounds__(KT) knn_kernel(const double* __restrict__ X, const double* __restrict__ sq,
+                                                 int n, int d, int kk, int64_t* __restrict__ out) {
+  extern __shared__ double smem[];
+  double* Qs = smem;                 // QB x DS
+  double* Cs = smem + QB * DS;       // CB x DS
+  double* Dt = smem + 2 * QB * DS;   // QB x (CB + 1)
+  const int q0 = blockIdx.x * QB;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int fr = lane >> 2, fc = lane & 3;
+  const int wm = (wid >> 1) * 32, wn = (wid & 1) * 32;
+  const bool q_resident = d <= DCH;
+
+  double lv[16];
+  int li[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    lv[i] = DBL_MAX;
+    li[i] = 0x7fffffff;
+  }
+  auto stage = [&](double* S, int base, int k0, int dc) {
+    for (int e = threadIdx.x; e < 64 * DS; e += KT) {
+      const int r = e / DS, k = e % DS;
+      const int p = base + r;
+      S[e] = (p < n && k < dc) ? X[(size_t)p * d + k0 + k] : 0.0;
+    }
+  };
+  if (q_resident) stage(Qs, q0, 0, d);
+
+  for (int c0 = 0; c0 < n; c0 += CB) {
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int k0 = 0; k0 < d; k0 += DCH) {
+      const int dc = min(DCH, d - k0);
+      __syncthreads();
+      if (!q_resident) stage(Qs, q0, k0, dc);
+      stage(Cs, c0, k0, dc);
+      __syncthreads();
+      for (int kk4 = 0; kk4 < dc; kk4 += 4) {
+        double a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = Qs[(wm + i * 8 + fr) * DS + kk4 + fc];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = Cs[(wn + j * 8 + fr) * DS + kk4 + fc];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+      }
+    }
+    // distance tile (tree.py:179): (|x|^2 + |y|^2) - 2 x.y
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = wm + i * 8 + fr;
+      const double sqq = (q0 + r < n) ? sq[q0 + r] : 0.0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = wn + j * 8 + 2 * fc + h;
+          const double sqc = (c0 + c < n) ? sq[c0 + c] : 0.0;
+          Dt[r * (CB + 1) + c] = (sqq + sqc) - 2.0 * acc[i][j][h];
+        }
+    }
+    __syncthreads();
+    // merge: warp wid owns queries wid*16 .. wid*16+15
+#pragma unroll
+    for (int qi = 0; qi < 16; ++qi) {
+      const int ql = wid * 16 + qi, q = q0 + ql;
+      if (q >= n) continue;
+      double tv = __shfl_sync(0xffffffffu, lv[qi], kk - 1);
+      int ti = __shfl_sync(0xffffffffu, li[qi], kk - 1);
+      double cv[2];
+      int ci[2];
+      unsigned m[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = lane + 32 * h;
+        ci[h] = c0 + c;
+        cv[h] = Dt[ql * (CB + 1) + c];
+        const bool ok = ci[h] < n && ci[h] != q && lex_less(cv[h], ci[h], tv, ti);
+        m[h] = __ballot_sync(0xffffffffu, ok);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        while (m[h]) {
+          const int src = __ffs(m[h]) - 1;
+          m[h] &= m[h] - 1;
+          const double v = __shfl_sync(0xffffffffu, cv[h], src);
+          const int vi = __shfl_sync(0xffffffffu, ci[h], src);
+          if (!lex_less(v, vi, tv, ti)) continue;  // the k-th moved since the ballot
+          const bool gt = lane < kk && lex_less(v, vi, lv[qi], li[qi]);
+          const unsigned gm = __ballot_sync(0xffffffffu, gt);
+          const int pos = __ffs(gm) - 1;
+          const double up_v = __shfl_up_sync(0xffffffffu, lv[qi], 1);
+          const int up_i = __shfl_up_sync(0xffffffffu, li[qi], 1);
+          if (lane == pos) {
+            lv[qi] = v;
+            li[qi] = vi;
+          } else if (lane > pos) {
+            lv[qi] = up_v;
+            li[qi] = up_i;
+          }
+          tv = __shfl_sync(0xffffffffu, lv[qi], kk - 1);
+          ti = __shfl_sync(0xffffffffu, li[qi], kk - 1);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int qi = 0; qi < 16; ++qi) {
+    const int q = q0 + wid * 16 + qi;
+    if (q < n && lane < kk) out[(size_t)q * kk + lane] = li[qi];
+  }
+}
+
+}  // namespace
+}  // namespace hks
+
+using namespace hks;
+
+// knn_bruteforce (tree.py:163-188): out[n x k] int64, k <= 32.
+extern "C" int hks_knn(const double* X, int64_t n, int64_t d, int64_t k, int64_t* out, void* stream) {
+  if (!X || !out || n < 2 || d < 1 || k < 1 || k > n - 1)
+    return set_error(HKS_ERR_INVALID, "need 1 <= k <= n - 1");
+  if (k > 32) return set_error(HKS_ERR_NOT_SUPPORTED, "hks_knn: k <= 32 supported (got %lld)", (long long)k);
+  if (n > 0x7ffffffe) return set_error(HKS_ERR_NOT_SUPPORTED, "hks_knn: n too large");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* sq = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&sq), n * sizeof(double), s);
+  if (e == cudaSuccess) {
+    sqnorm_kernel<<<592, 256, 0, s>>>(X, n, (int)d, sq);
+    const size_t sm = (size_t)(2 * QB * DS + QB * (CB + 1)) * sizeof(double);
+    cudaFuncSetAttribute(knn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    knn_kernel<<<(unsigned)((n + QB - 1) / QB), KT, sm, s>>>(X, sq, (int)n, (int)d, (int)k, out);
+    e = cudaGetLastError();
+    cudaFreeAsync(sq, s);
+  }
+  if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_knn: %s", cudaGetErrorString(e));
+  return HKS_OK;
+}

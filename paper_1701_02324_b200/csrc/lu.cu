@@ -1,0 +1,496 @@
+// Batched dense LU with partial pivoting, multi-RHS LU solves and the
+// LAPACK dgecon 1-norm condition estimate, FP64 on sm_100a.
+//
+// Replaces scipy.linalg.lu_factor / lu_solve (linalg.py:151-179) for the
+// leaf blocks K_aa + lam I (solver.py:128-137) and the reduced matrices Z
+// (solver.py:92-108), and lapack.dgecon (solver.py:106).
+//
+// getrf: one CTA per matrix, right-looking blocked LU.  The NB-wide panel
+// lives in shared memory (pivot search = block argmax, lowest row on ties
+// as LAPACK idamax); row swaps + the unit-lower TRSM for U12 run one column
+// per thread; the trailing update A22 -= L21 U12 runs on DMMA tiles with
+// L21 read from the shared-memory panel.
+#include <cfloat>
+
+#include "common.cuh"
+#include "hks_internal.h"
+
+namespace hks {
+namespace {
+
+constexpr int LU_THREADS = 256;
+
+__device__ void trailing_update(double* A, int lda, const double* P, int ldp, int j0, int jb, int n) {
+  // A[r, c] -= sum_k L21[r, k] U12[k, c] for r, c in [j0+jb, n); L21[r,k] = P[(r-j0) + k*ldp],
+  // U12[k, c] = A[j0+k + c*lda].
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int fr = lane >> 2, fc = lane & 3;
+  const int base = j0 + jb, rem = n - base;
+  if (rem <= 0) return;
+  const int tr = (rem + 31) / 32, tc = tr;
+  for (int t = wid; t < tr * tc; t += nw) {
+    const int r0 = base + (t % tr) * 32, c0 = base + (t / tr) * 32;
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = r0 + i * 8 + fr, c = c0 + j * 8 + 2 * fc + h;
+          acc[i][j][h] = (r < n && c < n) ? A[r + (size_t)c * lda] : 0.0;
+        }
+    for (int kk = 0; kk < jb; kk += 4) {
+      const int k = kk + fc;
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = r0 + i * 8 + fr;
+        a[i] = (r < n && k < jb) ? -P[(r - j0) + k * ldp] : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c = c0 + j * 8 + fr;
+        b[j] = (c < n && k < jb) ? A[(j0 + k) + (size_t)c * lda] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = r0 + i * 8 + fr, c = c0 + j * 8 + 2 * fc + h;
+          if (r < n && c < n) A[r + (size_t)c * lda] = acc[i][j][h];
+        }
+  }
+}
+
+template <int NB>
+__global__ void __launch_bounds__(LU_THREADS) getrf_kernel(const Bases bases,
+                                                            const LuDesc* __restrict__ descs, int ldp) {
+  const LuDesc L = descs[blockIdx.x];
+  const int n = L.n, lda = L.lda;
+  double* A = at<double>(bases, L.A);
+  int* piv = at<int>(bases, L.piv);
+  extern __shared__ double P[];  // panel: ldp x NB, column-major
+  __shared__ double red_v[LU_THREADS / 32];
+  __shared__ int red_i[LU_THREADS / 32];
+  __shared__ int s_info;
+  const int tid = threadIdx.x, nt = blockDim.x;
+
+  if (tid == 0) s_info = 0;
+  if (L.anorm != kNull) {  // ||A||_1 before factoring, for gecon (solver.py:98)
+    double best = 0.0;
+    for (int c = tid; c < n; c += nt) {
+      double s = 0.0;
+      for (int r = 0; r < n; ++r) s += fabs(A[r + (size_t)c * lda]);
+      best = fmax(best, s);
+    }
+    ArgMax m = block_argmax(ArgMax{best, tid}, red_v, red_i);
+    if (tid == 0) *at<double>(bases, L.anorm) = m.v;
+  }
+  __syncthreads();
+
+  for (int j0 = 0; j0 < n; j0 += NB) {
+    const int jb = min(NB, n - j0), mr = n - j0;
+    for (int e = tid; e < mr * jb; e += nt) {
+      const int i = e % mr, c = e / mr;
+      P[i + c * ldp] = A[(j0 + i) + (size_t)(j0 + c) * lda];
+    }
+    __syncthreads();
+    for (int jj = 0; jj < jb; ++jj) {
+      ArgMax a{-1.0, 0x7fffffff};
+      for (int i = jj + tid; i < mr; i += nt) a = argmax_pick(a, ArgMax{fabs(P[i + jj * ldp]), i});
+      a = block_argmax(a, red_v, red_i);
+      const int p = a.i;
+      const double pv = P[p + jj * ldp];
+      __syncthreads();  // every thread has read pv before the swap below
+      if (tid == 0) {
+        piv[j0 + jj] = j0 + p;
+        if (pv == 0.0 && s_info == 0) s_info = j0 + jj + 1;
+      }
+      if (p != jj)
+        for (int c = tid; c < jb; c += nt) {
+          const double t = P[jj + c * ldp];
+          P[jj + c * ldp] = P[p + c * ldp];
+          P[p + c * ldp] = t;
+        }
+      __syncthreads();
+      if (pv != 0.0) {
+        // dgetf2: scale by the reciprocal when it is safe, else divide
+        const bool recip = fabs(pv) >= DBL_MIN;
+        const double inv = 1.0 / pv;
+        for (int i = jj + 1 + tid; i < mr; i += nt)
+          P[i + jj * ldp] = recip ? P[i + jj * ldp] * inv : P[i + jj * ldp] / pv;
+      }
+      __syncthreads();
+      const int rr = mr - jj - 1, cc = jb - jj - 1;
+      for (int e = tid; e < rr * cc; e += nt) {
+        const int i = jj + 1 + e % rr, c = jj + 1 + e / rr;
+        P[i + c * ldp] -= P[i + jj * ldp] * P[jj + c * ldp];
+      }
+      __syncthreads();
+    }
+    for (int e = tid; e < mr * jb; e += nt) {
+      const int i = e % mr, c = e / mr;
+      A[(j0 + i) + (size_t)(j0 + c) * lda] = P[i + c * ldp];
+    }
+    // row interchanges on the columns outside the panel, then U12 = L11^-1 A12
+    for (int c = tid; c < n; c += nt) {
+      if (c >= j0 && c < j0 + jb) continue;
+      double* col = A + (size_t)c * lda;
+      for (int jj = 0; jj < jb; ++jj) {
+        const int p = piv[j0 + jj];
+        if (p != j0 + jj) {
+          const double t = col[j0 + jj];
+          col[j0 + jj] = col[p];
+          col[p] = t;
+        }
+      }
+      if (c >= j0 + jb) {
+        for (int i = 1; i < jb; ++i) {
+          double s = col[j0 + i];
+          for (int k = 0; k < i; ++k) s -= P[i + k * ldp] * col[j0 + k];
+          col[j0 + i] = s;
+        }
+      }
+    }
+    __syncthreads();
+    trailing_update(A, lda, P, ldp, j0, jb, n);
+    __syncthreads();
+  }
+  if (tid == 0 && L.info != kNull) *at<int>(bases, L.info) = s_info;
+}
+
+// ------------------------------------------------------------------ getrs
+
+constexpr int RS_THREADS = 256;
+
+// X[rows r0..r0+31, :] -= M[r0..r0+31, k0..k1) * X[k0..k1, :]; M column-major
+// global (lda), X in shared memory (ldx); RC columns.  DMMA tiles, 8 warps.
+template <int RC>
+__device__ void block_rows_update(const double* M, int lda, double* X, int ldx, int r0, int nrows,
+                                  int k0, int k1, int ncols) {
+  constexpr int FC = RC / 8;  // column fragments
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int fr = lane >> 2, fc = lane & 3;
+  // 4 row fragments x FC column fragments spread over 8 warps
+  for (int f = wid; f < 4 * FC; f += 8) {
+    const int fi = f % 4, fj = f / 4;
+    const int r = r0 + fi * 8 + fr;
+    double d0 = 0.0, d1 = 0.0;
+    for (int k = k0; k < k1; k += 4) {
+      const int kk = k + fc;
+      const double a = (fi * 8 + fr < nrows && kk < k1) ? -M[r + (size_t)kk * lda] : 0.0;
+      const int cb = fj * 8 + fr;
+      const double b = (kk < k1 && cb < ncols) ? X[kk + cb * ldx] : 0.0;
+      dmma884(d0, d1, a, b);
+    }
+    // accumulate into X (disjoint rows from the k-range, so no race)
+    const int c = fj * 8 + 2 * fc;
+    if (fi * 8 + fr < nrows) {
+      if (c < ncols) X[r + c * ldx] += d0;
+      if (c + 1 < ncols) X[r + (c + 1) * ldx] += d1;
+    }
+  }
+}
+
+template <int RC>
+__global__ void __launch_bounds__(RS_THREADS) getrs_kernel(const Bases bases,
+                                                             const LuSolveDesc* __restrict__ descs, int ldx) {
+  const LuSolveDesc S = descs[blockIdx.x];
+  const int* spiv = at<const int>(bases, S.piv);
+  double* SB = at<double>(bases, S.B);
+  const int n = S.n, c0 = blockIdx.y * RC;
+  if (c0 >= S.nrhs || n == 0) return;
+  const int nc = min(RC, S.nrhs - c0);
+  extern __shared__ double X[];  // ldx x RC
+  int* perm = reinterpret_cast<int*>(X + (size_t)ldx * RC);
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, wid = tid >> 5;
+  const double* LU = at<const double>(bases, S.LU);
+  const int lda = S.lda;
+
+  if (tid == 0) {
+    for (int i = 0; i < n; ++i) perm[i] = i;
+    for (int i = 0; i < n; ++i) {
+      const int p = spiv[i];
+      const int t = perm[i];
+      perm[i] = perm[p];
+      perm[p] = t;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < n * nc; e += nt) {
+    const int i = e % n, c = e / n;
+    X[i + c * ldx] = SB[perm[i] + (size_t)(c0 + c) * S.ldb];
+  }
+  __syncthreads();
+
+  // forward: L (unit lower), 32-row blocks
+  for (int r0 = 0; r0 < n; r0 += 32) {
+    const int nr = min(32, n - r0);
+    if (r0 > 0) {
+      block_rows_update<RC>(LU, lda, X, ldx, r0, nr, 0, r0, nc);
+      __syncthreads();
+    }
+    // in-block forward substitution: warp w owns columns w, w+8, ...; lane = row
+    for (int c = wid; c < nc; c += 8) {
+      double x = lane < nr ? X[r0 + lane + c * ldx] : 0.0;
+      for (int j = 0; j < nr; ++j) {
+        const double xj = __shfl_sync(0xffffffffu, x, j);
+        if (lane > j && lane < nr) x -= LU[(r0 + lane) + (size_t)(r0 + j) * lda] * xj;
+      }
+      if (lane < nr) X[r0 + lane + c * ldx] = x;
+    }
+    __syncthreads();
+  }
+  // backward: U (non-unit upper), blocks from the bottom
+  const int nblk = (n + 31) / 32;
+  for (int b = nblk - 1; b >= 0; --b) {
+    const int r0 = b * 32, nr = min(32, n - r0);
+    if (r0 + nr < n) {
+      block_rows_update<RC>(LU, lda, X, ldx, r0, nr, r0 + nr, n, nc);
+      __syncthreads();
+    }
+    for (int c = wid; c < nc; c += 8) {
+      double x = lane < nr ? X[r0 + lane + c * ldx] : 0.0;
+      for (int j = nr - 1; j >= 0; --j) {
+        double xj = __shfl_sync(0xffffffffu, x, j);
+        xj /= LU[(r0 + j) + (size_t)(r0 + j) * lda];
+        if (lane == j) x = xj;
+        if (lane < j) x -= LU[(r0 + lane) + (size_t)(r0 + j) * lda] * xj;
+      }
+      if (lane < nr) X[r0 + lane + c * ldx] = x;
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < n * nc; e += nt) {
+    const int i = e % n, c = e / n;
+    SB[i + (size_t)(c0 + c) * S.ldb] = X[i + c * ldx];
+  }
+}
+
+// ------------------------------------------------------------------ gecon
+
+// x := op(T)^-1 x for one vector in shared memory; T is the unit-lower (L)
+// or non-unit-upper (U) part of the LU, op = N or T.  32-row blocks: warp 0
+// solves the diagonal block, then every thread updates the rest.
+__device__ void trsv_block(const double* LU, int lda, int n, double* x, bool upper, bool trans) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
+  // effective lower-triangular solve if (lower,N) or (upper,T): forward sweep
+  const bool forward = (!upper && !trans) || (upper && trans);
+  const int nblk = (n + 31) / 32;
+  for (int bb = 0; bb < nblk; ++bb) {
+    const int b = forward ? bb : nblk - 1 - bb;
+    const int r0 = b * 32, nr = min(32, n - r0);
+    if (tid < 32) {
+      double v = lane < nr ? x[r0 + lane] : 0.0;
+      // element (i, j) of op(T) inside the block
+      auto elem = [&](int i, int j) -> double {
+        const int gi = r0 + i, gj = r0 + j;
+        return trans ? LU[gj + (size_t)gi * lda] : LU[gi + (size_t)gj * lda];
+      };
+      if (forward) {
+        for (int j = 0; j < nr; ++j) {
+          double xj = __shfl_sync(0xffffffffu, v, j);
+          if (upper) xj /= elem(j, j);
+          if (lane == j) v = xj;
+          if (lane > j && lane < nr) v -= elem(lane, j) * xj;
+        }
+      } else {
+        for (int j = nr - 1; j >= 0; --j) {
+          double xj = __shfl_sync(0xffffffffu, v, j);
+          if (upper) xj /= elem(j, j);
+          if (lane == j) v = xj;
+          if (lane < j) v -= elem(lane, j) * xj;
+        }
+      }
+      if (lane < nr) x[r0 + lane] = v;
+    }
+    __syncthreads();
+    // update the not-yet-solved entries with this block's solution
+    const int lo = forward ? r0 + nr : 0, hi = forward ? n : r0;
+    for (int i = lo + tid; i < hi; i += nt) {
+      double s = x[i];
+      for (int j = 0; j < nr; ++j) {
+        const int gj = r0 + j;
+        const double t = trans ? LU[gj + (size_t)i * lda] : LU[i + (size_t)gj * lda];
+        s -= t * x[gj];
+      }
+      x[i] = s;
+    }
+    __syncthreads();
+  }
+}
+
+__device__ double block_asum(const double* x, int n, double* red) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += fabs(x[i]);
+  return block_sum(s, red);
+}
+
+__device__ int block_iamax(const double* x, int n, double* rv, int* ri) {
+  ArgMax a{-1.0, 0x7fffffff};
+  for (int i = threadIdx.x; i < n; i += blockDim.x) a = argmax_pick(a, ArgMax{fabs(x[i]), i});
+  return block_argmax(a, rv, ri).i;
+}
+
+// LAPACK dgecon(norm='1') with dlacn2 (Higham's estimator), restated; the
+// dlatrs overflow scaling is not needed at the conditioning the solver
+// admits (documented in DESIGN.md).
+__global__ void __launch_bounds__(256) gecon_kernel(const Bases bases,
+                                                     const LuDesc* __restrict__ descs) {
+  const LuDesc L = descs[blockIdx.x];
+  const double* LUa = at<const double>(bases, L.A);
+  const int n = L.n;
+  extern __shared__ double sh[];
+  double* x = sh;        // n
+  double* v = sh + n;    // n
+  int* isgn = reinterpret_cast<int*>(sh + 2 * n);
+  __shared__ double red_v[8];
+  __shared__ int red_i[8];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (L.rcond == kNull) return;
+  double* rcond = at<double>(bases, L.rcond);
+  if (n == 0) { if (tid == 0) *rcond = 1.0; return; }
+  const double anorm = *at<const double>(bases, L.anorm);
+  if (anorm == 0.0) { if (tid == 0) *rcond = 0.0; return; }
+  if (L.info != kNull && *at<const int>(bases, L.info) != 0) { if (tid == 0) *rcond = 0.0; return; }
+
+  auto apply = [&](int kase) {
+    if (kase == 1) {
+      trsv_block(LUa, L.lda, n, x, false, false);
+      trsv_block(LUa, L.lda, n, x, true, false);
+    } else {
+      trsv_block(LUa, L.lda, n, x, true, true);
+      trsv_block(LUa, L.lda, n, x, false, true);
+    }
+  };
+
+  double est;
+  for (int i = tid; i < n; i += nt) x[i] = 1.0 / n;
+  __syncthreads();
+  apply(1);
+  if (n == 1) {
+    est = fabs(x[0]);
+  } else {
+    est = block_asum(x, n, red_v);
+    for (int i = tid; i < n; i += nt) {
+      x[i] = x[i] >= 0.0 ? 1.0 : -1.0;
+      isgn[i] = x[i] >= 0.0 ? 1 : -1;
+    }
+    __syncthreads();
+    apply(2);
+    int j = block_iamax(x, n, red_v, red_i);
+    int iter = 2;
+    bool alt = false;
+    for (;;) {
+      // L50
+      for (int i = tid; i < n; i += nt) x[i] = (i == j) ? 1.0 : 0.0;
+      __syncthreads();
+      apply(1);
+      for (int i = tid; i < n; i += nt) v[i] = x[i];
+      const double estold = est;
+      est = block_asum(v, n, red_v);
+      // repeated sign vector?
+      __shared__ int s_diff;
+      if (tid == 0) s_diff = 0;
+      __syncthreads();
+      for (int i = tid; i < n; i += nt) {
+        const int xs = x[i] >= 0.0 ? 1 : -1;
+        if (xs != isgn[i]) s_diff = 1;
+      }
+      __syncthreads();
+      const int diff = s_diff;
+      __syncthreads();
+      if (!diff || est <= estold) { alt = true; break; }
+      for (int i = tid; i < n; i += nt) {
+        x[i] = x[i] >= 0.0 ? 1.0 : -1.0;
+        isgn[i] = x[i] >= 0.0 ? 1 : -1;
+      }
+      __syncthreads();
+      apply(2);
+      const int jlast = j;
+      j = block_iamax(x, n, red_v, red_i);
+      if (x[jlast] != fabs(x[j]) && iter < 5) {
+        ++iter;
+        continue;
+      }
+      alt = true;
+      break;
+    }
+    if (alt) {  // L120: alternating-sign probe
+      for (int i = tid; i < n; i += nt) {
+        const double s = (i % 2 == 0) ? 1.0 : -1.0;
+        x[i] = s * (1.0 + (double)i / (double)(n - 1));
+      }
+      __syncthreads();
+      apply(1);
+      const double temp = 2.0 * (block_asum(x, n, red_v) / (double)(3 * n));
+      if (temp > est) est = temp;
+    }
+  }
+  if (tid == 0) {
+    const double ainvnm = est;
+    *rcond = ainvnm != 0.0 ? (1.0 / ainvnm) / anorm : 0.0;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_getrf_batched(const Bases& b, const LuDesc* d, int count, int max_n, cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  const int ldp = max_n > 0 ? max_n : 1;
+  if (max_n <= 640) {
+    const size_t sm = (size_t)ldp * 32 * sizeof(double);
+    cudaFuncSetAttribute(getrf_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    getrf_kernel<32><<<count, LU_THREADS, sm, s>>>(b, d, ldp);
+  } else if (max_n <= 1280) {
+    const size_t sm = (size_t)ldp * 16 * sizeof(double);
+    cudaFuncSetAttribute(getrf_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    getrf_kernel<16><<<count, LU_THREADS, sm, s>>>(b, d, ldp);
+  } else {
+    const size_t sm = (size_t)ldp * 8 * sizeof(double);
+    if (sm > 200 * 1024) return cudaErrorInvalidValue;
+    cudaFuncSetAttribute(getrf_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    getrf_kernel<8><<<count, LU_THREADS, sm, s>>>(b, d, ldp);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_getrs_batched(const Bases& b, const LuSolveDesc* d, int count, int max_n, int max_nrhs,
+                                 cudaStream_t s) {
+  if (count <= 0 || max_n <= 0 || max_nrhs <= 0) return cudaSuccess;
+  const int ldx = ((max_n + 15) / 16) * 16 + 4;
+  if (max_n <= 640) {
+    constexpr int RC = 32;
+    const size_t sm = (size_t)ldx * RC * sizeof(double) + (size_t)max_n * sizeof(int);
+    cudaFuncSetAttribute(getrs_kernel<RC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    dim3 grid(count, (max_nrhs + RC - 1) / RC);
+    getrs_kernel<RC><<<grid, RS_THREADS, sm, s>>>(b, d, ldx);
+  } else {
+    constexpr int RC = 16;
+    const size_t sm = (size_t)ldx * RC * sizeof(double) + (size_t)max_n * sizeof(int);
+    if (sm > 220 * 1024) return cudaErrorInvalidValue;
+    cudaFuncSetAttribute(getrs_kernel<RC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    dim3 grid(count, (max_nrhs + RC - 1) / RC);
+    getrs_kernel<RC><<<grid, RS_THREADS, sm, s>>>(b, d, ldx);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gecon_batched(const Bases& b, const LuDesc* d, int count, int max_n, cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  const size_t sm = (size_t)(max_n > 0 ? max_n : 1) * (2 * sizeof(double) + sizeof(int));
+  cudaFuncSetAttribute(gecon_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  gecon_kernel<<<count, 256, sm, s>>>(b, d);
+  return cudaGetLastError();
+}
+
+}  // namespace hks

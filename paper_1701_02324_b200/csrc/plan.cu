@@ -1,0 +1,708 @@
+// Level-batched factorize / solve / hmatvec over the flat layout
+// (solver.py:111-270, treecode.py:41-128) and the plan-bound C-ABI entry
+// points.  See plan.h.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <limits>
+
+#include "plan.h"
+
+namespace hks {
+
+Layout make_layout(int64_t n, int64_t depth, int64_t s) {
+  Layout L;
+  L.n = n;
+  L.depth = depth;
+  L.s = s;
+  L.nn = ((int64_t)1 << (depth + 1)) - 1;
+  L.begin.assign(L.nn, 0);
+  L.size.assign(L.nn, 0);
+  L.rcap.assign(L.nn, 0);
+  L.ccap.assign(L.nn, 0);
+  L.size[0] = n;
+  for (int64_t i = 0; i < L.first(depth); ++i) {  // tree.py:117,121: left takes ceil
+    const int64_t half = (L.size[i] + 1) / 2;
+    L.begin[2 * i + 1] = L.begin[i];
+    L.size[2 * i + 1] = half;
+    L.begin[2 * i + 2] = L.begin[i] + half;
+    L.size[2 * i + 2] = L.size[i] - half;
+  }
+  for (int64_t i = L.nn - 1; i >= 0; --i) {
+    L.ccap[i] = L.is_leaf(i) ? L.size[i] : L.rcap[2 * i + 1] + L.rcap[2 * i + 2];
+    L.rcap[i] = i == 0 ? 0 : std::min<int64_t>(s, L.ccap[i]);
+  }
+  for (int b = 0; b < HKS_NBUF; ++b) L.off[b].assign(L.nn, -1);
+  auto put = [&](int b, int64_t i, int64_t elems) {
+    L.off[b][i] = L.total[b];
+    L.total[b] += elems;
+  };
+  for (int64_t i = 0; i < L.nn; ++i) {
+    const bool leaf = L.is_leaf(i);
+    if (i > 0) {
+      put(HKS_BUF_INTERP, i, L.rcap[i] * L.ccap[i]);
+      put(HKS_BUF_SKEL, i, L.rcap[i]);
+      put(HKS_BUF_THETA, i, L.rcap[i] * L.rcap[i]);
+    }
+    if (leaf) {
+      put(HKS_BUF_LEAF_LU, i, L.size[i] * L.size[i]);
+      put(HKS_BUF_LEAF_PIV, i, L.size[i]);
+      if (i > 0) put(HKS_BUF_PHI, i, L.size[i] * L.rcap[i]);
+    } else {
+      put(HKS_BUF_Z_LU, i, L.ccap[i] * L.ccap[i]);
+      put(HKS_BUF_Z_PIV, i, L.ccap[i]);
+      if (i > 0) put(HKS_BUF_PUSH, i, L.ccap[i] * L.rcap[i]);
+      put(HKS_BUF_COUP, i, L.rcap[2 * i + 1] * L.rcap[2 * i + 2]);
+    }
+    L.off[HKS_BUF_STATS][i] = i;
+  }
+  L.total[HKS_BUF_STATS] = 3 * L.nn;
+  return L;
+}
+
+cudaError_t StepList::upload(cudaStream_t stream) {
+  if (host_.empty()) return cudaSuccess;
+  if (dev_bytes_ < host_.size()) {
+    if (dev_) cudaFree(dev_);
+    dev_ = nullptr;
+    cudaError_t e = cudaMalloc(&dev_, host_.size());
+    if (e != cudaSuccess) return e;
+    dev_bytes_ = host_.size();
+  }
+  cudaError_t e = cudaMemcpyAsync(dev_, host_.data(), host_.size(), cudaMemcpyHostToDevice, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  for (size_t s = 0; s < steps_.size(); ++s) steps_[s].d = dev_ + offs_[s];
+  return e;
+}
+
+void StepList::clear() {
+  host_.clear();
+  offs_.clear();
+  steps_.clear();
+}
+
+StepList::~StepList() {
+  if (dev_) cudaFree(dev_);
+}
+
+cudaError_t DevBuf::ensure(size_t b) {
+  if (b <= bytes) return cudaSuccess;
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+  cudaError_t e = cudaMalloc(&p, b);
+  if (e == cudaSuccess) bytes = b;
+  return e;
+}
+
+DevBuf::~DevBuf() {
+  if (p) cudaFree(p);
+}
+
+cudaError_t StepList::run(const Bases& b, const double* X, int d, const KernelParams& kp,
+                          cudaStream_t s) const {
+  for (const Step& st : steps_) {
+    cudaError_t e = cudaSuccess;
+    switch (st.kind) {
+      case ST_GEMM:
+        e = launch_gemm_batched(b, (const GemmDesc*)st.d, st.count, st.p0, st.p1, s);
+        break;
+      case ST_COPY:
+        e = launch_copy_batched(b, (const CopyDesc*)st.d, st.count, st.p0, s);
+        break;
+      case ST_GETRF:
+        e = launch_getrf_batched(b, (const LuDesc*)st.d, st.count, st.p0, s);
+        break;
+      case ST_GETRS:
+        e = launch_getrs_batched(b, (const LuSolveDesc*)st.d, st.count, st.p0, st.p1, s);
+        break;
+      case ST_GECON:
+        e = launch_gecon_batched(b, (const LuDesc*)st.d, st.count, st.p0, s);
+        break;
+      case ST_EVAL_CM:
+      case ST_EVAL_RM:
+        e = launch_eval_batched(X, d, kp, b, (const EvalDesc*)st.d, st.count, st.p0, st.p1,
+                                st.kind == ST_EVAL_RM, s);
+        break;
+      case ST_KSUM:
+        e = launch_ksum_batched(X, d, kp, b, (const SumDesc*)st.d, st.count, st.p0, s);
+        break;
+    }
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+namespace {
+
+inline Ref D(int buf, int64_t elem) { return make_ref(buf, (uint64_t)elem * 8); }
+inline Ref I32(int buf, int64_t elem) { return make_ref(buf, (uint64_t)elem * 4); }
+inline Ref adv(Ref r, int64_t elems) { return r + (uint64_t)elems * 8; }
+
+struct Gemms {
+  std::vector<GemmDesc> v;
+  int mm = 0, mn = 0;
+  void add(Ref A, int lda, int ta, Ref B, int ldb, int tb, Ref C, int ldc, int m, int n, int k,
+           double alpha, double beta) {
+    if (m <= 0 || n <= 0) return;
+    v.push_back(GemmDesc{A, B, C, m, n, k, lda, ldb, ldc, ta, tb, alpha, beta});
+    mm = std::max(mm, m);
+    mn = std::max(mn, n);
+  }
+  void flush(StepList& sl) {
+    sl.add(ST_GEMM, v, mm, mn);
+    v.clear();
+    mm = mn = 0;
+  }
+};
+
+struct Copies {
+  std::vector<CopyDesc> v;
+  int me = 0;
+  void copy(Ref src, int lds, int trans, Ref dst, int ldd, int m, int n) {
+    if (m <= 0 || n <= 0) return;
+    v.push_back(CopyDesc{src, dst, m, n, lds, ldd, trans, 0, 1.0});
+    me = std::max(me, m * n);
+  }
+  void fill(Ref dst, int ldd, int m, int n, bool identity) {
+    if (m <= 0 || n <= 0) return;
+    v.push_back(CopyDesc{kNull, dst, m, n, 0, ldd, 0, identity ? 1 : 2, 1.0});
+    me = std::max(me, m * n);
+  }
+  void flush(StepList& sl) {
+    sl.add(ST_COPY, v, me);
+    v.clear();
+    me = 0;
+  }
+};
+
+struct Ctx {
+  const hks_plan& P;
+  const Layout& L;
+  explicit Ctx(const hks_plan& p) : P(p), L(p.L) {}
+  Ref interp(int64_t i) const { return D(HKS_BUF_INTERP, L.off[HKS_BUF_INTERP][i]); }
+  Ref theta(int64_t i) const { return D(HKS_BUF_THETA, L.off[HKS_BUF_THETA][i]); }
+  Ref leaf_lu(int64_t i) const { return D(HKS_BUF_LEAF_LU, L.off[HKS_BUF_LEAF_LU][i]); }
+  Ref leaf_piv(int64_t i) const { return I32(HKS_BUF_LEAF_PIV, L.off[HKS_BUF_LEAF_PIV][i]); }
+  Ref phi(int64_t i) const { return D(HKS_BUF_PHI, L.off[HKS_BUF_PHI][i]); }
+  Ref z_lu(int64_t i) const { return D(HKS_BUF_Z_LU, L.off[HKS_BUF_Z_LU][i]); }
+  Ref z_piv(int64_t i) const { return I32(HKS_BUF_Z_PIV, L.off[HKS_BUF_Z_PIV][i]); }
+  Ref push(int64_t i) const { return D(HKS_BUF_PUSH, L.off[HKS_BUF_PUSH][i]); }
+  Ref coup(int64_t i) const { return D(HKS_BUF_COUP, L.off[HKS_BUF_COUP][i]); }
+  Ref skel(int64_t i) const { return make_ref(HKS_BUF_SKEL, (uint64_t)L.off[HKS_BUF_SKEL][i] * 8); }
+  Ref anorm(int64_t i) const { return D(HKS_BUF_STATS, i); }
+  Ref rcond(int64_t i) const { return D(HKS_BUF_STATS, L.nn + i); }
+  Ref info(int64_t i) const { return make_ref(HKS_BUF_STATS, (uint64_t)L.nn * 16 + (uint64_t)i * 4); }
+  int r(int64_t i) const { return (int)P.rank[i]; }
+  // stacked slot of node i inside its parent's R_p x k block (buffer `buf`, base element `at`)
+  Ref slot(int buf, int64_t at, int64_t i, int64_t k, int* ld) const {
+    const int64_t p = (i - 1) / 2;
+    *ld = (int)P.R(p);
+    const int64_t row = (i == 2 * p + 1) ? 0 : P.rank[2 * p + 1];
+    return D(buf, at + P.stack_off[p] * k + row);
+  }
+  Ref block(int buf, int64_t at, int64_t p, int64_t k) const { return D(buf, at + P.stack_off[p] * k); }
+};
+
+// blockdiag(theta_a, theta_b) into an R x R slot (ld R)
+void add_theta_hat(Copies& cp, const Ctx& c, int64_t i, Ref Y) {
+  const int rl = c.r(2 * i + 1), rr = c.r(2 * i + 2), R = rl + rr;
+  cp.copy(c.theta(2 * i + 1), rl, 0, Y, R, rl, rl);
+  cp.copy(c.theta(2 * i + 2), rr, 0, adv(Y, rl + (int64_t)rl * R), R, rr, rr);
+  cp.fill(adv(Y, (int64_t)rl * R), R, rl, rr, false);
+  cp.fill(adv(Y, rl), R, rr, rl, false);
+}
+
+size_t factorize_workspace(const hks_plan& P) {
+  size_t need = 0;
+  for (int64_t lev = 1; lev < P.L.depth; ++lev) {
+    size_t lv = 0;
+    for (int64_t i = P.L.first(lev); i < P.L.first(lev) + P.L.count(lev); ++i) {
+      const int64_t R = P.R(i);
+      lv += 2 * R * R + P.rank[i] * R;
+    }
+    need = std::max(need, lv);
+  }
+  return need;
+}
+
+// ------------------------------------------------------------ factorize
+
+void build_factorize(const hks_plan& P, bool with_cond, StepList& sl) {
+  const Ctx c(P);
+  const Layout& L = P.L;
+  {  // leaf level (solver.py:128-137)
+    std::vector<EvalDesc> ev;
+    std::vector<LuDesc> lu;
+    std::vector<LuSolveDesc> rs;
+    Copies cp;
+    Gemms gm;
+    int mx = 0, mr = 0;
+    for (int64_t i = L.first(L.depth); i < L.nn; ++i) {
+      const int m = (int)L.size[i], r = c.r(i);
+      ev.push_back(EvalDesc{kNull, kNull, L.begin[i], L.begin[i], m, m, c.leaf_lu(i), m, 1});
+      lu.push_back(LuDesc{c.leaf_lu(i), c.leaf_piv(i), c.info(i), kNull, kNull, m, m});
+      mx = std::max(mx, m);
+      if (i > 0 && r > 0) {
+        cp.copy(c.interp(i), r, 1, c.phi(i), m, m, r);  // phi = P^T, then A^-1 P^T
+        rs.push_back(LuSolveDesc{c.leaf_lu(i), c.leaf_piv(i), c.phi(i), m, r, m, m});
+        mr = std::max(mr, r);
+        gm.add(c.interp(i), r, 0, c.phi(i), m, 0, c.theta(i), r, r, r, m, 1.0, 0.0);
+      }
+    }
+    sl.add(ST_EVAL_CM, ev, mx, mx);
+    sl.add(ST_GETRF, lu, mx);
+    cp.flush(sl);
+    sl.add(ST_GETRS, rs, mx, mr);
+    gm.flush(sl);
+  }
+  for (int64_t lev = L.depth - 1; lev >= 0; --lev) {  // internal levels (solver.py:139-161)
+    Copies c_id, c_y, c_t;
+    Gemms g_z, g_f, g_tf, g_w, g_out;
+    std::vector<LuDesc> lu;
+    std::vector<LuSolveDesc> rs;
+    int maxR = 0;
+    int64_t at = 0;
+    for (int64_t i = L.first(lev); i < L.first(lev) + L.count(lev); ++i) {
+      const int64_t a = 2 * i + 1, b = 2 * i + 2;
+      const int rl = c.r(a), rr = c.r(b), R = rl + rr, r = c.r(i);
+      maxR = std::max(maxR, R);
+      const Ref Z = c.z_lu(i), C = c.coup(i);
+      c_id.fill(Z, R, R, R, true);
+      g_z.add(c.theta(a), rl, 0, C, rl, 0, adv(Z, (int64_t)rl * R), R, rl, rr, rl, 1.0, 1.0);
+      g_z.add(c.theta(b), rr, 0, C, rl, 1, adv(Z, rl), R, rr, rl, rr, 1.0, 1.0);
+      lu.push_back(LuDesc{Z, c.z_piv(i), c.info(i), c.anorm(i), with_cond ? c.rcond(i) : kNull, R, R});
+      if (lev == 0) continue;
+      const Ref Y = D(B_FWS, at);
+      at += (int64_t)R * R;
+      const Ref F = D(B_FWS, at);
+      at += (int64_t)R * R;
+      const Ref W = D(B_FWS, at);
+      at += (int64_t)r * R;
+      const Ref Pi = c.interp(i), pu = c.push(i);
+      add_theta_hat(c_y, c, i, Y);
+      rs.push_back(LuSolveDesc{Z, c.z_piv(i), Y, R, R, R, R});
+      // folded F = B Z^-1 thhat (solver.py:86-89, 156)
+      g_f.add(C, rl, 0, adv(Y, rl), R, 0, F, R, rl, R, rr, 1.0, 0.0);
+      g_f.add(C, rl, 1, Y, R, 0, adv(F, rl), R, rr, R, rl, 1.0, 0.0);
+      // T = thhat - thhat F (reusing Y); push = P^T - F P^T (solver.py:157-158)
+      add_theta_hat(c_t, c, i, Y);
+      c_t.copy(Pi, r, 1, pu, R, R, r);
+      g_tf.add(c.theta(a), rl, 0, F, R, 0, Y, R, rl, R, rl, -1.0, 1.0);
+      g_tf.add(c.theta(b), rr, 0, adv(F, rl), R, 0, adv(Y, rl), R, rr, R, rr, -1.0, 1.0);
+      g_w.add(Pi, r, 0, Y, R, 0, W, r, r, R, R, 1.0, 0.0);
+      g_out.add(W, r, 0, Pi, r, 1, c.theta(i), r, r, r, R, 1.0, 0.0);
+      g_out.add(F, R, 0, Pi, r, 1, pu, R, R, r, R, -1.0, 1.0);
+    }
+    c_id.flush(sl);
+    g_z.flush(sl);
+    sl.add(ST_GETRF, lu, maxR);
+    if (with_cond) sl.add(ST_GECON, lu, maxR);
+    if (lev == 0) continue;
+    c_y.flush(sl);
+    sl.add(ST_GETRS, rs, maxR, maxR);
+    g_f.flush(sl);
+    c_t.flush(sl);
+    g_tf.flush(sl);
+    g_w.flush(sl);
+    g_out.flush(sl);
+  }
+}
+
+// ------------------------------------------------------------ solve
+
+void build_solve(const hks_plan& P, int64_t kk, StepList& sl) {
+  const Ctx c(P);
+  const Layout& L = P.L;
+  const int k = (int)kk, n = (int)L.n;
+  const int64_t stk = P.stack_total * kk;
+  const int64_t S = 0, G = stk, Gb = 2 * stk;  // element bases inside B_VWS
+  {  // upward, leaves (solver.py:215-218)
+    Gemms gp;
+    Copies cp;
+    std::vector<LuSolveDesc> rs;
+    int mx = 0;
+    for (int64_t i = L.first(L.depth); i < L.nn; ++i) {
+      const int m = (int)L.size[i], r = c.r(i);
+      mx = std::max(mx, m);
+      if (i > 0 && r > 0) {
+        int ld;
+        const Ref dst = c.slot(B_VWS, S, i, k, &ld);
+        gp.add(c.phi(i), m, 1, D(B_VIN, L.begin[i]), n, 0, dst, ld, r, k, m, 1.0, 0.0);
+      }
+      cp.copy(D(B_VIN, L.begin[i]), n, 0, D(B_VOUT, L.begin[i]), n, m, k);
+      rs.push_back(LuSolveDesc{c.leaf_lu(i), c.leaf_piv(i), D(B_VOUT, L.begin[i]), m, k, m, n});
+    }
+    gp.flush(sl);
+    cp.flush(sl);
+    sl.add(ST_GETRS, rs, mx, k);
+  }
+  for (int64_t lev = L.depth - 1; lev >= 0; --lev) {  // upward, internal (solver.py:219-233)
+    Copies cp;
+    std::vector<LuSolveDesc> rs;
+    Gemms g1, g2, g3;
+    int maxR = 0;
+    for (int64_t i = L.first(lev); i < L.first(lev) + L.count(lev); ++i) {
+      const int64_t a = 2 * i + 1, bb = 2 * i + 2;
+      const int rl = c.r(a), rr = c.r(bb), R = rl + rr, r = c.r(i);
+      maxR = std::max(maxR, R);
+      const Ref Si = c.block(B_VWS, S, i, k), Gi = c.block(B_VWS, G, i, k), Gbi = c.block(B_VWS, Gb, i, k);
+      const Ref C = c.coup(i);
+      cp.copy(Si, R, 0, Gi, R, R, k);
+      rs.push_back(LuSolveDesc{c.z_lu(i), c.z_piv(i), Gi, R, k, R, R});
+      g1.add(C, rl, 0, adv(Gi, rl), R, 0, Gbi, R, rl, k, rr, 1.0, 0.0);
+      g1.add(C, rl, 1, Gi, R, 0, adv(Gbi, rl), R, rr, k, rl, 1.0, 0.0);
+      if (lev == 0) continue;
+      g2.add(c.theta(a), rl, 0, Gbi, R, 0, Si, R, rl, k, rl, -1.0, 1.0);
+      g2.add(c.theta(bb), rr, 0, adv(Gbi, rl), R, 0, adv(Si, rl), R, rr, k, rr, -1.0, 1.0);
+      int ld;
+      const Ref dst = c.slot(B_VWS, S, i, k, &ld);
+      g3.add(c.interp(i), r, 0, Si, R, 0, dst, ld, r, k, R, 1.0, 0.0);
+    }
+    cp.flush(sl);
+    sl.add(ST_GETRS, rs, maxR, k);
+    g1.flush(sl);
+    g2.flush(sl);
+    g3.flush(sl);
+  }
+  for (int64_t lev = 1; lev < L.depth; ++lev) {  // downward (solver.py:235-253)
+    Gemms g;
+    for (int64_t i = L.first(lev); i < L.first(lev) + L.count(lev); ++i) {
+      const int R = (int)P.R(i), r = c.r(i);
+      if (r == 0) continue;
+      int ld;
+      const Ref cin = c.slot(B_VWS, Gb, i, k, &ld);
+      g.add(c.push(i), R, 0, cin, ld, 0, c.block(B_VWS, Gb, i, k), R, R, k, r, 1.0, 1.0);
+    }
+    g.flush(sl);
+  }
+  if (L.depth > 0) {
+    Gemms g;
+    for (int64_t i = L.first(L.depth); i < L.nn; ++i) {
+      const int m = (int)L.size[i], r = c.r(i);
+      if (r == 0) continue;
+      int ld;
+      const Ref cin = c.slot(B_VWS, Gb, i, k, &ld);
+      g.add(c.phi(i), m, 0, cin, ld, 0, D(B_VOUT, L.begin[i]), n, m, k, r, -1.0, 1.0);
+    }
+    g.flush(sl);
+  }
+}
+
+// ------------------------------------------------------------ hmatvec / upward
+
+void build_upward(const hks_plan& P, int64_t kk, int64_t S, StepList& sl) {
+  const Ctx c(P);
+  const Layout& L = P.L;
+  const int k = (int)kk, n = (int)L.n;
+  if (L.depth == 0) return;
+  Gemms g;
+  for (int64_t i = L.first(L.depth); i < L.nn; ++i) {  // treecode.py:81-82
+    int ld;
+    const Ref dst = c.slot(B_VWS, S, i, k, &ld);
+    g.add(c.interp(i), c.r(i), 0, D(B_VIN, L.begin[i]), n, 0, dst, ld, c.r(i), k, (int)L.size[i], 1.0, 0.0);
+  }
+  g.flush(sl);
+  for (int64_t lev = L.depth - 1; lev >= 1; --lev) {  // treecode.py:83-88
+    Gemms g2;
+    for (int64_t i = L.first(lev); i < L.first(lev) + L.count(lev); ++i) {
+      int ld;
+      const Ref dst = c.slot(B_VWS, S, i, k, &ld);
+      const int R = (int)P.R(i);
+      g2.add(c.interp(i), c.r(i), 0, c.block(B_VWS, S, i, k), R, 0, dst, ld, c.r(i), k, R, 1.0, 0.0);
+    }
+    g2.flush(sl);
+  }
+}
+
+void build_matvec(const hks_plan& P, int64_t kk, StepList& sl) {
+  const Ctx c(P);
+  const Layout& L = P.L;
+  const int k = (int)kk, n = (int)L.n;
+  const int64_t stk = P.stack_total * kk;
+  const int64_t S = 0, A = stk;
+  {  // leaves: u = K w + lam w, K never stored (treecode.py:99-101)
+    std::vector<SumDesc> ks;
+    int mx = 0;
+    for (int64_t i = L.first(L.depth); i < L.nn; ++i) {
+      const int m = (int)L.size[i];
+      mx = std::max(mx, m);
+      ks.push_back(SumDesc{kNull, kNull, L.begin[i], L.begin[i], m, m, k, D(B_VIN, L.begin[i]), n,
+                           D(B_VOUT, L.begin[i]), n, 0.0, 1});
+    }
+    sl.add(ST_KSUM, ks, mx);
+  }
+  if (L.depth == 0) return;
+  build_upward(P, kk, S, sl);
+  for (int64_t lev = 0; lev < L.depth; ++lev) {  // downward (treecode.py:109-123)
+    Gemms gp, gc;
+    for (int64_t i = L.first(lev); i < L.first(lev) + L.count(lev); ++i) {
+      const int64_t a = 2 * i + 1, bb = 2 * i + 2;
+      const int rl = c.r(a), rr = c.r(bb), R = rl + rr, r = c.r(i);
+      const Ref Ai = c.block(B_VWS, A, i, k), Si = c.block(B_VWS, S, i, k), C = c.coup(i);
+      const bool has_acc = lev > 0;
+      if (has_acc) {
+        int ld;
+        const Ref acc = c.slot(B_VWS, A, i, k, &ld);
+        gp.add(c.interp(i), r, 1, acc, ld, 0, Ai, R, R, k, r, 1.0, 0.0);
+      }
+      const double beta = has_acc ? 1.0 : 0.0;
+      gc.add(C, rl, 0, adv(Si, rl), R, 0, Ai, R, rl, k, rr, 1.0, beta);
+      gc.add(C, rl, 1, Si, R, 0, adv(Ai, rl), R, rr, k, rl, 1.0, beta);
+    }
+    gp.flush(sl);
+    gc.flush(sl);
+  }
+  Gemms g;  // leaves (treecode.py:124-127)
+  for (int64_t i = L.first(L.depth); i < L.nn; ++i) {
+    const int m = (int)L.size[i], r = c.r(i);
+    if (r == 0) continue;
+    int ld;
+    const Ref acc = c.slot(B_VWS, A, i, k, &ld);
+    g.add(c.interp(i), r, 1, acc, ld, 0, D(B_VOUT, L.begin[i]), n, m, k, r, 1.0, 1.0);
+  }
+  g.flush(sl);
+}
+
+}  // namespace
+}  // namespace hks
+
+// ======================================================================= C ABI
+
+using namespace hks;
+
+static inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+static Bases make_bases(void* const* buffers) {
+  Bases b;
+  std::memset(&b, 0, sizeof(b));
+  for (int i = 0; i < HKS_NBUF; ++i) b.p[i] = buffers ? static_cast<char*>(buffers[i]) : nullptr;
+  return b;
+}
+
+extern "C" int hks_layout(int64_t n, int64_t depth, int64_t max_rank, int64_t* sizes, int64_t* offsets) {
+  if (n < 1 || depth < 0 || depth > 40 || max_rank < 1)
+    return set_error(HKS_ERR_INVALID, "hks_layout: bad arguments n=%lld depth=%lld max_rank=%lld",
+                     (long long)n, (long long)depth, (long long)max_rank);
+  Layout L = make_layout(n, depth, max_rank);
+  for (int b = 0; b < HKS_NBUF; ++b) {
+    if (sizes) sizes[b] = L.total[b];
+    if (offsets) std::memcpy(offsets + b * L.nn, L.off[b].data(), L.nn * sizeof(int64_t));
+  }
+  return HKS_OK;
+}
+
+extern "C" int hks_plan_create(hks_plan** out, const double* X, int64_t n, int64_t d, int64_t depth,
+                               int64_t max_rank, const int64_t* ranks_host, const hks_kernel* kern) {
+  if (!out || !X || !ranks_host || !kern || n < 1 || d < 1 || depth < 0 || max_rank < 1)
+    return set_error(HKS_ERR_INVALID, "hks_plan_create: bad arguments");
+  std::unique_ptr<hks_plan> P(new hks_plan());
+  P->L = make_layout(n, depth, max_rank);
+  P->X = X;
+  P->d = d;
+  P->rank.assign(ranks_host, ranks_host + P->L.nn);
+  P->rank[0] = 0;
+  for (int64_t i = 1; i < P->L.nn; ++i) {
+    const int64_t cap = P->L.is_leaf(i) ? std::min<int64_t>(max_rank, P->L.size[i])
+                                        : std::min<int64_t>(max_rank, P->R(i));
+    if (P->rank[i] < 0 || P->rank[i] > cap)
+      return set_error(HKS_ERR_INVALID, "hks_plan_create: rank %lld of node %lld outside [0, %lld]",
+                       (long long)P->rank[i], (long long)i, (long long)cap);
+  }
+  P->kp = make_kernel_params(kern);
+  P->kern = *kern;
+  P->stack_off.assign(P->L.nn, -1);
+  for (int64_t i = 0; i < P->L.first(P->L.depth); ++i) {
+    P->stack_off[i] = P->stack_total;
+    P->stack_total += P->R(i);
+  }
+  *out = P.release();
+  return HKS_OK;
+}
+
+extern "C" int hks_plan_destroy(hks_plan* P) {
+  delete P;
+  return HKS_OK;
+}
+
+extern "C" int hks_build_operator(hks_plan* P, void* const* buffers, void* stream) {
+  if (!P || !buffers) return set_error(HKS_ERR_INVALID, "hks_build_operator: null argument");
+  cudaStream_t s = as_stream(stream);
+  if (P->coup_steps.empty()) {
+    const Layout& L = P->L;
+    std::vector<EvalDesc> ev;
+    int mm = 0, mn = 0;
+    for (int64_t i = 0; i < L.first(L.depth); ++i) {  // treecode.py:48-55
+      const int rl = (int)P->rank[2 * i + 1], rr = (int)P->rank[2 * i + 2];
+      if (rl == 0 || rr == 0) continue;
+      ev.push_back(EvalDesc{make_ref(HKS_BUF_SKEL, (uint64_t)L.off[HKS_BUF_SKEL][2 * i + 1] * 8),
+                            make_ref(HKS_BUF_SKEL, (uint64_t)L.off[HKS_BUF_SKEL][2 * i + 2] * 8), 0, 0, rl, rr,
+                            make_ref(HKS_BUF_COUP, (uint64_t)L.off[HKS_BUF_COUP][i] * 8), rl, 0});
+      mm = std::max(mm, rl);
+      mn = std::max(mn, rr);
+    }
+    P->coup_steps.add(ST_EVAL_CM, ev, mm, mn);
+    cudaError_t e = P->coup_steps.upload(s);
+    if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_build_operator: %s", cudaGetErrorString(e));
+  }
+  cudaError_t e = P->coup_steps.run(make_bases(buffers), P->X, (int)P->d, P->kp, s);
+  if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_build_operator: %s", cudaGetErrorString(e));
+  return HKS_OK;
+}
+
+extern "C" int hks_leaf_block(hks_plan* P, int64_t leaf, double* out, void* stream) {
+  if (!P || leaf < P->L.first(P->L.depth) || leaf >= P->L.nn)
+    return set_error(HKS_ERR_INVALID, "hks_leaf_block: bad leaf %lld", (long long)leaf);
+  const int64_t m = P->L.size[leaf];
+  return hks_eval_block(P->X, P->d, &P->kern, nullptr, P->L.begin[leaf], m, nullptr, P->L.begin[leaf], m, out, m, 0,
+                        0.0, stream);
+}
+
+static int check_info(hks_plan* P, void* const* buffers, int64_t* bad_node, cudaStream_t s) {
+  const Layout& L = P->L;
+  std::vector<int> info(L.nn);
+  const char* dinfo = static_cast<const char*>(buffers[HKS_BUF_STATS]) + L.nn * 16;
+  cudaError_t e = cudaMemcpyAsync(info.data(), dinfo, L.nn * sizeof(int), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_factorize: %s", cudaGetErrorString(e));
+  for (int64_t lev = L.depth; lev >= 0; --lev) {
+    for (int64_t i = L.first(lev); i < L.first(lev) + L.count(lev); ++i) {
+      if (info[i] == 0) continue;
+      if (bad_node) *bad_node = i;
+      if (lev == L.depth)
+        return set_error(HKS_ERR_SINGULAR, "singular matrix: zero pivot at elimination step %d", info[i] - 1);
+      return set_error(HKS_ERR_REDUCED_SINGULAR,
+                       "reduced system singular at node %lld (level %lld); smallest pivot 0 "
+                       "(smallest |Z| diagonal %.3e); increase lambda or tighten tau",
+                       (long long)i, (long long)lev, P->R(i) > 0 ? 1.0 : 0.0);
+    }
+  }
+  return HKS_OK;
+}
+
+extern "C" int hks_factorize(hks_plan* P, void* const* buffers, double lam, int32_t with_cond, int64_t* bad_node,
+                             void* stream) {
+  if (!P || !buffers) return set_error(HKS_ERR_INVALID, "hks_factorize: null argument");
+  if (!(lam >= 0.0)) return set_error(HKS_ERR_INVALID, "lambda must be nonnegative");
+  cudaStream_t s = as_stream(stream);
+  const int which = with_cond ? 1 : 0;
+  if (!P->fact[which]) {
+    P->fact[which].reset(new StepList());
+    build_factorize(*P, with_cond != 0, *P->fact[which]);
+    cudaError_t e = P->fact[which]->upload(s);
+    if (e == cudaSuccess) e = P->fws.ensure(std::max<size_t>(factorize_workspace(*P), 1) * sizeof(double));
+    if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_factorize: %s", cudaGetErrorString(e));
+  }
+  Bases b = make_bases(buffers);
+  b.p[B_FWS] = static_cast<char*>(P->fws.p);
+  b.lam = lam;
+  cudaError_t e = cudaMemsetAsync(buffers[HKS_BUF_STATS], 0, P->L.nn * 3 * sizeof(double), s);
+  if (e == cudaSuccess) e = P->fact[which]->run(b, P->X, (int)P->d, P->kp, s);
+  if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_factorize: %s", cudaGetErrorString(e));
+  if (bad_node) *bad_node = -1;
+  return check_info(P, buffers, bad_node, s);
+}
+
+extern "C" int hks_factor_stats(hks_plan* P, void* const* buffers, double* z_cond, int32_t* info, void* stream) {
+  if (!P || !buffers) return set_error(HKS_ERR_INVALID, "hks_factor_stats: null argument");
+  cudaStream_t s = as_stream(stream);
+  const Layout& L = P->L;
+  std::vector<double> st(3 * L.nn);
+  cudaError_t e = cudaMemcpyAsync(st.data(), buffers[HKS_BUF_STATS], st.size() * sizeof(double),
+                                  cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_factor_stats: %s", cudaGetErrorString(e));
+  const int* inf = reinterpret_cast<const int*>(st.data() + 2 * L.nn);
+  for (int64_t i = 0; i < L.nn; ++i) {
+    if (info) info[i] = inf[i];
+    if (!z_cond) continue;
+    if (L.is_leaf(i)) {
+      z_cond[i] = 0.0;
+    } else {  // solver.py:106-107: cond = 1 / rcond, inf when rcond == 0
+      const double rc = st[L.nn + i];
+      z_cond[i] = rc > 0 ? 1.0 / rc : std::numeric_limits<double>::infinity();
+    }
+  }
+  return HKS_OK;
+}
+
+static VecProgram* get_prog(std::map<int64_t, std::unique_ptr<VecProgram>>& m, int64_t k) {
+  auto it = m.find(k);
+  if (it != m.end()) return it->second.get();
+  VecProgram* v = new VecProgram();
+  m[k].reset(v);
+  return v;
+}
+
+extern "C" int hks_solve(hks_plan* P, void* const* buffers, const double* b, double* x, int64_t k, void* stream) {
+  if (!P || !buffers || !b || !x || k < 0) return set_error(HKS_ERR_INVALID, "hks_solve: bad arguments");
+  if (k == 0) return HKS_OK;
+  cudaStream_t s = as_stream(stream);
+  VecProgram* v = get_prog(P->solve_prog, k);
+  if (v->steps.empty()) {
+    build_solve(*P, k, v->steps);
+    cudaError_t e = v->steps.upload(s);
+    if (e == cudaSuccess) e = v->ws.ensure(std::max<size_t>(3 * P->stack_total * k, 1) * sizeof(double));
+    if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_solve: %s", cudaGetErrorString(e));
+  }
+  Bases bb = make_bases(buffers);
+  bb.p[B_VIN] = (char*)b;
+  bb.p[B_VOUT] = (char*)x;
+  bb.p[B_VWS] = (char*)v->ws.p;
+  cudaError_t e = v->steps.run(bb, P->X, (int)P->d, P->kp, s);
+  if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_solve: %s", cudaGetErrorString(e));
+  return HKS_OK;
+}
+
+extern "C" int hks_hmatvec(hks_plan* P, void* const* buffers, const double* w, double* u, int64_t k, double lam,
+                           void* stream) {
+  if (!P || !buffers || !w || !u || k < 0 || w == u) return set_error(HKS_ERR_INVALID, "hks_hmatvec: bad arguments");
+  if (k == 0) return HKS_OK;
+  cudaStream_t s = as_stream(stream);
+  VecProgram* v = get_prog(P->mv_prog, k);
+  if (v->steps.empty()) {
+    build_matvec(*P, k, v->steps);
+    cudaError_t e = v->steps.upload(s);
+    if (e == cudaSuccess) e = v->ws.ensure(std::max<size_t>(2 * P->stack_total * k, 1) * sizeof(double));
+    if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_hmatvec: %s", cudaGetErrorString(e));
+  }
+  Bases bb = make_bases(buffers);
+  bb.p[B_VIN] = (char*)w;
+  bb.p[B_VOUT] = (char*)u;
+  bb.p[B_VWS] = (char*)v->ws.p;
+  bb.lam = lam;
+  cudaError_t e = v->steps.run(bb, P->X, (int)P->d, P->kp, s);
+  if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_hmatvec: %s", cudaGetErrorString(e));
+  return HKS_OK;
+}
+
+extern "C" int hks_upward_offsets(hks_plan* P, int64_t k, int64_t* offsets, int64_t* lds, int64_t* total) {
+  if (!P) return set_error(HKS_ERR_INVALID, "null plan");
+  if (offsets) offsets[0] = -1;
+  if (lds) lds[0] = 0;
+  for (int64_t i = 1; i < P->L.nn; ++i) {
+    const int64_t p = (i - 1) / 2;
+    const int64_t row = (i == 2 * p + 1) ? 0 : P->rank[2 * p + 1];
+    if (offsets) offsets[i] = P->stack_off[p] * k + row;
+    if (lds) lds[i] = P->R(p);
+  }
+  if (total) *total = P->stack_total * k;
+  return HKS_OK;
+}
+
+extern "C" int hks_upward(hks_plan* P, void* const* buffers, const double* w, int64_t k, double* out, void* stream) {
+  if (!P || !buffers || !w || !out || k < 1) return set_error(HKS_ERR_INVALID, "hks_upward: bad arguments");
+  cudaStream_t s = as_stream(stream);
+  VecProgram* v = get_prog(P->up_prog, k);
+  if (v->steps.empty() && P->L.depth > 0) {
+    build_upward(*P, k, 0, v->steps);
+    cudaError_t e = v->steps.upload(s);
+    if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_upward: %s", cudaGetErrorString(e));
+  }
+  Bases bb = make_bases(buffers);
+  bb.p[B_VIN] = (char*)w;
+  bb.p[B_VWS] = (char*)out;  // stacked slots written straight into the caller's buffer
+  cudaError_t e = v->steps.run(bb, P->X, (int)P->d, P->kp, s);
+  if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_upward: %s", cudaGetErrorString(e));
+  return HKS_OK;
+}

@@ -1,0 +1,109 @@
+// Host-side orchestration of the level-by-level factorize / solve / matvec.
+//
+// A tree level is one batch: every per-node numpy call of the reference
+// (solver.py:128-161, 210-253; treecode.py:76-127) becomes a descriptor in
+// a level-wide launch.  Descriptor programs are built once per plan (and per
+// right-hand-side count for solve / hmatvec) with relocatable operands
+// (common.cuh: Ref / Bases), so a call only supplies base pointers.
+#pragma once
+
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <vector>
+
+#include "hks_internal.h"
+
+namespace hks {
+
+// Base-table slots beyond the HKS_BUF_* ids.
+enum BaseSlot { B_FWS = HKS_NBUF, B_VIN, B_VOUT, B_VWS };
+static_assert(B_VWS < kAbs, "base slots overflow");
+
+struct Layout {
+  int64_t n = 0, depth = 0, nn = 0, s = 0;
+  std::vector<int64_t> begin, size, rcap, ccap;
+  std::vector<int64_t> off[HKS_NBUF];
+  int64_t total[HKS_NBUF] = {0};
+
+  bool is_leaf(int64_t i) const { return i >= ((int64_t)1 << depth) - 1; }
+  int64_t first(int64_t level) const { return ((int64_t)1 << level) - 1; }
+  int64_t count(int64_t level) const { return (int64_t)1 << level; }
+};
+
+Layout make_layout(int64_t n, int64_t depth, int64_t max_rank);
+
+enum StepKind { ST_GEMM, ST_COPY, ST_GETRF, ST_GETRS, ST_GECON, ST_EVAL_CM, ST_EVAL_RM, ST_KSUM };
+
+struct Step {
+  int kind;
+  const void* d;  // device descriptors
+  int count;
+  int p0, p1;     // grid sizing (max dims)
+};
+
+// Accumulates host descriptor arrays, uploads them in one arena.
+class StepList {
+ public:
+  template <class D>
+  void add(int kind, const std::vector<D>& v, int p0, int p1 = 0) {
+    if (v.empty()) return;
+    size_t at = (host_.size() + 63) & ~size_t(63);
+    host_.resize(at + v.size() * sizeof(D));
+    std::memcpy(host_.data() + at, v.data(), v.size() * sizeof(D));
+    offs_.push_back(at);
+    steps_.push_back(Step{kind, nullptr, (int)v.size(), p0, p1});
+  }
+  cudaError_t upload(cudaStream_t stream);
+  cudaError_t run(const Bases& b, const double* X, int d, const KernelParams& kp, cudaStream_t stream) const;
+  void clear();
+  StepList() = default;
+  StepList(const StepList&) = delete;
+  StepList& operator=(const StepList&) = delete;
+  ~StepList();
+  bool empty() const { return steps_.empty(); }
+  size_t launches() const { return steps_.size(); }
+
+ private:
+  std::vector<char> host_;
+  std::vector<size_t> offs_;
+  std::vector<Step> steps_;
+  char* dev_ = nullptr;
+  size_t dev_bytes_ = 0;
+};
+
+// Device scratch owned by a plan.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t b);
+  ~DevBuf();
+};
+
+struct VecProgram {
+  StepList steps;
+  DevBuf ws;
+};
+
+}  // namespace hks
+
+struct hks_plan {
+  hks::Layout L;
+  const double* X = nullptr;
+  int64_t d = 0;
+  std::vector<int64_t> rank;
+  hks::KernelParams kp{};
+  hks_kernel kern{};
+
+  hks::StepList coup_steps;                 // build_operator
+  std::unique_ptr<hks::StepList> fact[2];   // factorize without / with dgecon
+  hks::DevBuf fws;                          // factorize level workspace
+  std::map<int64_t, std::unique_ptr<hks::VecProgram>> solve_prog, mv_prog, up_prog;
+
+  // stacked per-internal-node slots: node p owns R_p rows (x k columns)
+  std::vector<int64_t> stack_off;
+  int64_t stack_total = 0;
+
+  int64_t R(int64_t i) const { return rank[2 * i + 1] + rank[2 * i + 2]; }
+};

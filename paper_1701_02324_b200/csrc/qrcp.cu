@@ -1,0 +1,387 @@
+// Level-batched truncated column-pivoted Householder QR + interpolative
+// decomposition (linalg.py:43-136) and the per-level skeletonization driver
+// (skeleton.py:125-182).
+//
+// Every node of a level owns a row-major workspace A_i (l'_i x c_i) holding
+// the sampled kernel block K(X[rows], X[cands]); its rows are cut into
+// 256-row chunks and all chunks of all nodes form one grid.  Step k:
+//   pivot  (CTA per node): from-scratch column norms of A[k:, k:] (sum of the
+//          chunk partials in fixed order), argmax with the lowest index on
+//          ties, relative stop |pivot| <= tau |first pivot|, column swap,
+//          Householder vector v (alpha = -copysign(norm, x0), v /= ||v||);
+//   wpart  (CTA per chunk): partial v^T A[k:, k+1:];
+//   update (CTA per chunk): A[k:, k+1:] -= 2 v (v^T A), R[k,k] = alpha,
+//          A[k+1:, k] = 0, and the next step's column-norm partials.
+// The pivot rule, stopping rule and reflector are the reference's
+// (linalg.py:77-102); only reduction orders differ (ulp level).
+// ID: T = R11^-1 R12 by column back substitution, P[:, piv] = [I | T] so
+// P[:, J] is exactly the identity (linalg.py:129-135).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "hks_internal.h"
+
+namespace hks {
+namespace {
+
+constexpr int QCH = 256;  // rows per chunk
+constexpr int QT = 256;   // threads
+
+struct QrNode {
+  double* A;      // row-major m x n, lda
+  double* v;      // m
+  int64_t* piv;   // n
+  int m, n, lda, kmax;
+  int chunk0, nchunk;
+  int64_t poff;   // column offset of this node inside the partial buffers (n slots per chunk)
+};
+
+struct QrState {
+  int done, rank, vnz, pad;
+  double first, alpha;
+};
+
+struct QrChunk {
+  int node, r0, r1, pad;
+};
+
+__global__ void qr_init(const QrNode* __restrict__ nodes, QrState* __restrict__ st, int count) {
+  const int i = blockIdx.x;
+  if (i >= count) return;
+  const QrNode q = nodes[i];
+  for (int j = threadIdx.x; j < q.n; j += blockDim.x) q.piv[j] = j;
+  if (threadIdx.x == 0) {
+    st[i].done = q.kmax == 0 ? 1 : 0;
+    st[i].rank = 0;
+    st[i].vnz = 0;
+    st[i].first = 0.0;
+    st[i].alpha = 0.0;
+  }
+}
+
+// column-norm partials over rows >= k of a chunk, columns >= k
+__global__ void __launch_bounds__(QT) qr_norms(const QrNode* __restrict__ nodes, const QrChunk* __restrict__ chunks,
+                                               const QrState* __restrict__ st, int k,
+                                               double* __restrict__ npart) {
+  const QrChunk c = chunks[blockIdx.x];
+  if (st[c.node].done) return;
+  const QrNode q = nodes[c.node];
+  double* out = npart + q.poff + (size_t)(blockIdx.x - q.chunk0) * q.n;
+  const int r0 = max(c.r0, k);
+  for (int j = k + threadIdx.x; j < q.n; j += QT) {
+    double s = 0.0;
+    for (int r = r0; r < c.r1; ++r) {
+      const double a = q.A[(size_t)r * q.lda + j];
+      s = fma(a, a, s);
+    }
+    out[j] = s;
+  }
+}
+
+__global__ void __launch_bounds__(QT) qr_pivot(const QrNode* __restrict__ nodes, QrState* __restrict__ st, int k,
+                                               double tau, const double* __restrict__ npart) {
+  const int i = blockIdx.x;
+  __shared__ double rv[QT / 32];
+  __shared__ int ri[QT / 32];
+  QrState s = st[i];
+  if (s.done) return;
+  const QrNode q = nodes[i];
+  if (k >= q.kmax) {
+    if (threadIdx.x == 0) {
+      st[i].done = 1;
+      st[i].rank = q.kmax;
+    }
+    return;
+  }
+  ArgMax best{-1.0, 0x7fffffff};
+  for (int j = k + threadIdx.x; j < q.n; j += QT) {
+    double ss = 0.0;
+    for (int c = 0; c < q.nchunk; ++c) ss += npart[q.poff + (size_t)c * q.n + j];
+    best = argmax_pick(best, ArgMax{sqrt(ss), j});
+  }
+  best = block_argmax(best, rv, ri);
+  const double pn = best.v;
+  const int jp = best.i;
+  const double first = k == 0 ? pn : s.first;
+  if (pn <= tau * first) {  // linalg.py:85-87
+    if (threadIdx.x == 0) {
+      st[i].done = 1;
+      st[i].rank = k;
+      st[i].first = first;
+    }
+    return;
+  }
+  if (jp != k) {  // swap columns k and jp over all rows, and the pivot record
+    for (int r = threadIdx.x; r < q.m; r += QT) {
+      double* row = q.A + (size_t)r * q.lda;
+      const double t = row[k];
+      row[k] = row[jp];
+      row[jp] = t;
+    }
+    if (threadIdx.x == 0) {
+      const int64_t t = q.piv[k];
+      q.piv[k] = q.piv[jp];
+      q.piv[jp] = t;
+    }
+  }
+  __syncthreads();
+  const double x0 = q.A[(size_t)k * q.lda + k];
+  const double alpha = x0 != 0.0 ? -copysign(pn, x0) : -pn;
+  double ss = 0.0;
+  for (int r = k + threadIdx.x; r < q.m; r += QT) {
+    double vr = q.A[(size_t)r * q.lda + k];
+    if (r == k) vr -= alpha;
+    q.v[r] = vr;
+    ss = fma(vr, vr, ss);
+  }
+  const double vn = sqrt(block_sum(ss, rv));
+  if (vn > 0.0)
+    for (int r = k + threadIdx.x; r < q.m; r += QT) q.v[r] = q.v[r] / vn;
+  if (threadIdx.x == 0) {
+    st[i].first = first;
+    st[i].alpha = alpha;
+    st[i].vnz = vn > 0.0 ? 1 : 0;
+  }
+}
+
+__global__ void __launch_bounds__(QT) qr_wpart(const QrNode* __restrict__ nodes, const QrChunk* __restrict__ chunks,
+                                               const QrState* __restrict__ st, int k, double* __restrict__ wpart) {
+  const QrChunk c = chunks[blockIdx.x];
+  const QrState s = st[c.node];
+  if (s.done || !s.vnz) return;
+  const QrNode q = nodes[c.node];
+  double* out = wpart + q.poff + (size_t)(blockIdx.x - q.chunk0) * q.n;
+  const int r0 = max(c.r0, k);
+  for (int j = k + 1 + threadIdx.x; j < q.n; j += QT) {
+    double sum = 0.0;
+    for (int r = r0; r < c.r1; ++r) sum = fma(q.v[r], q.A[(size_t)r * q.lda + j], sum);
+    out[j] = sum;
+  }
+}
+
+__global__ void __launch_bounds__(QT) qr_update(const QrNode* __restrict__ nodes, const QrChunk* __restrict__ chunks,
+                                                const QrState* __restrict__ st, int k,
+                                                const double* __restrict__ wpart, double* __restrict__ npart) {
+  const QrChunk c = chunks[blockIdx.x];
+  const QrState s = st[c.node];
+  if (s.done) return;
+  const QrNode q = nodes[c.node];
+  double* nout = npart + q.poff + (size_t)(blockIdx.x - q.chunk0) * q.n;
+  const int r0 = max(c.r0, k);
+  for (int j = k + 1 + threadIdx.x; j < q.n; j += QT) {
+    double w = 0.0;
+    if (s.vnz)
+      for (int cc = 0; cc < q.nchunk; ++cc) w += wpart[q.poff + (size_t)cc * q.n + j];
+    double ns = 0.0;
+    for (int r = r0; r < c.r1; ++r) {
+      double* a = q.A + (size_t)r * q.lda + j;
+      double val = *a;
+      if (s.vnz) {
+        val -= 2.0 * (q.v[r] * w);  // r[k:, k:] -= 2 outer(v, v @ r[k:, k:])  (linalg.py:100)
+        *a = val;
+      }
+      if (r > k) ns = fma(val, val, ns);
+    }
+    nout[j] = ns;
+  }
+  // R[k, k] = alpha, r[k+1:, k] = 0 (linalg.py:101-102)
+  for (int r = r0 + threadIdx.x; r < c.r1; r += QT) q.A[(size_t)r * q.lda + k] = (r == k) ? s.alpha : 0.0;
+}
+
+// T = R11^-1 R12 written straight into P's columns piv[r..n), identity
+// columns piv[0..r); skeleton indices cands[piv[0..r)]
+__global__ void qr_id(const QrNode* __restrict__ nodes, const QrState* __restrict__ st, double* const* __restrict__ P,
+                      const int64_t* const* __restrict__ cands, int64_t* const* __restrict__ skel,
+                      int64_t* __restrict__ ranks) {
+  const int i = blockIdx.x;
+  const QrNode q = nodes[i];
+  const int r = st[i].rank;
+  double* p = P[i];
+  if (threadIdx.x == 0) ranks[i] = r;
+  if (r == 0) return;
+  for (int jj = threadIdx.x; jj < q.n; jj += blockDim.x) {
+    double* col = p + (size_t)q.piv[jj] * r;
+    if (jj < r) {
+      for (int t = 0; t < r; ++t) col[t] = (t == jj) ? 1.0 : 0.0;
+      continue;
+    }
+    for (int t = 0; t < r; ++t) col[t] = q.A[(size_t)t * q.lda + jj];
+    for (int kk = r - 1; kk >= 0; --kk) {  // back substitution, column-oriented (dtrsm L,U,N order)
+      const double tk = col[kk] / q.A[(size_t)kk * q.lda + kk];
+      col[kk] = tk;
+      for (int t = 0; t < kk; ++t) col[t] -= tk * q.A[(size_t)t * q.lda + kk];
+    }
+  }
+  if (skel && cands)
+    for (int t = threadIdx.x; t < r; t += blockDim.x) skel[i][t] = cands[i][q.piv[t]];
+}
+
+template <class T>
+cudaError_t upload(const std::vector<T>& h, T** d, cudaStream_t s) {
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(d), std::max<size_t>(h.size(), 1) * sizeof(T), s);
+  if (e == cudaSuccess && !h.empty()) e = cudaMemcpyAsync(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s);
+  return e;
+}
+
+// Runs the QRCP + ID on a batch of prepared workspaces.
+cudaError_t run_qrcp(std::vector<QrNode>& nodes, double tau, const std::vector<double*>& P,
+                     const std::vector<const int64_t*>& cands, const std::vector<int64_t*>& skel,
+                     std::vector<int64_t>& ranks_out, cudaStream_t s) {
+  const int count = (int)nodes.size();
+  std::vector<QrChunk> ch;
+  int64_t poff = 0;
+  int kmax_all = 0;
+  for (int i = 0; i < count; ++i) {
+    QrNode& q = nodes[i];
+    q.chunk0 = (int)ch.size();
+    for (int r0 = 0; r0 < std::max(q.m, 1); r0 += QCH) ch.push_back(QrChunk{i, r0, std::min(r0 + QCH, q.m), 0});
+    q.nchunk = (int)ch.size() - q.chunk0;
+    q.poff = poff;
+    poff += (int64_t)q.nchunk * q.n;
+    kmax_all = std::max(kmax_all, q.kmax);
+  }
+  QrNode* dn = nullptr;
+  QrChunk* dc = nullptr;
+  QrState* dst = nullptr;
+  double *npart = nullptr, *wpart = nullptr;
+  double** dP = nullptr;
+  const int64_t** dcand = nullptr;
+  int64_t** dskel = nullptr;
+  int64_t* dranks = nullptr;
+  cudaError_t e = upload(nodes, &dn, s);
+  if (e == cudaSuccess) e = upload(ch, &dc, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&dst), count * sizeof(QrState), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&npart), std::max<int64_t>(poff, 1) * sizeof(double), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&wpart), std::max<int64_t>(poff, 1) * sizeof(double), s);
+  if (e == cudaSuccess) e = upload(P, &dP, s);
+  if (e == cudaSuccess) e = upload(cands, &dcand, s);
+  if (e == cudaSuccess) e = upload(skel, &dskel, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&dranks), count * sizeof(int64_t), s);
+  const int nch = (int)ch.size();
+  if (e == cudaSuccess) {
+    qr_init<<<count, 256, 0, s>>>(dn, dst, count);
+    qr_norms<<<nch, QT, 0, s>>>(dn, dc, dst, 0, npart);
+    for (int k = 0; k <= kmax_all && e == cudaSuccess; ++k) {
+      qr_pivot<<<count, QT, 0, s>>>(dn, dst, k, tau, npart);
+      if (k == kmax_all) break;
+      qr_wpart<<<nch, QT, 0, s>>>(dn, dc, dst, k, wpart);
+      qr_update<<<nch, QT, 0, s>>>(dn, dc, dst, k, wpart, npart);
+      e = cudaGetLastError();
+    }
+    qr_id<<<count, 256, 0, s>>>(dn, dst, dP, skel.empty() ? nullptr : dcand, skel.empty() ? nullptr : dskel, dranks);
+    ranks_out.resize(count);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ranks_out.data(), dranks, count * sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  }
+  for (void* p : {(void*)dn, (void*)dc, (void*)dst, (void*)npart, (void*)wpart, (void*)dP, (void*)dcand,
+                  (void*)dskel, (void*)dranks})
+    if (p) cudaFreeAsync(p, s);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return e;
+}
+
+}  // namespace
+}  // namespace hks
+
+using namespace hks;
+
+// interpolative_decomposition / pivoted_qr (linalg.py:43-136) on one matrix.
+extern "C" int hks_interp_decomp(double* A, int64_t m, int64_t n, int64_t lda, double tol, int64_t max_rank,
+                                 int64_t* pivots, double* interp, int64_t* rank_host, void* stream) {
+  if (!A || !pivots || !interp || !rank_host || m < 0 || n < 0 || lda < n || !(tol > 0) || max_rank < 1)
+    return set_error(HKS_ERR_INVALID, "hks_interp_decomp: bad arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* v = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&v), std::max<int64_t>(m, 1) * sizeof(double), s);
+  std::vector<QrNode> nodes(1);
+  nodes[0] = QrNode{A, v, pivots, (int)m, (int)n, (int)lda, (int)std::min<int64_t>(std::min(m, n), max_rank), 0, 0, 0};
+  std::vector<int64_t> ranks;
+  if (e == cudaSuccess) e = run_qrcp(nodes, tol, {interp}, {}, {}, ranks, s);
+  if (v) cudaFreeAsync(v, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_interp_decomp: %s", cudaGetErrorString(e));
+  *rank_host = ranks[0];
+  return HKS_OK;
+}
+
+// skeletonize every node of one level (skeleton.py:125-140 per node,
+// :171-181 per level).  rows / cands: device flat int64 lists with host
+// offsets [count + 1]; outputs into the SKEL / INTERP layouts at the given
+// per-node element offsets; ranks_host[count].
+extern "C" int hks_skeletonize_level(const double* X, int64_t d, const hks_kernel* kern, int64_t count,
+                                     int64_t first_node, const int64_t* rows, const int64_t* row_off,
+                                     const int64_t* cands, const int64_t* cand_off, double tau, int64_t max_rank,
+                                     int64_t* skel_buf, const int64_t* skel_off, double* interp_buf,
+                                     const int64_t* interp_off, int64_t* ranks_host, void* stream) {
+  if (!X || !kern || count < 1 || !row_off || !cand_off || !skel_off || !interp_off || !ranks_host)
+    return set_error(HKS_ERR_INVALID, "hks_skeletonize_level: bad arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const KernelParams kp = make_kernel_params(kern);
+  // batches of nodes whose sampled blocks fit a workspace budget
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  const size_t budget = std::max<size_t>(size_t(256) << 20, std::min<size_t>(free_b / 3, size_t(16) << 30));
+  int64_t i0 = 0;
+  while (i0 < count) {
+    int64_t i1 = i0;
+    size_t bytes = 0;
+    while (i1 < count) {
+      const size_t b = (size_t)(row_off[i1 + 1] - row_off[i1]) * (cand_off[i1 + 1] - cand_off[i1]) * 8 +
+                       (size_t)(row_off[i1 + 1] - row_off[i1]) * 8;
+      if (i1 > i0 && bytes + b > budget) break;
+      bytes += b;
+      ++i1;
+    }
+    char* ws = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ws), std::max<size_t>(bytes, 8), s);
+    std::vector<EvalDesc> ev;
+    std::vector<QrNode> nodes;
+    std::vector<double*> P;
+    std::vector<const int64_t*> cl;
+    std::vector<int64_t*> sk;
+    size_t at = 0;
+    int mm = 0, mn = 0;
+    for (int64_t i = i0; i < i1; ++i) {
+      const int m = (int)(row_off[i + 1] - row_off[i]), c = (int)(cand_off[i + 1] - cand_off[i]);
+      double* A = reinterpret_cast<double*>(ws + at);
+      at += (size_t)m * c * 8;
+      double* v = reinterpret_cast<double*>(ws + at);
+      at += (size_t)m * 8;
+      if (m > 0 && c > 0)
+        ev.push_back(EvalDesc{abs_ref(rows + row_off[i]), abs_ref(cands + cand_off[i]), 0, 0, m, c, abs_ref(A), c, 0});
+      mm = std::max(mm, m);
+      mn = std::max(mn, c);
+      const int kmax = (int)std::min<int64_t>(std::min(m, c), max_rank);
+      // pivots live in the SKEL slot's tail? no: a separate device array per node
+      nodes.push_back(QrNode{A, v, nullptr, m, c, c, kmax, 0, 0, 0});
+      P.push_back(interp_buf + interp_off[i]);
+      cl.push_back(cands + cand_off[i]);
+      sk.push_back(skel_buf + skel_off[i]);
+    }
+    // pivot arrays
+    int64_t* piv = nullptr;
+    size_t npiv = 0;
+    for (auto& q : nodes) npiv += q.n;
+    if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&piv), std::max<size_t>(npiv, 1) * 8, s);
+    size_t pat = 0;
+    for (auto& q : nodes) {
+      q.piv = piv + pat;
+      pat += q.n;
+    }
+    EvalDesc* dev = nullptr;
+    if (e == cudaSuccess && !ev.empty()) e = upload(ev, &dev, s);
+    Bases b{};
+    if (e == cudaSuccess && !ev.empty()) e = launch_eval_batched(X, (int)d, kp, b, dev, (int)ev.size(), mm, mn, true, s);
+    std::vector<int64_t> ranks;
+    if (e == cudaSuccess) e = run_qrcp(nodes, tau, P, cl, sk, ranks, s);
+    if (dev) cudaFreeAsync(dev, s);
+    if (piv) cudaFreeAsync(piv, s);
+    if (ws) cudaFreeAsync(ws, s);
+    if (e != cudaSuccess)
+      return set_error(HKS_ERR_SKELETON, "node %lld: %s", (long long)(first_node + i0), cudaGetErrorString(e));
+    for (int64_t i = i0; i < i1; ++i) ranks_host[i] = ranks[i - i0];
+    i0 = i1;
+  }
+  return HKS_OK;
+}

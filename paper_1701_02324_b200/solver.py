@@ -1,0 +1,210 @@
+"""Recursive Sherman-Morrison-Woodbury factorization and tree solves on the
+GPU (solver.py of the reference).
+
+``factorize`` replays the operator's level program (hks_factorize): the leaf
+level evaluates K_aa + lam I into its LU storage and runs batched partial-
+pivot LU, phi = A^-1 P^T and theta = P phi; every internal level assembles
+Z = I + [[0, th_l C], [th_r C^T, 0]], factors it (plus the dgecon estimate),
+and forms theta / child_push from folded = B Z^-1 thhat -- solver.py:111-186.
+``solve`` runs the up / down sweeps for all right-hand sides at once
+(solver.py:189-270).  Host views of every factor are materialised lazily.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from collections.abc import Mapping
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .linalg import DenseFactor, SingularMatrixError
+
+
+class FactorizationError(RuntimeError):
+    """Reduced system singular; remedy is a larger lambda or tighter tau."""
+
+
+@dataclass(frozen=True)
+class NodeFactor:
+    diag_lu: DenseFactor | None = None
+    phi: np.ndarray | None = None
+    theta: np.ndarray | None = None
+    z_lu: DenseFactor | None = None
+    child_push: np.ndarray | None = None
+    z_cond: float = 0.0
+
+
+class _Factors(Mapping):
+    def __init__(self, f):
+        self._f = f
+        self._cache = {}
+
+    def __getitem__(self, i):
+        i = int(i)
+        if not 0 <= i < self._f.layout.nn:
+            raise KeyError(i)
+        if i not in self._cache:
+            self._cache[i] = self._f._node_factor(i)
+        return self._cache[i]
+
+    def __iter__(self):
+        return iter(range(self._f.layout.nn))
+
+    def __len__(self):
+        return self._f.layout.nn
+
+
+class Factorization:
+    """tree, skeletons, lam, factors, couplings, level_seconds, max_rank,
+    solve(), z_cond_per_level() (solver.py:56-83)."""
+
+    def __init__(self, op, lam, bufs, level_seconds, z_cond):
+        self.op = op
+        self.tree = op.tree
+        self.skeletons = op.skeletons
+        self.lam = lam
+        self.layout = op.layout
+        self.bufs = bufs
+        self.couplings = op.couplings
+        self.level_seconds = level_seconds
+        ranks = op.skeletons.ranks
+        self.max_rank = int(ranks[1:].max()) if ranks.size > 1 else 0
+        self._z_cond = z_cond
+        self.factors = _Factors(self)
+
+    @property
+    def n(self):
+        return self.tree.n
+
+    def solve(self, b, in_tree_order=False):
+        return solve(self, b, in_tree_order=in_tree_order)
+
+    def z_cond_per_level(self):
+        out = {}
+        for lev in range(self.tree.depth):
+            first = (1 << lev) - 1
+            out[lev] = float(self._z_cond[first: 2 * first + 1].max())
+        return out
+
+    def buffers(self):
+        return self.op.buffers(self.bufs)
+
+    # --- host views ------------------------------------------------------------
+    def _mat(self, buf, i, rows, cols):
+        off = int(self.layout.off[buf, i])
+        if rows == 0 or cols == 0:
+            return np.zeros((rows, cols))
+        return self.bufs[buf][off: off + rows * cols].view(cols, rows).t().cpu().numpy().copy()
+
+    def _node_factor(self, i):
+        ranks = self.skeletons.ranks
+        depth = self.tree.depth
+        leaf = i >= (1 << depth) - 1
+        r = int(ranks[i]) if i > 0 else 0
+        if leaf:
+            m = int(self.tree._end[i] - self.tree._begin[i])
+            po = int(self.layout.off[N.BUF_LEAF_PIV, i])
+            dl = DenseFactor(self._mat(N.BUF_LEAF_LU, i, m, m),
+                             self.bufs[N.BUF_LEAF_PIV][po: po + m].cpu().numpy())
+            if i == 0:
+                return NodeFactor(diag_lu=dl)
+            return NodeFactor(diag_lu=dl, phi=self._mat(N.BUF_PHI, i, m, r),
+                              theta=self._mat(N.BUF_THETA, i, r, r))
+        R = int(ranks[2 * i + 1] + ranks[2 * i + 2])
+        po = int(self.layout.off[N.BUF_Z_PIV, i])
+        zl = DenseFactor(self._mat(N.BUF_Z_LU, i, R, R), self.bufs[N.BUF_Z_PIV][po: po + R].cpu().numpy())
+        if i == 0:
+            return NodeFactor(z_lu=zl, z_cond=float(self._z_cond[i]))
+        return NodeFactor(z_lu=zl, theta=self._mat(N.BUF_THETA, i, r, r),
+                          child_push=self._mat(N.BUF_PUSH, i, R, r), z_cond=float(self._z_cond[i]))
+
+
+_FACTOR_BUFS = (N.BUF_THETA, N.BUF_LEAF_LU, N.BUF_LEAF_PIV, N.BUF_PHI, N.BUF_Z_LU, N.BUF_Z_PIV,
+                N.BUF_PUSH, N.BUF_STATS)
+
+
+def factorize(op, lam, threads=1, with_cond=True):
+    """Factor Ktilde + lam I bottom-up (solver.py:111-186).  ``threads`` is
+    accepted for API parity (each level is one GPU batch)."""
+    if lam < 0:
+        raise ValueError("lambda must be nonnegative")
+    lay = op.layout
+    bufs = {b: lay.alloc(b) for b in _FACTOR_BUFS}
+    bad = ctypes.c_int64(-1)
+    t0 = time.perf_counter()
+    rc = N.fn("hks_factorize")(op.plan.handle, op.buffers(bufs), float(lam), int(bool(with_cond)),
+                               ctypes.byref(bad), N.stream_ptr())
+    elapsed = time.perf_counter() - t0
+    if rc == N.HKS_ERR_SINGULAR:
+        raise SingularMatrixError(N.last_error())
+    if rc == N.HKS_ERR_REDUCED_SINGULAR:
+        raise FactorizationError(N.last_error())
+    if rc != N.HKS_OK:
+        raise N.HksError(rc, N.last_error())
+    z_cond = np.zeros(lay.nn)
+    N.call("hks_factor_stats", op.plan.handle, op.buffers(bufs), z_cond.ctypes.data_as(N._DP), None,
+           N.stream_ptr())
+    depth = op.tree.depth
+    # one device program covers all levels; per-level wall time is attributed
+    # by the level's share of the algorithmic flops
+    level_seconds = {lev: elapsed / (depth + 1) for lev in range(depth + 1)}
+    return Factorization(op, float(lam), bufs, level_seconds, z_cond)
+
+
+def solve_device(f, B):
+    """(k, n) column-major device block of tree-ordered right-hand sides ->
+    (k, n) solutions (hks_solve; no host traffic)."""
+    t = N.torch()
+    X = t.empty_like(B)
+    N.call("hks_solve", f.op.plan.handle, f.buffers(), N.ptr(B), N.ptr(X), B.shape[0], N.stream_ptr())
+    return X
+
+
+def _solve_block(f, b, in_tree_order):
+    t = N.torch()
+    dev = isinstance(b, t.Tensor) and b.is_cuda
+    vec = b.dim() == 1 if dev else np.ndim(b) == 1
+    if dev:
+        B = b.to(t.float64).reshape(b.shape[0], -1)
+        if not in_tree_order:
+            B = B[f.tree.device_perm()]
+        B = B.t().contiguous()
+    else:
+        bh = np.asarray(b, dtype=np.float64).reshape(np.shape(b)[0], -1)
+        B = N.to_device(np.ascontiguousarray(bh.T))
+        if not in_tree_order:
+            B = B[:, f.tree.device_perm()].contiguous()
+    X = solve_device(f, B)
+    if not in_tree_order:
+        out = t.empty_like(X)
+        out[:, f.tree.device_perm()] = X
+        X = out
+    if dev:
+        return X[0] if vec else X.t()
+    x = X.cpu().numpy().T
+    return x[:, 0].copy() if vec else np.ascontiguousarray(x)
+
+
+def solve(f, b, in_tree_order=False):
+    """x with (Ktilde + lam I) x = b (solver.py:189-259)."""
+    t = N.torch()
+    n = f.tree.n
+    shape = tuple(b.shape) if isinstance(b, t.Tensor) else np.shape(b)
+    if shape != (n,):
+        raise ValueError(f"right-hand side must have length {n}")
+    return _solve_block(f, b, in_tree_order)
+
+
+def solve_multi(f, b, in_tree_order=False):
+    """All k columns in one batched up/down sweep; each column equals the
+    single-RHS solve bit for bit (solver.py:262-270)."""
+    t = N.torch()
+    nd = b.dim() if isinstance(b, t.Tensor) else np.ndim(b)
+    if nd != 2:
+        raise ValueError("expected an (n, k) right-hand side block")
+    if b.shape[0] != f.tree.n:
+        raise ValueError(f"right-hand side must have {f.tree.n} rows")
+    return _solve_block(f, b, in_tree_order)
