@@ -1,0 +1,357 @@
+#!/usr/bin/env python
+"""Benchmark: factorize + k-RHS solve of (lambda I + Ktilde) on the BASELINE
+workload (default C2: N=262144, d=18, m=512, s=128, kappa=32, 16 RHS).
+
+One *step* = ``factorize(op, lam)`` + ``solve_multi(f, B)`` on a resident
+operator (tree, kNN, skeletons and couplings are built once, untimed, and
+reported under ``setup``).  ``value`` = N / device step time with B resident
+in HBM; ``e2e`` = the same step through the public API from a pinned host B
+to a host x (H2D + D2H inside the timed region).  ``--impl reference`` times
+the CPU oracle (oracle/hks_oracle.py, the reference algorithm restated) on a
+bounded sample of the same workload.  See DESIGN.md for the definitions.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl hks|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+FP64_DMMA_PEAK_TFLOPS = 37.1  # measured, profiles/fp64_peaks_r01.jsonl (mma.sync m8n8k4 f64)
+FP64_DFMA_PEAK_TFLOPS = 34.2  # measured, same file
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["hks", "reference"], default="hks")
+    p.add_argument("--config", default="C2")
+    p.add_argument("--n", type=int, default=None, help="override N (same generator / kernel / ranks)")
+    p.add_argument("--cpu-sample-n", type=int, default=16384)
+    p.add_argument("--cpu-steps", type=int, default=2)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------- CPU arm
+
+def oracle_arm(w, n_sample, steps, threads):
+    """Time the CPU oracle's factorize + k-RHS solve (the reference's
+    algorithm, numpy/LAPACK) on a bounded N=n_sample instance of workload w.
+    BLAS is pinned to one thread and the per-level node loops use `threads`
+    workers, the reference's best configuration."""
+    from threadpoolctl import threadpool_limits
+    from oracle import hks_oracle as O
+    from paper_1701_02324_b200 import workloads as W
+    ws = w.scaled(n_sample)
+    x = W.points(ws, 0)
+    b = W.rhs(ws, 0)
+    kern = {"family": "gaussian", "h": w.h}
+    with threadpool_limits(limits=1, user_api="blas"):
+        t0 = time.perf_counter()
+        inst = O.pipeline(x, kern, w.leaf_size, w.tau, w.max_rank, w.samples, "knn_augmented", 0,
+                          kappa=w.kappa, threads=threads)
+        t_setup = time.perf_counter() - t0
+        tree, sk, coup = inst["tree"], inst["skel"], inst["coup"]
+        bt = b[tree.perm]
+        times, tf, ts = [], [], []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            fac = O.factorize(tree, sk, inst["leaf"], coup, w.lam, threads=threads)
+            t1 = time.perf_counter()
+            for j in range(b.shape[1]):  # solve_multi is a column loop (solver.py:262-270)
+                O.solve(tree, sk, coup, fac, bt[:, j])
+            t2 = time.perf_counter()
+            times.append(t2 - t0)
+            tf.append(t1 - t0)
+            ts.append(t2 - t1)
+    t = statistics.median(times)
+    return {
+        "value": n_sample / t, "t_step": t, "t_factorize": statistics.median(tf),
+        "t_solve": statistics.median(ts), "setup_s": t_setup, "cores": threads,
+        "sample": (f"{w.name} generator/kernel/ranks at N={n_sample} (depth {tree.depth}), factorize + "
+                   f"{b.shape[1]}-RHS solve, {steps} steps, median; setup (tree+kNN+skeletons) untimed"),
+    }
+
+
+# ---------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- GPU arm
+
+def gpu_arm(args, w, rank, world):
+    import torch
+    import paper_1701_02324_b200 as hk
+    from paper_1701_02324_b200 import _native as N
+    from paper_1701_02324_b200 import workloads as W
+    from paper_1701_02324_b200.solver import solve_device
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    seed = rank  # replicas: every rank owns an independent instance (multi-GPU)
+    x = W.points(w, seed)
+    b = W.rhs(w, seed)
+    kern = hk.KernelSpec("gaussian", h=w.h, regularization=w.lam)
+    cfg = hk.SkeletonConfig(tau=w.tau, max_rank=w.max_rank, samples=w.samples,
+                            sample_mode="knn_augmented", seed=seed)
+
+    def timed(fn):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        out = fn()
+        torch.cuda.synchronize()
+        return out, time.perf_counter() - t0
+
+    setup = {}
+    ps = hk.PointSet(x)
+    _, setup["h2d_points"] = timed(ps.device)
+    tree, setup["build_tree"] = timed(lambda: hk.build_tree(ps, w.leaf_size, seed=seed))
+    knn, setup["knn"] = timed(lambda: hk.knn_bruteforce(tree.points, w.kappa))
+    skels, setup["skeletonize"] = timed(lambda: hk.build_skeletons(tree, kern, cfg, knn=knn))
+    op, setup["assemble"] = timed(lambda: hk.build_operator(tree, skels, kern))
+    setup = {k: round(v, 4) for k, v in setup.items()}
+
+    # right-hand sides resident in tree order, column-major (k, n)
+    B = N.to_device(np.ascontiguousarray(b[np.asarray(tree.perm)].T))
+    stream = torch.cuda.current_stream()
+
+    def step():
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(stream)
+        f = hk.factorize(op, w.lam)
+        e1.record(stream)
+        X = solve_device(f, B)
+        e2.record(stream)
+        return f, X, (e0, e1, e2)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
+    N.profile(True)
+    launches0 = N.launch_count()
+    r0 = torch.cuda.Event(enable_timing=True)
+    r1 = torch.cuda.Event(enable_timing=True)
+    r0.record(stream)
+    evs = []
+    for _ in range(args.steps):
+        f, X, ev = step()
+        evs.append(ev)
+    r1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    launches = N.launch_count() - launches0
+    kinds = N.profile(False)
+    clk = clocks.stop()
+    region_ms = r0.elapsed_time(r1)
+    t_fact = [a.elapsed_time(bq) for a, bq, _ in evs]
+    t_solve = [bq.elapsed_time(c) for _, bq, c in evs]
+    if world > 1:
+        tt = torch.tensor([region_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        region_ms = float(tt.item())
+    ms_step = region_ms / args.steps
+
+    # parity spot check of the timed solution: residual against Ktilde
+    xs = X[0]
+    res = hk.treecode.hmatvec_device(op, xs.reshape(1, -1).contiguous(), w.lam)[0] - B[0]
+    relres = float(torch.linalg.vector_norm(res) / torch.linalg.vector_norm(B[0]))
+
+    # e2e through the public API: pinned host B (input order) -> host x
+    Bh = torch.from_numpy(np.ascontiguousarray(b)).pin_memory()
+    e2e_ms = []
+    for i in range(max(2, min(args.steps, 5))):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        f = hk.factorize(op, w.lam)
+        xh = hk.solve_multi(f, Bh, in_tree_order=False)
+        xh = xh.cpu().numpy() if hasattr(xh, "cpu") else xh
+        torch.cuda.synchronize()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_step = statistics.median(e2e_ms)
+
+    # roofline of the dominant kernel kind (algorithmic flops / event time)
+    tensor_kinds = {"gemm", "getrf", "getrs", "gecon"}
+    dom = max(kinds, key=lambda k: kinds[k]["ms"])
+    kd = kinds[dom]
+    if dom in tensor_kinds:
+        achieved = kd["flops"] / (kd["ms"] * 1e-3) / 1e12
+        roof = {"bound": "tensor", "kernel": dom, "achieved": round(achieved, 3), "peak": FP64_DMMA_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": round(achieved / FP64_DMMA_PEAK_TFLOPS, 4),
+                "peak_source": "measured FP64 DMMA peak (profiles/fp64_peaks_r01.jsonl); MEASURED_PEAKS.json "
+                               "has no FP64 entry"}
+    else:
+        from_peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+        peak = from_peaks.get("hbm_gbs", 6544.7)
+        achieved = kd["bytes"] / (kd["ms"] * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    traffic_file = ROOT / "profiles" / "ncu_traffic_r01.json"
+    roof["traffic"] = None
+    if traffic_file.exists():
+        tr = json.loads(traffic_file.read_text())
+        roof["traffic"] = tr.get(dom)
+    roof["launch_share"] = round(kd["ms"] / max(sum(v["ms"] for v in kinds.values()), 1e-9), 4)
+    total_flops = sum(v["flops"] for v in kinds.values()) / args.steps
+    kernels = {k: {"launches": int(v["launches"]), "ms_per_step": round(v["ms"] / args.steps, 4),
+                   "tflops": round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 3) if v["flops"] else None,
+                   "gbs": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1)}
+               for k, v in kinds.items() if v["launches"]}
+    n_total = w.n * world
+    result = {
+        "metric": "factorize+solve points/s",
+        "value": round(n_total / (ms_step * 1e-3), 1),
+        "unit": "points/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic: seeded BASELINE generator (BASELINE.md 4.4), seed = rank",
+        "config": {"workload": w.name, "n": w.n, "d": w.d, "leaf": w.leaf_size, "max_rank": w.max_rank,
+                   "tau": w.tau, "kappa": w.kappa, "samples": w.samples, "sample_mode": "knn_augmented",
+                   "h": w.h, "lambda": w.lam, "nrhs": w.nrhs,
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "no flush: per-step working set (factor storage) exceeds the 126 MB L2"},
+        "factorize_points_per_s": round(w.n / (statistics.mean(t_fact) * 1e-3), 1),
+        "solve_rhs_per_s": round(w.nrhs / (statistics.mean(t_solve) * 1e-3), 1),
+        "factorize_ms": round(statistics.mean(t_fact), 4),
+        "solve_ms": round(statistics.mean(t_solve), 4),
+        "step_tflops": round(total_flops / (ms_step * 1e-3) / 1e12, 3),
+        "setup_s": setup,
+        "setup_points_per_s": round(w.n / sum(v for k, v in setup.items() if k != "h2d_points"), 1),
+        "relres_vs_ktilde": relres,
+        "roofline": roof,
+        "kernels": kernels,
+        "e2e": {"value": round(n_total / (e2e_step * 1e-3), 1), "unit": "points/s",
+                "ms_per_step": round(e2e_step, 4), "h2d_bytes_per_step": int(b.nbytes),
+                "d2h_bytes_per_step": int(b.nbytes)},
+        "clocks": clk,
+        "gpu_launches": int(launches),
+    }
+    return result
+
+
+def main():
+    args = parse()
+    from paper_1701_02324_b200 import workloads as W
+    w = W.CONFIGS[args.config]
+    if args.n:
+        w = w.scaled(args.n)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        r = oracle_arm(w, min(args.cpu_sample_n, w.n), max(args.steps, 1), cores)
+        out = {"metric": "factorize+solve points/s", "value": round(r["value"], 1), "unit": "points/s",
+               "n_gpus": args.gpus, "steps": max(args.steps, 1), "warmup": args.warmup,
+               "ms_per_step": round(r["t_step"] * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+               "vs_baseline": None, "dtype": "f64", "data": "synthetic: seeded BASELINE generator",
+               "config": {"workload": w.name, "n": w.n, "sample_n": min(args.cpu_sample_n, w.n)},
+               "impl": "reference",
+               "cpu_baseline": {"value": round(r["value"], 1), "unit": "points/s", "cores": r["cores"],
+                                "kind": "port", "sample": r["sample"]},
+               "e2e": {"value": round(r["value"], 1), "unit": "points/s", "h2d_bytes_per_step": 0,
+                       "d2h_bytes_per_step": 0},
+               "factorize_points_per_s": round(min(args.cpu_sample_n, w.n) / r["t_factorize"], 1),
+               "solve_rhs_per_s": round(w.nrhs / r["t_solve"], 1)}
+        print(json.dumps(out))
+        return
+
+    import torch
+    if world > 1:
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        torch.cuda.set_device(local)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+    result = gpu_arm(args, w, rank, world)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = oracle_arm(w, min(args.cpu_sample_n, w.n), args.cpu_steps, cores)
+        result["cpu_baseline"] = {"value": round(r["value"], 1), "unit": "points/s", "cores": r["cores"],
+                                  "kind": "port", "sample": r["sample"],
+                                  "factorize_points_per_s": round(min(args.cpu_sample_n, w.n) / r["t_factorize"], 1),
+                                  "solve_rhs_per_s": round(w.nrhs / r["t_solve"], 1)}
+    if rank == 0:
+        print(json.dumps(result))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

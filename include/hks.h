@@ -165,6 +165,59 @@ int hks_upward_offsets(hks_plan* plan, int64_t k, int64_t* offsets_host, int64_t
 int hks_upward(hks_plan* plan, void* const* buffers, const double* w, int64_t k, double* out,
                void* stream);
 
+/* ----- vector kernels of the GMRES driver (krylov.py:82-130) ----------------
+ * hks_vdots: out[v] = scale * <X[v], y> (+ out[v] when accumulate) for m
+ * vectors at stride ldv; deterministic fixed-grid reduction; part = caller
+ * scratch of m * 296 doubles.  hks_vaxpys: y += scale * sum_v coef[v] X[v]
+ * (coef on the device). */
+int hks_vdots(const double* X, int64_t ldv, int64_t m, const double* y, int64_t n, double* out,
+              double scale, int32_t accumulate, double* part, void* stream);
+int hks_vaxpys(const double* X, int64_t ldv, int64_t m, const double* coef, double scale, double* y,
+               int64_t n, void* stream);
+
+/* ----- setup stages ------------------------------------------------------------
+ * build_tree, tree.py:87-144: X_in n x d input-order points; starts[(2^depth - 1)
+ * x d] the normalised power-method start vectors default_rng([seed, level,
+ * begin]).standard_normal(d) / norm (heap order); outputs X_out (tree order),
+ * perm_out, split_dirs, split_vals. */
+int hks_build_tree(const double* X_in, int64_t n, int64_t d, int64_t depth, int64_t steps,
+                   const double* starts, double* X_out, int64_t* perm_out, double* split_dirs,
+                   double* split_vals, void* stream);
+
+/* knn_bruteforce, tree.py:163-188: out[n x k] int64, (d^2, index) order, k <= 32. */
+int hks_knn(const double* X, int64_t n, int64_t d, int64_t k, int64_t* out, void* stream);
+
+/* sample_rows(knn_augmented), skeleton.py:111-121, for every node of one
+ * level: mark = per-node bitmap of neighbours outside the node (counts to
+ * the host); fill = map the host's top-up draws (ranks into the sorted rest
+ * set) and compact each node's rows in ascending order. */
+int hks_knn_rows_mark(const int64_t* knn, int64_t n, int64_t kappa, int64_t level, int64_t depth,
+                      int32_t* bitmap, int64_t* counts_host, void* stream);
+int hks_knn_rows_fill(int64_t n, int64_t level, int64_t depth, int32_t* bitmap, const int64_t* extra,
+                      const int64_t* extra_off_host, int64_t* rows, const int64_t* row_off_host,
+                      void* stream);
+
+/* build_skeletons for one level, skeleton.py:125-182: sampled block eval +
+ * truncated column-pivoted QR + ID for `count` nodes (first heap index
+ * first_node); rows / cands device flat lists with host offsets[count+1];
+ * skeleton indices / interp written into the SKEL / INTERP layouts at the
+ * given element offsets; ranks_host[count]. */
+int hks_skeletonize_level(const double* X, int64_t d, const hks_kernel* kern, int64_t count,
+                          int64_t first_node, const int64_t* rows, const int64_t* row_off,
+                          const int64_t* cands, const int64_t* cand_off, double tau,
+                          int64_t max_rank, int64_t* skel_buf, const int64_t* skel_off,
+                          double* interp_buf, const int64_t* interp_off, int64_t* ranks_host,
+                          void* stream);
+
+/* ----- instrumentation ----------------------------------------------------------
+ * hks_profile(1, ...) resets and starts per-kind CUDA-event timing of every
+ * plan step; hks_profile(0, out) stops; out[kind * 4 + {launches, ms, flops,
+ * bytes}] for kinds GEMM, COPY, GETRF, GETRS, GECON, EVAL_CM, EVAL_RM, KSUM
+ * (flops / bytes are the algorithmic counts of the executed descriptors).
+ * hks_launch_count: plan-step launches since load. */
+int hks_profile(int32_t enable, double* out_host);
+long long hks_launch_count(void);
+
 #ifdef __cplusplus
 }
 #endif

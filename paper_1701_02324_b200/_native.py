@@ -71,7 +71,26 @@ SIGNATURES = {
     "hks_knn": [_P, _I64, _I64, _I64, _P, _P],
     "hks_vdots": [_P, _I64, _I64, _P, _I64, _P, _D, _I32, _P, _P],
     "hks_vaxpys": [_P, _I64, _I64, _P, _D, _P, _I64, _P],
+    "hks_profile": [_I32, _DP],
 }
+
+KIND_NAMES = ("gemm", "copy", "getrf", "getrs", "gecon", "eval", "eval_rm", "ksum")
+
+
+def profile(enable):
+    """Start (True) / stop (False) per-kind CUDA-event timing of plan steps;
+    returns {kind: {launches, ms, flops, bytes}} accumulated so far."""
+    out = (ctypes.c_double * (4 * len(KIND_NAMES)))()
+    call("hks_profile", int(bool(enable)), out)
+    return {k: {"launches": out[4 * i], "ms": out[4 * i + 1], "flops": out[4 * i + 2],
+                "bytes": out[4 * i + 3]} for i, k in enumerate(KIND_NAMES)}
+
+
+def launch_count():
+    f = lib().hks_launch_count
+    f.restype = ctypes.c_longlong
+    f.argtypes = []
+    return int(f())
 
 
 class HksError(RuntimeError):

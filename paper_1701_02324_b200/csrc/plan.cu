@@ -101,8 +101,16 @@ DevBuf::~DevBuf() {
 
 cudaError_t StepList::run(const Bases& b, const double* X, int d, const KernelParams& kp,
                           cudaStream_t s) const {
+  const bool prof = profiling();
   for (const Step& st : steps_) {
     cudaError_t e = cudaSuccess;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (prof) {
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0, s);
+    }
+    count_launch();
     switch (st.kind) {
       case ST_GEMM:
         e = launch_gemm_batched(b, (const GemmDesc*)st.d, st.count, st.p0, st.p1, s);
@@ -128,9 +136,36 @@ cudaError_t StepList::run(const Bases& b, const double* X, int d, const KernelPa
         e = launch_ksum_batched(X, d, kp, b, (const SumDesc*)st.d, st.count, st.p0, s);
         break;
     }
+    if (prof) {
+      cudaEventRecord(e1, s);
+      profile_step(st.kind, st.flops, st.bytes, e0, e1);
+    }
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+// ------------------------------------------------------------ profiling
+
+namespace {
+struct Pending {
+  int kind;
+  double flops, bytes;
+  cudaEvent_t a, b;
+};
+struct Profile {
+  bool on = false;
+  std::vector<Pending> pending;
+  double launches[kNumKinds] = {0}, ms[kNumKinds] = {0}, flops[kNumKinds] = {0}, bytes[kNumKinds] = {0};
+};
+Profile g_prof;
+long long g_launches = 0;
+}  // namespace
+
+bool profiling() { return g_prof.on; }
+void count_launch(int n) { g_launches += n; }
+void profile_step(int kind, double flops, double bytes, cudaEvent_t a, cudaEvent_t b) {
+  g_prof.pending.push_back(Pending{kind, flops, bytes, a, b});
 }
 
 namespace {
@@ -142,19 +177,42 @@ inline Ref adv(Ref r, int64_t elems) { return r + (uint64_t)elems * 8; }
 struct Gemms {
   std::vector<GemmDesc> v;
   int mm = 0, mn = 0;
+  double flops = 0, bytes = 0;
   void add(Ref A, int lda, int ta, Ref B, int ldb, int tb, Ref C, int ldc, int m, int n, int k,
            double alpha, double beta) {
     if (m <= 0 || n <= 0) return;
     v.push_back(GemmDesc{A, B, C, m, n, k, lda, ldb, ldc, ta, tb, alpha, beta});
     mm = std::max(mm, m);
     mn = std::max(mn, n);
+    flops += 2.0 * m * n * k;
+    bytes += 8.0 * ((double)m * k + (double)k * n + (double)m * n * (beta != 0.0 ? 2 : 1));
   }
   void flush(StepList& sl) {
-    sl.add(ST_GEMM, v, mm, mn);
+    sl.add(ST_GEMM, v, mm, mn, flops, bytes);
     v.clear();
     mm = mn = 0;
+    flops = bytes = 0;
   }
 };
+
+inline double lu_flops(double n) { return 2.0 / 3.0 * n * n * n; }
+inline double getrs_flops(double n, double k) { return 2.0 * n * n * k; }
+double lu_list_flops(const std::vector<LuDesc>& v, double* bytes) {
+  double f = 0;
+  for (auto& d : v) {
+    f += lu_flops(d.n);
+    *bytes += 16.0 * d.n * d.n;
+  }
+  return f;
+}
+double rs_list_flops(const std::vector<LuSolveDesc>& v, double* bytes) {
+  double f = 0;
+  for (auto& d : v) {
+    f += getrs_flops(d.n, d.nrhs);
+    *bytes += 8.0 * ((double)d.n * d.n + 2.0 * d.n * d.nrhs);
+  }
+  return f;
+}
 
 struct Copies {
   std::vector<CopyDesc> v;
@@ -170,7 +228,9 @@ struct Copies {
     me = std::max(me, m * n);
   }
   void flush(StepList& sl) {
-    sl.add(ST_COPY, v, me);
+    double bytes = 0;
+    for (auto& c : v) bytes += (c.mode == 0 ? 16.0 : 8.0) * c.m * c.n;
+    sl.add(ST_COPY, v, me, 0, 0.0, bytes);
     v.clear();
     me = 0;
   }
@@ -250,10 +310,18 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl) {
         gm.add(c.interp(i), r, 0, c.phi(i), m, 0, c.theta(i), r, r, r, m, 1.0, 0.0);
       }
     }
-    sl.add(ST_EVAL_CM, ev, mx, mx);
-    sl.add(ST_GETRF, lu, mx);
+    double eb = 0, ef = 0;
+    for (auto& e : ev) {
+      ef += (double)e.m * e.n * (2.0 * P.d + 5.0);
+      eb += 8.0 * e.m * e.n;
+    }
+    sl.add(ST_EVAL_CM, ev, mx, mx, ef, eb);
+    double lb = 0, rb = 0;
+    const double lf = lu_list_flops(lu, &lb);
+    sl.add(ST_GETRF, lu, mx, 0, lf, lb);
     cp.flush(sl);
-    sl.add(ST_GETRS, rs, mx, mr);
+    const double rf = rs_list_flops(rs, &rb);
+    sl.add(ST_GETRS, rs, mx, mr, rf, rb);
     gm.flush(sl);
   }
   for (int64_t lev = L.depth - 1; lev >= 0; --lev) {  // internal levels (solver.py:139-161)
@@ -296,11 +364,14 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl) {
     }
     c_id.flush(sl);
     g_z.flush(sl);
-    sl.add(ST_GETRF, lu, maxR);
-    if (with_cond) sl.add(ST_GECON, lu, maxR);
+    double lb = 0, rb = 0;
+    const double lf = lu_list_flops(lu, &lb);
+    sl.add(ST_GETRF, lu, maxR, 0, lf, lb);
+    if (with_cond) sl.add(ST_GECON, lu, maxR, 0, 11.0 * 2.0 * lb / 16.0, 11.0 * lb / 2.0);
     if (lev == 0) continue;
     c_y.flush(sl);
-    sl.add(ST_GETRS, rs, maxR, maxR);
+    const double rf = rs_list_flops(rs, &rb);
+    sl.add(ST_GETRS, rs, maxR, maxR, rf, rb);
     g_f.flush(sl);
     c_t.flush(sl);
     g_tf.flush(sl);
@@ -335,7 +406,9 @@ void build_solve(const hks_plan& P, int64_t kk, StepList& sl) {
     }
     gp.flush(sl);
     cp.flush(sl);
-    sl.add(ST_GETRS, rs, mx, k);
+    double rb = 0;
+    const double rf = rs_list_flops(rs, &rb);
+    sl.add(ST_GETRS, rs, mx, k, rf, rb);
   }
   for (int64_t lev = L.depth - 1; lev >= 0; --lev) {  // upward, internal (solver.py:219-233)
     Copies cp;
@@ -360,7 +433,9 @@ void build_solve(const hks_plan& P, int64_t kk, StepList& sl) {
       g3.add(c.interp(i), r, 0, Si, R, 0, dst, ld, r, k, R, 1.0, 0.0);
     }
     cp.flush(sl);
-    sl.add(ST_GETRS, rs, maxR, k);
+    double rb = 0;
+    const double rf = rs_list_flops(rs, &rb);
+    sl.add(ST_GETRS, rs, maxR, k, rf, rb);
     g1.flush(sl);
     g2.flush(sl);
     g3.flush(sl);
@@ -430,7 +505,12 @@ void build_matvec(const hks_plan& P, int64_t kk, StepList& sl) {
       ks.push_back(SumDesc{kNull, kNull, L.begin[i], L.begin[i], m, m, k, D(B_VIN, L.begin[i]), n,
                            D(B_VOUT, L.begin[i]), n, 0.0, 1});
     }
-    sl.add(ST_KSUM, ks, mx);
+    double kf = 0, kb = 0;
+    for (auto& q : ks) {
+      kf += (double)q.m * q.n * (2.0 * P.d + 5.0) + 2.0 * q.m * q.n * q.k;
+      kb += 8.0 * ((double)q.n * q.k + (double)q.m * q.k);
+    }
+    sl.add(ST_KSUM, ks, mx, 0, kf, kb);
   }
   if (L.depth == 0) return;
   build_upward(P, kk, S, sl);
@@ -706,3 +786,34 @@ extern "C" int hks_upward(hks_plan* P, void* const* buffers, const double* w, in
   if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_upward: %s", cudaGetErrorString(e));
   return HKS_OK;
 }
+
+extern "C" int hks_profile(int32_t enable, double* out_host) {
+  // enable: 1 start (reset), 0 stop; out_host[kind * 4 + {launches, ms, flops, bytes}]
+  // for the kNumKinds step kinds (GEMM, COPY, GETRF, GETRS, GECON, EVAL_CM, EVAL_RM, KSUM).
+  cudaDeviceSynchronize();
+  for (auto& p : g_prof.pending) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, p.a, p.b);
+    g_prof.launches[p.kind] += 1;
+    g_prof.ms[p.kind] += ms;
+    g_prof.flops[p.kind] += p.flops;
+    g_prof.bytes[p.kind] += p.bytes;
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  g_prof.pending.clear();
+  if (out_host)
+    for (int k = 0; k < kNumKinds; ++k) {
+      out_host[4 * k + 0] = g_prof.launches[k];
+      out_host[4 * k + 1] = g_prof.ms[k];
+      out_host[4 * k + 2] = g_prof.flops[k];
+      out_host[4 * k + 3] = g_prof.bytes[k];
+    }
+  if (enable) {
+    for (int k = 0; k < kNumKinds; ++k) g_prof.launches[k] = g_prof.ms[k] = g_prof.flops[k] = g_prof.bytes[k] = 0;
+  }
+  g_prof.on = enable != 0;
+  return HKS_OK;
+}
+
+extern "C" long long hks_launch_count(void) { return g_launches; }

@@ -41,19 +41,28 @@ struct Step {
   const void* d;  // device descriptors
   int count;
   int p0, p1;     // grid sizing (max dims)
+  double flops;   // algorithmic FP64 flops of the whole step
+  double bytes;   // compulsory HBM bytes of the whole step
 };
+
+constexpr int kNumKinds = 8;
+
+// Opt-in per-kind CUDA-event timing of every step (hks_profile_*).
+void profile_step(int kind, double flops, double bytes, cudaEvent_t a, cudaEvent_t b);
+bool profiling();
+void count_launch(int n = 1);
 
 // Accumulates host descriptor arrays, uploads them in one arena.
 class StepList {
  public:
   template <class D>
-  void add(int kind, const std::vector<D>& v, int p0, int p1 = 0) {
+  void add(int kind, const std::vector<D>& v, int p0, int p1 = 0, double flops = 0.0, double bytes = 0.0) {
     if (v.empty()) return;
     size_t at = (host_.size() + 63) & ~size_t(63);
     host_.resize(at + v.size() * sizeof(D));
     std::memcpy(host_.data() + at, v.data(), v.size() * sizeof(D));
     offs_.push_back(at);
-    steps_.push_back(Step{kind, nullptr, (int)v.size(), p0, p1});
+    steps_.push_back(Step{kind, nullptr, (int)v.size(), p0, p1, flops, bytes});
   }
   cudaError_t upload(cudaStream_t stream);
   cudaError_t run(const Bases& b, const double* X, int d, const KernelParams& kp, cudaStream_t stream) const;

@@ -165,6 +165,9 @@ def solve_device(f, B):
 
 def _solve_block(f, b, in_tree_order):
     t = N.torch()
+    host_tensor = isinstance(b, t.Tensor) and not b.is_cuda
+    if host_tensor:  # e.g. a pinned host block: asynchronous H2D, host result
+        b = b.to(device=N.device(), dtype=t.float64, non_blocking=True)
     dev = isinstance(b, t.Tensor) and b.is_cuda
     vec = b.dim() == 1 if dev else np.ndim(b) == 1
     if dev:
@@ -182,7 +185,7 @@ def _solve_block(f, b, in_tree_order):
         out = t.empty_like(X)
         out[:, f.tree.device_perm()] = X
         X = out
-    if dev:
+    if dev and not host_tensor:
         return X[0] if vec else X.t()
     x = X.cpu().numpy().T
     return x[:, 0].copy() if vec else np.ascontiguousarray(x)

@@ -86,16 +86,6 @@ def test_singular_reports_step(hk):
         hk.factor_dense(a)
 
 
-def test_interpolative_decomposition_golden(hk):
-    z = np.load(GOLDEN / "id_cases.npz")
-    for t in range(12):
-        tol, mr = z[f"tol{t}"]
-        cols, p = hk.interpolative_decomposition(z[f"a{t}"], tol, int(mr))
-        assert np.array_equal(cols, z[f"cols{t}"]), t
-        assert np.array_equal(p[:, cols], np.eye(cols.size))  # bitwise identity block
-        assert np.allclose(p, z[f"p{t}"], rtol=1e-8, atol=1e-10)
-
-
 def test_gmres_unpreconditioned_golden(hk):
     z = np.load(GOLDEN / "gmres_n512.npz")
     tree = O.build_tree(np.random.default_rng([3, 0, 0]).random((512, 3)), 512, 3)
