@@ -143,6 +143,10 @@ int hks_leaf_block(hks_plan* plan, int64_t leaf, double* out, void* stream);
 int hks_factorize(hks_plan* plan, void* const* buffers, double lam, int32_t with_cond,
                   int64_t* bad_node_host, void* stream);
 
+/* Device milliseconds per level of the last hks_factorize (ms_host[level],
+ * level 0..depth; Factorization.level_seconds, solver.py:164-176). */
+int hks_factor_level_ms(hks_plan* plan, double* ms_host);
+
 /* z_cond (1 / dgecon rcond; 0 for leaves) and info per node, host outputs. */
 int hks_factor_stats(hks_plan* plan, void* const* buffers, double* z_cond_host, int32_t* info_host,
                      void* stream);

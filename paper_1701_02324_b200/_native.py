@@ -72,9 +72,11 @@ SIGNATURES = {
     "hks_vdots": [_P, _I64, _I64, _P, _I64, _P, _D, _I32, _P, _P],
     "hks_vaxpys": [_P, _I64, _I64, _P, _D, _P, _I64, _P],
     "hks_profile": [_I32, _DP],
+    "hks_factor_level_ms": [_P, _DP],
 }
 
-KIND_NAMES = ("gemm", "copy", "getrf", "getrs", "gecon", "eval", "eval_rm", "ksum")
+KIND_NAMES = ("gemm", "copy", "getrf", "getrs", "gecon", "eval", "eval_rm", "ksum", "panel", "swap",
+              "trsm_l", "trsm_u", "norm1")
 
 
 def profile(enable):

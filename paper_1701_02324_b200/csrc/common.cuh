@@ -155,6 +155,25 @@ struct LuSolveDesc {
   int lda, ldb;
 };
 
+// Factor rows p0..n-1 of panel columns [p0, p0 + pb) (partial pivoting).
+struct PanelDesc {
+  Ref A, piv, info;
+  int lda, n, p0, pb;
+};
+
+// Row interchanges piv[r0..r1) applied to columns [c0, c1) of A.
+struct SwapDesc {
+  Ref A, piv;
+  int lda, r0, r1, c0, c1;
+  int pad;
+};
+
+// B := T^-1 B, T the k x k unit-lower (or non-unit upper) block at T.
+struct TrsmDesc {
+  Ref T, B;
+  int ldt, ldb, k, ncols;
+};
+
 }  // namespace hks
 
 #define HKS_CUDA_CHECK(expr)                                                 \

@@ -22,6 +22,12 @@ cudaError_t launch_getrf_batched(const Bases& bases, const LuDesc* d_descs, int 
                                  cudaStream_t stream);
 cudaError_t launch_getrs_batched(const Bases& bases, const LuSolveDesc* d_descs, int count, int max_n,
                                  int max_nrhs, cudaStream_t stream);
+cudaError_t launch_panel_batched(const Bases& b, const PanelDesc* d, int count, int max_rows, int pb,
+                                 cudaStream_t s);
+cudaError_t launch_swap_batched(const Bases& b, const SwapDesc* d, int count, int max_cols, cudaStream_t s);
+cudaError_t launch_trsm_batched(const Bases& b, const TrsmDesc* d, int count, int max_cols, bool upper,
+                                cudaStream_t s);
+cudaError_t launch_norm1_batched(const Bases& b, const LuDesc* d, int count, cudaStream_t s);
 cudaError_t launch_gecon_batched(const Bases& bases, const LuDesc* d_descs, int count, int max_n,
                                  cudaStream_t stream);
 

@@ -1,0 +1,242 @@
+// Building blocks of the level-batched blocked LU / triangular-solve
+// programs (plan.cu: add_lu_program, add_lu_solve_program).
+//
+// The LU of every matrix of a tree level (leaf blocks K_aa + lam I, reduced
+// matrices Z) runs as one descriptor program: 128-column groups, each
+// factored as 32-column panels (left-looking inside the group), then one
+// row-interchange pass, one unit-lower TRSM and one DMMA GEMM trailing
+// update of rank 128 for all matrices at once.  Right-hand-side columns
+// (P^T for phi, thhat for Z^-1 thhat) ride along in the swaps, TRSMs and
+// GEMMs, so the forward substitution costs GEMM time; a backward sweep of
+// upper TRSMs + GEMMs finishes the solve.  Results are those of LAPACK
+// getrf / getrs (partial pivoting, row interchanges applied to the whole
+// row, 0-based pivots) up to roundoff.
+#include <cfloat>
+
+#include "common.cuh"
+#include "hks_internal.h"
+
+namespace hks {
+namespace {
+
+constexpr int PT = 256;  // panel threads
+
+// Factor rows p0..n-1 of columns [p0, p0+pb) in shared memory: pivot search
+// (lowest row on ties, LAPACK idamax), swap inside the panel, scale by the
+// reciprocal (dgetf2), rank-1 update.  piv[p0 + jj] = global pivot row.
+template <int PB>
+__global__ void __launch_bounds__(PT) panel_kernel(const Bases bases, const PanelDesc* __restrict__ descs, int ldp) {
+  const PanelDesc D = descs[blockIdx.x];
+  double* A = at<double>(bases, D.A);
+  int* piv = at<int>(bases, D.piv);
+  const int lda = D.lda, p0 = D.p0, pb = D.pb, mr = D.n - D.p0;
+  extern __shared__ double P[];
+  __shared__ double red_v[PT / 32];
+  __shared__ int red_i[PT / 32];
+  __shared__ int s_info;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_info = 0;
+  for (int e = tid; e < mr * pb; e += PT) {
+    const int i = e % mr, c = e / mr;
+    P[i + c * ldp] = A[(p0 + i) + (size_t)(p0 + c) * lda];
+  }
+  __syncthreads();
+  for (int jj = 0; jj < pb; ++jj) {
+    ArgMax a{-1.0, 0x7fffffff};
+    for (int i = jj + tid; i < mr; i += PT) a = argmax_pick(a, ArgMax{fabs(P[i + jj * ldp]), i});
+    a = block_argmax(a, red_v, red_i);
+    const int p = a.i;
+    const double pv = P[p + jj * ldp];
+    __syncthreads();
+    if (tid == 0) {
+      piv[p0 + jj] = p0 + p;
+      if (pv == 0.0 && s_info == 0) s_info = p0 + jj + 1;
+    }
+    if (p != jj)
+      for (int c = tid; c < pb; c += PT) {
+        const double t = P[jj + c * ldp];
+        P[jj + c * ldp] = P[p + c * ldp];
+        P[p + c * ldp] = t;
+      }
+    __syncthreads();
+    if (pv != 0.0) {
+      const bool recip = fabs(pv) >= DBL_MIN;
+      const double inv = 1.0 / pv;
+      for (int i = jj + 1 + tid; i < mr; i += PT) P[i + jj * ldp] = recip ? P[i + jj * ldp] * inv : P[i + jj * ldp] / pv;
+    }
+    __syncthreads();
+    const int rr = mr - jj - 1, cc = pb - jj - 1;
+    for (int e = tid; e < rr * cc; e += PT) {
+      const int i = jj + 1 + e % rr, c = jj + 1 + e / rr;
+      P[i + c * ldp] -= P[i + jj * ldp] * P[jj + c * ldp];
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < mr * pb; e += PT) {
+    const int i = e % mr, c = e / mr;
+    A[(p0 + i) + (size_t)(p0 + c) * lda] = P[i + c * ldp];
+  }
+  if (tid == 0 && s_info && D.info != kNull) {
+    int* info = at<int>(bases, D.info);
+    if (*info == 0) *info = s_info;  // panels run in order: keep the first zero pivot
+  }
+}
+
+// Row interchanges piv[r0..r1) applied in order to columns [c0, c1).
+__global__ void swap_kernel(const Bases bases, const SwapDesc* __restrict__ descs) {
+  const SwapDesc D = descs[blockIdx.y];
+  const int c = D.c0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= D.c1) return;
+  double* col = at<double>(bases, D.A) + (size_t)c * D.lda;
+  const int* piv = at<const int>(bases, D.piv);
+  for (int jj = D.r0; jj < D.r1; ++jj) {
+    const int p = piv[jj];
+    if (p != jj) {
+      const double t = col[jj];
+      col[jj] = col[p];
+      col[p] = t;
+    }
+  }
+}
+
+// B := T^-1 B for a k x k triangular block T (unit lower, or non-unit
+// upper), k <= 128, B k x ncols; CTA = 32 columns in shared memory, 32-row
+// blocks: DMMA update from the solved blocks, then warp substitution.
+constexpr int TR = 32;
+constexpr int TT = 256;
+
+template <bool UPPER>
+__global__ void __launch_bounds__(TT) trsm_kernel(const Bases bases, const TrsmDesc* __restrict__ descs) {
+  const TrsmDesc D = descs[blockIdx.y];
+  const int c0 = blockIdx.x * TR;
+  if (c0 >= D.ncols) return;
+  const int nc = min(TR, D.ncols - c0), k = D.k;
+  const double* T = at<const double>(bases, D.T);
+  double* B = at<double>(bases, D.B) + (size_t)c0 * D.ldb;
+  __shared__ double X[128 * (TR + 1)];  // row-major k x TR (+1 pad)
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int e = tid; e < k * nc; e += TT) {
+    const int i = e % k, c = e / k;
+    X[i * (TR + 1) + c] = B[i + (size_t)c * D.ldb];
+  }
+  __syncthreads();
+  const int nblk = (k + 31) / 32;
+  const int fr = lane >> 2, fc = lane & 3;
+  for (int bb = 0; bb < nblk; ++bb) {
+    const int b = UPPER ? nblk - 1 - bb : bb;
+    const int r0 = b * 32, nr = min(32, k - r0);
+    // update rows r0..r0+nr with the already-solved rows (DMMA, 16 fragments over 8 warps)
+    const int klo = UPPER ? r0 + nr : 0, khi = UPPER ? k : r0;
+    if (khi > klo) {
+      for (int f = wid; f < 16; f += 8) {
+        const int fi = f & 3, fj = f >> 2;
+        double d0 = 0.0, d1 = 0.0;
+        const int r = r0 + fi * 8 + fr;
+        for (int kk = klo; kk < khi; kk += 4) {
+          const int kq = kk + fc;
+          const double a = (fi * 8 + fr < nr && kq < khi) ? -T[r + (size_t)kq * D.ldt] : 0.0;
+          const double bv = (kq < khi && fj * 8 + fr < nc) ? X[kq * (TR + 1) + fj * 8 + fr] : 0.0;
+          dmma884(d0, d1, a, bv);
+        }
+        const int c = fj * 8 + 2 * fc;
+        if (fi * 8 + fr < nr) {
+          if (c < nc) X[r * (TR + 1) + c] += d0;
+          if (c + 1 < nc) X[r * (TR + 1) + c + 1] += d1;
+        }
+      }
+      __syncthreads();
+    }
+    // substitution inside the 32-row block: warp w owns columns w, w+8, ...
+    for (int c = wid; c < nc; c += 8) {
+      double x = lane < nr ? X[(r0 + lane) * (TR + 1) + c] : 0.0;
+      const double* tcol;
+      if (!UPPER) {
+        for (int j = 0; j < nr; ++j) {
+          const double xj = __shfl_sync(0xffffffffu, x, j);
+          tcol = T + (size_t)(r0 + j) * D.ldt;
+          if (lane > j && lane < nr) x -= tcol[r0 + lane] * xj;
+        }
+      } else {
+        for (int j = nr - 1; j >= 0; --j) {
+          tcol = T + (size_t)(r0 + j) * D.ldt;
+          double xj = __shfl_sync(0xffffffffu, x, j);
+          xj /= tcol[r0 + j];
+          if (lane == j) x = xj;
+          if (lane < j) x -= tcol[r0 + lane] * xj;
+        }
+      }
+      if (lane < nr) X[(r0 + lane) * (TR + 1) + c] = x;
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < k * nc; e += TT) {
+    const int i = e % k, c = e / k;
+    B[i + (size_t)c * D.ldb] = X[i * (TR + 1) + c];
+  }
+}
+
+// ||A||_1 (max column abs sum) of each n x n matrix, before factoring.
+__global__ void norm1_kernel(const Bases bases, const LuDesc* __restrict__ descs) {
+  const LuDesc L = descs[blockIdx.x];
+  __shared__ double rv[8];
+  __shared__ int ri[8];
+  const double* A = at<const double>(bases, L.A);
+  double best = 0.0;
+  for (int c = threadIdx.x; c < L.n; c += blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < L.n; ++r) s += fabs(A[r + (size_t)c * L.lda]);
+    best = fmax(best, s);
+  }
+  ArgMax m = block_argmax(ArgMax{best, (int)threadIdx.x}, rv, ri);
+  if (threadIdx.x == 0 && L.anorm != kNull) *at<double>(bases, L.anorm) = m.v;
+  if (threadIdx.x == 0 && L.info != kNull) *at<int>(bases, L.info) = 0;
+}
+
+}  // namespace
+
+cudaError_t launch_panel_batched(const Bases& b, const PanelDesc* d, int count, int max_rows, int pb,
+                                 cudaStream_t s) {
+  if (count <= 0 || max_rows <= 0) return cudaSuccess;
+  const int ldp = max_rows;
+  if (pb <= 16) {
+    const size_t sm = (size_t)ldp * 16 * sizeof(double);
+    cudaFuncSetAttribute(panel_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    panel_kernel<16><<<count, PT, sm, s>>>(b, d, ldp);
+  } else {
+    const size_t sm = (size_t)ldp * 32 * sizeof(double);
+    cudaFuncSetAttribute(panel_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    panel_kernel<32><<<count, PT, sm, s>>>(b, d, ldp);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_swap_batched(const Bases& b, const SwapDesc* d, int count, int max_cols, cudaStream_t s) {
+  if (count <= 0 || max_cols <= 0) return cudaSuccess;
+  for (int first = 0; first < count; first += 65535) {
+    const int cnt = count - first < 65535 ? count - first : 65535;
+    swap_kernel<<<dim3((max_cols + 127) / 128, cnt), 128, 0, s>>>(b, d + first);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_trsm_batched(const Bases& b, const TrsmDesc* d, int count, int max_cols, bool upper,
+                                cudaStream_t s) {
+  if (count <= 0 || max_cols <= 0) return cudaSuccess;
+  for (int first = 0; first < count; first += 65535) {
+    const int cnt = count - first < 65535 ? count - first : 65535;
+    dim3 grid((max_cols + TR - 1) / TR, cnt);
+    if (upper)
+      trsm_kernel<true><<<grid, TT, 0, s>>>(b, d + first);
+    else
+      trsm_kernel<false><<<grid, TT, 0, s>>>(b, d + first);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_norm1_batched(const Bases& b, const LuDesc* d, int count, cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  norm1_kernel<<<count, 256, 0, s>>>(b, d);
+  return cudaGetLastError();
+}
+
+}  // namespace hks

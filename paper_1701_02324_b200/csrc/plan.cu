@@ -79,6 +79,7 @@ void StepList::clear() {
   host_.clear();
   offs_.clear();
   steps_.clear();
+  marks_.clear();
 }
 
 StepList::~StepList() {
@@ -100,9 +101,12 @@ DevBuf::~DevBuf() {
 }
 
 cudaError_t StepList::run(const Bases& b, const double* X, int d, const KernelParams& kp,
-                          cudaStream_t s) const {
+                          cudaStream_t s, cudaEvent_t* ev) const {
   const bool prof = profiling();
-  for (const Step& st : steps_) {
+  size_t next_mark = 0;
+  for (size_t si = 0; si < steps_.size(); ++si) {
+    const Step& st = steps_[si];
+    while (ev && next_mark < marks_.size() && marks_[next_mark] == si) cudaEventRecord(ev[next_mark++], s);
     cudaError_t e = cudaSuccess;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (prof) {
@@ -135,6 +139,19 @@ cudaError_t StepList::run(const Bases& b, const double* X, int d, const KernelPa
       case ST_KSUM:
         e = launch_ksum_batched(X, d, kp, b, (const SumDesc*)st.d, st.count, st.p0, s);
         break;
+      case ST_PANEL:
+        e = launch_panel_batched(b, (const PanelDesc*)st.d, st.count, st.p0, st.p1, s);
+        break;
+      case ST_SWAP:
+        e = launch_swap_batched(b, (const SwapDesc*)st.d, st.count, st.p0, s);
+        break;
+      case ST_TRSM_L:
+      case ST_TRSM_U:
+        e = launch_trsm_batched(b, (const TrsmDesc*)st.d, st.count, st.p0, st.kind == ST_TRSM_U, s);
+        break;
+      case ST_NORM1:
+        e = launch_norm1_batched(b, (const LuDesc*)st.d, st.count, s);
+        break;
     }
     if (prof) {
       cudaEventRecord(e1, s);
@@ -142,6 +159,8 @@ cudaError_t StepList::run(const Bases& b, const double* X, int d, const KernelPa
     }
     if (e != cudaSuccess) return e;
   }
+  while (ev && next_mark < marks_.size()) cudaEventRecord(ev[next_mark++], s);
+  if (ev) cudaEventRecord(ev[marks_.size()], s);
   return cudaSuccess;
 }
 
@@ -264,6 +283,197 @@ struct Ctx {
   Ref block(int buf, int64_t at, int64_t p, int64_t k) const { return D(buf, at + P.stack_off[p] * k); }
 };
 
+// ------------------------------------------------------------ LU programs
+
+// One matrix of a level-batched LU: A (n x n, lda) factored in place with
+// partial pivoting; optional right-hand sides B (n x r, ldb) carried through
+// the factorization (forward substitution) and solved backward at the end,
+// leaving B := A^-1 B (getrf + getrs, solver.py:131-135, 148-156).
+struct LuJob {
+  Ref A;
+  int n, lda;
+  Ref piv, info, anorm;
+  Ref B;
+  int r, ldb;
+};
+
+constexpr int kGroup = 128;  // rank of each trailing update (and TRSM block)
+
+inline Ref elem(Ref base, int row, int col, int ld) { return adv(base, (int64_t)row + (int64_t)col * ld); }
+
+struct Panels {
+  std::vector<PanelDesc> v;
+  int rows = 0;
+  void flush(StepList& sl, int pb) {
+    double f = 0;
+    for (auto& d : v) f += (double)(d.n - d.p0) * d.pb * d.pb;
+    sl.add(ST_PANEL, v, rows, pb, f, 0.0);
+    v.clear();
+    rows = 0;
+  }
+};
+
+struct Swaps {
+  std::vector<SwapDesc> v;
+  int mc = 0;
+  void add(Ref A, Ref piv, int lda, int r0, int r1, int c0, int c1) {
+    if (r1 <= r0 || c1 <= c0) return;
+    v.push_back(SwapDesc{A, piv, lda, r0, r1, c0, c1, 0});
+    mc = std::max(mc, c1 - c0);
+  }
+  void flush(StepList& sl) {
+    double bytes = 0;
+    for (auto& d : v) bytes += 32.0 * (d.r1 - d.r0) * (d.c1 - d.c0);
+    sl.add(ST_SWAP, v, mc, 0, 0.0, bytes);
+    v.clear();
+    mc = 0;
+  }
+};
+
+struct Trsms {
+  std::vector<TrsmDesc> v;
+  int mc = 0;
+  void add(Ref T, int ldt, Ref B, int ldb, int k, int ncols) {
+    if (k <= 0 || ncols <= 0) return;
+    v.push_back(TrsmDesc{T, B, ldt, ldb, k, ncols});
+    mc = std::max(mc, ncols);
+  }
+  void flush(StepList& sl, bool upper) {
+    double f = 0, bytes = 0;
+    for (auto& d : v) {
+      f += (double)d.k * d.k * d.ncols;
+      bytes += 8.0 * ((double)d.k * d.k / 2 + 2.0 * d.k * d.ncols);
+    }
+    sl.add(upper ? ST_TRSM_U : ST_TRSM_L, v, mc, 0, f, bytes);
+    v.clear();
+    mc = 0;
+  }
+};
+
+// Appends the blocked, level-batched LU (+ carried right-hand sides) of
+// `jobs` to `sl`.  Groups of 128 columns: 32-column panels (16 for n > 640)
+// factored left-looking inside the group (swap, unit-lower TRSM and GEMM
+// from the group's earlier panels), then the group's interchanges on every
+// other column, one TRSM for the group's U rows and one rank-128 GEMM
+// trailing update -- all matrices of the level in the same launches.
+void add_lu_program(StepList& sl, const std::vector<LuJob>& jobs, bool with_norm) {
+  if (jobs.empty()) return;
+  int nmax = 0;
+  for (auto& j : jobs) nmax = std::max(nmax, j.n);
+  if (nmax == 0) return;
+  const int PB = nmax <= 640 ? 32 : 16;
+  if (with_norm) {
+    std::vector<LuDesc> nd;
+    for (auto& j : jobs) nd.push_back(LuDesc{j.A, j.piv, j.info, j.anorm, kNull, j.n, j.lda});
+    sl.add(ST_NORM1, nd, nmax);
+  }
+  for (int g0 = 0; g0 < nmax; g0 += kGroup) {
+    for (int p0 = g0; p0 < g0 + kGroup && p0 < nmax; p0 += PB) {
+      Swaps sw;
+      Trsms tr;
+      Gemms gm;
+      Panels pn;
+      for (auto& j : jobs) {
+        if (p0 >= j.n) continue;
+        const int gb = std::min(kGroup, j.n - g0), pb = std::min(PB, g0 + gb - p0);
+        if (pb <= 0) continue;
+        if (p0 > g0) {
+          // previous panel's interchanges on the group's earlier L columns, and
+          // all of the group's interchanges so far on this panel's columns
+          const int q0 = p0 - PB;
+          sw.add(j.A, j.piv, j.lda, q0, p0, g0, q0);
+          sw.add(j.A, j.piv, j.lda, g0, p0, p0, p0 + pb);
+          tr.add(elem(j.A, g0, g0, j.lda), j.lda, elem(j.A, g0, p0, j.lda), j.lda, p0 - g0, pb);
+          gm.add(elem(j.A, p0, g0, j.lda), j.lda, 0, elem(j.A, g0, p0, j.lda), j.lda, 0, elem(j.A, p0, p0, j.lda),
+                 j.lda, j.n - p0, pb, p0 - g0, -1.0, 1.0);
+        }
+        pn.v.push_back(PanelDesc{j.A, j.piv, j.info, j.lda, j.n, p0, pb});
+        pn.rows = std::max(pn.rows, j.n - p0);
+      }
+      sw.flush(sl);
+      tr.flush(sl, false);
+      gm.flush(sl);
+      pn.flush(sl, PB);
+    }
+    // the group's interchanges everywhere else, U rows of the group, trailing update
+    Swaps sw;
+    Trsms tr;
+    Gemms gm;
+    for (auto& j : jobs) {
+      if (g0 >= j.n) continue;
+      const int gb = std::min(kGroup, j.n - g0), ge = g0 + gb;
+      const int last = g0 + ((gb - 1) / PB) * PB;  // first column of the group's last panel
+      sw.add(j.A, j.piv, j.lda, last, ge, g0, last);
+      sw.add(j.A, j.piv, j.lda, g0, ge, 0, g0);
+      sw.add(j.A, j.piv, j.lda, g0, ge, ge, j.n);
+      if (j.r > 0) sw.add(j.B, j.piv, j.ldb, g0, ge, 0, j.r);
+      tr.add(elem(j.A, g0, g0, j.lda), j.lda, elem(j.A, g0, ge, j.lda), j.lda, gb, j.n - ge);
+      if (j.r > 0) tr.add(elem(j.A, g0, g0, j.lda), j.lda, elem(j.B, g0, 0, j.ldb), j.ldb, gb, j.r);
+      gm.add(elem(j.A, ge, g0, j.lda), j.lda, 0, elem(j.A, g0, ge, j.lda), j.lda, 0, elem(j.A, ge, ge, j.lda), j.lda,
+             j.n - ge, j.n - ge, gb, -1.0, 1.0);
+      if (j.r > 0)
+        gm.add(elem(j.A, ge, g0, j.lda), j.lda, 0, elem(j.B, g0, 0, j.ldb), j.ldb, 0, elem(j.B, ge, 0, j.ldb), j.ldb,
+               j.n - ge, j.r, gb, -1.0, 1.0);
+    }
+    sw.flush(sl);
+    tr.flush(sl, false);
+    gm.flush(sl);
+  }
+  // backward: B := U^-1 B, groups from the bottom (right-looking)
+  bool any_rhs = false;
+  for (auto& j : jobs) any_rhs |= j.r > 0;
+  if (!any_rhs) return;
+  for (int g0 = ((nmax - 1) / kGroup) * kGroup; g0 >= 0; g0 -= kGroup) {
+    Trsms tr;
+    Gemms gm;
+    for (auto& j : jobs) {
+      if (j.r == 0 || g0 >= j.n) continue;
+      const int gb = std::min(kGroup, j.n - g0);
+      tr.add(elem(j.A, g0, g0, j.lda), j.lda, elem(j.B, g0, 0, j.ldb), j.ldb, gb, j.r);
+      gm.add(elem(j.A, 0, g0, j.lda), j.lda, 0, elem(j.B, g0, 0, j.ldb), j.ldb, 0, j.B, j.ldb, g0, j.r, gb, -1.0, 1.0);
+    }
+    tr.flush(sl, true);
+    gm.flush(sl);
+  }
+}
+
+// B := A^-1 B with an LU from add_lu_program (getrs): interchanges, then
+// unit-lower and upper sweeps in 128-row blocks (TRSM + GEMM updates).
+void add_lu_solve_program(StepList& sl, const std::vector<LuJob>& jobs) {
+  int nmax = 0;
+  for (auto& j : jobs) nmax = std::max(nmax, j.n);
+  if (nmax == 0) return;
+  Swaps sw;
+  for (auto& j : jobs)
+    if (j.r > 0) sw.add(j.B, j.piv, j.ldb, 0, j.n, 0, j.r);
+  sw.flush(sl);
+  for (int g0 = 0; g0 < nmax; g0 += kGroup) {
+    Trsms tr;
+    Gemms gm;
+    for (auto& j : jobs) {
+      if (j.r == 0 || g0 >= j.n) continue;
+      const int gb = std::min(kGroup, j.n - g0), ge = g0 + gb;
+      tr.add(elem(j.A, g0, g0, j.lda), j.lda, elem(j.B, g0, 0, j.ldb), j.ldb, gb, j.r);
+      gm.add(elem(j.A, ge, g0, j.lda), j.lda, 0, elem(j.B, g0, 0, j.ldb), j.ldb, 0, elem(j.B, ge, 0, j.ldb), j.ldb,
+             j.n - ge, j.r, gb, -1.0, 1.0);
+    }
+    tr.flush(sl, false);
+    gm.flush(sl);
+  }
+  for (int g0 = ((nmax - 1) / kGroup) * kGroup; g0 >= 0; g0 -= kGroup) {
+    Trsms tr;
+    Gemms gm;
+    for (auto& j : jobs) {
+      if (j.r == 0 || g0 >= j.n) continue;
+      const int gb = std::min(kGroup, j.n - g0);
+      tr.add(elem(j.A, g0, g0, j.lda), j.lda, elem(j.B, g0, 0, j.ldb), j.ldb, gb, j.r);
+      gm.add(elem(j.A, 0, g0, j.lda), j.lda, 0, elem(j.B, g0, 0, j.ldb), j.ldb, 0, j.B, j.ldb, g0, j.r, gb, -1.0, 1.0);
+    }
+    tr.flush(sl, true);
+    gm.flush(sl);
+  }
+}
+
 // blockdiag(theta_a, theta_b) into an R x R slot (ld R)
 void add_theta_hat(Copies& cp, const Ctx& c, int64_t i, Ref Y) {
   const int rl = c.r(2 * i + 1), rr = c.r(2 * i + 2), R = rl + rr;
@@ -291,44 +501,37 @@ size_t factorize_workspace(const hks_plan& P) {
 void build_factorize(const hks_plan& P, bool with_cond, StepList& sl) {
   const Ctx c(P);
   const Layout& L = P.L;
-  {  // leaf level (solver.py:128-137)
+  sl.mark();
+  {  // leaf level (solver.py:128-137): A = K + lam I, LU with P^T carried -> phi, theta = P phi
     std::vector<EvalDesc> ev;
-    std::vector<LuDesc> lu;
-    std::vector<LuSolveDesc> rs;
+    std::vector<LuJob> jobs;
     Copies cp;
     Gemms gm;
-    int mx = 0, mr = 0;
+    int mx = 0;
     for (int64_t i = L.first(L.depth); i < L.nn; ++i) {
-      const int m = (int)L.size[i], r = c.r(i);
+      const int m = (int)L.size[i], r = i > 0 ? c.r(i) : 0;
       ev.push_back(EvalDesc{kNull, kNull, L.begin[i], L.begin[i], m, m, c.leaf_lu(i), m, 1});
-      lu.push_back(LuDesc{c.leaf_lu(i), c.leaf_piv(i), c.info(i), kNull, kNull, m, m});
       mx = std::max(mx, m);
-      if (i > 0 && r > 0) {
-        cp.copy(c.interp(i), r, 1, c.phi(i), m, m, r);  // phi = P^T, then A^-1 P^T
-        rs.push_back(LuSolveDesc{c.leaf_lu(i), c.leaf_piv(i), c.phi(i), m, r, m, m});
-        mr = std::max(mr, r);
-        gm.add(c.interp(i), r, 0, c.phi(i), m, 0, c.theta(i), r, r, r, m, 1.0, 0.0);
-      }
+      if (r > 0) cp.copy(c.interp(i), r, 1, c.phi(i), m, m, r);  // phi = P^T, then A^-1 P^T
+      jobs.push_back(LuJob{c.leaf_lu(i), m, m, c.leaf_piv(i), c.info(i), kNull, r > 0 ? c.phi(i) : kNull, r, m});
+      if (r > 0) gm.add(c.interp(i), r, 0, c.phi(i), m, 0, c.theta(i), r, r, r, m, 1.0, 0.0);
     }
-    double eb = 0, ef = 0;
+    double ef = 0, eb = 0;
     for (auto& e : ev) {
       ef += (double)e.m * e.n * (2.0 * P.d + 5.0);
       eb += 8.0 * e.m * e.n;
     }
     sl.add(ST_EVAL_CM, ev, mx, mx, ef, eb);
-    double lb = 0, rb = 0;
-    const double lf = lu_list_flops(lu, &lb);
-    sl.add(ST_GETRF, lu, mx, 0, lf, lb);
     cp.flush(sl);
-    const double rf = rs_list_flops(rs, &rb);
-    sl.add(ST_GETRS, rs, mx, mr, rf, rb);
+    add_lu_program(sl, jobs, false);
     gm.flush(sl);
   }
   for (int64_t lev = L.depth - 1; lev >= 0; --lev) {  // internal levels (solver.py:139-161)
+    sl.mark();
     Copies c_id, c_y, c_t;
     Gemms g_z, g_f, g_tf, g_w, g_out;
+    std::vector<LuJob> jobs;
     std::vector<LuDesc> lu;
-    std::vector<LuSolveDesc> rs;
     int maxR = 0;
     int64_t at = 0;
     for (int64_t i = L.first(lev); i < L.first(lev) + L.count(lev); ++i) {
@@ -340,7 +543,10 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl) {
       g_z.add(c.theta(a), rl, 0, C, rl, 0, adv(Z, (int64_t)rl * R), R, rl, rr, rl, 1.0, 1.0);
       g_z.add(c.theta(b), rr, 0, C, rl, 1, adv(Z, rl), R, rr, rl, rr, 1.0, 1.0);
       lu.push_back(LuDesc{Z, c.z_piv(i), c.info(i), c.anorm(i), with_cond ? c.rcond(i) : kNull, R, R});
-      if (lev == 0) continue;
+      if (lev == 0) {
+        jobs.push_back(LuJob{Z, R, R, c.z_piv(i), c.info(i), c.anorm(i), kNull, 0, R});
+        continue;
+      }
       const Ref Y = D(B_FWS, at);
       at += (int64_t)R * R;
       const Ref F = D(B_FWS, at);
@@ -349,7 +555,7 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl) {
       at += (int64_t)r * R;
       const Ref Pi = c.interp(i), pu = c.push(i);
       add_theta_hat(c_y, c, i, Y);
-      rs.push_back(LuSolveDesc{Z, c.z_piv(i), Y, R, R, R, R});
+      jobs.push_back(LuJob{Z, R, R, c.z_piv(i), c.info(i), c.anorm(i), Y, R, R});  // Y = Z^-1 thhat
       // folded F = B Z^-1 thhat (solver.py:86-89, 156)
       g_f.add(C, rl, 0, adv(Y, rl), R, 0, F, R, rl, R, rr, 1.0, 0.0);
       g_f.add(C, rl, 1, Y, R, 0, adv(F, rl), R, rr, R, rl, 1.0, 0.0);
@@ -364,14 +570,14 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl) {
     }
     c_id.flush(sl);
     g_z.flush(sl);
-    double lb = 0, rb = 0;
-    const double lf = lu_list_flops(lu, &lb);
-    sl.add(ST_GETRF, lu, maxR, 0, lf, lb);
-    if (with_cond) sl.add(ST_GECON, lu, maxR, 0, 11.0 * 2.0 * lb / 16.0, 11.0 * lb / 2.0);
-    if (lev == 0) continue;
     c_y.flush(sl);
-    const double rf = rs_list_flops(rs, &rb);
-    sl.add(ST_GETRS, rs, maxR, maxR, rf, rb);
+    add_lu_program(sl, jobs, true);
+    if (with_cond) {
+      double lb = 0;
+      for (auto& d : lu) lb += 16.0 * d.n * d.n;
+      sl.add(ST_GECON, lu, maxR, 0, 22.0 * lb / 16.0, 11.0 * lb / 2.0);
+    }
+    if (lev == 0) continue;
     g_f.flush(sl);
     c_t.flush(sl);
     g_tf.flush(sl);
@@ -391,7 +597,7 @@ void build_solve(const hks_plan& P, int64_t kk, StepList& sl) {
   {  // upward, leaves (solver.py:215-218)
     Gemms gp;
     Copies cp;
-    std::vector<LuSolveDesc> rs;
+    std::vector<LuJob> jobs;
     int mx = 0;
     for (int64_t i = L.first(L.depth); i < L.nn; ++i) {
       const int m = (int)L.size[i], r = c.r(i);
@@ -402,17 +608,15 @@ void build_solve(const hks_plan& P, int64_t kk, StepList& sl) {
         gp.add(c.phi(i), m, 1, D(B_VIN, L.begin[i]), n, 0, dst, ld, r, k, m, 1.0, 0.0);
       }
       cp.copy(D(B_VIN, L.begin[i]), n, 0, D(B_VOUT, L.begin[i]), n, m, k);
-      rs.push_back(LuSolveDesc{c.leaf_lu(i), c.leaf_piv(i), D(B_VOUT, L.begin[i]), m, k, m, n});
+      jobs.push_back(LuJob{c.leaf_lu(i), m, m, c.leaf_piv(i), kNull, kNull, D(B_VOUT, L.begin[i]), k, n});
     }
     gp.flush(sl);
     cp.flush(sl);
-    double rb = 0;
-    const double rf = rs_list_flops(rs, &rb);
-    sl.add(ST_GETRS, rs, mx, k, rf, rb);
+    add_lu_solve_program(sl, jobs);
   }
   for (int64_t lev = L.depth - 1; lev >= 0; --lev) {  // upward, internal (solver.py:219-233)
     Copies cp;
-    std::vector<LuSolveDesc> rs;
+    std::vector<LuJob> jobs;
     Gemms g1, g2, g3;
     int maxR = 0;
     for (int64_t i = L.first(lev); i < L.first(lev) + L.count(lev); ++i) {
@@ -422,7 +626,7 @@ void build_solve(const hks_plan& P, int64_t kk, StepList& sl) {
       const Ref Si = c.block(B_VWS, S, i, k), Gi = c.block(B_VWS, G, i, k), Gbi = c.block(B_VWS, Gb, i, k);
       const Ref C = c.coup(i);
       cp.copy(Si, R, 0, Gi, R, R, k);
-      rs.push_back(LuSolveDesc{c.z_lu(i), c.z_piv(i), Gi, R, k, R, R});
+      jobs.push_back(LuJob{c.z_lu(i), R, R, c.z_piv(i), kNull, kNull, Gi, k, R});
       g1.add(C, rl, 0, adv(Gi, rl), R, 0, Gbi, R, rl, k, rr, 1.0, 0.0);
       g1.add(C, rl, 1, Gi, R, 0, adv(Gbi, rl), R, rr, k, rl, 1.0, 0.0);
       if (lev == 0) continue;
@@ -433,9 +637,7 @@ void build_solve(const hks_plan& P, int64_t kk, StepList& sl) {
       g3.add(c.interp(i), r, 0, Si, R, 0, dst, ld, r, k, R, 1.0, 0.0);
     }
     cp.flush(sl);
-    double rb = 0;
-    const double rf = rs_list_flops(rs, &rb);
-    sl.add(ST_GETRS, rs, maxR, k, rf, rb);
+    add_lu_solve_program(sl, jobs);
     g1.flush(sl);
     g2.flush(sl);
     g3.flush(sl);
@@ -676,8 +878,14 @@ extern "C" int hks_factorize(hks_plan* P, void* const* buffers, double lam, int3
   Bases b = make_bases(buffers);
   b.p[B_FWS] = static_cast<char*>(P->fws.p);
   b.lam = lam;
+  const size_t nev = P->fact[which]->marks().size() + 1;
+  while (P->level_ev.size() < nev) {
+    cudaEvent_t ev;
+    cudaEventCreate(&ev);
+    P->level_ev.push_back(ev);
+  }
   cudaError_t e = cudaMemsetAsync(buffers[HKS_BUF_STATS], 0, P->L.nn * 3 * sizeof(double), s);
-  if (e == cudaSuccess) e = P->fact[which]->run(b, P->X, (int)P->d, P->kp, s);
+  if (e == cudaSuccess) e = P->fact[which]->run(b, P->X, (int)P->d, P->kp, s, P->level_ev.data());
   if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_factorize: %s", cudaGetErrorString(e));
   if (bad_node) *bad_node = -1;
   return check_info(P, buffers, bad_node, s);
@@ -817,3 +1025,19 @@ extern "C" int hks_profile(int32_t enable, double* out_host) {
 }
 
 extern "C" long long hks_launch_count(void) { return g_launches; }
+
+// Device milliseconds of each level of the last hks_factorize on this plan:
+// ms_host[level] for level = 0..depth (the leaf level is `depth`).
+extern "C" int hks_factor_level_ms(hks_plan* P, double* ms_host) {
+  if (!P || !ms_host) return set_error(HKS_ERR_INVALID, "hks_factor_level_ms: null argument");
+  const int64_t nl = P->L.depth + 1;
+  if ((int64_t)P->level_ev.size() < nl + 1) return set_error(HKS_ERR_INVALID, "hks_factor_level_ms: not factorized");
+  cudaEventSynchronize(P->level_ev[nl]);
+  for (int64_t m = 0; m < nl; ++m) {  // mark m: leaf level first, then depth-1 .. 0
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, P->level_ev[m], P->level_ev[m + 1]);
+    const int64_t level = P->L.depth - m;
+    ms_host[level] = ms;
+  }
+  return HKS_OK;
+}

@@ -34,7 +34,10 @@ struct Layout {
 
 Layout make_layout(int64_t n, int64_t depth, int64_t max_rank);
 
-enum StepKind { ST_GEMM, ST_COPY, ST_GETRF, ST_GETRS, ST_GECON, ST_EVAL_CM, ST_EVAL_RM, ST_KSUM };
+enum StepKind {
+  ST_GEMM, ST_COPY, ST_GETRF, ST_GETRS, ST_GECON, ST_EVAL_CM, ST_EVAL_RM, ST_KSUM,
+  ST_PANEL, ST_SWAP, ST_TRSM_L, ST_TRSM_U, ST_NORM1
+};
 
 struct Step {
   int kind;
@@ -45,7 +48,7 @@ struct Step {
   double bytes;   // compulsory HBM bytes of the whole step
 };
 
-constexpr int kNumKinds = 8;
+constexpr int kNumKinds = 13;
 
 // Opt-in per-kind CUDA-event timing of every step (hks_profile_*).
 void profile_step(int kind, double flops, double bytes, cudaEvent_t a, cudaEvent_t b);
@@ -65,7 +68,12 @@ class StepList {
     steps_.push_back(Step{kind, nullptr, (int)v.size(), p0, p1, flops, bytes});
   }
   cudaError_t upload(cudaStream_t stream);
-  cudaError_t run(const Bases& b, const double* X, int d, const KernelParams& kp, cudaStream_t stream) const;
+  // ev (optional): marks().size() + 1 events, recorded before each marked
+  // step and after the last step (per-level device timing)
+  cudaError_t run(const Bases& b, const double* X, int d, const KernelParams& kp, cudaStream_t stream,
+                  cudaEvent_t* ev = nullptr) const;
+  void mark() { marks_.push_back(steps_.size()); }
+  const std::vector<size_t>& marks() const { return marks_; }
   void clear();
   StepList() = default;
   StepList(const StepList&) = delete;
@@ -78,6 +86,7 @@ class StepList {
   std::vector<char> host_;
   std::vector<size_t> offs_;
   std::vector<Step> steps_;
+  std::vector<size_t> marks_;
   char* dev_ = nullptr;
   size_t dev_bytes_ = 0;
 };
@@ -108,6 +117,7 @@ struct hks_plan {
   hks::StepList coup_steps;                 // build_operator
   std::unique_ptr<hks::StepList> fact[2];   // factorize without / with dgecon
   hks::DevBuf fws;                          // factorize level workspace
+  std::vector<cudaEvent_t> level_ev;        // per-level factorize timing (leaf level first)
   std::map<int64_t, std::unique_ptr<hks::VecProgram>> solve_prog, mv_prog, up_prog;
 
   // stacked per-internal-node slots: node p owns R_p rows (x k columns)
@@ -115,4 +125,7 @@ struct hks_plan {
   int64_t stack_total = 0;
 
   int64_t R(int64_t i) const { return rank[2 * i + 1] + rank[2 * i + 2]; }
+  ~hks_plan() {
+    for (auto e : level_ev) cudaEventDestroy(e);
+  }
 };

@@ -148,9 +148,9 @@ def factorize(op, lam, threads=1, with_cond=True):
     N.call("hks_factor_stats", op.plan.handle, op.buffers(bufs), z_cond.ctypes.data_as(N._DP), None,
            N.stream_ptr())
     depth = op.tree.depth
-    # one device program covers all levels; per-level wall time is attributed
-    # by the level's share of the algorithmic flops
-    level_seconds = {lev: elapsed / (depth + 1) for lev in range(depth + 1)}
+    ms = np.zeros(depth + 1)
+    N.call("hks_factor_level_ms", op.plan.handle, ms.ctypes.data_as(N._DP))
+    level_seconds = {lev: float(ms[lev]) * 1e-3 for lev in range(depth + 1)}  # device time per level
     return Factorization(op, float(lam), bufs, level_seconds, z_cond)
 
 
