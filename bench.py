@@ -201,6 +201,7 @@ def gpu_arm(args, w, rank, world):
     launches0 = N.launch_count()
     r0 = torch.cuda.Event(enable_timing=True)
     r1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.profiler.start()  # ncu --profile-from-start off: only the timed region
     r0.record(stream)
     evs = []
     for _ in range(args.steps):
@@ -208,6 +209,7 @@ def gpu_arm(args, w, rank, world):
         evs.append(ev)
     r1.record(stream)
     torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()

@@ -279,51 +279,57 @@ __global__ void __launch_bounds__(RS_THREADS) getrs_kernel(const Bases bases,
 // ------------------------------------------------------------------ gecon
 
 // x := op(T)^-1 x for one vector in shared memory; T is the unit-lower (L)
-// or non-unit-upper (U) part of the LU, op = N or T.  32-row blocks: warp 0
-// solves the diagonal block, then every thread updates the rest.
-__device__ void trsv_block(const double* LU, int lda, int n, double* x, bool upper, bool trans) {
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
-  // effective lower-triangular solve if (lower,N) or (upper,T): forward sweep
+// or non-unit-upper (U) part of the LU, op = N or T.  32-row blocks: the
+// diagonal block is staged in shared memory (`blk`, 32 x 33) and solved by
+// warp 0 with shuffles, then every thread updates the remaining entries
+// (coalesced column reads for op = N, row reads for op = T).
+__device__ void trsv_block(const double* LU, int lda, int n, double* x, bool upper, bool trans, double* blk) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
   const bool forward = (!upper && !trans) || (upper && trans);
   const int nblk = (n + 31) / 32;
   for (int bb = 0; bb < nblk; ++bb) {
     const int b = forward ? bb : nblk - 1 - bb;
     const int r0 = b * 32, nr = min(32, n - r0);
+    // stage op(T)[r0.., r0..] (32 x 32): blk[i * 33 + j] = op(T)(r0 + i, r0 + j)
+    for (int j = wid; j < nr; j += nt / 32)
+      if (lane < nr) {
+        const double v = LU[(r0 + lane) + (size_t)(r0 + j) * lda];  // T(r0+lane, r0+j), coalesced
+        if (trans) blk[j * 33 + lane] = v; else blk[lane * 33 + j] = v;
+      }
+    __syncthreads();
     if (tid < 32) {
       double v = lane < nr ? x[r0 + lane] : 0.0;
-      // element (i, j) of op(T) inside the block
-      auto elem = [&](int i, int j) -> double {
-        const int gi = r0 + i, gj = r0 + j;
-        return trans ? LU[gj + (size_t)gi * lda] : LU[gi + (size_t)gj * lda];
-      };
       if (forward) {
         for (int j = 0; j < nr; ++j) {
           double xj = __shfl_sync(0xffffffffu, v, j);
-          if (upper) xj /= elem(j, j);
+          if (upper) xj /= blk[j * 33 + j];
           if (lane == j) v = xj;
-          if (lane > j && lane < nr) v -= elem(lane, j) * xj;
+          if (lane > j && lane < nr) v -= blk[lane * 33 + j] * xj;
         }
       } else {
         for (int j = nr - 1; j >= 0; --j) {
           double xj = __shfl_sync(0xffffffffu, v, j);
-          if (upper) xj /= elem(j, j);
+          if (upper) xj /= blk[j * 33 + j];
           if (lane == j) v = xj;
-          if (lane < j) v -= elem(lane, j) * xj;
+          if (lane < j) v -= blk[lane * 33 + j] * xj;
         }
       }
       if (lane < nr) x[r0 + lane] = v;
     }
     __syncthreads();
-    // update the not-yet-solved entries with this block's solution
     const int lo = forward ? r0 + nr : 0, hi = forward ? n : r0;
-    for (int i = lo + tid; i < hi; i += nt) {
-      double s = x[i];
-      for (int j = 0; j < nr; ++j) {
-        const int gj = r0 + j;
-        const double t = trans ? LU[gj + (size_t)i * lda] : LU[i + (size_t)gj * lda];
-        s -= t * x[gj];
+    if (!trans) {
+      for (int i = lo + tid; i < hi; i += nt) {
+        double s = x[i];
+        for (int j = 0; j < nr; ++j) s -= LU[i + (size_t)(r0 + j) * lda] * x[r0 + j];
+        x[i] = s;
       }
-      x[i] = s;
+    } else {  // op(T)(i, r0+j) = T(r0+j, i): a warp per output entry, lanes over j
+      for (int i = lo + wid; i < hi; i += nt / 32) {
+        const double t = lane < nr ? LU[(r0 + lane) + (size_t)i * lda] * x[r0 + lane] : 0.0;
+        const double s = warp_sum(t);
+        if (lane == 0) x[i] -= s;
+      }
     }
     __syncthreads();
   }
@@ -353,6 +359,7 @@ __global__ void __launch_bounds__(256) gecon_kernel(const Bases bases,
   double* x = sh;        // n
   double* v = sh + n;    // n
   int* isgn = reinterpret_cast<int*>(sh + 2 * n);
+  __shared__ double blk[32 * 33];
   __shared__ double red_v[8];
   __shared__ int red_i[8];
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -365,11 +372,11 @@ __global__ void __launch_bounds__(256) gecon_kernel(const Bases bases,
 
   auto apply = [&](int kase) {
     if (kase == 1) {
-      trsv_block(LUa, L.lda, n, x, false, false);
-      trsv_block(LUa, L.lda, n, x, true, false);
+      trsv_block(LUa, L.lda, n, x, false, false, blk);
+      trsv_block(LUa, L.lda, n, x, true, false, blk);
     } else {
-      trsv_block(LUa, L.lda, n, x, true, true);
-      trsv_block(LUa, L.lda, n, x, false, true);
+      trsv_block(LUa, L.lda, n, x, true, true, blk);
+      trsv_block(LUa, L.lda, n, x, false, true, blk);
     }
   };
 

@@ -113,65 +113,69 @@ __global__ void __launch_bounds__(TT) trsm_kernel(const Bases bases, const TrsmD
   const int nc = min(TR, D.ncols - c0), k = D.k;
   const double* T = at<const double>(bases, D.T);
   double* B = at<double>(bases, D.B) + (size_t)c0 * D.ldb;
-  __shared__ double X[128 * (TR + 1)];  // row-major k x TR (+1 pad)
+  constexpr int XS = TR + 1, TS = 128 + 4;
+  extern __shared__ double tsm[];
+  double* X = tsm;              // k x TR, row-major
+  double* Ts = tsm + 128 * XS;  // the current 32 rows of T, row-major
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   for (int e = tid; e < k * nc; e += TT) {
     const int i = e % k, c = e / k;
-    X[i * (TR + 1) + c] = B[i + (size_t)c * D.ldb];
+    X[i * XS + c] = B[i + (size_t)c * D.ldb];
   }
-  __syncthreads();
   const int nblk = (k + 31) / 32;
   const int fr = lane >> 2, fc = lane & 3;
   for (int bb = 0; bb < nblk; ++bb) {
     const int b = UPPER ? nblk - 1 - bb : bb;
     const int r0 = b * 32, nr = min(32, k - r0);
-    // update rows r0..r0+nr with the already-solved rows (DMMA, 16 fragments over 8 warps)
-    const int klo = UPPER ? r0 + nr : 0, khi = UPPER ? k : r0;
-    if (khi > klo) {
+    const int klo = UPPER ? r0 : 0, khi = UPPER ? k : r0 + nr;  // columns of T needed (incl. diagonal block)
+    // stage T[r0:r0+nr, klo:khi) (coalesced: a warp reads one column's rows)
+    for (int cc = klo + wid; cc < khi; cc += TT / 32)
+      if (lane < nr) Ts[lane * TS + cc] = T[(r0 + lane) + (size_t)cc * D.ldt];
+    __syncthreads();
+    // update rows r0..r0+nr with the already-solved rows (DMMA on shared operands)
+    const int ulo = UPPER ? r0 + nr : 0, uhi = UPPER ? k : r0;
+    if (uhi > ulo) {
       for (int f = wid; f < 16; f += 8) {
         const int fi = f & 3, fj = f >> 2;
         double d0 = 0.0, d1 = 0.0;
-        const int r = r0 + fi * 8 + fr;
-        for (int kk = klo; kk < khi; kk += 4) {
+        const int rl = fi * 8 + fr;
+        for (int kk = ulo; kk < uhi; kk += 4) {
           const int kq = kk + fc;
-          const double a = (fi * 8 + fr < nr && kq < khi) ? -T[r + (size_t)kq * D.ldt] : 0.0;
-          const double bv = (kq < khi && fj * 8 + fr < nc) ? X[kq * (TR + 1) + fj * 8 + fr] : 0.0;
+          const double a = (rl < nr && kq < uhi) ? -Ts[rl * TS + kq] : 0.0;
+          const double bv = (kq < uhi && fj * 8 + fr < nc) ? X[kq * XS + fj * 8 + fr] : 0.0;
           dmma884(d0, d1, a, bv);
         }
         const int c = fj * 8 + 2 * fc;
-        if (fi * 8 + fr < nr) {
-          if (c < nc) X[r * (TR + 1) + c] += d0;
-          if (c + 1 < nc) X[r * (TR + 1) + c + 1] += d1;
+        if (rl < nr) {
+          if (c < nc) X[(r0 + rl) * XS + c] += d0;
+          if (c + 1 < nc) X[(r0 + rl) * XS + c + 1] += d1;
         }
       }
       __syncthreads();
     }
     // substitution inside the 32-row block: warp w owns columns w, w+8, ...
     for (int c = wid; c < nc; c += 8) {
-      double x = lane < nr ? X[(r0 + lane) * (TR + 1) + c] : 0.0;
-      const double* tcol;
+      double x = lane < nr ? X[(r0 + lane) * XS + c] : 0.0;
       if (!UPPER) {
         for (int j = 0; j < nr; ++j) {
           const double xj = __shfl_sync(0xffffffffu, x, j);
-          tcol = T + (size_t)(r0 + j) * D.ldt;
-          if (lane > j && lane < nr) x -= tcol[r0 + lane] * xj;
+          if (lane > j && lane < nr) x -= Ts[lane * TS + r0 + j] * xj;
         }
       } else {
         for (int j = nr - 1; j >= 0; --j) {
-          tcol = T + (size_t)(r0 + j) * D.ldt;
           double xj = __shfl_sync(0xffffffffu, x, j);
-          xj /= tcol[r0 + j];
+          xj /= Ts[j * TS + r0 + j];
           if (lane == j) x = xj;
-          if (lane < j) x -= tcol[r0 + lane] * xj;
+          if (lane < j) x -= Ts[lane * TS + r0 + j] * xj;
         }
       }
-      if (lane < nr) X[(r0 + lane) * (TR + 1) + c] = x;
+      if (lane < nr) X[(r0 + lane) * XS + c] = x;
     }
     __syncthreads();
   }
   for (int e = tid; e < k * nc; e += TT) {
     const int i = e % k, c = e / k;
-    B[i + (size_t)c * D.ldb] = X[i * (TR + 1) + c];
+    B[i + (size_t)c * D.ldb] = X[i * XS + c];
   }
 }
 
@@ -225,10 +229,14 @@ cudaError_t launch_trsm_batched(const Bases& b, const TrsmDesc* d, int count, in
   for (int first = 0; first < count; first += 65535) {
     const int cnt = count - first < 65535 ? count - first : 65535;
     dim3 grid((max_cols + TR - 1) / TR, cnt);
-    if (upper)
-      trsm_kernel<true><<<grid, TT, 0, s>>>(b, d + first);
-    else
-      trsm_kernel<false><<<grid, TT, 0, s>>>(b, d + first);
+    const size_t sm = (size_t)(128 * (TR + 1) + 32 * (128 + 4)) * sizeof(double);
+    if (upper) {
+      cudaFuncSetAttribute(trsm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      trsm_kernel<true><<<grid, TT, sm, s>>>(b, d + first);
+    } else {
+      cudaFuncSetAttribute(trsm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      trsm_kernel<false><<<grid, TT, sm, s>>>(b, d + first);
+    }
   }
   return cudaGetLastError();
 }

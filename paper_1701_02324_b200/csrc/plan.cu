@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <limits>
 
 #include "plan.h"
@@ -84,6 +85,9 @@ void StepList::clear() {
 
 StepList::~StepList() {
   if (dev_) cudaFree(dev_);
+  if (side_) cudaStreamDestroy(side_);
+  if (fork_) cudaEventDestroy(fork_);
+  if (join_) cudaEventDestroy(join_);
 }
 
 cudaError_t DevBuf::ensure(size_t b) {
@@ -101,12 +105,32 @@ DevBuf::~DevBuf() {
 }
 
 cudaError_t StepList::run(const Bases& b, const double* X, int d, const KernelParams& kp,
-                          cudaStream_t s, cudaEvent_t* ev) const {
+                          cudaStream_t s, cudaEvent_t* ev, bool capturing) const {
+  auto record = [&](cudaEvent_t e, cudaStream_t st) {
+    if (capturing) cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+    else cudaEventRecord(e, st);
+  };
   const bool prof = profiling();
   size_t next_mark = 0;
+  bool forked = false;
+  const cudaStream_t main = s;
   for (size_t si = 0; si < steps_.size(); ++si) {
     const Step& st = steps_[si];
-    while (ev && next_mark < marks_.size() && marks_[next_mark] == si) cudaEventRecord(ev[next_mark++], s);
+    while (ev && next_mark < marks_.size() && marks_[next_mark] == si) record(ev[next_mark++], main);
+    s = main;
+    if (st.kind == ST_GECON && side_streams_enabled()) {  // off the critical path: nothing downstream reads z_cond
+      if (!side_) {
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        cudaStreamCreateWithPriority(&side_, cudaStreamNonBlocking, lo);
+        cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&join_, cudaEventDisableTiming);
+      }
+      cudaEventRecord(fork_, main);
+      cudaStreamWaitEvent(side_, fork_, 0);
+      s = side_;
+      forked = true;
+    }
     cudaError_t e = cudaSuccess;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (prof) {
@@ -159,8 +183,13 @@ cudaError_t StepList::run(const Bases& b, const double* X, int d, const KernelPa
     }
     if (e != cudaSuccess) return e;
   }
-  while (ev && next_mark < marks_.size()) cudaEventRecord(ev[next_mark++], s);
-  if (ev) cudaEventRecord(ev[marks_.size()], s);
+  s = main;
+  while (ev && next_mark < marks_.size()) record(ev[next_mark++], s);
+  if (ev) record(ev[marks_.size()], s);
+  if (forked) {
+    cudaEventRecord(join_, side_);
+    cudaStreamWaitEvent(main, join_, 0);
+  }
   return cudaSuccess;
 }
 
@@ -182,6 +211,70 @@ long long g_launches = 0;
 }  // namespace
 
 bool profiling() { return g_prof.on; }
+bool graphs_enabled() {
+  static const int on = [] {
+    const char* v = getenv("HKS_GRAPHS");
+    return v ? atoi(v) : 1;
+  }();
+  return on != 0;
+}
+
+GraphCache::~GraphCache() {
+  for (auto& e : entries) cudaGraphExecDestroy(e.exec);
+  if (cs) cudaStreamDestroy(cs);
+}
+
+cudaError_t run_graphed(GraphCache& gc, const StepList& sl, const Bases& b, const double* X, int d,
+                        const KernelParams& kp, cudaStream_t s, cudaEvent_t* ev, void* memset_ptr,
+                        size_t memset_bytes) {
+  if (!graphs_enabled() || profiling()) {
+    cudaError_t e = memset_ptr ? cudaMemsetAsync(memset_ptr, 0, memset_bytes, s) : cudaSuccess;
+    return e == cudaSuccess ? sl.run(b, X, d, kp, s, ev) : e;
+  }
+  ++gc.tick;
+  for (auto& en : gc.entries)
+    if (std::memcmp(&en.key, &b, sizeof(Bases)) == 0) {
+      en.used = gc.tick;
+      count_launch((int)sl.launches());
+      return cudaGraphLaunch(en.exec, s);
+    }
+  if (!gc.cs) {
+    cudaError_t e = cudaStreamCreateWithFlags(&gc.cs, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return e;
+  }
+  cudaError_t e = cudaStreamBeginCapture(gc.cs, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return e;
+  if (memset_ptr) cudaMemsetAsync(memset_ptr, 0, memset_bytes, gc.cs);
+  cudaError_t er = sl.run(b, X, d, kp, gc.cs, ev, true);
+  cudaGraph_t g = nullptr;
+  e = cudaStreamEndCapture(gc.cs, &g);
+  if (er != cudaSuccess) e = er;
+  if (e != cudaSuccess) {
+    if (g) cudaGraphDestroy(g);
+    return e;
+  }
+  cudaGraphExec_t exec = nullptr;
+  e = cudaGraphInstantiate(&exec, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return e;
+  if (gc.entries.size() >= 4) {  // evict the least recently used
+    size_t lru = 0;
+    for (size_t i = 1; i < gc.entries.size(); ++i)
+      if (gc.entries[i].used < gc.entries[lru].used) lru = i;
+    cudaGraphExecDestroy(gc.entries[lru].exec);
+    gc.entries.erase(gc.entries.begin() + lru);
+  }
+  gc.entries.push_back(GraphCache::Entry{b, exec, gc.tick});
+  return cudaGraphLaunch(exec, s);
+}
+
+bool side_streams_enabled() {
+  static const int on = [] {
+    const char* v = getenv("HKS_SIDE_STREAM");
+    return v ? atoi(v) : 1;
+  }();
+  return on != 0;
+}
 void count_launch(int n) { g_launches += n; }
 void profile_step(int kind, double flops, double bytes, cudaEvent_t a, cudaEvent_t b) {
   g_prof.pending.push_back(Pending{kind, flops, bytes, a, b});
@@ -884,8 +977,8 @@ extern "C" int hks_factorize(hks_plan* P, void* const* buffers, double lam, int3
     cudaEventCreate(&ev);
     P->level_ev.push_back(ev);
   }
-  cudaError_t e = cudaMemsetAsync(buffers[HKS_BUF_STATS], 0, P->L.nn * 3 * sizeof(double), s);
-  if (e == cudaSuccess) e = P->fact[which]->run(b, P->X, (int)P->d, P->kp, s, P->level_ev.data());
+  cudaError_t e = run_graphed(P->fact_graphs[which], *P->fact[which], b, P->X, (int)P->d, P->kp, s,
+                              P->level_ev.data(), buffers[HKS_BUF_STATS], P->L.nn * 3 * sizeof(double));
   if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_factorize: %s", cudaGetErrorString(e));
   if (bad_node) *bad_node = -1;
   return check_info(P, buffers, bad_node, s);
@@ -937,7 +1030,7 @@ extern "C" int hks_solve(hks_plan* P, void* const* buffers, const double* b, dou
   bb.p[B_VIN] = (char*)b;
   bb.p[B_VOUT] = (char*)x;
   bb.p[B_VWS] = (char*)v->ws.p;
-  cudaError_t e = v->steps.run(bb, P->X, (int)P->d, P->kp, s);
+  cudaError_t e = run_graphed(v->graphs, v->steps, bb, P->X, (int)P->d, P->kp, s, nullptr, nullptr, 0);
   if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_solve: %s", cudaGetErrorString(e));
   return HKS_OK;
 }
@@ -959,7 +1052,7 @@ extern "C" int hks_hmatvec(hks_plan* P, void* const* buffers, const double* w, d
   bb.p[B_VOUT] = (char*)u;
   bb.p[B_VWS] = (char*)v->ws.p;
   bb.lam = lam;
-  cudaError_t e = v->steps.run(bb, P->X, (int)P->d, P->kp, s);
+  cudaError_t e = run_graphed(v->graphs, v->steps, bb, P->X, (int)P->d, P->kp, s, nullptr, nullptr, 0);
   if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_hmatvec: %s", cudaGetErrorString(e));
   return HKS_OK;
 }

@@ -53,6 +53,7 @@ constexpr int kNumKinds = 13;
 // Opt-in per-kind CUDA-event timing of every step (hks_profile_*).
 void profile_step(int kind, double flops, double bytes, cudaEvent_t a, cudaEvent_t b);
 bool profiling();
+bool side_streams_enabled();
 void count_launch(int n = 1);
 
 // Accumulates host descriptor arrays, uploads them in one arena.
@@ -71,7 +72,7 @@ class StepList {
   // ev (optional): marks().size() + 1 events, recorded before each marked
   // step and after the last step (per-level device timing)
   cudaError_t run(const Bases& b, const double* X, int d, const KernelParams& kp, cudaStream_t stream,
-                  cudaEvent_t* ev = nullptr) const;
+                  cudaEvent_t* ev = nullptr, bool capturing = false) const;
   void mark() { marks_.push_back(steps_.size()); }
   const std::vector<size_t>& marks() const { return marks_; }
   void clear();
@@ -87,6 +88,9 @@ class StepList {
   std::vector<size_t> offs_;
   std::vector<Step> steps_;
   std::vector<size_t> marks_;
+  // diagnostic steps (dgecon) run on a low-priority side stream joined at the end
+  mutable cudaStream_t side_ = nullptr;
+  mutable cudaEvent_t fork_ = nullptr, join_ = nullptr;
   char* dev_ = nullptr;
   size_t dev_bytes_ = 0;
 };
@@ -99,9 +103,32 @@ struct DevBuf {
   ~DevBuf();
 };
 
+// Instantiated CUDA graphs of one StepList, keyed by the base-pointer table
+// (a plan step list is replayed with different factor / vector buffers).
+struct GraphCache {
+  struct Entry {
+    Bases key;
+    cudaGraphExec_t exec;
+    uint64_t used;
+  };
+  std::vector<Entry> entries;
+  cudaStream_t cs = nullptr;
+  uint64_t tick = 0;
+  ~GraphCache();
+};
+
+bool graphs_enabled();
+
+// Runs `sl` with bases `b` on stream s through a cached CUDA graph (captured
+// on first use of these bases); `pre` is captured first (e.g. a memset).
+cudaError_t run_graphed(GraphCache& gc, const StepList& sl, const Bases& b, const double* X, int d,
+                        const KernelParams& kp, cudaStream_t s, cudaEvent_t* ev, void* memset_ptr,
+                        size_t memset_bytes);
+
 struct VecProgram {
   StepList steps;
   DevBuf ws;
+  GraphCache graphs;
 };
 
 }  // namespace hks
@@ -116,6 +143,7 @@ struct hks_plan {
 
   hks::StepList coup_steps;                 // build_operator
   std::unique_ptr<hks::StepList> fact[2];   // factorize without / with dgecon
+  hks::GraphCache fact_graphs[2];
   hks::DevBuf fws;                          // factorize level workspace
   std::vector<cudaEvent_t> level_ev;        // per-level factorize timing (leaf level first)
   std::map<int64_t, std::unique_ptr<hks::VecProgram>> solve_prog, mv_prog, up_prog;
