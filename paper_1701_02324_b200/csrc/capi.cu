@@ -27,6 +27,12 @@ static cudaError_t one_desc(const D& h, D** d, cudaStream_t s) {
   return cudaMemcpyAsync(*d, &h, sizeof(D), cudaMemcpyHostToDevice, s);
 }
 
+cudaError_t upload_bases(const Bases& b, Bases** dev, cudaStream_t s) {
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(dev), sizeof(Bases), s);
+  if (e != cudaSuccess) return e;
+  return cudaMemcpyAsync(*dev, &b, sizeof(Bases), cudaMemcpyHostToDevice, s);
+}
+
 }  // namespace hks
 
 using namespace hks;
@@ -56,10 +62,13 @@ extern "C" int hks_eval_block(const double* X, int64_t d, const hks_kernel* kern
   Bases b{};
   b.lam = diag;
   EvalDesc* dd = nullptr;
+  Bases* db = nullptr;
   cudaError_t e = one_desc(h, &dd, s);
+  if (e == cudaSuccess) e = upload_bases(b, &db, s);
   if (e == cudaSuccess)
-    e = launch_eval_batched(X, (int)d, make_kernel_params(kern), b, dd, 1, (int)nrows, (int)ncols, row_major != 0, s);
+    e = launch_eval_batched(X, (int)d, make_kernel_params(kern), db, dd, 1, (int)nrows, (int)ncols, row_major != 0, s);
   if (dd) cudaFreeAsync(dd, s);
+  if (db) cudaFreeAsync(db, s);
   if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_eval_block: %s", cudaGetErrorString(e));
   return HKS_OK;
 }
@@ -77,9 +86,12 @@ extern "C" int hks_kernel_sum(const double* X, int64_t d, const hks_kernel* kern
   Bases b{};
   b.lam = diag;
   SumDesc* dd = nullptr;
+  Bases* db = nullptr;
   cudaError_t e = one_desc(h, &dd, s);
-  if (e == cudaSuccess) e = launch_ksum_batched(X, (int)d, make_kernel_params(kern), b, dd, 1, (int)nrows, s);
+  if (e == cudaSuccess) e = upload_bases(b, &db, s);
+  if (e == cudaSuccess) e = launch_ksum_batched(X, (int)d, make_kernel_params(kern), db, dd, 1, (int)nrows, s);
   if (dd) cudaFreeAsync(dd, s);
+  if (db) cudaFreeAsync(db, s);
   if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_kernel_sum: %s", cudaGetErrorString(e));
   return HKS_OK;
 }
@@ -96,8 +108,11 @@ extern "C" int hks_lu_factor(double* A, int64_t n, int64_t lda, int32_t* piv, in
   LuDesc h{abs_ref(A), abs_ref(piv), abs_ref(dinfo), kNull, kNull, (int)n, (int)lda};
   Bases b{};
   LuDesc* dd = nullptr;
+  Bases* db = nullptr;
   if (e == cudaSuccess) e = one_desc(h, &dd, s);
-  if (e == cudaSuccess) e = launch_getrf_batched(b, dd, 1, (int)n, s);
+  if (e == cudaSuccess) e = upload_bases(b, &db, s);
+  if (e == cudaSuccess) e = launch_getrf_batched(db, dd, 1, (int)n, s);
+  if (db) cudaFreeAsync(db, s);
   int info = 0;
   if (e == cudaSuccess) e = cudaMemcpyAsync(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost, s);
   if (dd) cudaFreeAsync(dd, s);
@@ -117,9 +132,12 @@ extern "C" int hks_lu_solve(const double* LU, const int32_t* piv, int64_t n, int
   LuSolveDesc h{abs_ref(LU), abs_ref(piv), abs_ref(B), (int)n, (int)nrhs, (int)lda, (int)ldb};
   Bases b{};
   LuSolveDesc* dd = nullptr;
+  Bases* db = nullptr;
   cudaError_t e = one_desc(h, &dd, s);
-  if (e == cudaSuccess) e = launch_getrs_batched(b, dd, 1, (int)n, (int)nrhs, s);
+  if (e == cudaSuccess) e = upload_bases(b, &db, s);
+  if (e == cudaSuccess) e = launch_getrs_batched(db, dd, 1, (int)n, (int)nrhs, s);
   if (dd) cudaFreeAsync(dd, s);
+  if (db) cudaFreeAsync(db, s);
   if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_lu_solve: %s", cudaGetErrorString(e));
   return HKS_OK;
 }

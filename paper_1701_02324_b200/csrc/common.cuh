@@ -128,7 +128,8 @@ struct GemmDesc {
   double alpha, beta;
 };
 
-// dst = alpha * op(src) (m x n result); mode 0: copy, 1: alpha * I, 2: zero.
+// dst = alpha * op(src) (m x n result); mode 0: copy, 1: alpha * I, 2: zero,
+// 3: accumulate (dst += alpha * op(src)).
 struct CopyDesc {
   Ref src, dst;
   int m, n;

@@ -80,8 +80,9 @@ __device__ __forceinline__ void stage(const double* X, int d, const int64_t* row
 
 template <bool ROW_MAJOR>
 __global__ void __launch_bounds__(256) eval_kernel(const double* __restrict__ X, int d, KernelParams kp,
-                                                   const Bases bases,
+                                                   const Bases* __restrict__ bases_ptr,
                                                    const EvalDesc* __restrict__ descs, int tiles_n) {
+  const Bases& bases = *bases_ptr;
   const EvalDesc e = descs[blockIdx.y];
   const int64_t* erows = e.rows == kNull ? nullptr : at<const int64_t>(bases, e.rows);
   const int64_t* ecols = e.cols == kNull ? nullptr : at<const int64_t>(bases, e.cols);
@@ -140,8 +141,9 @@ __global__ void __launch_bounds__(256) eval_kernel(const double* __restrict__ X,
 constexpr int KC = 16;  // right-hand sides per pass
 
 __global__ void __launch_bounds__(256) ksum_kernel(const double* __restrict__ X, int d, KernelParams kp,
-                                                   const Bases bases,
+                                                   const Bases* __restrict__ bases_ptr,
                                                    const SumDesc* __restrict__ descs) {
+  const Bases& bases = *bases_ptr;
   const SumDesc s = descs[blockIdx.y];
   const int64_t* srows = s.rows == kNull ? nullptr : at<const int64_t>(bases, s.rows);
   const int64_t* scols = s.cols == kNull ? nullptr : at<const int64_t>(bases, s.cols);
@@ -213,7 +215,7 @@ __global__ void __launch_bounds__(256) ksum_kernel(const double* __restrict__ X,
 
 }  // namespace
 
-cudaError_t launch_eval_batched(const double* X, int d, KernelParams kp, const Bases& bases,
+cudaError_t launch_eval_batched(const double* X, int d, KernelParams kp, const Bases* bases,
                                 const EvalDesc* d_descs, int count, int max_m, int max_n, bool row_major,
                                       cudaStream_t stream) {
   if (count <= 0 || max_m <= 0 || max_n <= 0) return cudaSuccess;
@@ -229,7 +231,7 @@ cudaError_t launch_eval_batched(const double* X, int d, KernelParams kp, const B
   return cudaGetLastError();
 }
 
-cudaError_t launch_ksum_batched(const double* X, int d, KernelParams kp, const Bases& bases,
+cudaError_t launch_ksum_batched(const double* X, int d, KernelParams kp, const Bases* bases,
                                 const SumDesc* d_descs, int count, int max_m, cudaStream_t stream) {
   if (count <= 0 || max_m <= 0) return cudaSuccess;
   for (int first = 0; first < count; first += 65535) {

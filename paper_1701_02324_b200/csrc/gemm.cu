@@ -16,6 +16,7 @@ namespace {
 
 constexpr int BM = 64, BN = 64, BK = 16, KS = BK + 4;  // KS: smem row stride (bank spread)
 constexpr int THREADS = 128;
+constexpr int STAGES = 3;  // cp.async pipeline depth
 
 struct GemmOp {
   const double* A;
@@ -25,73 +26,66 @@ struct GemmOp {
   double alpha, beta;
 };
 
-__device__ __forceinline__ void load_tile_a(const GemmOp& g, int m0, int k0, double (&r)[8]) {
-  const int t = threadIdx.x;
-  if (!g.transA) {  // A(m,k) = A[m + k*lda], coalesced along m
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      int m = m0 + (t & 63), k = k0 + (t >> 6) + 2 * j;
-      r[j] = (m < g.m && k < g.k) ? __ldg(g.A + m + (size_t)k * g.lda) : 0.0;
-    }
-  } else {  // A(m,k) = A[k + m*lda], coalesced along k
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      int k = k0 + (t & 15), m = m0 + (t >> 4) + 8 * j;
-      r[j] = (m < g.m && k < g.k) ? __ldg(g.A + k + (size_t)m * g.lda) : 0.0;
-    }
-  }
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool pred) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(src), "r"(pred ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-__device__ __forceinline__ void store_tile_a(const GemmOp& g, double* As, const double (&r)[8]) {
+// Stage the A (64 x 16) and B (16 x 64) tiles of k-block k0 into shared
+// memory as As[m][k], Bs[n][k]; global reads are coalesced along whichever
+// index is contiguous, out-of-range elements are zero-filled.
+__device__ __forceinline__ void load_stage(const GemmOp& g, int m0, int n0, int k0, double* As, double* Bs) {
   const int t = threadIdx.x;
   if (!g.transA) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) As[(t & 63) * KS + (t >> 6) + 2 * j] = r[j];
+    for (int j = 0; j < 8; ++j) {
+      const int m = m0 + (t & 63), k = k0 + (t >> 6) + 2 * j;
+      const bool ok = m < g.m && k < g.k;
+      cp_async8(As + (t & 63) * KS + (t >> 6) + 2 * j, ok ? g.A + m + (size_t)k * g.lda : g.A, ok);
+    }
   } else {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) As[((t >> 4) + 8 * j) * KS + (t & 15)] = r[j];
-  }
-}
-
-__device__ __forceinline__ void load_tile_b(const GemmOp& g, int n0, int k0, double (&r)[8]) {
-  const int t = threadIdx.x;
-  if (!g.transB) {  // B(k,n) = B[k + n*ldb], coalesced along k
-#pragma unroll
     for (int j = 0; j < 8; ++j) {
-      int k = k0 + (t & 15), n = n0 + (t >> 4) + 8 * j;
-      r[j] = (n < g.n && k < g.k) ? __ldg(g.B + k + (size_t)n * g.ldb) : 0.0;
-    }
-  } else {  // B(k,n) = B[n + k*ldb], coalesced along n
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      int n = n0 + (t & 63), k = k0 + (t >> 6) + 2 * j;
-      r[j] = (n < g.n && k < g.k) ? __ldg(g.B + n + (size_t)k * g.ldb) : 0.0;
+      const int k = k0 + (t & 15), m = m0 + (t >> 4) + 8 * j;
+      const bool ok = m < g.m && k < g.k;
+      cp_async8(As + ((t >> 4) + 8 * j) * KS + (t & 15), ok ? g.A + k + (size_t)m * g.lda : g.A, ok);
     }
   }
-}
-
-__device__ __forceinline__ void store_tile_b(const GemmOp& g, double* Bs, const double (&r)[8]) {
-  const int t = threadIdx.x;
   if (!g.transB) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) Bs[((t >> 4) + 8 * j) * KS + (t & 15)] = r[j];
+    for (int j = 0; j < 8; ++j) {
+      const int k = k0 + (t & 15), n = n0 + (t >> 4) + 8 * j;
+      const bool ok = n < g.n && k < g.k;
+      cp_async8(Bs + ((t >> 4) + 8 * j) * KS + (t & 15), ok ? g.B + k + (size_t)n * g.ldb : g.B, ok);
+    }
   } else {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) Bs[(t & 63) * KS + (t >> 6) + 2 * j] = r[j];
+    for (int j = 0; j < 8; ++j) {
+      const int n = n0 + (t & 63), k = k0 + (t >> 6) + 2 * j;
+      const bool ok = n < g.n && k < g.k;
+      cp_async8(Bs + (t & 63) * KS + (t >> 6) + 2 * j, ok ? g.B + n + (size_t)k * g.ldb : g.B, ok);
+    }
   }
 }
 
-__global__ void __launch_bounds__(THREADS) gemm_batched_kernel(const Bases bases,
+__global__ void __launch_bounds__(THREADS) gemm_batched_kernel(const Bases* __restrict__ bases_ptr,
                                                                 const GemmDesc* __restrict__ descs,
                                                                 int tiles_n) {
+  const Bases& bases = *bases_ptr;
   const GemmDesc gd = descs[blockIdx.y];
   const GemmOp g{at<const double>(bases, gd.A), at<const double>(bases, gd.B), at<double>(bases, gd.C),
                  gd.m, gd.n, gd.k, gd.lda, gd.ldb, gd.ldc, gd.transA, gd.transB, gd.alpha, gd.beta};
   const int m0 = (blockIdx.x / tiles_n) * BM, n0 = (blockIdx.x % tiles_n) * BN;
   if (m0 >= g.m || n0 >= g.n) return;
 
-  __shared__ double As[BM * KS];
-  __shared__ double Bs[BN * KS];
+  extern __shared__ double gsm[];
+  double* As = gsm;                       // STAGES x BM x KS
+  double* Bs = gsm + STAGES * BM * KS;    // STAGES x BN x KS
 
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int wm = (wid >> 1) * 32, wn = (wid & 1) * 32;
@@ -103,33 +97,34 @@ __global__ void __launch_bounds__(THREADS) gemm_batched_kernel(const Bases bases
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  double ra[8], rb[8];
-  if (g.k > 0) {
-    load_tile_a(g, m0, 0, ra);
-    load_tile_b(g, n0, 0, rb);
+  const int nk = (g.k + BK - 1) / BK;
+#pragma unroll
+  for (int st = 0; st < STAGES - 1; ++st) {
+    if (st < nk) load_stage(g, m0, n0, st * BK, As + st * BM * KS, Bs + st * BN * KS);
+    cp_async_commit();
   }
-  for (int k0 = 0; k0 < g.k; k0 += BK) {
-    store_tile_a(g, As, ra);
-    store_tile_b(g, Bs, rb);
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<STAGES - 2>();
     __syncthreads();
-    if (k0 + BK < g.k) {
-      load_tile_a(g, m0, k0 + BK, ra);
-      load_tile_b(g, n0, k0 + BK, rb);
-    }
+    const int pf = kt + STAGES - 1;
+    if (pf < nk) load_stage(g, m0, n0, pf * BK, As + (pf % STAGES) * BM * KS, Bs + (pf % STAGES) * BN * KS);
+    cp_async_commit();
+    const double* as = As + (kt % STAGES) * BM * KS;
+    const double* bs = Bs + (kt % STAGES) * BN * KS;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       double a[4], b[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[(wm + i * 8 + fr) * KS + kk + fc];
+      for (int i = 0; i < 4; ++i) a[i] = as[(wm + i * 8 + fr) * KS + kk + fc];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[(wn + j * 8 + fr) * KS + kk + fc];
+      for (int j = 0; j < 4; ++j) b[j] = bs[(wn + j * 8 + fr) * KS + kk + fc];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
-    __syncthreads();
   }
+  cp_async_wait<0>();
 
   const double alpha = g.alpha, beta = g.beta;
 #pragma unroll
@@ -151,18 +146,20 @@ __global__ void __launch_bounds__(THREADS) gemm_batched_kernel(const Bases bases
   }
 }
 
-// dst = alpha * op(src) / alpha * I / 0, one descriptor per block row-set.
-__global__ void copy_batched_kernel(const Bases bases, const CopyDesc* __restrict__ descs) {
+// dst = alpha * op(src) / alpha * I / 0 / dst + alpha * op(src), one descriptor per block.
+__global__ void copy_batched_kernel(const Bases* __restrict__ bases_ptr, const CopyDesc* __restrict__ descs) {
+  const Bases& bases = *bases_ptr;
   const CopyDesc c = descs[blockIdx.y];
-  const double* src = c.mode == 0 ? at<const double>(bases, c.src) : nullptr;
+  const double* src = (c.mode == 0 || c.mode == 3) ? at<const double>(bases, c.src) : nullptr;
   double* dst = at<double>(bases, c.dst);
   const int total = c.m * c.n;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
     const int i = e % c.m, j = e / c.m;
     double v;
-    if (c.mode == 0) {
+    if (c.mode == 0 || c.mode == 3) {
       v = c.trans ? src[j + (size_t)i * c.lds] : src[i + (size_t)j * c.lds];
       v *= c.alpha;
+      if (c.mode == 3) v += dst[i + (size_t)j * c.ldd];
     } else {
       v = (c.mode == 1 && i == j) ? c.alpha : 0.0;
     }
@@ -172,19 +169,25 @@ __global__ void copy_batched_kernel(const Bases bases, const CopyDesc* __restric
 
 }  // namespace
 
-cudaError_t launch_gemm_batched(const Bases& bases, const GemmDesc* d_descs, int count, int max_m,
+cudaError_t launch_gemm_batched(const Bases* bases, const GemmDesc* d_descs, int count, int max_m,
                                 int max_n, cudaStream_t stream) {
   if (count <= 0 || max_m <= 0 || max_n <= 0) return cudaSuccess;
   const int tm = (max_m + BM - 1) / BM, tn = (max_n + BN - 1) / BN;
   for (int first = 0; first < count; first += 65535) {
     const int cnt = count - first < 65535 ? count - first : 65535;
     dim3 grid(tm * tn, cnt);
-    gemm_batched_kernel<<<grid, THREADS, 0, stream>>>(bases, d_descs + first, tn);
+    const size_t sm = (size_t)STAGES * (BM + BN) * KS * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(gemm_batched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      attr = true;
+    }
+    gemm_batched_kernel<<<grid, THREADS, sm, stream>>>(bases, d_descs + first, tn);
   }
   return cudaGetLastError();
 }
 
-cudaError_t launch_copy_batched(const Bases& bases, const CopyDesc* d_descs, int count, int max_elems,
+cudaError_t launch_copy_batched(const Bases* bases, const CopyDesc* d_descs, int count, int max_elems,
                                 cudaStream_t stream) {
   if (count <= 0 || max_elems <= 0) return cudaSuccess;
   int bx = (max_elems + 255) / 256;

@@ -10,25 +10,29 @@
 
 namespace hks {
 
+// Device copy of a base table for one-off launches (stream-ordered upload
+// from host memory; free with cudaFreeAsync).
+cudaError_t upload_bases(const Bases& b, Bases** dev, cudaStream_t s);
+
 // Records a thread-local error message (read back through hks_last_error)
 // and returns `code` so call sites can `return set_error(...)`.
 int set_error(int code, const char* fmt, ...);
 
-cudaError_t launch_gemm_batched(const Bases& bases, const GemmDesc* d_descs, int count, int max_m,
+cudaError_t launch_gemm_batched(const Bases* bases, const GemmDesc* d_descs, int count, int max_m,
                                 int max_n, cudaStream_t stream);
-cudaError_t launch_copy_batched(const Bases& bases, const CopyDesc* d_descs, int count, int max_elems,
+cudaError_t launch_copy_batched(const Bases* bases, const CopyDesc* d_descs, int count, int max_elems,
                                 cudaStream_t stream);
-cudaError_t launch_getrf_batched(const Bases& bases, const LuDesc* d_descs, int count, int max_n,
+cudaError_t launch_getrf_batched(const Bases* bases, const LuDesc* d_descs, int count, int max_n,
                                  cudaStream_t stream);
-cudaError_t launch_getrs_batched(const Bases& bases, const LuSolveDesc* d_descs, int count, int max_n,
+cudaError_t launch_getrs_batched(const Bases* bases, const LuSolveDesc* d_descs, int count, int max_n,
                                  int max_nrhs, cudaStream_t stream);
-cudaError_t launch_panel_batched(const Bases& b, const PanelDesc* d, int count, int max_rows, int pb,
+cudaError_t launch_panel_batched(const Bases* b, const PanelDesc* d, int count, int max_rows, int pb,
                                  cudaStream_t s);
-cudaError_t launch_swap_batched(const Bases& b, const SwapDesc* d, int count, int max_cols, cudaStream_t s);
-cudaError_t launch_trsm_batched(const Bases& b, const TrsmDesc* d, int count, int max_cols, bool upper,
+cudaError_t launch_swap_batched(const Bases* b, const SwapDesc* d, int count, int max_cols, cudaStream_t s);
+cudaError_t launch_trsm_batched(const Bases* b, const TrsmDesc* d, int count, int max_cols, bool upper,
                                 cudaStream_t s);
-cudaError_t launch_norm1_batched(const Bases& b, const LuDesc* d, int count, cudaStream_t s);
-cudaError_t launch_gecon_batched(const Bases& bases, const LuDesc* d_descs, int count, int max_n,
+cudaError_t launch_norm1_batched(const Bases* b, const LuDesc* d, int count, cudaStream_t s);
+cudaError_t launch_gecon_batched(const Bases* bases, const LuDesc* d_descs, int count, int max_n,
                                  cudaStream_t stream);
 
 // Kernel-block evaluation (K1/K2/K3).  Rows/cols are either explicit global
@@ -53,7 +57,7 @@ struct KernelParams {
 
 KernelParams make_kernel_params(const hks_kernel* k);
 
-cudaError_t launch_eval_batched(const double* X, int d, KernelParams kp, const Bases& bases,
+cudaError_t launch_eval_batched(const double* X, int d, KernelParams kp, const Bases* bases,
                                 const EvalDesc* d_descs, int count, int max_m, int max_n, bool row_major,
                                 cudaStream_t stream);
 
@@ -74,7 +78,7 @@ struct SumDesc {
   int diag;  // add Bases::lam * W (rows == cols ranges only)
 };
 
-cudaError_t launch_ksum_batched(const double* X, int d, KernelParams kp, const Bases& bases,
+cudaError_t launch_ksum_batched(const double* X, int d, KernelParams kp, const Bases* bases,
                                 const SumDesc* d_descs, int count, int max_m, cudaStream_t stream);
 
 }  // namespace hks

@@ -71,8 +71,9 @@ __device__ void trailing_update(double* A, int lda, const double* P, int ldp, in
 }
 
 template <int NB>
-__global__ void __launch_bounds__(LU_THREADS) getrf_kernel(const Bases bases,
+__global__ void __launch_bounds__(LU_THREADS) getrf_kernel(const Bases* __restrict__ bases_ptr,
                                                             const LuDesc* __restrict__ descs, int ldp) {
+  const Bases& bases = *bases_ptr;
   const LuDesc L = descs[blockIdx.x];
   const int n = L.n, lda = L.lda;
   double* A = at<double>(bases, L.A);
@@ -201,8 +202,9 @@ __device__ void block_rows_update(const double* M, int lda, double* X, int ldx, 
 }
 
 template <int RC>
-__global__ void __launch_bounds__(RS_THREADS) getrs_kernel(const Bases bases,
+__global__ void __launch_bounds__(RS_THREADS) getrs_kernel(const Bases* __restrict__ bases_ptr,
                                                              const LuSolveDesc* __restrict__ descs, int ldx) {
+  const Bases& bases = *bases_ptr;
   const LuSolveDesc S = descs[blockIdx.x];
   const int* spiv = at<const int>(bases, S.piv);
   double* SB = at<double>(bases, S.B);
@@ -350,8 +352,9 @@ __device__ int block_iamax(const double* x, int n, double* rv, int* ri) {
 // LAPACK dgecon(norm='1') with dlacn2 (Higham's estimator), restated; the
 // dlatrs overflow scaling is not needed at the conditioning the solver
 // admits (documented in DESIGN.md).
-__global__ void __launch_bounds__(256) gecon_kernel(const Bases bases,
+__global__ void __launch_bounds__(256) gecon_kernel(const Bases* __restrict__ bases_ptr,
                                                      const LuDesc* __restrict__ descs) {
+  const Bases& bases = *bases_ptr;
   const LuDesc L = descs[blockIdx.x];
   const double* LUa = at<const double>(bases, L.A);
   const int n = L.n;
@@ -451,7 +454,7 @@ __global__ void __launch_bounds__(256) gecon_kernel(const Bases bases,
 
 }  // namespace
 
-cudaError_t launch_getrf_batched(const Bases& b, const LuDesc* d, int count, int max_n, cudaStream_t s) {
+cudaError_t launch_getrf_batched(const Bases* b, const LuDesc* d, int count, int max_n, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
   const int ldp = max_n > 0 ? max_n : 1;
   if (max_n <= 640) {
@@ -471,7 +474,7 @@ cudaError_t launch_getrf_batched(const Bases& b, const LuDesc* d, int count, int
   return cudaGetLastError();
 }
 
-cudaError_t launch_getrs_batched(const Bases& b, const LuSolveDesc* d, int count, int max_n, int max_nrhs,
+cudaError_t launch_getrs_batched(const Bases* b, const LuSolveDesc* d, int count, int max_n, int max_nrhs,
                                  cudaStream_t s) {
   if (count <= 0 || max_n <= 0 || max_nrhs <= 0) return cudaSuccess;
   const int ldx = ((max_n + 15) / 16) * 16 + 4;
@@ -492,7 +495,7 @@ cudaError_t launch_getrs_batched(const Bases& b, const LuSolveDesc* d, int count
   return cudaGetLastError();
 }
 
-cudaError_t launch_gecon_batched(const Bases& b, const LuDesc* d, int count, int max_n, cudaStream_t s) {
+cudaError_t launch_gecon_batched(const Bases* b, const LuDesc* d, int count, int max_n, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
   const size_t sm = (size_t)(max_n > 0 ? max_n : 1) * (2 * sizeof(double) + sizeof(int));
   cudaFuncSetAttribute(gecon_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

@@ -25,7 +25,8 @@ constexpr int PT = 256;  // panel threads
 // (lowest row on ties, LAPACK idamax), swap inside the panel, scale by the
 // reciprocal (dgetf2), rank-1 update.  piv[p0 + jj] = global pivot row.
 template <int PB>
-__global__ void __launch_bounds__(PT) panel_kernel(const Bases bases, const PanelDesc* __restrict__ descs, int ldp) {
+__global__ void __launch_bounds__(PT) panel_kernel(const Bases* __restrict__ bases_ptr, const PanelDesc* __restrict__ descs, int ldp) {
+  const Bases& bases = *bases_ptr;
   const PanelDesc D = descs[blockIdx.x];
   double* A = at<double>(bases, D.A);
   int* piv = at<int>(bases, D.piv);
@@ -83,7 +84,8 @@ __global__ void __launch_bounds__(PT) panel_kernel(const Bases bases, const Pane
 }
 
 // Row interchanges piv[r0..r1) applied in order to columns [c0, c1).
-__global__ void swap_kernel(const Bases bases, const SwapDesc* __restrict__ descs) {
+__global__ void swap_kernel(const Bases* __restrict__ bases_ptr, const SwapDesc* __restrict__ descs) {
+  const Bases& bases = *bases_ptr;
   const SwapDesc D = descs[blockIdx.y];
   const int c = D.c0 + blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= D.c1) return;
@@ -106,7 +108,8 @@ constexpr int TR = 32;
 constexpr int TT = 256;
 
 template <bool UPPER>
-__global__ void __launch_bounds__(TT) trsm_kernel(const Bases bases, const TrsmDesc* __restrict__ descs) {
+__global__ void __launch_bounds__(TT) trsm_kernel(const Bases* __restrict__ bases_ptr, const TrsmDesc* __restrict__ descs) {
+  const Bases& bases = *bases_ptr;
   const TrsmDesc D = descs[blockIdx.y];
   const int c0 = blockIdx.x * TR;
   if (c0 >= D.ncols) return;
@@ -180,7 +183,8 @@ __global__ void __launch_bounds__(TT) trsm_kernel(const Bases bases, const TrsmD
 }
 
 // ||A||_1 (max column abs sum) of each n x n matrix, before factoring.
-__global__ void norm1_kernel(const Bases bases, const LuDesc* __restrict__ descs) {
+__global__ void norm1_kernel(const Bases* __restrict__ bases_ptr, const LuDesc* __restrict__ descs) {
+  const Bases& bases = *bases_ptr;
   const LuDesc L = descs[blockIdx.x];
   __shared__ double rv[8];
   __shared__ int ri[8];
@@ -198,7 +202,7 @@ __global__ void norm1_kernel(const Bases bases, const LuDesc* __restrict__ descs
 
 }  // namespace
 
-cudaError_t launch_panel_batched(const Bases& b, const PanelDesc* d, int count, int max_rows, int pb,
+cudaError_t launch_panel_batched(const Bases* b, const PanelDesc* d, int count, int max_rows, int pb,
                                  cudaStream_t s) {
   if (count <= 0 || max_rows <= 0) return cudaSuccess;
   const int ldp = max_rows;
@@ -214,7 +218,7 @@ cudaError_t launch_panel_batched(const Bases& b, const PanelDesc* d, int count, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_swap_batched(const Bases& b, const SwapDesc* d, int count, int max_cols, cudaStream_t s) {
+cudaError_t launch_swap_batched(const Bases* b, const SwapDesc* d, int count, int max_cols, cudaStream_t s) {
   if (count <= 0 || max_cols <= 0) return cudaSuccess;
   for (int first = 0; first < count; first += 65535) {
     const int cnt = count - first < 65535 ? count - first : 65535;
@@ -223,7 +227,7 @@ cudaError_t launch_swap_batched(const Bases& b, const SwapDesc* d, int count, in
   return cudaGetLastError();
 }
 
-cudaError_t launch_trsm_batched(const Bases& b, const TrsmDesc* d, int count, int max_cols, bool upper,
+cudaError_t launch_trsm_batched(const Bases* b, const TrsmDesc* d, int count, int max_cols, bool upper,
                                 cudaStream_t s) {
   if (count <= 0 || max_cols <= 0) return cudaSuccess;
   for (int first = 0; first < count; first += 65535) {
@@ -241,7 +245,7 @@ cudaError_t launch_trsm_batched(const Bases& b, const TrsmDesc* d, int count, in
   return cudaGetLastError();
 }
 
-cudaError_t launch_norm1_batched(const Bases& b, const LuDesc* d, int count, cudaStream_t s) {
+cudaError_t launch_norm1_batched(const Bases* b, const LuDesc* d, int count, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
   norm1_kernel<<<count, 256, 0, s>>>(b, d);
   return cudaGetLastError();

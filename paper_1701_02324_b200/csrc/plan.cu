@@ -104,7 +104,7 @@ DevBuf::~DevBuf() {
   if (p) cudaFree(p);
 }
 
-cudaError_t StepList::run(const Bases& b, const double* X, int d, const KernelParams& kp,
+cudaError_t StepList::run(const Bases* b, const double* X, int d, const KernelParams& kp,
                           cudaStream_t s, cudaEvent_t* ev, bool capturing) const {
   auto record = [&](cudaEvent_t e, cudaStream_t st) {
     if (capturing) cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
@@ -220,52 +220,62 @@ bool graphs_enabled() {
 }
 
 GraphCache::~GraphCache() {
-  for (auto& e : entries) cudaGraphExecDestroy(e.exec);
+  if (exec) cudaGraphExecDestroy(exec);
   if (cs) cudaStreamDestroy(cs);
+  for (auto& e : ring_ev)
+    if (e) cudaEventDestroy(e);
+  if (host) cudaFreeHost(host);
+  if (dev) cudaFree(dev);
+}
+
+cudaError_t GraphCache::write(const Bases& b, cudaStream_t s) {
+  if (!dev) {
+    cudaError_t e = cudaMalloc(&dev, sizeof(Bases));
+    if (e == cudaSuccess) e = cudaMallocHost(&host, kRing * sizeof(Bases));
+    for (int i = 0; i < kRing && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&ring_ev[i], cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  }
+  const int slot = next;
+  next = (next + 1) % kRing;
+  cudaError_t e = cudaEventSynchronize(ring_ev[slot]);  // the copy that last read this slot has run
+  if (e != cudaSuccess) return e;
+  host[slot] = b;
+  e = cudaMemcpyAsync(dev, host + slot, sizeof(Bases), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaEventRecord(ring_ev[slot], s);
+  return e;
 }
 
 cudaError_t run_graphed(GraphCache& gc, const StepList& sl, const Bases& b, const double* X, int d,
                         const KernelParams& kp, cudaStream_t s, cudaEvent_t* ev, void* memset_ptr,
-                        size_t memset_bytes) {
-  if (!graphs_enabled() || profiling()) {
-    cudaError_t e = memset_ptr ? cudaMemsetAsync(memset_ptr, 0, memset_bytes, s) : cudaSuccess;
-    return e == cudaSuccess ? sl.run(b, X, d, kp, s, ev) : e;
+                        size_t memset_bytes, bool allow_graph) {
+  cudaError_t e = gc.write(b, s);
+  if (e != cudaSuccess) return e;
+  if (!allow_graph || !graphs_enabled() || profiling()) {
+    e = memset_ptr ? cudaMemsetAsync(memset_ptr, 0, memset_bytes, s) : cudaSuccess;
+    return e == cudaSuccess ? sl.run(gc.dev, X, d, kp, s, ev) : e;
   }
-  ++gc.tick;
-  for (auto& en : gc.entries)
-    if (std::memcmp(&en.key, &b, sizeof(Bases)) == 0) {
-      en.used = gc.tick;
-      count_launch((int)sl.launches());
-      return cudaGraphLaunch(en.exec, s);
+  if (!gc.exec) {  // capture once: the graph reads its bases from gc.dev
+    if (!gc.cs) {
+      e = cudaStreamCreateWithFlags(&gc.cs, cudaStreamNonBlocking);
+      if (e != cudaSuccess) return e;
     }
-  if (!gc.cs) {
-    cudaError_t e = cudaStreamCreateWithFlags(&gc.cs, cudaStreamNonBlocking);
+    e = cudaStreamBeginCapture(gc.cs, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return e;
+    cudaError_t er = sl.run(gc.dev, X, d, kp, gc.cs, ev, true);
+    cudaGraph_t g = nullptr;
+    e = cudaStreamEndCapture(gc.cs, &g);
+    if (er != cudaSuccess) e = er;
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&gc.exec, g, 0);
+    if (g) cudaGraphDestroy(g);
+    if (e != cudaSuccess) return e;
+  } else {
+    count_launch((int)sl.launches());
+  }
+  if (memset_ptr) {
+    e = cudaMemsetAsync(memset_ptr, 0, memset_bytes, s);
     if (e != cudaSuccess) return e;
   }
-  cudaError_t e = cudaStreamBeginCapture(gc.cs, cudaStreamCaptureModeThreadLocal);
-  if (e != cudaSuccess) return e;
-  if (memset_ptr) cudaMemsetAsync(memset_ptr, 0, memset_bytes, gc.cs);
-  cudaError_t er = sl.run(b, X, d, kp, gc.cs, ev, true);
-  cudaGraph_t g = nullptr;
-  e = cudaStreamEndCapture(gc.cs, &g);
-  if (er != cudaSuccess) e = er;
-  if (e != cudaSuccess) {
-    if (g) cudaGraphDestroy(g);
-    return e;
-  }
-  cudaGraphExec_t exec = nullptr;
-  e = cudaGraphInstantiate(&exec, g, 0);
-  cudaGraphDestroy(g);
-  if (e != cudaSuccess) return e;
-  if (gc.entries.size() >= 4) {  // evict the least recently used
-    size_t lru = 0;
-    for (size_t i = 1; i < gc.entries.size(); ++i)
-      if (gc.entries[i].used < gc.entries[lru].used) lru = i;
-    cudaGraphExecDestroy(gc.entries[lru].exec);
-    gc.entries.erase(gc.entries.begin() + lru);
-  }
-  gc.entries.push_back(GraphCache::Entry{b, exec, gc.tick});
-  return cudaGraphLaunch(exec, s);
+  return cudaGraphLaunch(gc.exec, s);
 }
 
 bool side_streams_enabled() {
@@ -334,6 +344,12 @@ struct Copies {
     v.push_back(CopyDesc{src, dst, m, n, lds, ldd, trans, 0, 1.0});
     me = std::max(me, m * n);
   }
+  // dst += alpha * src (m x n)
+  void accumulate(Ref src, int lds, Ref dst, int ldd, int m, int n, double alpha) {
+    if (m <= 0 || n <= 0) return;
+    v.push_back(CopyDesc{src, dst, m, n, lds, ldd, 0, 3, alpha});
+    me = std::max(me, m * n);
+  }
   void fill(Ref dst, int ldd, int m, int n, bool identity) {
     if (m <= 0 || n <= 0) return;
     v.push_back(CopyDesc{kNull, dst, m, n, 0, ldd, 0, identity ? 1 : 2, 1.0});
@@ -341,7 +357,7 @@ struct Copies {
   }
   void flush(StepList& sl) {
     double bytes = 0;
-    for (auto& c : v) bytes += (c.mode == 0 ? 16.0 : 8.0) * c.m * c.n;
+    for (auto& c : v) bytes += (c.mode == 0 ? 16.0 : c.mode == 3 ? 24.0 : 8.0) * c.m * c.n;
     sl.add(ST_COPY, v, me, 0, 0.0, bytes);
     v.clear();
     me = 0;
@@ -582,7 +598,7 @@ size_t factorize_workspace(const hks_plan& P) {
     size_t lv = 0;
     for (int64_t i = P.L.first(lev); i < P.L.first(lev) + P.L.count(lev); ++i) {
       const int64_t R = P.R(i);
-      lv += 2 * R * R + P.rank[i] * R;
+      lv += 3 * R * P.rank[i];
     }
     need = std::max(need, lv);
   }
@@ -621,8 +637,12 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl) {
   }
   for (int64_t lev = L.depth - 1; lev >= 0; --lev) {  // internal levels (solver.py:139-161)
     sl.mark();
-    Copies c_id, c_y, c_t;
-    Gemms g_z, g_f, g_tf, g_w, g_out;
+    // Algebraically identical to solver.py:145-158 with the interpolation
+    // folded in before the reduced solve: V = thhat P^T (R x r), Y = Z^-1 V,
+    // F = B Y (= folded P^T), push = P^T - F, theta = P (V - thhat F).
+    // Solving for r instead of R right-hand sides halves the node's flops.
+    Copies c_id, c_t, c_p;
+    Gemms g_z, g_v, g_f, g_tf, g_out;
     std::vector<LuJob> jobs;
     std::vector<LuDesc> lu;
     int maxR = 0;
@@ -641,29 +661,31 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl) {
         continue;
       }
       const Ref Y = D(B_FWS, at);
-      at += (int64_t)R * R;
+      at += (int64_t)R * r;
       const Ref F = D(B_FWS, at);
-      at += (int64_t)R * R;
+      at += (int64_t)R * r;
       const Ref W = D(B_FWS, at);
-      at += (int64_t)r * R;
+      at += (int64_t)R * r;
       const Ref Pi = c.interp(i), pu = c.push(i);
-      add_theta_hat(c_y, c, i, Y);
-      jobs.push_back(LuJob{Z, R, R, c.z_piv(i), c.info(i), c.anorm(i), Y, R, R});  // Y = Z^-1 thhat
-      // folded F = B Z^-1 thhat (solver.py:86-89, 156)
-      g_f.add(C, rl, 0, adv(Y, rl), R, 0, F, R, rl, R, rr, 1.0, 0.0);
-      g_f.add(C, rl, 1, Y, R, 0, adv(F, rl), R, rr, R, rl, 1.0, 0.0);
-      // T = thhat - thhat F (reusing Y); push = P^T - F P^T (solver.py:157-158)
-      add_theta_hat(c_t, c, i, Y);
+      // V = thhat P^T into Y (the LU's right-hand sides) and into W
+      g_v.add(c.theta(a), rl, 0, Pi, r, 1, Y, R, rl, r, rl, 1.0, 0.0);
+      g_v.add(c.theta(b), rr, 0, adv(Pi, (int64_t)rl * r), r, 1, adv(Y, rl), R, rr, r, rr, 1.0, 0.0);
+      g_v.add(c.theta(a), rl, 0, Pi, r, 1, W, R, rl, r, rl, 1.0, 0.0);
+      g_v.add(c.theta(b), rr, 0, adv(Pi, (int64_t)rl * r), r, 1, adv(W, rl), R, rr, r, rr, 1.0, 0.0);
+      jobs.push_back(LuJob{Z, R, R, c.z_piv(i), c.info(i), c.anorm(i), Y, r, R});  // Y = Z^-1 V
+      // F = B Y (solver.py:86-89, 156); push = P^T - F (solver.py:158)
+      g_f.add(C, rl, 0, adv(Y, rl), R, 0, F, R, rl, r, rr, 1.0, 0.0);
+      g_f.add(C, rl, 1, Y, R, 0, adv(F, rl), R, rr, r, rl, 1.0, 0.0);
       c_t.copy(Pi, r, 1, pu, R, R, r);
-      g_tf.add(c.theta(a), rl, 0, F, R, 0, Y, R, rl, R, rl, -1.0, 1.0);
-      g_tf.add(c.theta(b), rr, 0, adv(F, rl), R, 0, adv(Y, rl), R, rr, R, rr, -1.0, 1.0);
-      g_w.add(Pi, r, 0, Y, R, 0, W, r, r, R, R, 1.0, 0.0);
-      g_out.add(W, r, 0, Pi, r, 1, c.theta(i), r, r, r, R, 1.0, 0.0);
-      g_out.add(F, R, 0, Pi, r, 1, pu, R, R, r, R, -1.0, 1.0);
+      c_p.accumulate(F, R, pu, R, R, r, -1.0);
+      // W = V - thhat F ; theta = P W (solver.py:157)
+      g_tf.add(c.theta(a), rl, 0, F, R, 0, W, R, rl, r, rl, -1.0, 1.0);
+      g_tf.add(c.theta(b), rr, 0, adv(F, rl), R, 0, adv(W, rl), R, rr, r, rr, -1.0, 1.0);
+      g_out.add(Pi, r, 0, W, R, 0, c.theta(i), r, r, r, R, 1.0, 0.0);
     }
     c_id.flush(sl);
     g_z.flush(sl);
-    c_y.flush(sl);
+    g_v.flush(sl);
     add_lu_program(sl, jobs, true);
     if (with_cond) {
       double lb = 0;
@@ -673,8 +695,8 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl) {
     if (lev == 0) continue;
     g_f.flush(sl);
     c_t.flush(sl);
+    c_p.flush(sl);
     g_tf.flush(sl);
-    g_w.flush(sl);
     g_out.flush(sl);
   }
 }
@@ -920,7 +942,8 @@ extern "C" int hks_build_operator(hks_plan* P, void* const* buffers, void* strea
     cudaError_t e = P->coup_steps.upload(s);
     if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_build_operator: %s", cudaGetErrorString(e));
   }
-  cudaError_t e = P->coup_steps.run(make_bases(buffers), P->X, (int)P->d, P->kp, s);
+  cudaError_t e = run_graphed(P->coup_exec, P->coup_steps, make_bases(buffers), P->X, (int)P->d, P->kp, s, nullptr,
+                              nullptr, 0, false);
   if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_build_operator: %s", cudaGetErrorString(e));
   return HKS_OK;
 }
@@ -1083,7 +1106,7 @@ extern "C" int hks_upward(hks_plan* P, void* const* buffers, const double* w, in
   Bases bb = make_bases(buffers);
   bb.p[B_VIN] = (char*)w;
   bb.p[B_VWS] = (char*)out;  // stacked slots written straight into the caller's buffer
-  cudaError_t e = v->steps.run(bb, P->X, (int)P->d, P->kp, s);
+  cudaError_t e = run_graphed(v->graphs, v->steps, bb, P->X, (int)P->d, P->kp, s, nullptr, nullptr, 0, false);
   if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_upward: %s", cudaGetErrorString(e));
   return HKS_OK;
 }

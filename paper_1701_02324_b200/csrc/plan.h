@@ -71,7 +71,7 @@ class StepList {
   cudaError_t upload(cudaStream_t stream);
   // ev (optional): marks().size() + 1 events, recorded before each marked
   // step and after the last step (per-level device timing)
-  cudaError_t run(const Bases& b, const double* X, int d, const KernelParams& kp, cudaStream_t stream,
+  cudaError_t run(const Bases* dev_b, const double* X, int d, const KernelParams& kp, cudaStream_t stream,
                   cudaEvent_t* ev = nullptr, bool capturing = false) const;
   void mark() { marks_.push_back(steps_.size()); }
   const std::vector<size_t>& marks() const { return marks_; }
@@ -103,27 +103,30 @@ struct DevBuf {
   ~DevBuf();
 };
 
-// Instantiated CUDA graphs of one StepList, keyed by the base-pointer table
-// (a plan step list is replayed with different factor / vector buffers).
+// Executable form of one StepList: a fixed device base table (the kernels
+// read their operand bases from it, so a captured graph stays valid while
+// the factor / vector buffers change between calls), a pinned ring that
+// feeds it, and the CUDA graph captured on first use.
 struct GraphCache {
-  struct Entry {
-    Bases key;
-    cudaGraphExec_t exec;
-    uint64_t used;
-  };
-  std::vector<Entry> entries;
+  static constexpr int kRing = 16;
+  Bases* dev = nullptr;
+  Bases* host = nullptr;
+  cudaEvent_t ring_ev[kRing] = {};
+  int next = 0;
+  cudaGraphExec_t exec = nullptr;
+  bool with_memset = false;
   cudaStream_t cs = nullptr;
-  uint64_t tick = 0;
+  cudaError_t write(const Bases& b, cudaStream_t s);
   ~GraphCache();
 };
 
 bool graphs_enabled();
 
-// Runs `sl` with bases `b` on stream s through a cached CUDA graph (captured
-// on first use of these bases); `pre` is captured first (e.g. a memset).
+// Runs `sl` with bases `b` on stream s (graph replay unless profiling or
+// HKS_GRAPHS=0); `memset_ptr` (if any) is zeroed first, inside the graph.
 cudaError_t run_graphed(GraphCache& gc, const StepList& sl, const Bases& b, const double* X, int d,
                         const KernelParams& kp, cudaStream_t s, cudaEvent_t* ev, void* memset_ptr,
-                        size_t memset_bytes);
+                        size_t memset_bytes, bool allow_graph = true);
 
 struct VecProgram {
   StepList steps;
@@ -142,6 +145,7 @@ struct hks_plan {
   hks_kernel kern{};
 
   hks::StepList coup_steps;                 // build_operator
+  hks::GraphCache coup_exec;
   std::unique_ptr<hks::StepList> fact[2];   // factorize without / with dgecon
   hks::GraphCache fact_graphs[2];
   hks::DevBuf fws;                          // factorize level workspace

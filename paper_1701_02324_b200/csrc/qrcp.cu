@@ -372,7 +372,10 @@ extern "C" int hks_skeletonize_level(const double* X, int64_t d, const hks_kerne
     EvalDesc* dev = nullptr;
     if (e == cudaSuccess && !ev.empty()) e = upload(ev, &dev, s);
     Bases b{};
-    if (e == cudaSuccess && !ev.empty()) e = launch_eval_batched(X, (int)d, kp, b, dev, (int)ev.size(), mm, mn, true, s);
+    Bases* db = nullptr;
+    if (e == cudaSuccess && !ev.empty()) e = upload_bases(b, &db, s);
+    if (e == cudaSuccess && !ev.empty()) e = launch_eval_batched(X, (int)d, kp, db, dev, (int)ev.size(), mm, mn, true, s);
+    if (db) cudaFreeAsync(db, s);
     std::vector<int64_t> ranks;
     if (e == cudaSuccess) e = run_qrcp(nodes, tau, P, cl, sk, ranks, s);
     if (dev) cudaFreeAsync(dev, s);

@@ -77,7 +77,7 @@ __device__ __forceinline__ unsigned blocked_bits(int64_t w, int64_t b, int64_t e
 __global__ void topup_kernel(unsigned* __restrict__ bm, int64_t words, int64_t n, const int64_t* __restrict__ beg,
                              const int64_t* __restrict__ sz, const int* __restrict__ nodes,
                              const int64_t* __restrict__ extra, const int64_t* __restrict__ eoff,
-                             int64_t* __restrict__ zpre_all) {
+                             int64_t* __restrict__ zpre_all, int64_t* __restrict__ posbuf) {
   const int j = nodes[blockIdx.x];
   unsigned* b = bm + (size_t)j * words;
   int64_t* zpre = zpre_all + (size_t)blockIdx.x * (words + 1);
@@ -91,6 +91,8 @@ __global__ void topup_kernel(unsigned* __restrict__ bm, int64_t words, int64_t n
     zpre[words] = acc;
   }
   __syncthreads();
+  // phase 1: map every draw against the ORIGINAL rest set (no bit is set
+  // yet, so concurrent draws cannot shift each other's ranks)
   for (int64_t t = eoff[blockIdx.x] + threadIdx.x; t < eoff[blockIdx.x + 1]; t += blockDim.x) {
     const int64_t r = extra[t];
     int64_t lo = 0, hi = words - 1;  // last word with zpre <= r
@@ -98,17 +100,25 @@ __global__ void topup_kernel(unsigned* __restrict__ bm, int64_t words, int64_t n
       const int64_t mid = (lo + hi + 1) >> 1;
       if (zpre[mid] <= r) lo = mid; else hi = mid - 1;
     }
-    unsigned freeb = ~(b[lo] | blocked_bits(lo, nb, ne, n));
+    const unsigned freeb = ~(b[lo] | blocked_bits(lo, nb, ne, n));
     int64_t k = r - zpre[lo];
+    int64_t pos = -1;
     for (int bit = 0; bit < 32; ++bit) {
       if (freeb & (1u << bit)) {
         if (k == 0) {
-          atomicOr(b + lo, 1u << bit);
+          pos = lo * 32 + bit;
           break;
         }
         --k;
       }
     }
+    posbuf[t] = pos;
+  }
+  __syncthreads();
+  // phase 2: add the drawn rows
+  for (int64_t t = eoff[blockIdx.x] + threadIdx.x; t < eoff[blockIdx.x + 1]; t += blockDim.x) {
+    const int64_t pos = posbuf[t];
+    if (pos >= 0) atomicOr(b + (pos >> 5), 1u << (pos & 31));
   }
 }
 
@@ -196,6 +206,7 @@ extern "C" int hks_knn_rows_fill(int64_t n, int64_t level, int64_t depth, int32_
   }
   cudaError_t e = cudaSuccess;
   int64_t *dbeg = nullptr, *dsz = nullptr, *deoff = nullptr, *dro = nullptr, *zpre = nullptr, *dextra = nullptr;
+  int64_t* dpos = nullptr;
   int* dnodes = nullptr;
   e = cudaMallocAsync(reinterpret_cast<void**>(&dro), (count + 1) * sizeof(int64_t), s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(dro, row_off_host, (count + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s);
@@ -209,6 +220,7 @@ extern "C" int hks_knn_rows_fill(int64_t n, int64_t level, int64_t depth, int32_
     if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&dnodes), nt * sizeof(int), s);
     if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&zpre), (size_t)nt * (words + 1) * sizeof(int64_t), s);
     if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&dextra), eoff.back() * sizeof(int64_t), s);
+    if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&dpos), eoff.back() * sizeof(int64_t), s);
     if (e == cudaSuccess) {
       cudaMemcpyAsync(dbeg, beg.data(), count * sizeof(int64_t), cudaMemcpyHostToDevice, s);
       cudaMemcpyAsync(dsz, sz.data(), count * sizeof(int64_t), cudaMemcpyHostToDevice, s);
@@ -220,14 +232,15 @@ extern "C" int hks_knn_rows_fill(int64_t n, int64_t level, int64_t depth, int32_
                         cudaMemcpyDeviceToDevice, s);
       }
       topup_kernel<<<nt, 256, 0, s>>>(reinterpret_cast<unsigned*>(bitmap), words, n, dbeg, dsz, dnodes, dextra,
-                                      deoff, zpre);
+                                      deoff, zpre, dpos);
     }
   }
   if (e == cudaSuccess) {
     compact_kernel<<<count, 1024, 0, s>>>(reinterpret_cast<unsigned*>(bitmap), words, dro, rows);
     e = cudaGetLastError();
   }
-  for (void* p : {(void*)dbeg, (void*)dsz, (void*)deoff, (void*)dro, (void*)zpre, (void*)dextra, (void*)dnodes})
+  for (void* p : {(void*)dbeg, (void*)dsz, (void*)deoff, (void*)dro, (void*)zpre, (void*)dextra, (void*)dnodes,
+                  (void*)dpos})
     if (p) cudaFreeAsync(p, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_knn_rows_fill: %s", cudaGetErrorString(e));
