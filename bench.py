@@ -45,6 +45,7 @@ def parse():
     p.add_argument("--cpu-sample-n", type=int, default=16384)
     p.add_argument("--cpu-steps", type=int, default=2)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-clocks", action="store_true", help="skip the nvidia-smi clock sampler (diagnostics)")
     return p.parse_args()
 
 
@@ -196,8 +197,8 @@ def gpu_arm(args, w, rank, world):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     clocks = ClockSampler(torch.cuda.current_device())
-    clocks.start()
-    N.profile(True)
+    if not args.no_clocks:
+        clocks.start()
     launches0 = N.launch_count()
     r0 = torch.cuda.Event(enable_timing=True)
     r1 = torch.cuda.Event(enable_timing=True)
@@ -214,8 +215,14 @@ def gpu_arm(args, w, rank, world):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     launches = N.launch_count() - launches0
-    kinds = N.profile(False)
     clk = clocks.stop()
+    # per-kernel CUDA-event breakdown: the same steps replayed once more with
+    # an event pair around every launch (graphs off while profiling)
+    N.profile(True)
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
+    kinds = N.profile(False)
     region_ms = r0.elapsed_time(r1)
     t_fact = [a.elapsed_time(bq) for a, bq, _ in evs]
     t_solve = [bq.elapsed_time(c) for _, bq, c in evs]

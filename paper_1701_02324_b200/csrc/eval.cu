@@ -68,13 +68,17 @@ __device__ __forceinline__ void accumulate16(const double* xa, const double* xb1
 __device__ __forceinline__ void stage(const double* X, int d, const int64_t* rows, int64_t row0,
                                       int m, int r0, const int64_t* cols, int64_t col0, int n,
                                       int c0, int k0, int dc, double* Xr, double* Xc) {
-  for (int e = threadIdx.x; e < TM * dc; e += blockDim.x) {
-    const int i = e / dc, k = e % dc;
-    Xr[i * XS + k] = (r0 + i < m) ? X[row_id(rows, row0, r0 + i) * d + k0 + k] : 0.0;
+  // one point per warp iteration, lanes over its (contiguous) coordinates
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = wid; i < TM; i += nw) {
+    const bool ok = r0 + i < m;
+    const double* src = ok ? X + row_id(rows, row0, r0 + i) * d + k0 : X;
+    for (int k = lane; k < dc; k += 32) Xr[i * XS + k] = ok ? src[k] : 0.0;
   }
-  for (int e = threadIdx.x; e < TN * dc; e += blockDim.x) {
-    const int j = e / dc, k = e % dc;
-    Xc[j * XS + k] = (c0 + j < n) ? X[row_id(cols, col0, c0 + j) * d + k0 + k] : 0.0;
+  for (int j = wid; j < TN; j += nw) {
+    const bool ok = c0 + j < n;
+    const double* src = ok ? X + row_id(cols, col0, c0 + j) * d + k0 : X;
+    for (int k = lane; k < dc; k += 32) Xc[j * XS + k] = ok ? src[k] : 0.0;
   }
 }
 

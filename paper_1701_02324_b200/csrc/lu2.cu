@@ -37,45 +37,44 @@ __global__ void __launch_bounds__(PT) panel_kernel(const Bases* __restrict__ bas
   __shared__ int s_info;
   const int tid = threadIdx.x;
   if (tid == 0) s_info = 0;
-  for (int e = tid; e < mr * pb; e += PT) {
-    const int i = e % mr, c = e / mr;
-    P[i + c * ldp] = A[(p0 + i) + (size_t)(p0 + c) * lda];
+  for (int c = 0; c < pb; ++c) {  // coalesced column loads, no div/mod
+    const double* src = A + p0 + (size_t)(p0 + c) * lda;
+    for (int i = tid; i < mr; i += PT) P[i + c * ldp] = src[i];
   }
   __syncthreads();
   for (int jj = 0; jj < pb; ++jj) {
     ArgMax a{-1.0, 0x7fffffff};
     for (int i = jj + tid; i < mr; i += PT) a = argmax_pick(a, ArgMax{fabs(P[i + jj * ldp]), i});
-    a = block_argmax(a, red_v, red_i);
+    a = block_argmax(a, red_v, red_i);  // ends with a barrier
     const int p = a.i;
     const double pv = P[p + jj * ldp];
-    __syncthreads();
     if (tid == 0) {
       piv[p0 + jj] = p0 + p;
       if (pv == 0.0 && s_info == 0) s_info = p0 + jj + 1;
     }
-    if (p != jj)
-      for (int c = tid; c < pb; c += PT) {
-        const double t = P[jj + c * ldp];
-        P[jj + c * ldp] = P[p + c * ldp];
-        P[p + c * ldp] = t;
-      }
-    __syncthreads();
-    if (pv != 0.0) {
-      const bool recip = fabs(pv) >= DBL_MIN;
-      const double inv = 1.0 / pv;
-      for (int i = jj + 1 + tid; i < mr; i += PT) P[i + jj * ldp] = recip ? P[i + jj * ldp] * inv : P[i + jj * ldp] / pv;
+    __syncthreads();  // every thread has read pv
+    if (p != jj && tid < pb) {  // interchange rows jj and p of the panel
+      const double t = P[jj + tid * ldp];
+      P[jj + tid * ldp] = P[p + tid * ldp];
+      P[p + tid * ldp] = t;
     }
     __syncthreads();
-    const int rr = mr - jj - 1, cc = pb - jj - 1;
-    for (int e = tid; e < rr * cc; e += PT) {
-      const int i = jj + 1 + e % rr, c = jj + 1 + e / rr;
-      P[i + c * ldp] -= P[i + jj * ldp] * P[jj + c * ldp];
+    // scale the column (dgetf2: reciprocal when safe) and rank-1 update, one row per thread
+    const bool recip = fabs(pv) >= DBL_MIN;
+    const double inv = 1.0 / pv;
+    for (int i = jj + 1 + tid; i < mr; i += PT) {
+      double l = P[i + jj * ldp];
+      if (pv != 0.0) {
+        l = recip ? l * inv : l / pv;
+        P[i + jj * ldp] = l;
+      }
+      for (int c = jj + 1; c < pb; ++c) P[i + c * ldp] -= l * P[jj + c * ldp];
     }
     __syncthreads();
   }
-  for (int e = tid; e < mr * pb; e += PT) {
-    const int i = e % mr, c = e / mr;
-    A[(p0 + i) + (size_t)(p0 + c) * lda] = P[i + c * ldp];
+  for (int c = 0; c < pb; ++c) {
+    double* dst = A + p0 + (size_t)(p0 + c) * lda;
+    for (int i = tid; i < mr; i += PT) dst[i] = P[i + c * ldp];
   }
   if (tid == 0 && s_info && D.info != kNull) {
     int* info = at<int>(bases, D.info);
@@ -116,7 +115,7 @@ __global__ void __launch_bounds__(TT) trsm_kernel(const Bases* __restrict__ base
   const int nc = min(TR, D.ncols - c0), k = D.k;
   const double* T = at<const double>(bases, D.T);
   double* B = at<double>(bases, D.B) + (size_t)c0 * D.ldb;
-  constexpr int XS = TR + 1, TS = 128 + 4;
+  constexpr int XS = TR + 4, TS = 128 + 4;  // both == 4 (mod 16): conflict-free DMMA fragments
   extern __shared__ double tsm[];
   double* X = tsm;              // k x TR, row-major
   double* Ts = tsm + 128 * XS;  // the current 32 rows of T, row-major
@@ -156,23 +155,33 @@ __global__ void __launch_bounds__(TT) trsm_kernel(const Bases* __restrict__ base
       }
       __syncthreads();
     }
-    // substitution inside the 32-row block: warp w owns columns w, w+8, ...
-    for (int c = wid; c < nc; c += 8) {
-      double x = lane < nr ? X[(r0 + lane) * XS + c] : 0.0;
-      if (!UPPER) {
-        for (int j = 0; j < nr; ++j) {
-          const double xj = __shfl_sync(0xffffffffu, x, j);
-          if (lane > j && lane < nr) x -= Ts[lane * TS + r0 + j] * xj;
+    // substitution inside the 32-row block: lane = row, the row of the
+    // diagonal block in registers; warp w owns columns w, w+8, ...
+    if (wid < nc) {
+      double t[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) t[j] = (lane < nr && j < nr) ? Ts[lane * TS + r0 + j] : 0.0;
+      for (int c = wid; c < nc; c += 8) {
+        double x = lane < nr ? X[(r0 + lane) * XS + c] : 0.0;
+        if (!UPPER) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const double xj = __shfl_sync(0xffffffffu, x, j);
+            if (lane > j) x -= t[j] * xj;
+          }
+        } else {
+#pragma unroll
+          for (int j = 31; j >= 0; --j) {
+            if (j < nr) {
+              double xj = __shfl_sync(0xffffffffu, x, j);
+              xj /= __shfl_sync(0xffffffffu, t[j], j);  // the diagonal entry U(j, j), held by lane j
+              if (lane == j) x = xj;
+              if (lane < j) x -= t[j] * xj;
+            }
+          }
         }
-      } else {
-        for (int j = nr - 1; j >= 0; --j) {
-          double xj = __shfl_sync(0xffffffffu, x, j);
-          xj /= Ts[j * TS + r0 + j];
-          if (lane == j) x = xj;
-          if (lane < j) x -= Ts[lane * TS + r0 + j] * xj;
-        }
+        if (lane < nr) X[(r0 + lane) * XS + c] = x;
       }
-      if (lane < nr) X[(r0 + lane) * XS + c] = x;
     }
     __syncthreads();
   }
@@ -233,7 +242,7 @@ cudaError_t launch_trsm_batched(const Bases* b, const TrsmDesc* d, int count, in
   for (int first = 0; first < count; first += 65535) {
     const int cnt = count - first < 65535 ? count - first : 65535;
     dim3 grid((max_cols + TR - 1) / TR, cnt);
-    const size_t sm = (size_t)(128 * (TR + 1) + 32 * (128 + 4)) * sizeof(double);
+    const size_t sm = (size_t)(128 * (TR + 4) + 32 * (128 + 4)) * sizeof(double);  // X (XS = TR + 4) + Ts
     if (upper) {
       cudaFuncSetAttribute(trsm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       trsm_kernel<true><<<grid, TT, sm, s>>>(b, d + first);

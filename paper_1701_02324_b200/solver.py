@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes
 import time
+import weakref
 from collections.abc import Mapping
 from dataclasses import dataclass
 
@@ -39,7 +40,9 @@ class NodeFactor:
 
 class _Factors(Mapping):
     def __init__(self, f):
-        self._f = f
+        # weak back-reference: no Factorization <-> _Factors cycle, so the
+        # factor storage is released as soon as the Factorization is dropped
+        self._f = weakref.proxy(f)
         self._cache = {}
 
     def __getitem__(self, i):
