@@ -76,7 +76,7 @@ SIGNATURES = {
 }
 
 KIND_NAMES = ("gemm", "copy", "getrf", "getrs", "gecon", "eval", "eval_rm", "ksum", "panel", "swap",
-              "trsm_l", "trsm_u", "norm1")
+              "trsm_l", "trsm_u", "norm1", "lu_fused")
 
 
 def profile(enable):

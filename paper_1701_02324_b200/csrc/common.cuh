@@ -175,6 +175,13 @@ struct TrsmDesc {
   int ldt, ldb, k, ncols;
 };
 
+// Whole LU (+ carried right-hand sides B, n x r, and backward solve) of one
+// matrix in one CTA (lu_fused.cu).
+struct LuFusedDesc {
+  Ref A, piv, info, B;
+  int n, lda, r, ldb;
+};
+
 }  // namespace hks
 
 #define HKS_CUDA_CHECK(expr)                                                 \

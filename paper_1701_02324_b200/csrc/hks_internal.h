@@ -31,6 +31,8 @@ cudaError_t launch_panel_batched(const Bases* b, const PanelDesc* d, int count, 
 cudaError_t launch_swap_batched(const Bases* b, const SwapDesc* d, int count, int max_cols, cudaStream_t s);
 cudaError_t launch_trsm_batched(const Bases* b, const TrsmDesc* d, int count, int max_cols, bool upper,
                                 cudaStream_t s);
+cudaError_t launch_lu_fused(const Bases* b, const LuFusedDesc* d, int count, int max_n, int max_r,
+                            cudaStream_t s);
 cudaError_t launch_norm1_batched(const Bases* b, const LuDesc* d, int count, cudaStream_t s);
 cudaError_t launch_gecon_batched(const Bases* bases, const LuDesc* d_descs, int count, int max_n,
                                  cudaStream_t stream);

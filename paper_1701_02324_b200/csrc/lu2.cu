@@ -101,94 +101,105 @@ __global__ void swap_kernel(const Bases* __restrict__ bases_ptr, const SwapDesc*
 }
 
 // B := T^-1 B for a k x k triangular block T (unit lower, or non-unit
-// upper), k <= 128, B k x ncols; CTA = 32 columns in shared memory, 32-row
-// blocks: DMMA update from the solved blocks, then warp substitution.
-constexpr int TR = 32;
-constexpr int TT = 256;
+// upper), k <= 128, B k x ncols.  A CTA owns 128 columns (one per thread)
+// held in shared memory.  Per 32-row block: the rows of T are staged, the
+// contribution of the already-solved rows is one DMMA product (each warp a
+// 32 x 32 tile), then every thread solves its column against the 32 x 32
+// diagonal block in registers, column-oriented (axpy) order so the 31
+// updates of each step are independent (no serial shuffle chain).
+constexpr int TNC = 128;            // columns per CTA (= threads)
+constexpr int TXS = TNC + 4;        // X row stride: == 4 (mod 16), conflict-free DMMA B fragments
+constexpr int TTS = 128 + 4;        // staged T row stride
 
 template <bool UPPER>
-__global__ void __launch_bounds__(TT) trsm_kernel(const Bases* __restrict__ bases_ptr, const TrsmDesc* __restrict__ descs) {
+__global__ void __launch_bounds__(TNC) trsm_kernel(const Bases* __restrict__ bases_ptr,
+                                                  const TrsmDesc* __restrict__ descs) {
   const Bases& bases = *bases_ptr;
   const TrsmDesc D = descs[blockIdx.y];
-  const int c0 = blockIdx.x * TR;
+  const int c0 = blockIdx.x * TNC;
   if (c0 >= D.ncols) return;
-  const int nc = min(TR, D.ncols - c0), k = D.k;
+  const int nc = min(TNC, D.ncols - c0), k = D.k;
   const double* T = at<const double>(bases, D.T);
   double* B = at<double>(bases, D.B) + (size_t)c0 * D.ldb;
-  constexpr int XS = TR + 4, TS = 128 + 4;  // both == 4 (mod 16): conflict-free DMMA fragments
   extern __shared__ double tsm[];
-  double* X = tsm;              // k x TR, row-major
-  double* Ts = tsm + 128 * XS;  // the current 32 rows of T, row-major
+  double* X = tsm;                    // k x TNC, row-major (ld TXS)
+  double* Ts = tsm + 128 * TXS;       // 32 rows of T, row-major (ld TTS)
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  for (int e = tid; e < k * nc; e += TT) {
-    const int i = e % k, c = e / k;
-    X[i * XS + c] = B[i + (size_t)c * D.ldb];
-  }
+  // coalesced load: lanes walk a column's rows
+  for (int c = wid; c < nc; c += TNC / 32)
+    for (int i = lane; i < k; i += 32) X[i * TXS + c] = B[i + (size_t)c * D.ldb];
   const int nblk = (k + 31) / 32;
   const int fr = lane >> 2, fc = lane & 3;
   for (int bb = 0; bb < nblk; ++bb) {
     const int b = UPPER ? nblk - 1 - bb : bb;
     const int r0 = b * 32, nr = min(32, k - r0);
-    const int klo = UPPER ? r0 : 0, khi = UPPER ? k : r0 + nr;  // columns of T needed (incl. diagonal block)
-    // stage T[r0:r0+nr, klo:khi) (coalesced: a warp reads one column's rows)
-    for (int cc = klo + wid; cc < khi; cc += TT / 32)
-      if (lane < nr) Ts[lane * TS + cc] = T[(r0 + lane) + (size_t)cc * D.ldt];
+    const int klo = UPPER ? r0 : 0, khi = UPPER ? k : r0 + nr;
+    __syncthreads();  // previous block's solve (and the initial load) is complete
+    for (int cc = klo + wid; cc < khi; cc += TNC / 32)
+      Ts[lane * TTS + cc] = lane < nr ? T[(r0 + lane) + (size_t)cc * D.ldt] : 0.0;
     __syncthreads();
-    // update rows r0..r0+nr with the already-solved rows (DMMA on shared operands)
+    // X[r0:r0+nr, :] -= T[r0:r0+nr, u] X[u, :] over the solved rows u (DMMA)
     const int ulo = UPPER ? r0 + nr : 0, uhi = UPPER ? k : r0;
     if (uhi > ulo) {
-      for (int f = wid; f < 16; f += 8) {
-        const int fi = f & 3, fj = f >> 2;
-        double d0 = 0.0, d1 = 0.0;
-        const int rl = fi * 8 + fr;
-        for (int kk = ulo; kk < uhi; kk += 4) {
-          const int kq = kk + fc;
-          const double a = (rl < nr && kq < uhi) ? -Ts[rl * TS + kq] : 0.0;
-          const double bv = (kq < uhi && fj * 8 + fr < nc) ? X[kq * XS + fj * 8 + fr] : 0.0;
-          dmma884(d0, d1, a, bv);
-        }
-        const int c = fj * 8 + 2 * fc;
-        if (rl < nr) {
-          if (c < nc) X[(r0 + rl) * XS + c] += d0;
-          if (c + 1 < nc) X[(r0 + rl) * XS + c + 1] += d1;
-        }
+      const int cb = wid * 32;  // this warp's 32 columns
+      double acc[4][4][2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int kk = ulo; kk < uhi; kk += 4) {
+        const int kq = kk + fc;
+        const bool kin = kq < uhi;
+        double a[4], bv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = kin ? Ts[(i * 8 + fr) * TTS + kq] : 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bv[j] = kin ? X[kq * TXS + cb + j * 8 + fr] : 0.0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], bv[j]);
       }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int rr = i * 8 + fr, c = cb + j * 8 + 2 * fc + h;
+            if (rr < nr) X[(r0 + rr) * TXS + c] -= acc[i][j][h];
+          }
       __syncthreads();
     }
-    // substitution inside the 32-row block: lane = row, the row of the
-    // diagonal block in registers; warp w owns columns w, w+8, ...
-    if (wid < nc) {
-      double t[32];
+    // diagonal block: thread = column, values in registers
+    if (tid < nc) {
+      double x[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) t[j] = (lane < nr && j < nr) ? Ts[lane * TS + r0 + j] : 0.0;
-      for (int c = wid; c < nc; c += 8) {
-        double x = lane < nr ? X[(r0 + lane) * XS + c] : 0.0;
-        if (!UPPER) {
+      for (int i = 0; i < 32; ++i) x[i] = i < nr ? X[(r0 + i) * TXS + tid] : 0.0;
+      if (!UPPER) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const double xj = __shfl_sync(0xffffffffu, x, j);
-            if (lane > j) x -= t[j] * xj;
-          }
-        } else {
+        for (int j = 0; j < 32; ++j) {
 #pragma unroll
-          for (int j = 31; j >= 0; --j) {
-            if (j < nr) {
-              double xj = __shfl_sync(0xffffffffu, x, j);
-              xj /= __shfl_sync(0xffffffffu, t[j], j);  // the diagonal entry U(j, j), held by lane j
-              if (lane == j) x = xj;
-              if (lane < j) x -= t[j] * xj;
-            }
+          for (int i = j + 1; i < 32; ++i) x[i] -= Ts[i * TTS + r0 + j] * x[j];
+        }
+      } else {
+#pragma unroll
+        for (int j = 31; j >= 0; --j) {
+          if (j < nr) {
+            x[j] /= Ts[j * TTS + r0 + j];
+#pragma unroll
+            for (int i = 0; i < j; ++i) x[i] -= Ts[i * TTS + r0 + j] * x[j];
           }
         }
-        if (lane < nr) X[(r0 + lane) * XS + c] = x;
       }
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (i < nr) X[(r0 + i) * TXS + tid] = x[i];
     }
-    __syncthreads();
   }
-  for (int e = tid; e < k * nc; e += TT) {
-    const int i = e % k, c = e / k;
-    B[i + (size_t)c * D.ldb] = X[i * XS + c];
-  }
+  __syncthreads();
+  for (int c = wid; c < nc; c += TNC / 32)
+    for (int i = lane; i < k; i += 32) B[i + (size_t)c * D.ldb] = X[i * TXS + c];
 }
 
 // ||A||_1 (max column abs sum) of each n x n matrix, before factoring.
@@ -241,14 +252,14 @@ cudaError_t launch_trsm_batched(const Bases* b, const TrsmDesc* d, int count, in
   if (count <= 0 || max_cols <= 0) return cudaSuccess;
   for (int first = 0; first < count; first += 65535) {
     const int cnt = count - first < 65535 ? count - first : 65535;
-    dim3 grid((max_cols + TR - 1) / TR, cnt);
-    const size_t sm = (size_t)(128 * (TR + 4) + 32 * (128 + 4)) * sizeof(double);  // X (XS = TR + 4) + Ts
+    dim3 grid((max_cols + TNC - 1) / TNC, cnt);
+    const size_t sm = (size_t)(128 * TXS + 32 * TTS) * sizeof(double);
     if (upper) {
       cudaFuncSetAttribute(trsm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      trsm_kernel<true><<<grid, TT, sm, s>>>(b, d + first);
+      trsm_kernel<true><<<grid, TNC, sm, s>>>(b, d + first);
     } else {
       cudaFuncSetAttribute(trsm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      trsm_kernel<false><<<grid, TT, sm, s>>>(b, d + first);
+      trsm_kernel<false><<<grid, TNC, sm, s>>>(b, d + first);
     }
   }
   return cudaGetLastError();

@@ -176,6 +176,9 @@ cudaError_t StepList::run(const Bases* b, const double* X, int d, const KernelPa
       case ST_NORM1:
         e = launch_norm1_batched(b, (const LuDesc*)st.d, st.count, s);
         break;
+      case ST_LU_FUSED:
+        e = launch_lu_fused(b, (const LuFusedDesc*)st.d, st.count, st.p0, st.p1, s);
+        break;
     }
     if (prof) {
       cudaEventRecord(e1, s);
@@ -465,6 +468,16 @@ struct Trsms {
 // from the group's earlier panels), then the group's interchanges on every
 // other column, one TRSM for the group's U rows and one rank-128 GEMM
 // trailing update -- all matrices of the level in the same launches.
+// Levels with at most this many matrices use the fused one-CTA-per-matrix
+// LU (lu_fused.cu) instead of the multi-launch program (HKS_FUSED_MAX).
+int fused_lu_max_count() {
+  static const int v = [] {
+    const char* e = getenv("HKS_FUSED_MAX");
+    return e ? atoi(e) : 300;
+  }();
+  return v;
+}
+
 void add_lu_program(StepList& sl, const std::vector<LuJob>& jobs, bool with_norm) {
   if (jobs.empty()) return;
   int nmax = 0;
@@ -475,6 +488,19 @@ void add_lu_program(StepList& sl, const std::vector<LuJob>& jobs, bool with_norm
     std::vector<LuDesc> nd;
     for (auto& j : jobs) nd.push_back(LuDesc{j.A, j.piv, j.info, j.anorm, kNull, j.n, j.lda});
     sl.add(ST_NORM1, nd, nmax);
+  }
+  if ((int)jobs.size() <= fused_lu_max_count()) {
+    std::vector<LuFusedDesc> fd;
+    double f = 0, bytes = 0;
+    int rmax = 0;
+    for (auto& j : jobs) {
+      rmax = std::max(rmax, j.r);
+      fd.push_back(LuFusedDesc{j.A, j.piv, j.info, j.r > 0 ? j.B : kNull, j.n, j.lda, j.r, j.ldb});
+      f += lu_flops(j.n) + 2.0 * j.n * j.n * (double)j.r;
+      bytes += 16.0 * ((double)j.n * j.n + (double)j.n * j.r);
+    }
+    sl.add(ST_LU_FUSED, fd, nmax, rmax, f, bytes);
+    return;
   }
   for (int g0 = 0; g0 < nmax; g0 += kGroup) {
     for (int p0 = g0; p0 < g0 + kGroup && p0 < nmax; p0 += PB) {
