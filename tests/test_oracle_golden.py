@@ -34,8 +34,11 @@ def test_tree_perm_and_splits_exact(name):
     inst = oracle_instance(name)
     t = inst["tree"]
     assert np.array_equal(t.perm, g["perm"])
+    # The split value is a BLAS dot product inside the power iteration
+    # (tree.py:70-84); its last bits follow the BLAS thread count, so it is
+    # compared to 1e-12 relative while the permutation stays bit-exact.
     for i, v in t.split_val.items():
-        assert v == g["split_value"][i]
+        assert v == pytest.approx(float(g["split_value"][i]), rel=1e-12, abs=1e-15)
     assert t.depth == g["meta"]["depth"]
 
 
