@@ -96,48 +96,3 @@ extern "C" int hks_kernel_sum(const double* X, int64_t d, const hks_kernel* kern
   return HKS_OK;
 }
 
-extern "C" int hks_lu_factor(double* A, int64_t n, int64_t lda, int32_t* piv, int32_t* info_host, void* stream) {
-  if (n < 0 || lda < n) return set_error(HKS_ERR_INVALID, "hks_lu_factor: bad dims");
-  if (n == 0) {
-    if (info_host) *info_host = 0;
-    return HKS_OK;
-  }
-  cudaStream_t s = as_stream(stream);
-  int* dinfo = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&dinfo), sizeof(int), s);
-  LuDesc h{abs_ref(A), abs_ref(piv), abs_ref(dinfo), kNull, kNull, (int)n, (int)lda};
-  Bases b{};
-  LuDesc* dd = nullptr;
-  Bases* db = nullptr;
-  if (e == cudaSuccess) e = one_desc(h, &dd, s);
-  if (e == cudaSuccess) e = upload_bases(b, &db, s);
-  if (e == cudaSuccess) e = launch_getrf_batched(db, dd, 1, (int)n, s);
-  if (db) cudaFreeAsync(db, s);
-  int info = 0;
-  if (e == cudaSuccess) e = cudaMemcpyAsync(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost, s);
-  if (dd) cudaFreeAsync(dd, s);
-  if (dinfo) cudaFreeAsync(dinfo, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_lu_factor: %s", cudaGetErrorString(e));
-  if (info_host) *info_host = info;
-  if (info) return set_error(HKS_ERR_SINGULAR, "singular matrix: zero pivot at elimination step %d", info - 1);
-  return HKS_OK;
-}
-
-extern "C" int hks_lu_solve(const double* LU, const int32_t* piv, int64_t n, int64_t lda, double* B, int64_t ldb,
-                            int64_t nrhs, void* stream) {
-  if (n < 0 || lda < n || ldb < n || nrhs < 0) return set_error(HKS_ERR_INVALID, "hks_lu_solve: bad dims");
-  if (n == 0 || nrhs == 0) return HKS_OK;
-  cudaStream_t s = as_stream(stream);
-  LuSolveDesc h{abs_ref(LU), abs_ref(piv), abs_ref(B), (int)n, (int)nrhs, (int)lda, (int)ldb};
-  Bases b{};
-  LuSolveDesc* dd = nullptr;
-  Bases* db = nullptr;
-  cudaError_t e = one_desc(h, &dd, s);
-  if (e == cudaSuccess) e = upload_bases(b, &db, s);
-  if (e == cudaSuccess) e = launch_getrs_batched(db, dd, 1, (int)n, (int)nrhs, s);
-  if (dd) cudaFreeAsync(dd, s);
-  if (db) cudaFreeAsync(db, s);
-  if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_lu_solve: %s", cudaGetErrorString(e));
-  return HKS_OK;
-}

@@ -18,6 +18,17 @@ constexpr int kWarp = 32;
 // D = A*B + D for one 8x8x4 FP64 tile (SASS: DMMA.884).  Fragment layout
 // (PTX ISA m8n8k4 .f64): lane t holds A[t/4][t%4], B[t%4][t/4] and
 // D[t/4][2*(t%4) + {0,1}].
+// 8-byte asynchronous global->shared copy (LDGSTS); pred false zero-fills.
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool pred) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(src), "r"(pred ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)

@@ -12,6 +12,7 @@
 // getrf / getrs (partial pivoting, row interchanges applied to the whole
 // row, 0-based pivots) up to roundoff.
 #include <cfloat>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "hks_internal.h"
@@ -37,10 +38,12 @@ __global__ void __launch_bounds__(PT) panel_kernel(const Bases* __restrict__ bas
   __shared__ int s_info;
   const int tid = threadIdx.x;
   if (tid == 0) s_info = 0;
-  for (int c = 0; c < pb; ++c) {  // coalesced column loads, no div/mod
+  for (int c = 0; c < pb; ++c) {  // coalesced column loads (LDGSTS: all in flight at once)
     const double* src = A + p0 + (size_t)(p0 + c) * lda;
-    for (int i = tid; i < mr; i += PT) P[i + c * ldp] = src[i];
+    for (int i = tid; i < mr; i += PT) cp_async8(P + i + c * ldp, src + i, true);
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
   for (int jj = 0; jj < pb; ++jj) {
     ArgMax a{-1.0, 0x7fffffff};
@@ -82,6 +85,418 @@ __global__ void __launch_bounds__(PT) panel_kernel(const Bases* __restrict__ bas
   }
 }
 
+// Register-resident panel factorization (same arithmetic as panel_kernel):
+// thread t owns local rows t, t + NT, ... (RPT of them) and keeps their PB
+// panel entries in registers, so the rank-1 update of each step is RPT * PB
+// independent FMAs against a broadcast pivot row.  One barrier per column:
+// every warp publishes its argmax candidate together with the candidate's
+// whole row (and the owner of row jj publishes row jj) into a
+// parity-double-buffered shared slot; after the barrier every thread picks
+// the winner redundantly and reads the pivot row straight from the winning
+// warp's slot.
+template <int PB, int RPT, int NT>
+__global__ void __launch_bounds__(NT) panel_reg_kernel(const Bases* __restrict__ bases_ptr,
+                                                       const PanelDesc* __restrict__ descs) {
+  constexpr int NW = NT / 32;
+  const Bases& bases = *bases_ptr;
+  const PanelDesc D = descs[blockIdx.x];
+  double* A = at<double>(bases, D.A);
+  int* piv = at<int>(bases, D.piv);
+  const int lda = D.lda, p0 = D.p0, pb = D.pb, mr = D.n - D.p0;
+  __shared__ double rows[2][NW + 1][PB];  // [parity][warp candidate rows..., row jj]
+  __shared__ double cval[2][NW];
+  __shared__ int cidx[2][NW];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  double v[RPT][PB];
+#pragma unroll
+  for (int c = 0; c < PB; ++c)
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int i = tid + q * NT;
+      v[q][c] = (i < mr && c < pb) ? A[p0 + i + (size_t)(p0 + c) * lda] : 0.0;
+    }
+  int info = 0;
+#pragma unroll
+  for (int jj = 0; jj < PB; ++jj) {
+    if (jj >= pb) break;
+    const int par = jj & 1;
+    ArgMax a{-1.0, 0x7fffffff};
+    int aq = 0;
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int i = tid + q * NT;
+      if (i >= jj && i < mr) {
+        const ArgMax b{fabs(v[q][jj]), i};
+        if (b.v > a.v || (b.v == a.v && b.i < a.i)) {
+          a = b;
+          aq = q;
+        }
+      }
+    }
+    const ArgMax w = warp_argmax(a);
+    if (a.i == w.i && a.i != 0x7fffffff) {  // this lane holds the warp's candidate
+#pragma unroll
+      for (int q = 0; q < RPT; ++q)
+        if (q == aq)
+#pragma unroll
+          for (int c = 0; c < PB; ++c) rows[par][wid][c] = v[q][c];
+    }
+    if (lane == 0) {
+      cval[par][wid] = w.v;
+      cidx[par][wid] = w.i;
+    }
+    if (tid == jj)  // jj < PB <= NT: row jj is thread jj's first row
+#pragma unroll
+      for (int c = 0; c < PB; ++c) rows[par][NW][c] = v[0][c];
+    __syncthreads();
+    ArgMax g{cval[par][0], cidx[par][0]};
+    int gw = 0;
+#pragma unroll
+    for (int w2 = 1; w2 < NW; ++w2) {
+      const ArgMax b{cval[par][w2], cidx[par][w2]};
+      if (b.v > g.v || (b.v == g.v && b.i < g.i)) {
+        g = b;
+        gw = w2;
+      }
+    }
+    if (g.i == 0x7fffffff) {  // no comparable candidate (NaN column): no interchange
+      g.i = jj;
+      gw = NW;
+    }
+    const int p = g.i;
+    const double* pr = rows[par][gw];
+    const double* jr = rows[par][NW];
+    const double pv = pr[jj];
+    if (tid == 0) {
+      piv[p0 + jj] = p0 + p;
+      if (pv == 0.0 && info == 0) info = p0 + jj + 1;
+    }
+    const bool recip = fabs(pv) >= DBL_MIN;
+    const double inv = 1.0 / pv;
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int i = tid + q * NT;
+      if (p != jj) {  // interchange rows jj and p
+        if (i == jj)
+#pragma unroll
+          for (int c = 0; c < PB; ++c) v[q][c] = pr[c];
+        if (i == p)
+#pragma unroll
+          for (int c = 0; c < PB; ++c) v[q][c] = jr[c];
+      }
+      if (i > jj && i < mr) {  // scale (dgetf2: reciprocal when safe), rank-1 update
+        double l = v[q][jj];
+        if (pv != 0.0) {
+          l = recip ? l * inv : l / pv;
+          v[q][jj] = l;
+        }
+#pragma unroll
+        for (int c = jj + 1; c < PB; ++c) v[q][c] -= l * pr[c];
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < PB; ++c)
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int i = tid + q * NT;
+      if (i < mr && c < pb) A[p0 + i + (size_t)(p0 + c) * lda] = v[q][c];
+    }
+  if (tid == 0 && info && D.info != kNull) {
+    int* g = at<int>(bases, D.info);
+    if (*g == 0) *g = info;  // panels run in order: keep the first zero pivot
+  }
+}
+
+#ifdef PANEL_PROF
+__device__ long long g_pprof[32][8];
+#define PPROF(m)                                                        \
+  do {                                                                  \
+    if (blockIdx.x == 0 && tid == 0) g_pprof[jj][m] = clock64();        \
+  } while (0)
+#else
+#define PPROF(m) \
+  do {           \
+  } while (0)
+#endif
+
+// Same panel, cheaper pivot search: |x| as a 64-bit key (IEEE order of a
+// non-negative double is its unsigned bit order; bit 63 marks a live row)
+// reduced with three 32-bit warp reductions (max high word, max low word
+// among the high-word winners, min row index among the key winners -- the
+// lowest index wins ties, as idamax), and the per-warp winners combined the
+// same way by the first NW lanes of every warp after the barrier.  The
+// winning warp follows from the pivot row (rows are dealt round-robin).
+template <int PB, int RPT, int NT>
+__global__ void __launch_bounds__(NT) panel_redux_kernel(const Bases* __restrict__ bases_ptr,
+                                                         const PanelDesc* __restrict__ descs) {
+  constexpr int NW = NT / 32;
+  const Bases& bases = *bases_ptr;
+  const PanelDesc D = descs[blockIdx.x];
+  double* A = at<double>(bases, D.A);
+  int* piv = at<int>(bases, D.piv);
+  const int lda = D.lda, p0 = D.p0, pb = D.pb, mr = D.n - D.p0;
+  __shared__ __align__(16) double rows[2][NW + 1][PB];  // [parity][warp candidate rows..., row jj]
+  __shared__ unsigned khi[2][NW], klo[2][NW], kid[2][NW];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  double v[RPT][PB];
+#pragma unroll
+  for (int c = 0; c < PB; ++c)
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int i = tid + q * NT;
+      v[q][c] = (i < mr && c < pb) ? A[p0 + i + (size_t)(p0 + c) * lda] : 0.0;
+    }
+  int info = 0;
+#pragma unroll
+  for (int jj = 0; jj < PB; ++jj) {
+    if (jj >= pb) break;
+    PPROF(0);
+    const int par = jj & 1;
+    unsigned long long key = 0;
+    int ai = 0x7fffffff, aq = 0;
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int i = tid + q * NT;
+      if (i >= jj && i < mr) {
+        const unsigned long long k = (unsigned long long)__double_as_longlong(fabs(v[q][jj])) | (1ull << 63);
+        if (k > key) {  // rows ascend with q: strict > keeps the lowest index on ties
+          key = k;
+          ai = i;
+          aq = q;
+        }
+      }
+    }
+    PPROF(1);
+    const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+    const unsigned m1 = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned m2 = __reduce_max_sync(0xffffffffu, hi == m1 ? lo : 0u);
+    const unsigned id = __reduce_min_sync(0xffffffffu, (hi == m1 && lo == m2) ? (unsigned)ai : 0xffffffffu);
+    PPROF(2);
+    if (m1 != 0u && (unsigned)ai == id) {  // this lane holds the warp's candidate row
+#pragma unroll
+      for (int q = 0; q < RPT; ++q)
+        if (q == aq)
+#pragma unroll
+          for (int c = 0; c < PB; c += 2)
+            *reinterpret_cast<double2*>(&rows[par][wid][c]) = make_double2(v[q][c], v[q][c + 1]);
+    }
+    if (lane == 0) {
+      khi[par][wid] = m1;
+      klo[par][wid] = m2;
+      kid[par][wid] = id;
+    }
+    if (tid == jj)  // jj < PB <= NT: row jj is thread jj's first row
+#pragma unroll
+      for (int c = 0; c < PB; c += 2)
+        *reinterpret_cast<double2*>(&rows[par][NW][c]) = make_double2(v[0][c], v[0][c + 1]);
+    PPROF(3);
+    __syncthreads();
+    PPROF(4);
+    const unsigned h2 = lane < NW ? khi[par][lane] : 0u, l2 = lane < NW ? klo[par][lane] : 0u;
+    const unsigned i2 = lane < NW ? kid[par][lane] : 0xffffffffu;
+    const unsigned g1 = __reduce_max_sync(0xffffffffu, h2);
+    const unsigned g2 = __reduce_max_sync(0xffffffffu, h2 == g1 ? l2 : 0u);
+    const unsigned gi = __reduce_min_sync(0xffffffffu, (h2 == g1 && l2 == g2) ? i2 : 0xffffffffu);
+    // no live candidate (NaN-free empty search cannot happen; guard anyway): no interchange
+    const int p = g1 != 0u ? (int)gi : jj;
+    const int gw = g1 != 0u ? (p % NT) >> 5 : NW;
+    PPROF(5);
+    const double* pr = rows[par][gw];
+    const double* jr = rows[par][NW];
+    const double pv = pr[jj];
+    if (tid == 0) {
+      piv[p0 + jj] = p0 + p;
+      if (pv == 0.0 && info == 0) info = p0 + jj + 1;
+    }
+    const bool recip = fabs(pv) >= DBL_MIN;
+    const double inv = 1.0 / pv;
+    PPROF(6);
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int i = tid + q * NT;
+      if (p != jj) {  // interchange rows jj and p
+        if (i == jj)
+#pragma unroll
+          for (int c = 0; c < PB; ++c) v[q][c] = pr[c];
+        if (i == p)
+#pragma unroll
+          for (int c = 0; c < PB; ++c) v[q][c] = jr[c];
+      }
+      if (i > jj && i < mr) {  // scale (dgetf2: reciprocal when safe), rank-1 update
+        double l = v[q][jj];
+        if (pv != 0.0) {
+          l = recip ? l * inv : l / pv;
+          v[q][jj] = l;
+        }
+#pragma unroll
+        for (int c = jj + 1; c < PB; ++c) v[q][c] -= l * pr[c];
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < PB; ++c)
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int i = tid + q * NT;
+      if (i < mr && c < pb) A[p0 + i + (size_t)(p0 + c) * lda] = v[q][c];
+    }
+  if (tid == 0 && info && D.info != kNull) {
+    int* g = at<int>(bases, D.info);
+    if (*g == 0) *g = info;  // panels run in order: keep the first zero pivot
+  }
+}
+
+// Panel factorization as a loop over blocks of U columns (fully unrolled
+// 32-column variants are instruction-cache bound: the straight-line code
+// does not fit and every column refetches it).  Row interchanges are
+// relabellings: each thread keeps its physical rows and the logical row
+// number (label) each one currently holds, so an interchange of rows jj and
+// p is two label updates, never a data movement.  The working columns live
+// in registers, shifted by U after every block so the block's columns sit at
+// compile-time indices; finished columns are parked in shared memory by
+// physical row and written to their final (label) rows at the end.  Pivot
+// search: |x| as a 64-bit key (IEEE order of a non-negative double is its
+// unsigned bit order; bit 63 marks a live row) reduced with three 32-bit
+// warp reductions (max high word, max low word among the high-word winners,
+// min row label among the key winners -- the lowest current row wins ties,
+// as idamax); per-warp winners publish key + working row into a
+// parity-double-buffered slot, so one barrier per column suffices.
+template <int PB, int RPT, int NT, int U>
+__global__ void __launch_bounds__(NT) panel_loop_kernel(const Bases* __restrict__ bases_ptr,
+                                                        const PanelDesc* __restrict__ descs) {
+  constexpr int NW = NT / 32, NR = NT * RPT;
+  const Bases& bases = *bases_ptr;
+  const PanelDesc D = descs[blockIdx.x];
+  double* A = at<double>(bases, D.A);
+  int* piv = at<int>(bases, D.piv);
+  const int lda = D.lda, p0 = D.p0, pb = D.pb, mr = D.n - D.p0;
+  extern __shared__ __align__(16) double psm[];
+  double* done = psm;               // [PB][NR] finished columns by physical row
+  double* cand = psm + (PB + U) * NR;  // [2][NW][PB] per-warp candidate working rows
+  __shared__ unsigned khi[2][NW], klo[2][NW], kid[2][NW];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  double w[RPT][PB];
+  int lab[RPT];
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) lab[q] = tid + q * NT < mr ? tid + q * NT : 0x7fffffff;
+#pragma unroll
+  for (int c = 0; c < PB; ++c)
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int i = tid + q * NT;
+      w[q][c] = (i < mr && c < pb) ? A[p0 + i + (size_t)(p0 + c) * lda] : 0.0;
+    }
+  int info = 0;
+#pragma unroll 1
+  for (int j0 = 0; j0 < pb; j0 += U) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int jj = j0 + u;
+      if (jj < pb) {
+        PPROF(0);
+        const int par = jj & 1;
+        unsigned long long key = 0;
+        int ai = 0x7fffffff, aq = 0;
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+          if (lab[q] >= jj && lab[q] < mr) {
+            const unsigned long long k = (unsigned long long)__double_as_longlong(fabs(w[q][u])) | (1ull << 63);
+            if (k > key || (k == key && lab[q] < ai)) {
+              key = k;
+              ai = lab[q];
+              aq = q;
+            }
+          }
+        }
+        PPROF(1);
+        const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+        const unsigned m1 = __reduce_max_sync(0xffffffffu, hi);
+        const unsigned m2 = __reduce_max_sync(0xffffffffu, hi == m1 ? lo : 0u);
+        const unsigned id = __reduce_min_sync(0xffffffffu, (hi == m1 && lo == m2) ? (unsigned)ai : 0xffffffffu);
+        PPROF(2);
+        double* mine = cand + (par * NW + wid) * PB;
+        if (m1 != 0u && (unsigned)ai == id) {  // this lane holds the warp's candidate row
+#pragma unroll
+          for (int q = 0; q < RPT; ++q)
+            if (q == aq)
+#pragma unroll
+              for (int c = (u & ~1); c < PB; c += 2)
+                *reinterpret_cast<double2*>(mine + c) = make_double2(w[q][c], w[q][c + 1]);
+        }
+        if (lane == 0) {
+          khi[par][wid] = m1;
+          klo[par][wid] = m2;
+          kid[par][wid] = id;
+        }
+        PPROF(3);
+        __syncthreads();
+        PPROF(4);
+        const unsigned h2 = lane < NW ? khi[par][lane] : 0u, l2 = lane < NW ? klo[par][lane] : 0u;
+        const unsigned i2 = lane < NW ? kid[par][lane] : 0xffffffffu;
+        const unsigned g1 = __reduce_max_sync(0xffffffffu, h2);
+        const unsigned g2 = __reduce_max_sync(0xffffffffu, h2 == g1 ? l2 : 0u);
+        const unsigned gi = __reduce_min_sync(0xffffffffu, (h2 == g1 && l2 == g2) ? i2 : 0xffffffffu);
+        const unsigned win = __ballot_sync(0xffffffffu, lane < NW && h2 == g1 && l2 == g2 && i2 == gi);
+        const int gw = win ? __ffs(win) - 1 : 0;
+        const int p = g1 != 0u ? (int)gi : jj;
+        PPROF(5);
+        const double* pr = cand + (par * NW + gw) * PB;
+        const double pv = pr[u];
+        if (tid == 0) {
+          piv[p0 + jj] = p0 + p;
+          if (pv == 0.0 && info == 0) info = p0 + jj + 1;
+        }
+        const bool recip = fabs(pv) >= DBL_MIN;
+        const double inv = 1.0 / pv;
+        PPROF(6);
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+          if (lab[q] == p)  // interchange rows jj and p: relabel
+            lab[q] = jj;
+          else if (lab[q] == jj)
+            lab[q] = p;
+          if (lab[q] > jj && lab[q] < mr) {  // scale (dgetf2: reciprocal when safe), rank-1 update
+            double l = w[q][u];
+            if (pv != 0.0) {
+              l = recip ? l * inv : l / pv;
+              w[q][u] = l;
+            }
+#pragma unroll
+            for (int c = u + 1; c < PB; ++c) w[q][c] -= l * pr[c];
+          }
+        }
+      }
+    }
+    // columns j0 .. j0+U-1 are final for every row: park them, shift the rest down
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) done[(j0 + u) * NR + tid + q * NT] = w[q][u];
+#pragma unroll
+      for (int c = 0; c + U < PB; ++c) w[q][c] = w[q][c + U];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < RPT; ++q)
+    if (lab[q] < mr)
+      for (int c = 0; c < pb; ++c) A[p0 + lab[q] + (size_t)(p0 + c) * lda] = done[c * NR + tid + q * NT];
+  if (tid == 0 && info && D.info != kNull) {
+    int* g = at<int>(bases, D.info);
+    if (*g == 0) *g = info;  // panels run in order: keep the first zero pivot
+  }
+}
+
+template <int PB, int RPT, int NT, int U>
+cudaError_t launch_panel_loop(const Bases* b, const PanelDesc* d, int count, cudaStream_t s) {
+  // done[] is PB + U rows deep: the last block may run past pb
+  const size_t sm = (size_t)((PB + U) * NT * RPT + 2 * (NT / 32) * PB) * sizeof(double);
+  cudaFuncSetAttribute(panel_loop_kernel<PB, RPT, NT, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  panel_loop_kernel<PB, RPT, NT, U><<<count, NT, sm, s>>>(b, d);
+  return cudaGetLastError();
+}
+
 // Row interchanges piv[r0..r1) applied in order to columns [c0, c1).
 __global__ void swap_kernel(const Bases* __restrict__ bases_ptr, const SwapDesc* __restrict__ descs) {
   const Bases& bases = *bases_ptr;
@@ -102,14 +517,28 @@ __global__ void swap_kernel(const Bases* __restrict__ bases_ptr, const SwapDesc*
 
 // B := T^-1 B for a k x k triangular block T (unit lower, or non-unit
 // upper), k <= 128, B k x ncols.  A CTA owns 128 columns (one per thread)
-// held in shared memory.  Per 32-row block: the rows of T are staged, the
-// contribution of the already-solved rows is one DMMA product (each warp a
-// 32 x 32 tile), then every thread solves its column against the 32 x 32
-// diagonal block in registers, column-oriented (axpy) order so the 31
-// updates of each step are independent (no serial shuffle chain).
+// held in shared memory.  Per 32-row block: the contribution of the
+// already-solved rows is one DMMA product (each warp a 32 x 32 tile), then
+// every thread solves its column against the 32 x 32 diagonal block in
+// registers, column-oriented (axpy) order so the 31 updates of each step are
+// independent (no serial shuffle chain).  All global reads are LDGSTS
+// (cp.async): the 128 x 128 block of B and the first 32 rows of T are in
+// flight together, and the next block's rows of T are prefetched into the
+// second buffer while the current block computes -- with one 200 KB CTA per
+// SM, synchronous loads would leave the kernel HBM-latency bound.
 constexpr int TNC = 128;            // columns per CTA (= threads)
 constexpr int TXS = TNC + 4;        // X row stride: == 4 (mod 16), conflict-free DMMA B fragments
 constexpr int TTS = 128 + 4;        // staged T row stride
+
+template <bool UPPER>
+__device__ __forceinline__ void trsm_stage_rows(double* Ts, const double* T, int ldt, int k, int b, int wid,
+                                                int lane) {
+  const int r0 = b * 32, nr = min(32, k - r0);
+  const int klo = UPPER ? r0 : 0, khi = UPPER ? k : r0 + nr;
+  const bool ok = lane < nr;
+  for (int cc = klo + wid; cc < khi; cc += TNC / 32)
+    cp_async8(Ts + lane * TTS + cc, ok ? T + (r0 + lane) + (size_t)cc * ldt : T, ok);
+}
 
 template <bool UPPER>
 __global__ void __launch_bounds__(TNC) trsm_kernel(const Bases* __restrict__ bases_ptr,
@@ -123,21 +552,25 @@ __global__ void __launch_bounds__(TNC) trsm_kernel(const Bases* __restrict__ bas
   double* B = at<double>(bases, D.B) + (size_t)c0 * D.ldb;
   extern __shared__ double tsm[];
   double* X = tsm;                    // k x TNC, row-major (ld TXS)
-  double* Ts = tsm + 128 * TXS;       // 32 rows of T, row-major (ld TTS)
+  double* Tbuf = tsm + 128 * TXS;     // 2 x 32 rows of T, row-major (ld TTS)
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  // coalesced load: lanes walk a column's rows
-  for (int c = wid; c < nc; c += TNC / 32)
-    for (int i = lane; i < k; i += 32) X[i * TXS + c] = B[i + (size_t)c * D.ldb];
   const int nblk = (k + 31) / 32;
+  // lanes walk a column's rows: 256-byte coalesced LDGSTS
+  for (int c = wid; c < nc; c += TNC / 32)
+    for (int i = lane; i < k; i += 32) cp_async8(X + i * TXS + c, B + i + (size_t)c * D.ldb, true);
+  trsm_stage_rows<UPPER>(Tbuf, T, D.ldt, k, UPPER ? nblk - 1 : 0, wid, lane);
+  cp_async_commit();
   const int fr = lane >> 2, fc = lane & 3;
   for (int bb = 0; bb < nblk; ++bb) {
     const int b = UPPER ? nblk - 1 - bb : bb;
     const int r0 = b * 32, nr = min(32, k - r0);
-    const int klo = UPPER ? r0 : 0, khi = UPPER ? k : r0 + nr;
-    __syncthreads();  // previous block's solve (and the initial load) is complete
-    for (int cc = klo + wid; cc < khi; cc += TNC / 32)
-      Ts[lane * TTS + cc] = lane < nr ? T[(r0 + lane) + (size_t)cc * D.ldt] : 0.0;
-    __syncthreads();
+    double* Ts = Tbuf + (bb & 1) * 32 * TTS;
+    cp_async_wait<0>();
+    __syncthreads();  // X / this block's rows of T landed; the previous block's solve is complete
+    if (bb + 1 < nblk) {
+      trsm_stage_rows<UPPER>(Tbuf + ((bb + 1) & 1) * 32 * TTS, T, D.ldt, k, UPPER ? b - 1 : b + 1, wid, lane);
+      cp_async_commit();
+    }
     // X[r0:r0+nr, :] -= T[r0:r0+nr, u] X[u, :] over the solved rows u (DMMA)
     const int ulo = UPPER ? r0 + nr : 0, uhi = UPPER ? k : r0;
     if (uhi > ulo) {
@@ -203,17 +636,20 @@ __global__ void __launch_bounds__(TNC) trsm_kernel(const Bases* __restrict__ bas
 }
 
 // ||A||_1 (max column abs sum) of each n x n matrix, before factoring.
+// One warp per column, lanes along the rows (coalesced).
 __global__ void norm1_kernel(const Bases* __restrict__ bases_ptr, const LuDesc* __restrict__ descs) {
   const Bases& bases = *bases_ptr;
   const LuDesc L = descs[blockIdx.x];
   __shared__ double rv[8];
   __shared__ int ri[8];
   const double* A = at<const double>(bases, L.A);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double best = 0.0;
-  for (int c = threadIdx.x; c < L.n; c += blockDim.x) {
+  for (int c = wid; c < L.n; c += nw) {
+    const double* col = A + (size_t)c * L.lda;
     double s = 0.0;
-    for (int r = 0; r < L.n; ++r) s += fabs(A[r + (size_t)c * L.lda]);
-    best = fmax(best, s);
+    for (int r = lane; r < L.n; r += 32) s += fabs(col[r]);
+    best = fmax(best, warp_sum(s));
   }
   ArgMax m = block_argmax(ArgMax{best, (int)threadIdx.x}, rv, ri);
   if (threadIdx.x == 0 && L.anorm != kNull) *at<double>(bases, L.anorm) = m.v;
@@ -225,6 +661,61 @@ __global__ void norm1_kernel(const Bases* __restrict__ bases_ptr, const LuDesc* 
 cudaError_t launch_panel_batched(const Bases* b, const PanelDesc* d, int count, int max_rows, int pb,
                                  cudaStream_t s) {
   if (count <= 0 || max_rows <= 0) return cudaSuccess;
+  // 256 threads, one to four rows each; PB x RPT doubles stay in registers
+  static const int impl = [] {
+    const char* e = getenv("HKS_PANEL_IMPL");
+    return e ? atoi(e) : 2;
+  }();
+  const int rpt = (max_rows + 255) / 256;
+  if (impl >= 10) {  // experiment variants (tools/kbench)
+    if (pb > 16 && max_rows <= 256) {
+      switch (impl) {
+        case 10: return launch_panel_loop<32, 1, 256, 1>(b, d, count, s);
+        case 11: return launch_panel_loop<32, 1, 256, 2>(b, d, count, s);
+        case 12: return launch_panel_loop<32, 1, 256, 4>(b, d, count, s);
+        case 13: return launch_panel_loop<32, 2, 128, 4>(b, d, count, s);
+        case 14: return launch_panel_loop<32, 4, 64, 4>(b, d, count, s);
+        case 15: return launch_panel_loop<32, 1, 256, 8>(b, d, count, s);
+        default: break;
+      }
+    }
+    if (pb <= 16 && max_rows <= 512) {
+      switch (impl) {
+        case 10: return launch_panel_loop<16, 2, 256, 1>(b, d, count, s);
+        case 11: return launch_panel_loop<16, 2, 256, 2>(b, d, count, s);
+        case 12: return launch_panel_loop<16, 2, 256, 4>(b, d, count, s);
+        case 13: return launch_panel_loop<16, 4, 128, 4>(b, d, count, s);
+        case 14: return launch_panel_loop<16, 1, 512, 4>(b, d, count, s);
+        case 15: return launch_panel_loop<16, 2, 256, 8>(b, d, count, s);
+        default: break;
+      }
+    }
+  }
+#define HKS_PANEL_CASE(PBV, R)                                                   \
+  case R:                                                                        \
+    if (impl == 2) return launch_panel_loop<PBV, R, 256, 8>(b, d, count, s);      \
+    if (impl == 1)                                                               \
+      panel_redux_kernel<PBV, R, 256><<<count, 256, 0, s>>>(b, d);               \
+    else                                                                         \
+      panel_reg_kernel<PBV, R, 256><<<count, 256, 0, s>>>(b, d);                 \
+    return cudaGetLastError();
+  if (pb > 16) {
+    switch (rpt) {
+      HKS_PANEL_CASE(32, 1)
+      HKS_PANEL_CASE(32, 2)
+      default: break;
+    }
+  } else {
+    switch (rpt) {
+      HKS_PANEL_CASE(16, 1)
+      HKS_PANEL_CASE(16, 2)
+      HKS_PANEL_CASE(16, 3)
+      HKS_PANEL_CASE(16, 4)
+      default: break;
+    }
+  }
+#undef HKS_PANEL_CASE
+  // taller panels: shared-memory panel
   const int ldp = max_rows;
   if (pb <= 16) {
     const size_t sm = (size_t)ldp * 16 * sizeof(double);
@@ -253,7 +744,7 @@ cudaError_t launch_trsm_batched(const Bases* b, const TrsmDesc* d, int count, in
   for (int first = 0; first < count; first += 65535) {
     const int cnt = count - first < 65535 ? count - first : 65535;
     dim3 grid((max_cols + TNC - 1) / TNC, cnt);
-    const size_t sm = (size_t)(128 * TXS + 32 * TTS) * sizeof(double);
+    const size_t sm = (size_t)(128 * TXS + 2 * 32 * TTS) * sizeof(double);
     if (upper) {
       cudaFuncSetAttribute(trsm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       trsm_kernel<true><<<grid, TNC, sm, s>>>(b, d + first);

@@ -473,7 +473,17 @@ struct Trsms {
 int fused_lu_max_count() {
   static const int v = [] {
     const char* e = getenv("HKS_FUSED_MAX");
-    return e ? atoi(e) : 300;
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+// Panel width: 32 while a panel's rows fit in registers without spilling
+// (lu2.cu: panel_reg_kernel), else 16.  HKS_PANEL_ROWS32 overrides the cut.
+int panel32_max_rows() {
+  static const int v = [] {
+    const char* e = getenv("HKS_PANEL_ROWS32");
+    return e ? atoi(e) : 256;
   }();
   return v;
 }
@@ -483,7 +493,7 @@ void add_lu_program(StepList& sl, const std::vector<LuJob>& jobs, bool with_norm
   int nmax = 0;
   for (auto& j : jobs) nmax = std::max(nmax, j.n);
   if (nmax == 0) return;
-  const int PB = nmax <= 640 ? 32 : 16;
+  const int PB = nmax <= panel32_max_rows() ? 32 : 16;
   if (with_norm) {
     std::vector<LuDesc> nd;
     for (auto& j : jobs) nd.push_back(LuDesc{j.A, j.piv, j.info, j.anorm, kNull, j.n, j.lda});
@@ -915,6 +925,54 @@ extern "C" int hks_layout(int64_t n, int64_t depth, int64_t max_rank, int64_t* s
   return HKS_OK;
 }
 
+// Dense LU / solve of one matrix through the same level programs the
+// factorization uses (add_lu_program / add_lu_solve_program), so the dense
+// entry points and the tree factorization share every kernel.
+extern "C" int hks_lu_factor(double* A, int64_t n, int64_t lda, int32_t* piv, int32_t* info_host, void* stream) {
+  if (n < 0 || lda < n) return set_error(HKS_ERR_INVALID, "hks_lu_factor: bad dims");
+  if (n == 0) {
+    if (info_host) *info_host = 0;
+    return HKS_OK;
+  }
+  cudaStream_t s = as_stream(stream);
+  int* dinfo = nullptr;
+  Bases* db = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&dinfo), sizeof(int), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(dinfo, 0, sizeof(int), s);
+  StepList sl;
+  add_lu_program(sl, {LuJob{abs_ref(A), (int)n, (int)lda, abs_ref(piv), abs_ref(dinfo), kNull, kNull, 0, 0}}, false);
+  if (e == cudaSuccess) e = upload_bases(make_bases(nullptr), &db, s);
+  if (e == cudaSuccess) e = sl.upload(s);
+  if (e == cudaSuccess) e = sl.run(db, nullptr, 0, KernelParams{}, s);
+  int info = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (db) cudaFreeAsync(db, s);
+  if (dinfo) cudaFreeAsync(dinfo, s);
+  if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_lu_factor: %s", cudaGetErrorString(e));
+  if (info_host) *info_host = info;
+  if (info) return set_error(HKS_ERR_SINGULAR, "singular matrix: zero pivot at elimination step %d", info - 1);
+  return HKS_OK;
+}
+
+extern "C" int hks_lu_solve(const double* LU, const int32_t* piv, int64_t n, int64_t lda, double* B, int64_t ldb,
+                            int64_t nrhs, void* stream) {
+  if (n < 0 || lda < n || ldb < n || nrhs < 0) return set_error(HKS_ERR_INVALID, "hks_lu_solve: bad dims");
+  if (n == 0 || nrhs == 0) return HKS_OK;
+  cudaStream_t s = as_stream(stream);
+  StepList sl;
+  add_lu_solve_program(sl, {LuJob{abs_ref(LU), (int)n, (int)lda, abs_ref(piv), kNull, kNull, abs_ref(B), (int)nrhs,
+                                  (int)ldb}});
+  Bases* db = nullptr;
+  cudaError_t e = upload_bases(make_bases(nullptr), &db, s);
+  if (e == cudaSuccess) e = sl.upload(s);
+  if (e == cudaSuccess) e = sl.run(db, nullptr, 0, KernelParams{}, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // before sl's device arena is freed
+  if (db) cudaFreeAsync(db, s);
+  if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_lu_solve: %s", cudaGetErrorString(e));
+  return HKS_OK;
+}
+
 extern "C" int hks_plan_create(hks_plan** out, const double* X, int64_t n, int64_t d, int64_t depth,
                                int64_t max_rank, const int64_t* ranks_host, const hks_kernel* kern) {
   if (!out || !X || !ranks_host || !kern || n < 1 || d < 1 || depth < 0 || max_rank < 1)
@@ -1144,6 +1202,7 @@ extern "C" int hks_profile(int32_t enable, double* out_host) {
   for (auto& p : g_prof.pending) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, p.a, p.b);
+    if (getenv("HKS_TRACE")) fprintf(stderr, "HKS_TRACE %d %.5f %.6g %.6g\n", p.kind, ms, p.flops, p.bytes);
     g_prof.launches[p.kind] += 1;
     g_prof.ms[p.kind] += ms;
     g_prof.flops[p.kind] += p.flops;
