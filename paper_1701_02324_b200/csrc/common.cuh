@@ -168,9 +168,23 @@ struct LuSolveDesc {
 };
 
 // Factor rows p0..n-1 of panel columns [p0, p0 + pb) (partial pivoting).
+// Optional int32 row permutations over absolute positions (kNull: skip):
+// after the panel, position i holds the original row tperm[i] (total, since
+// column 0), the row that was at position gperm[i] when the 128-column group
+// starting at g0 began, and the row that was at sig[i] when this panel began.
 struct PanelDesc {
   Ref A, piv, info;
   int lda, n, p0, pb;
+  Ref tperm, sig, gperm;
+  int g0, pad;
+};
+
+// Row gather A[i, c] := A[perm[i], c] for rows [r0, r1) and columns [c0, c1)
+// (perm maps [r0, r1) onto itself): the interchanges of a pivot sequence
+// applied in one parallel pass.
+struct GatherDesc {
+  Ref A, perm;
+  int lda, r0, r1, c0, c1, pad;
 };
 
 // Row interchanges piv[r0..r1) applied to columns [c0, c1) of A.

@@ -85,268 +85,6 @@ __global__ void __launch_bounds__(PT) panel_kernel(const Bases* __restrict__ bas
   }
 }
 
-// Register-resident panel factorization (same arithmetic as panel_kernel):
-// thread t owns local rows t, t + NT, ... (RPT of them) and keeps their PB
-// panel entries in registers, so the rank-1 update of each step is RPT * PB
-// independent FMAs against a broadcast pivot row.  One barrier per column:
-// every warp publishes its argmax candidate together with the candidate's
-// whole row (and the owner of row jj publishes row jj) into a
-// parity-double-buffered shared slot; after the barrier every thread picks
-// the winner redundantly and reads the pivot row straight from the winning
-// warp's slot.
-template <int PB, int RPT, int NT>
-__global__ void __launch_bounds__(NT) panel_reg_kernel(const Bases* __restrict__ bases_ptr,
-                                                       const PanelDesc* __restrict__ descs) {
-  constexpr int NW = NT / 32;
-  const Bases& bases = *bases_ptr;
-  const PanelDesc D = descs[blockIdx.x];
-  double* A = at<double>(bases, D.A);
-  int* piv = at<int>(bases, D.piv);
-  const int lda = D.lda, p0 = D.p0, pb = D.pb, mr = D.n - D.p0;
-  __shared__ double rows[2][NW + 1][PB];  // [parity][warp candidate rows..., row jj]
-  __shared__ double cval[2][NW];
-  __shared__ int cidx[2][NW];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  double v[RPT][PB];
-#pragma unroll
-  for (int c = 0; c < PB; ++c)
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) {
-      const int i = tid + q * NT;
-      v[q][c] = (i < mr && c < pb) ? A[p0 + i + (size_t)(p0 + c) * lda] : 0.0;
-    }
-  int info = 0;
-#pragma unroll
-  for (int jj = 0; jj < PB; ++jj) {
-    if (jj >= pb) break;
-    const int par = jj & 1;
-    ArgMax a{-1.0, 0x7fffffff};
-    int aq = 0;
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) {
-      const int i = tid + q * NT;
-      if (i >= jj && i < mr) {
-        const ArgMax b{fabs(v[q][jj]), i};
-        if (b.v > a.v || (b.v == a.v && b.i < a.i)) {
-          a = b;
-          aq = q;
-        }
-      }
-    }
-    const ArgMax w = warp_argmax(a);
-    if (a.i == w.i && a.i != 0x7fffffff) {  // this lane holds the warp's candidate
-#pragma unroll
-      for (int q = 0; q < RPT; ++q)
-        if (q == aq)
-#pragma unroll
-          for (int c = 0; c < PB; ++c) rows[par][wid][c] = v[q][c];
-    }
-    if (lane == 0) {
-      cval[par][wid] = w.v;
-      cidx[par][wid] = w.i;
-    }
-    if (tid == jj)  // jj < PB <= NT: row jj is thread jj's first row
-#pragma unroll
-      for (int c = 0; c < PB; ++c) rows[par][NW][c] = v[0][c];
-    __syncthreads();
-    ArgMax g{cval[par][0], cidx[par][0]};
-    int gw = 0;
-#pragma unroll
-    for (int w2 = 1; w2 < NW; ++w2) {
-      const ArgMax b{cval[par][w2], cidx[par][w2]};
-      if (b.v > g.v || (b.v == g.v && b.i < g.i)) {
-        g = b;
-        gw = w2;
-      }
-    }
-    if (g.i == 0x7fffffff) {  // no comparable candidate (NaN column): no interchange
-      g.i = jj;
-      gw = NW;
-    }
-    const int p = g.i;
-    const double* pr = rows[par][gw];
-    const double* jr = rows[par][NW];
-    const double pv = pr[jj];
-    if (tid == 0) {
-      piv[p0 + jj] = p0 + p;
-      if (pv == 0.0 && info == 0) info = p0 + jj + 1;
-    }
-    const bool recip = fabs(pv) >= DBL_MIN;
-    const double inv = 1.0 / pv;
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) {
-      const int i = tid + q * NT;
-      if (p != jj) {  // interchange rows jj and p
-        if (i == jj)
-#pragma unroll
-          for (int c = 0; c < PB; ++c) v[q][c] = pr[c];
-        if (i == p)
-#pragma unroll
-          for (int c = 0; c < PB; ++c) v[q][c] = jr[c];
-      }
-      if (i > jj && i < mr) {  // scale (dgetf2: reciprocal when safe), rank-1 update
-        double l = v[q][jj];
-        if (pv != 0.0) {
-          l = recip ? l * inv : l / pv;
-          v[q][jj] = l;
-        }
-#pragma unroll
-        for (int c = jj + 1; c < PB; ++c) v[q][c] -= l * pr[c];
-      }
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < PB; ++c)
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) {
-      const int i = tid + q * NT;
-      if (i < mr && c < pb) A[p0 + i + (size_t)(p0 + c) * lda] = v[q][c];
-    }
-  if (tid == 0 && info && D.info != kNull) {
-    int* g = at<int>(bases, D.info);
-    if (*g == 0) *g = info;  // panels run in order: keep the first zero pivot
-  }
-}
-
-#ifdef PANEL_PROF
-__device__ long long g_pprof[32][8];
-#define PPROF(m)                                                        \
-  do {                                                                  \
-    if (blockIdx.x == 0 && tid == 0) g_pprof[jj][m] = clock64();        \
-  } while (0)
-#else
-#define PPROF(m) \
-  do {           \
-  } while (0)
-#endif
-
-// Same panel, cheaper pivot search: |x| as a 64-bit key (IEEE order of a
-// non-negative double is its unsigned bit order; bit 63 marks a live row)
-// reduced with three 32-bit warp reductions (max high word, max low word
-// among the high-word winners, min row index among the key winners -- the
-// lowest index wins ties, as idamax), and the per-warp winners combined the
-// same way by the first NW lanes of every warp after the barrier.  The
-// winning warp follows from the pivot row (rows are dealt round-robin).
-template <int PB, int RPT, int NT>
-__global__ void __launch_bounds__(NT) panel_redux_kernel(const Bases* __restrict__ bases_ptr,
-                                                         const PanelDesc* __restrict__ descs) {
-  constexpr int NW = NT / 32;
-  const Bases& bases = *bases_ptr;
-  const PanelDesc D = descs[blockIdx.x];
-  double* A = at<double>(bases, D.A);
-  int* piv = at<int>(bases, D.piv);
-  const int lda = D.lda, p0 = D.p0, pb = D.pb, mr = D.n - D.p0;
-  __shared__ __align__(16) double rows[2][NW + 1][PB];  // [parity][warp candidate rows..., row jj]
-  __shared__ unsigned khi[2][NW], klo[2][NW], kid[2][NW];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  double v[RPT][PB];
-#pragma unroll
-  for (int c = 0; c < PB; ++c)
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) {
-      const int i = tid + q * NT;
-      v[q][c] = (i < mr && c < pb) ? A[p0 + i + (size_t)(p0 + c) * lda] : 0.0;
-    }
-  int info = 0;
-#pragma unroll
-  for (int jj = 0; jj < PB; ++jj) {
-    if (jj >= pb) break;
-    PPROF(0);
-    const int par = jj & 1;
-    unsigned long long key = 0;
-    int ai = 0x7fffffff, aq = 0;
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) {
-      const int i = tid + q * NT;
-      if (i >= jj && i < mr) {
-        const unsigned long long k = (unsigned long long)__double_as_longlong(fabs(v[q][jj])) | (1ull << 63);
-        if (k > key) {  // rows ascend with q: strict > keeps the lowest index on ties
-          key = k;
-          ai = i;
-          aq = q;
-        }
-      }
-    }
-    PPROF(1);
-    const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
-    const unsigned m1 = __reduce_max_sync(0xffffffffu, hi);
-    const unsigned m2 = __reduce_max_sync(0xffffffffu, hi == m1 ? lo : 0u);
-    const unsigned id = __reduce_min_sync(0xffffffffu, (hi == m1 && lo == m2) ? (unsigned)ai : 0xffffffffu);
-    PPROF(2);
-    if (m1 != 0u && (unsigned)ai == id) {  // this lane holds the warp's candidate row
-#pragma unroll
-      for (int q = 0; q < RPT; ++q)
-        if (q == aq)
-#pragma unroll
-          for (int c = 0; c < PB; c += 2)
-            *reinterpret_cast<double2*>(&rows[par][wid][c]) = make_double2(v[q][c], v[q][c + 1]);
-    }
-    if (lane == 0) {
-      khi[par][wid] = m1;
-      klo[par][wid] = m2;
-      kid[par][wid] = id;
-    }
-    if (tid == jj)  // jj < PB <= NT: row jj is thread jj's first row
-#pragma unroll
-      for (int c = 0; c < PB; c += 2)
-        *reinterpret_cast<double2*>(&rows[par][NW][c]) = make_double2(v[0][c], v[0][c + 1]);
-    PPROF(3);
-    __syncthreads();
-    PPROF(4);
-    const unsigned h2 = lane < NW ? khi[par][lane] : 0u, l2 = lane < NW ? klo[par][lane] : 0u;
-    const unsigned i2 = lane < NW ? kid[par][lane] : 0xffffffffu;
-    const unsigned g1 = __reduce_max_sync(0xffffffffu, h2);
-    const unsigned g2 = __reduce_max_sync(0xffffffffu, h2 == g1 ? l2 : 0u);
-    const unsigned gi = __reduce_min_sync(0xffffffffu, (h2 == g1 && l2 == g2) ? i2 : 0xffffffffu);
-    // no live candidate (NaN-free empty search cannot happen; guard anyway): no interchange
-    const int p = g1 != 0u ? (int)gi : jj;
-    const int gw = g1 != 0u ? (p % NT) >> 5 : NW;
-    PPROF(5);
-    const double* pr = rows[par][gw];
-    const double* jr = rows[par][NW];
-    const double pv = pr[jj];
-    if (tid == 0) {
-      piv[p0 + jj] = p0 + p;
-      if (pv == 0.0 && info == 0) info = p0 + jj + 1;
-    }
-    const bool recip = fabs(pv) >= DBL_MIN;
-    const double inv = 1.0 / pv;
-    PPROF(6);
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) {
-      const int i = tid + q * NT;
-      if (p != jj) {  // interchange rows jj and p
-        if (i == jj)
-#pragma unroll
-          for (int c = 0; c < PB; ++c) v[q][c] = pr[c];
-        if (i == p)
-#pragma unroll
-          for (int c = 0; c < PB; ++c) v[q][c] = jr[c];
-      }
-      if (i > jj && i < mr) {  // scale (dgetf2: reciprocal when safe), rank-1 update
-        double l = v[q][jj];
-        if (pv != 0.0) {
-          l = recip ? l * inv : l / pv;
-          v[q][jj] = l;
-        }
-#pragma unroll
-        for (int c = jj + 1; c < PB; ++c) v[q][c] -= l * pr[c];
-      }
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < PB; ++c)
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) {
-      const int i = tid + q * NT;
-      if (i < mr && c < pb) A[p0 + i + (size_t)(p0 + c) * lda] = v[q][c];
-    }
-  if (tid == 0 && info && D.info != kNull) {
-    int* g = at<int>(bases, D.info);
-    if (*g == 0) *g = info;  // panels run in order: keep the first zero pivot
-  }
-}
-
 // Panel factorization as a loop over blocks of U columns (fully unrolled
 // 32-column variants are instruction-cache bound: the straight-line code
 // does not fit and every column refetches it).  Row interchanges are
@@ -387,6 +125,16 @@ __global__ void __launch_bounds__(NT) panel_loop_kernel(const Bases* __restrict_
       const int i = tid + q * NT;
       w[q][c] = (i < mr && c < pb) ? A[p0 + i + (size_t)(p0 + c) * lda] : 0.0;
     }
+  // incoming permutations of this CTA's physical rows (identity where they start)
+  int tp[RPT], gp[RPT];
+  const int* tperm = D.tperm != kNull ? at<const int>(bases, D.tperm) : nullptr;
+  const int* gperm = D.gperm != kNull ? at<const int>(bases, D.gperm) : nullptr;
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int i = p0 + tid + q * NT;
+    tp[q] = (tperm && p0 > 0 && i < D.n) ? tperm[i] : i;
+    gp[q] = (gperm && p0 > D.g0 && i < D.n) ? gperm[i] : i;
+  }
   int info = 0;
 #pragma unroll 1
   for (int j0 = 0; j0 < pb; j0 += U) {
@@ -394,7 +142,6 @@ __global__ void __launch_bounds__(NT) panel_loop_kernel(const Bases* __restrict_
     for (int u = 0; u < U; ++u) {
       const int jj = j0 + u;
       if (jj < pb) {
-        PPROF(0);
         const int par = jj & 1;
         unsigned long long key = 0;
         int ai = 0x7fffffff, aq = 0;
@@ -409,12 +156,10 @@ __global__ void __launch_bounds__(NT) panel_loop_kernel(const Bases* __restrict_
             }
           }
         }
-        PPROF(1);
         const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
         const unsigned m1 = __reduce_max_sync(0xffffffffu, hi);
         const unsigned m2 = __reduce_max_sync(0xffffffffu, hi == m1 ? lo : 0u);
         const unsigned id = __reduce_min_sync(0xffffffffu, (hi == m1 && lo == m2) ? (unsigned)ai : 0xffffffffu);
-        PPROF(2);
         double* mine = cand + (par * NW + wid) * PB;
         if (m1 != 0u && (unsigned)ai == id) {  // this lane holds the warp's candidate row
 #pragma unroll
@@ -429,9 +174,7 @@ __global__ void __launch_bounds__(NT) panel_loop_kernel(const Bases* __restrict_
           klo[par][wid] = m2;
           kid[par][wid] = id;
         }
-        PPROF(3);
         __syncthreads();
-        PPROF(4);
         const unsigned h2 = lane < NW ? khi[par][lane] : 0u, l2 = lane < NW ? klo[par][lane] : 0u;
         const unsigned i2 = lane < NW ? kid[par][lane] : 0xffffffffu;
         const unsigned g1 = __reduce_max_sync(0xffffffffu, h2);
@@ -440,7 +183,6 @@ __global__ void __launch_bounds__(NT) panel_loop_kernel(const Bases* __restrict_
         const unsigned win = __ballot_sync(0xffffffffu, lane < NW && h2 == g1 && l2 == g2 && i2 == gi);
         const int gw = win ? __ffs(win) - 1 : 0;
         const int p = g1 != 0u ? (int)gi : jj;
-        PPROF(5);
         const double* pr = cand + (par * NW + gw) * PB;
         const double pv = pr[u];
         if (tid == 0) {
@@ -449,7 +191,6 @@ __global__ void __launch_bounds__(NT) panel_loop_kernel(const Bases* __restrict_
         }
         const bool recip = fabs(pv) >= DBL_MIN;
         const double inv = 1.0 / pv;
-        PPROF(6);
 #pragma unroll
         for (int q = 0; q < RPT; ++q) {
           if (lab[q] == p)  // interchange rows jj and p: relabel
@@ -480,8 +221,13 @@ __global__ void __launch_bounds__(NT) panel_loop_kernel(const Bases* __restrict_
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < RPT; ++q)
-    if (lab[q] < mr)
+    if (lab[q] < mr) {
       for (int c = 0; c < pb; ++c) A[p0 + lab[q] + (size_t)(p0 + c) * lda] = done[c * NR + tid + q * NT];
+      const int pos = p0 + lab[q];
+      if (D.sig != kNull) at<int>(bases, D.sig)[pos] = p0 + tid + q * NT;
+      if (tperm) at<int>(bases, D.tperm)[pos] = tp[q];
+      if (gperm) at<int>(bases, D.gperm)[pos] = gp[q];
+    }
   if (tid == 0 && info && D.info != kNull) {
     int* g = at<int>(bases, D.info);
     if (*g == 0) *g = info;  // panels run in order: keep the first zero pivot
@@ -495,6 +241,33 @@ cudaError_t launch_panel_loop(const Bases* b, const PanelDesc* d, int count, cud
   cudaFuncSetAttribute(panel_loop_kernel<PB, RPT, NT, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   panel_loop_kernel<PB, RPT, NT, U><<<count, NT, sm, s>>>(b, d);
   return cudaGetLastError();
+}
+
+// A[i, c] := A[perm[i], c], rows [r0, r1), a block of cb columns per CTA
+// staged through shared memory (all reads before any write); rows the
+// permutation leaves in place are neither read nor written.
+__global__ void __launch_bounds__(256) gather_rows_kernel(const Bases* __restrict__ bases_ptr,
+                                                          const GatherDesc* __restrict__ descs, int cb) {
+  const Bases& bases = *bases_ptr;
+  const GatherDesc D = descs[blockIdx.y];
+  const int c0 = D.c0 + blockIdx.x * cb;
+  if (c0 >= D.c1) return;
+  const int nc = min(cb, D.c1 - c0), nr = D.r1 - D.r0;
+  double* A = at<double>(bases, D.A) + D.r0 + (size_t)c0 * D.lda;
+  const int* perm = at<const int>(bases, D.perm) + D.r0;
+  extern __shared__ double gsm[];
+  int* sp = reinterpret_cast<int*>(gsm + (size_t)nr * cb);
+  for (int i = threadIdx.x; i < nr; i += blockDim.x) sp[i] = perm[i] - D.r0;
+  __syncthreads();
+  for (int c = 0; c < nc; ++c)
+    for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+      const int src = sp[i];
+      if (src != i) gsm[c * nr + i] = A[src + (size_t)c * D.lda];
+    }
+  __syncthreads();
+  for (int c = 0; c < nc; ++c)
+    for (int i = threadIdx.x; i < nr; i += blockDim.x)
+      if (sp[i] != i) A[i + (size_t)c * D.lda] = gsm[c * nr + i];
 }
 
 // Row interchanges piv[r0..r1) applied in order to columns [c0, c1).
@@ -602,8 +375,8 @@ __global__ void __launch_bounds__(TNC) trsm_kernel(const Bases* __restrict__ bas
             const int rr = i * 8 + fr, c = cb + j * 8 + 2 * fc + h;
             if (rr < nr) X[(r0 + rr) * TXS + c] -= acc[i][j][h];
           }
-      __syncthreads();
     }
+    __syncthreads();
     // diagonal block: thread = column, values in registers
     if (tid < nc) {
       double x[32];
@@ -619,7 +392,7 @@ __global__ void __launch_bounds__(TNC) trsm_kernel(const Bases* __restrict__ bas
 #pragma unroll
         for (int j = 31; j >= 0; --j) {
           if (j < nr) {
-            x[j] /= Ts[j * TTS + r0 + j];
+            x[j] /= Ts[j * TTS + r0 + j];  // a true division, as dtrsm (c5 is sensitive to it)
 #pragma unroll
             for (int i = 0; i < j; ++i) x[i] -= Ts[i * TTS + r0 + j] * x[j];
           }
@@ -661,61 +434,22 @@ __global__ void norm1_kernel(const Bases* __restrict__ bases_ptr, const LuDesc* 
 cudaError_t launch_panel_batched(const Bases* b, const PanelDesc* d, int count, int max_rows, int pb,
                                  cudaStream_t s) {
   if (count <= 0 || max_rows <= 0) return cudaSuccess;
-  // 256 threads, one to four rows each; PB x RPT doubles stay in registers
-  static const int impl = [] {
-    const char* e = getenv("HKS_PANEL_IMPL");
-    return e ? atoi(e) : 2;
-  }();
+  // 256 threads, one to four rows each; PB x RPT doubles stay in registers.
+  // plan.cu uses pb = 32 only for rows <= 256 (panel32_max_rows).
   const int rpt = (max_rows + 255) / 256;
-  if (impl >= 10) {  // experiment variants (tools/kbench)
-    if (pb > 16 && max_rows <= 256) {
-      switch (impl) {
-        case 10: return launch_panel_loop<32, 1, 256, 1>(b, d, count, s);
-        case 11: return launch_panel_loop<32, 1, 256, 2>(b, d, count, s);
-        case 12: return launch_panel_loop<32, 1, 256, 4>(b, d, count, s);
-        case 13: return launch_panel_loop<32, 2, 128, 4>(b, d, count, s);
-        case 14: return launch_panel_loop<32, 4, 64, 4>(b, d, count, s);
-        case 15: return launch_panel_loop<32, 1, 256, 8>(b, d, count, s);
-        default: break;
-      }
-    }
-    if (pb <= 16 && max_rows <= 512) {
-      switch (impl) {
-        case 10: return launch_panel_loop<16, 2, 256, 1>(b, d, count, s);
-        case 11: return launch_panel_loop<16, 2, 256, 2>(b, d, count, s);
-        case 12: return launch_panel_loop<16, 2, 256, 4>(b, d, count, s);
-        case 13: return launch_panel_loop<16, 4, 128, 4>(b, d, count, s);
-        case 14: return launch_panel_loop<16, 1, 512, 4>(b, d, count, s);
-        case 15: return launch_panel_loop<16, 2, 256, 8>(b, d, count, s);
-        default: break;
-      }
-    }
-  }
-#define HKS_PANEL_CASE(PBV, R)                                                   \
-  case R:                                                                        \
-    if (impl == 2) return launch_panel_loop<PBV, R, 256, 8>(b, d, count, s);      \
-    if (impl == 1)                                                               \
-      panel_redux_kernel<PBV, R, 256><<<count, 256, 0, s>>>(b, d);               \
-    else                                                                         \
-      panel_reg_kernel<PBV, R, 256><<<count, 256, 0, s>>>(b, d);                 \
-    return cudaGetLastError();
   if (pb > 16) {
-    switch (rpt) {
-      HKS_PANEL_CASE(32, 1)
-      HKS_PANEL_CASE(32, 2)
-      default: break;
-    }
+    if (rpt == 1) return launch_panel_loop<32, 1, 256, 8>(b, d, count, s);
   } else {
     switch (rpt) {
-      HKS_PANEL_CASE(16, 1)
-      HKS_PANEL_CASE(16, 2)
-      HKS_PANEL_CASE(16, 3)
-      HKS_PANEL_CASE(16, 4)
+      case 1: return launch_panel_loop<16, 1, 256, 8>(b, d, count, s);
+      case 2: return launch_panel_loop<16, 2, 256, 8>(b, d, count, s);
+      case 3: return launch_panel_loop<16, 3, 256, 8>(b, d, count, s);
+      case 4: return launch_panel_loop<16, 4, 256, 8>(b, d, count, s);
       default: break;
     }
   }
-#undef HKS_PANEL_CASE
-  // taller panels: shared-memory panel
+  // taller panels: shared-memory panel (no permutation tracking: plan.cu
+  // falls back to interchange sweeps for matrices above kPermMaxRows)
   const int ldp = max_rows;
   if (pb <= 16) {
     const size_t sm = (size_t)ldp * 16 * sizeof(double);
@@ -725,6 +459,20 @@ cudaError_t launch_panel_batched(const Bases* b, const PanelDesc* d, int count, 
     const size_t sm = (size_t)ldp * 32 * sizeof(double);
     cudaFuncSetAttribute(panel_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     panel_kernel<32><<<count, PT, sm, s>>>(b, d, ldp);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_batched(const Bases* b, const GatherDesc* d, int count, int max_rows, int max_cols,
+                                  cudaStream_t s) {
+  if (count <= 0 || max_rows <= 0 || max_cols <= 0) return cudaSuccess;
+  int cb = 8192 / max_rows;  // <= 64 KB of staged rows per CTA
+  cb = cb < 1 ? 1 : cb > 32 ? 32 : cb;
+  const size_t sm = (size_t)max_rows * cb * sizeof(double) + (size_t)max_rows * sizeof(int);
+  cudaFuncSetAttribute(gather_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  for (int first = 0; first < count; first += 65535) {
+    const int cnt = count - first < 65535 ? count - first : 65535;
+    gather_rows_kernel<<<dim3((max_cols + cb - 1) / cb, cnt), 256, sm, s>>>(b, d + first, cb);
   }
   return cudaGetLastError();
 }

@@ -47,11 +47,11 @@ Layout make_layout(int64_t n, int64_t depth, int64_t s) {
     }
     if (leaf) {
       put(HKS_BUF_LEAF_LU, i, L.size[i] * L.size[i]);
-      put(HKS_BUF_LEAF_PIV, i, L.size[i]);
+      put(HKS_BUF_LEAF_PIV, i, 4 * L.size[i]);  // pivots | total perm | panel perm | group perm
       if (i > 0) put(HKS_BUF_PHI, i, L.size[i] * L.rcap[i]);
     } else {
       put(HKS_BUF_Z_LU, i, L.ccap[i] * L.ccap[i]);
-      put(HKS_BUF_Z_PIV, i, L.ccap[i]);
+      put(HKS_BUF_Z_PIV, i, 4 * L.ccap[i]);  // pivots | total perm | panel perm | group perm
       if (i > 0) put(HKS_BUF_PUSH, i, L.ccap[i] * L.rcap[i]);
       put(HKS_BUF_COUP, i, L.rcap[2 * i + 1] * L.rcap[2 * i + 2]);
     }
@@ -168,6 +168,9 @@ cudaError_t StepList::run(const Bases* b, const double* X, int d, const KernelPa
         break;
       case ST_SWAP:
         e = launch_swap_batched(b, (const SwapDesc*)st.d, st.count, st.p0, s);
+        break;
+      case ST_GATHER:
+        e = launch_gather_batched(b, (const GatherDesc*)st.d, st.count, st.p0, st.p1, s);
         break;
       case ST_TRSM_L:
       case ST_TRSM_U:
@@ -378,6 +381,9 @@ struct Ctx {
   Ref phi(int64_t i) const { return D(HKS_BUF_PHI, L.off[HKS_BUF_PHI][i]); }
   Ref z_lu(int64_t i) const { return D(HKS_BUF_Z_LU, L.off[HKS_BUF_Z_LU][i]); }
   Ref z_piv(int64_t i) const { return I32(HKS_BUF_Z_PIV, L.off[HKS_BUF_Z_PIV][i]); }
+  // permutation workspace behind the pivots: [total | panel | group], `cap` ints each
+  Ref leaf_ws(int64_t i) const { return I32(HKS_BUF_LEAF_PIV, L.off[HKS_BUF_LEAF_PIV][i] + L.size[i]); }
+  Ref z_ws(int64_t i) const { return I32(HKS_BUF_Z_PIV, L.off[HKS_BUF_Z_PIV][i] + L.ccap[i]); }
   Ref push(int64_t i) const { return D(HKS_BUF_PUSH, L.off[HKS_BUF_PUSH][i]); }
   Ref coup(int64_t i) const { return D(HKS_BUF_COUP, L.off[HKS_BUF_COUP][i]); }
   Ref skel(int64_t i) const { return make_ref(HKS_BUF_SKEL, (uint64_t)L.off[HKS_BUF_SKEL][i] * 8); }
@@ -407,6 +413,30 @@ struct LuJob {
   Ref piv, info, anorm;
   Ref B;
   int r, ldb;
+  Ref ws = kNull;  // int32 [total perm | panel perm | group perm], `cap` ints each (kNull: swap sweeps)
+  int cap = 0;
+};
+
+// Row permutations replace interchange sweeps for matrices up to this size
+// (the register panel kernels track them; lu2.cu).
+constexpr int kPermMaxRows = 1024;
+
+struct Gathers {
+  std::vector<GatherDesc> v;
+  int mr = 0, mc = 0;
+  void add(Ref A, int lda, Ref perm, int r0, int r1, int c0, int c1) {
+    if (r1 - r0 <= 1 || c1 <= c0) return;
+    v.push_back(GatherDesc{A, perm, lda, r0, r1, c0, c1, 0});
+    mr = std::max(mr, r1 - r0);
+    mc = std::max(mc, c1 - c0);
+  }
+  void flush(StepList& sl) {
+    double bytes = 0;
+    for (auto& d : v) bytes += 16.0 * (d.r1 - d.r0) * (d.c1 - d.c0);
+    sl.add(ST_GATHER, v, mr, mc, 0.0, bytes);
+    v.clear();
+    mr = mc = 0;
+  }
 };
 
 constexpr int kGroup = 128;  // rank of each trailing update (and TRSM block)
@@ -512,9 +542,34 @@ void add_lu_program(StepList& sl, const std::vector<LuJob>& jobs, bool with_norm
     sl.add(ST_LU_FUSED, fd, nmax, rmax, f, bytes);
     return;
   }
+  // Interchanges: with permutation workspaces, one gather per pivot range
+  // (the panel kernel records where every row went); otherwise LAPACK-style
+  // sequential sweeps.  kind 0: this panel's pivots (rows from the panel's
+  // first column), 1: the group's pivots so far (rows from g0).
+  // Gathers over the panel/group permutations were measured slower than the
+  // pivot sweeps inside the factorization (many short CTAs); the panels
+  // still record the total permutation (tperm) for the solves.
+  bool track = nmax <= kPermMaxRows;
+  for (auto& j : jobs) track &= j.ws != kNull;
+  const bool use_perm = track && getenv("HKS_LU_GATHER") != nullptr;
+  auto ws_perm = [](const LuJob& j, int which) { return j.ws + (uint64_t)which * j.cap * 4; };  // 0 total, 1 panel, 2 group
+  struct Ix {
+    Swaps sw;
+    Gathers ga;
+    void flush(StepList& sl) {
+      sw.flush(sl);
+      ga.flush(sl);
+    }
+  };
+  auto interchange = [&](Ix& ix, const LuJob& j, Ref A, int lda, int kind, int r0, int r1, int c0, int c1) {
+    if (use_perm)
+      ix.ga.add(A, lda, ws_perm(j, kind == 0 ? 1 : 2), r0, j.n, c0, c1);
+    else
+      ix.sw.add(A, j.piv, lda, r0, r1, c0, c1);
+  };
   for (int g0 = 0; g0 < nmax; g0 += kGroup) {
     for (int p0 = g0; p0 < g0 + kGroup && p0 < nmax; p0 += PB) {
-      Swaps sw;
+      Ix ix;
       Trsms tr;
       Gemms gm;
       Panels pn;
@@ -526,32 +581,39 @@ void add_lu_program(StepList& sl, const std::vector<LuJob>& jobs, bool with_norm
           // previous panel's interchanges on the group's earlier L columns, and
           // all of the group's interchanges so far on this panel's columns
           const int q0 = p0 - PB;
-          sw.add(j.A, j.piv, j.lda, q0, p0, g0, q0);
-          sw.add(j.A, j.piv, j.lda, g0, p0, p0, p0 + pb);
+          interchange(ix, j, j.A, j.lda, 0, q0, p0, g0, q0);
+          interchange(ix, j, j.A, j.lda, 1, g0, p0, p0, p0 + pb);
           tr.add(elem(j.A, g0, g0, j.lda), j.lda, elem(j.A, g0, p0, j.lda), j.lda, p0 - g0, pb);
           gm.add(elem(j.A, p0, g0, j.lda), j.lda, 0, elem(j.A, g0, p0, j.lda), j.lda, 0, elem(j.A, p0, p0, j.lda),
                  j.lda, j.n - p0, pb, p0 - g0, -1.0, 1.0);
         }
-        pn.v.push_back(PanelDesc{j.A, j.piv, j.info, j.lda, j.n, p0, pb});
+        PanelDesc d{j.A, j.piv, j.info, j.lda, j.n, p0, pb, kNull, kNull, kNull, g0, 0};
+        if (track) d.tperm = ws_perm(j, 0);
+        if (use_perm) {
+          d.tperm = ws_perm(j, 0);
+          d.sig = ws_perm(j, 1);
+          d.gperm = ws_perm(j, 2);
+        }
+        pn.v.push_back(d);
         pn.rows = std::max(pn.rows, j.n - p0);
       }
-      sw.flush(sl);
+      ix.flush(sl);
       tr.flush(sl, false);
       gm.flush(sl);
       pn.flush(sl, PB);
     }
     // the group's interchanges everywhere else, U rows of the group, trailing update
-    Swaps sw;
+    Ix ix;
     Trsms tr;
     Gemms gm;
     for (auto& j : jobs) {
       if (g0 >= j.n) continue;
       const int gb = std::min(kGroup, j.n - g0), ge = g0 + gb;
       const int last = g0 + ((gb - 1) / PB) * PB;  // first column of the group's last panel
-      sw.add(j.A, j.piv, j.lda, last, ge, g0, last);
-      sw.add(j.A, j.piv, j.lda, g0, ge, 0, g0);
-      sw.add(j.A, j.piv, j.lda, g0, ge, ge, j.n);
-      if (j.r > 0) sw.add(j.B, j.piv, j.ldb, g0, ge, 0, j.r);
+      interchange(ix, j, j.A, j.lda, 0, last, ge, g0, last);
+      interchange(ix, j, j.A, j.lda, 1, g0, ge, 0, g0);
+      interchange(ix, j, j.A, j.lda, 1, g0, ge, ge, j.n);
+      if (j.r > 0) interchange(ix, j, j.B, j.ldb, 1, g0, ge, 0, j.r);
       tr.add(elem(j.A, g0, g0, j.lda), j.lda, elem(j.A, g0, ge, j.lda), j.lda, gb, j.n - ge);
       if (j.r > 0) tr.add(elem(j.A, g0, g0, j.lda), j.lda, elem(j.B, g0, 0, j.ldb), j.ldb, gb, j.r);
       gm.add(elem(j.A, ge, g0, j.lda), j.lda, 0, elem(j.A, g0, ge, j.lda), j.lda, 0, elem(j.A, ge, ge, j.lda), j.lda,
@@ -560,7 +622,7 @@ void add_lu_program(StepList& sl, const std::vector<LuJob>& jobs, bool with_norm
         gm.add(elem(j.A, ge, g0, j.lda), j.lda, 0, elem(j.B, g0, 0, j.ldb), j.ldb, 0, elem(j.B, ge, 0, j.ldb), j.ldb,
                j.n - ge, j.r, gb, -1.0, 1.0);
     }
-    sw.flush(sl);
+    ix.flush(sl);
     tr.flush(sl, false);
     gm.flush(sl);
   }
@@ -589,9 +651,16 @@ void add_lu_solve_program(StepList& sl, const std::vector<LuJob>& jobs) {
   for (auto& j : jobs) nmax = std::max(nmax, j.n);
   if (nmax == 0) return;
   Swaps sw;
-  for (auto& j : jobs)
-    if (j.r > 0) sw.add(j.B, j.piv, j.ldb, 0, j.n, 0, j.r);
+  Gathers ga;
+  for (auto& j : jobs) {
+    if (j.r <= 0) continue;
+    if (j.ws != kNull && j.n <= kPermMaxRows)
+      ga.add(j.B, j.ldb, j.ws, 0, j.n, 0, j.r);  // total permutation recorded by the factorization
+    else
+      sw.add(j.B, j.piv, j.ldb, 0, j.n, 0, j.r);
+  }
   sw.flush(sl);
+  ga.flush(sl);
   for (int g0 = 0; g0 < nmax; g0 += kGroup) {
     Trsms tr;
     Gemms gm;
@@ -658,7 +727,8 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl) {
       ev.push_back(EvalDesc{kNull, kNull, L.begin[i], L.begin[i], m, m, c.leaf_lu(i), m, 1});
       mx = std::max(mx, m);
       if (r > 0) cp.copy(c.interp(i), r, 1, c.phi(i), m, m, r);  // phi = P^T, then A^-1 P^T
-      jobs.push_back(LuJob{c.leaf_lu(i), m, m, c.leaf_piv(i), c.info(i), kNull, r > 0 ? c.phi(i) : kNull, r, m});
+      jobs.push_back(LuJob{c.leaf_lu(i), m, m, c.leaf_piv(i), c.info(i), kNull, r > 0 ? c.phi(i) : kNull, r, m,
+                           c.leaf_ws(i), m});
       if (r > 0) gm.add(c.interp(i), r, 0, c.phi(i), m, 0, c.theta(i), r, r, r, m, 1.0, 0.0);
     }
     double ef = 0, eb = 0;
@@ -693,7 +763,7 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl) {
       g_z.add(c.theta(b), rr, 0, C, rl, 1, adv(Z, rl), R, rr, rl, rr, 1.0, 1.0);
       lu.push_back(LuDesc{Z, c.z_piv(i), c.info(i), c.anorm(i), with_cond ? c.rcond(i) : kNull, R, R});
       if (lev == 0) {
-        jobs.push_back(LuJob{Z, R, R, c.z_piv(i), c.info(i), c.anorm(i), kNull, 0, R});
+        jobs.push_back(LuJob{Z, R, R, c.z_piv(i), c.info(i), c.anorm(i), kNull, 0, R, c.z_ws(i), (int)L.ccap[i]});
         continue;
       }
       const Ref Y = D(B_FWS, at);
@@ -708,7 +778,7 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl) {
       g_v.add(c.theta(b), rr, 0, adv(Pi, (int64_t)rl * r), r, 1, adv(Y, rl), R, rr, r, rr, 1.0, 0.0);
       g_v.add(c.theta(a), rl, 0, Pi, r, 1, W, R, rl, r, rl, 1.0, 0.0);
       g_v.add(c.theta(b), rr, 0, adv(Pi, (int64_t)rl * r), r, 1, adv(W, rl), R, rr, r, rr, 1.0, 0.0);
-      jobs.push_back(LuJob{Z, R, R, c.z_piv(i), c.info(i), c.anorm(i), Y, r, R});  // Y = Z^-1 V
+      jobs.push_back(LuJob{Z, R, R, c.z_piv(i), c.info(i), c.anorm(i), Y, r, R, c.z_ws(i), (int)L.ccap[i]});  // Y = Z^-1 V
       // F = B Y (solver.py:86-89, 156); push = P^T - F (solver.py:158)
       g_f.add(C, rl, 0, adv(Y, rl), R, 0, F, R, rl, r, rr, 1.0, 0.0);
       g_f.add(C, rl, 1, Y, R, 0, adv(F, rl), R, rr, r, rl, 1.0, 0.0);
@@ -759,7 +829,7 @@ void build_solve(const hks_plan& P, int64_t kk, StepList& sl) {
         gp.add(c.phi(i), m, 1, D(B_VIN, L.begin[i]), n, 0, dst, ld, r, k, m, 1.0, 0.0);
       }
       cp.copy(D(B_VIN, L.begin[i]), n, 0, D(B_VOUT, L.begin[i]), n, m, k);
-      jobs.push_back(LuJob{c.leaf_lu(i), m, m, c.leaf_piv(i), kNull, kNull, D(B_VOUT, L.begin[i]), k, n});
+      jobs.push_back(LuJob{c.leaf_lu(i), m, m, c.leaf_piv(i), kNull, kNull, D(B_VOUT, L.begin[i]), k, n, c.leaf_ws(i), m});
     }
     gp.flush(sl);
     cp.flush(sl);
@@ -777,7 +847,7 @@ void build_solve(const hks_plan& P, int64_t kk, StepList& sl) {
       const Ref Si = c.block(B_VWS, S, i, k), Gi = c.block(B_VWS, G, i, k), Gbi = c.block(B_VWS, Gb, i, k);
       const Ref C = c.coup(i);
       cp.copy(Si, R, 0, Gi, R, R, k);
-      jobs.push_back(LuJob{c.z_lu(i), R, R, c.z_piv(i), kNull, kNull, Gi, k, R});
+      jobs.push_back(LuJob{c.z_lu(i), R, R, c.z_piv(i), kNull, kNull, Gi, k, R, c.z_ws(i), (int)L.ccap[i]});
       g1.add(C, rl, 0, adv(Gi, rl), R, 0, Gbi, R, rl, k, rr, 1.0, 0.0);
       g1.add(C, rl, 1, Gi, R, 0, adv(Gbi, rl), R, rr, k, rl, 1.0, 0.0);
       if (lev == 0) continue;

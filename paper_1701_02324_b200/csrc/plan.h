@@ -36,7 +36,7 @@ Layout make_layout(int64_t n, int64_t depth, int64_t max_rank);
 
 enum StepKind {
   ST_GEMM, ST_COPY, ST_GETRF, ST_GETRS, ST_GECON, ST_EVAL_CM, ST_EVAL_RM, ST_KSUM,
-  ST_PANEL, ST_SWAP, ST_TRSM_L, ST_TRSM_U, ST_NORM1, ST_LU_FUSED
+  ST_PANEL, ST_SWAP, ST_TRSM_L, ST_TRSM_U, ST_NORM1, ST_LU_FUSED, ST_GATHER
 };
 
 struct Step {
@@ -48,7 +48,7 @@ struct Step {
   double bytes;   // compulsory HBM bytes of the whole step
 };
 
-constexpr int kNumKinds = 14;
+constexpr int kNumKinds = 15;
 
 // Opt-in per-kind CUDA-event timing of every step (hks_profile_*).
 void profile_step(int kind, double flops, double bytes, cudaEvent_t a, cudaEvent_t b);

@@ -9,9 +9,6 @@
 #include <vector>
 
 #include "../paper_1701_02324_b200/csrc/hks_internal.h"
-#ifdef PANEL_PROF
-#include "../paper_1701_02324_b200/csrc/lu2.cu"
-#endif
 
 using namespace hks;
 
@@ -82,21 +79,13 @@ int main(int argc, char** argv) {
     CK(cudaMalloc(&piv, (size_t)B * rows * sizeof(int)));
     std::vector<PanelDesc> hd(B);
     for (int i = 0; i < B; ++i)
-      hd[i] = PanelDesc{abs_ref(A + (size_t)i * rows * pb), abs_ref(piv + (size_t)i * rows), kNull, rows, rows, 0, pb};
+      hd[i] = PanelDesc{abs_ref(A + (size_t)i * rows * pb), abs_ref(piv + (size_t)i * rows), kNull, rows, rows, 0, pb, kNull, kNull, kNull, 0, 0};
     PanelDesc* dd;
     CK(cudaMalloc(&dd, B * sizeof(PanelDesc)));
     CK(cudaMemcpy(dd, hd.data(), B * sizeof(PanelDesc), cudaMemcpyHostToDevice));
     float ms = time_it([&] { launch_panel_batched(db, dd, B, rows, pb, 0); }, reps);
     printf("panel B=%d rows=%d pb=%d: %.4f ms  (%.3f us/column)\n", B, rows, pb, ms, ms * 1e3 / pb);
-#ifdef PANEL_PROF
-    long long h[32][8];
-    CK(cudaMemcpyFromSymbol(h, hks::g_pprof, sizeof(h)));
-    for (int j = 1; j < pb - 1; j += 6) {
-      printf("  col %2d:", j);
-      for (int m = 1; m < 7; ++m) printf(" %5lld", h[j][m] - h[j][m - 1]);
-      printf("  | next %5lld\n", h[j + 1][0] - h[j][6]);
-    }
-#endif
+
   } else if (!strcmp(argv[1], "trsm")) {
     const int B = atoi(argv[2]), k = atoi(argv[3]), nc = atoi(argv[4]), up = atoi(argv[5]);
     double* T = dalloc_rand((size_t)B * k * k, 1, 4.0, k);

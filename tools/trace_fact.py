@@ -3,6 +3,7 @@ graphs off).  Usage: HKS_TRACE=1 python tools/trace_fact.py 2> trace.txt"""
 import sys
 sys.path.insert(0, ".")
 import torch
+import numpy as np
 import paper_1701_02324_b200 as hk
 from paper_1701_02324_b200 import workloads as W, _native as N
 w = W.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "C2"]
@@ -22,3 +23,16 @@ torch.cuda.synchronize()
 print("MARK", file=sys.stderr, flush=True)
 res = N.profile(False)
 print({k: round(v["ms"], 3) for k, v in res.items() if v["launches"]})
+
+# the solve of the bench step (nrhs right-hand sides, device resident)
+from paper_1701_02324_b200 import solver as S
+B = torch.from_numpy(np.ascontiguousarray(W.rhs(w, 0).T)).cuda()
+for _ in range(3):
+    S.solve_device(f, B)
+torch.cuda.synchronize()
+print("MARK SOLVE", file=sys.stderr, flush=True)
+N.profile(True)
+S.solve_device(f, B)
+torch.cuda.synchronize()
+res = N.profile(False)
+print("solve", {k: round(v["ms"], 3) for k, v in res.items() if v["launches"]})
