@@ -270,7 +270,8 @@ def gpu_arm(args, w, rank, world):
     roof["traffic"] = None
     if traffic_file.exists():
         tr = json.loads(traffic_file.read_text())
-        roof["traffic"] = tr.get(dom)
+        roof["traffic"] = tr.get(dom)  # ncu DRAM bytes per launch of this kind (one bench step)
+    roof["algorithmic_bytes_per_launch"] = round(kd["bytes"] / max(kd["launches"], 1))
     roof["launch_share"] = round(kd["ms"] / max(sum(v["ms"] for v in kinds.values()), 1e-9), 4)
     total_flops = sum(v["flops"] for v in kinds.values()) / args.steps
     kernels = {k: {"launches": int(v["launches"]), "ms_per_step": round(v["ms"] / args.steps, 4),

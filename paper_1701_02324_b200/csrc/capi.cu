@@ -5,6 +5,9 @@
 #include <cstring>
 #include <vector>
 
+#include <mutex>
+#include <unordered_map>
+
 #include "hks_internal.h"
 
 namespace hks {
@@ -25,6 +28,17 @@ static cudaError_t one_desc(const D& h, D** d, cudaStream_t s) {
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(d), sizeof(D), s);
   if (e != cudaSuccess) return e;
   return cudaMemcpyAsync(*d, &h, sizeof(D), cudaMemcpyHostToDevice, s);
+}
+
+cudaError_t raise_smem_limit(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> cur;
+  std::lock_guard<std::mutex> g(mu);
+  size_t& have = cur[func];
+  if (bytes <= have) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
 }
 
 cudaError_t upload_bases(const Bases& b, Bases** dev, cudaStream_t s) {

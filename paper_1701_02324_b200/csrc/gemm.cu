@@ -204,11 +204,7 @@ cudaError_t launch_gemm_batched(const Bases* bases, const GemmDesc* d_descs, int
     const int cnt = count - first < 65535 ? count - first : 65535;
     dim3 grid(tm * tn, cnt);
     const size_t sm = (size_t)STAGES * (BM + BN) * KS * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(gemm_batched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      attr = true;
-    }
+    raise_smem_limit(gemm_batched_kernel, sm);
     gemm_batched_kernel<<<grid, THREADS, sm, stream>>>(bases, d_descs + first, tn);
   }
   return cudaGetLastError();

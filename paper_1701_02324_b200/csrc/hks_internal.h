@@ -14,6 +14,15 @@ namespace hks {
 // from host memory; free with cudaFreeAsync).
 cudaError_t upload_bases(const Bases& b, Bases** dev, cudaStream_t s);
 
+// Raise (never lower) a kernel's dynamic shared-memory limit.  Launches
+// with different smem sizes share one function attribute; lowering it after
+// a larger launch was captured into a CUDA graph makes that node invalid.
+cudaError_t raise_smem_limit(const void* func, size_t bytes);
+template <class F>
+inline cudaError_t raise_smem_limit(F* func, size_t bytes) {
+  return raise_smem_limit(reinterpret_cast<const void*>(func), bytes);
+}
+
 // Records a thread-local error message (read back through hks_last_error)
 // and returns `code` so call sites can `return set_error(...)`.
 int set_error(int code, const char* fmt, ...);

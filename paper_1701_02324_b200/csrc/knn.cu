@@ -164,7 +164,7 @@ extern "C" int hks_knn(const double* X, int64_t n, int64_t d, int64_t k, int64_t
   if (e == cudaSuccess) {
     sqnorm_kernel<<<592, 256, 0, s>>>(X, n, (int)d, sq);
     const size_t sm = (size_t)(2 * QB * DS + QB * (CB + 1)) * sizeof(double);
-    cudaFuncSetAttribute(knn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    raise_smem_limit(knn_kernel, sm);
     knn_kernel<<<(unsigned)((n + QB - 1) / QB), KT, sm, s>>>(X, sq, (int)n, (int)d, (int)k, out);
     e = cudaGetLastError();
     cudaFreeAsync(sq, s);

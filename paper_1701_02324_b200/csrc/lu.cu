@@ -459,16 +459,16 @@ cudaError_t launch_getrf_batched(const Bases* b, const LuDesc* d, int count, int
   const int ldp = max_n > 0 ? max_n : 1;
   if (max_n <= 640) {
     const size_t sm = (size_t)ldp * 32 * sizeof(double);
-    cudaFuncSetAttribute(getrf_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    raise_smem_limit(getrf_kernel<32>, sm);
     getrf_kernel<32><<<count, LU_THREADS, sm, s>>>(b, d, ldp);
   } else if (max_n <= 1280) {
     const size_t sm = (size_t)ldp * 16 * sizeof(double);
-    cudaFuncSetAttribute(getrf_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    raise_smem_limit(getrf_kernel<16>, sm);
     getrf_kernel<16><<<count, LU_THREADS, sm, s>>>(b, d, ldp);
   } else {
     const size_t sm = (size_t)ldp * 8 * sizeof(double);
     if (sm > 200 * 1024) return cudaErrorInvalidValue;
-    cudaFuncSetAttribute(getrf_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    raise_smem_limit(getrf_kernel<8>, sm);
     getrf_kernel<8><<<count, LU_THREADS, sm, s>>>(b, d, ldp);
   }
   return cudaGetLastError();
@@ -481,14 +481,14 @@ cudaError_t launch_getrs_batched(const Bases* b, const LuSolveDesc* d, int count
   if (max_n <= 640) {
     constexpr int RC = 32;
     const size_t sm = (size_t)ldx * RC * sizeof(double) + (size_t)max_n * sizeof(int);
-    cudaFuncSetAttribute(getrs_kernel<RC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    raise_smem_limit(getrs_kernel<RC>, sm);
     dim3 grid(count, (max_nrhs + RC - 1) / RC);
     getrs_kernel<RC><<<grid, RS_THREADS, sm, s>>>(b, d, ldx);
   } else {
     constexpr int RC = 16;
     const size_t sm = (size_t)ldx * RC * sizeof(double) + (size_t)max_n * sizeof(int);
     if (sm > 220 * 1024) return cudaErrorInvalidValue;
-    cudaFuncSetAttribute(getrs_kernel<RC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    raise_smem_limit(getrs_kernel<RC>, sm);
     dim3 grid(count, (max_nrhs + RC - 1) / RC);
     getrs_kernel<RC><<<grid, RS_THREADS, sm, s>>>(b, d, ldx);
   }
@@ -498,7 +498,7 @@ cudaError_t launch_getrs_batched(const Bases* b, const LuSolveDesc* d, int count
 cudaError_t launch_gecon_batched(const Bases* b, const LuDesc* d, int count, int max_n, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
   const size_t sm = (size_t)(max_n > 0 ? max_n : 1) * (2 * sizeof(double) + sizeof(int));
-  cudaFuncSetAttribute(gecon_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  raise_smem_limit(gecon_kernel, sm);
   gecon_kernel<<<count, 256, sm, s>>>(b, d);
   return cudaGetLastError();
 }

@@ -238,7 +238,7 @@ template <int PB, int RPT, int NT, int U>
 cudaError_t launch_panel_loop(const Bases* b, const PanelDesc* d, int count, cudaStream_t s) {
   // done[] is PB + U rows deep: the last block may run past pb
   const size_t sm = (size_t)((PB + U) * NT * RPT + 2 * (NT / 32) * PB) * sizeof(double);
-  cudaFuncSetAttribute(panel_loop_kernel<PB, RPT, NT, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  raise_smem_limit(panel_loop_kernel<PB, RPT, NT, U>, sm);
   panel_loop_kernel<PB, RPT, NT, U><<<count, NT, sm, s>>>(b, d);
   return cudaGetLastError();
 }
@@ -453,11 +453,11 @@ cudaError_t launch_panel_batched(const Bases* b, const PanelDesc* d, int count, 
   const int ldp = max_rows;
   if (pb <= 16) {
     const size_t sm = (size_t)ldp * 16 * sizeof(double);
-    cudaFuncSetAttribute(panel_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    raise_smem_limit(panel_kernel<16>, sm);
     panel_kernel<16><<<count, PT, sm, s>>>(b, d, ldp);
   } else {
     const size_t sm = (size_t)ldp * 32 * sizeof(double);
-    cudaFuncSetAttribute(panel_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    raise_smem_limit(panel_kernel<32>, sm);
     panel_kernel<32><<<count, PT, sm, s>>>(b, d, ldp);
   }
   return cudaGetLastError();
@@ -469,7 +469,7 @@ cudaError_t launch_gather_batched(const Bases* b, const GatherDesc* d, int count
   int cb = 8192 / max_rows;  // <= 64 KB of staged rows per CTA
   cb = cb < 1 ? 1 : cb > 32 ? 32 : cb;
   const size_t sm = (size_t)max_rows * cb * sizeof(double) + (size_t)max_rows * sizeof(int);
-  cudaFuncSetAttribute(gather_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  raise_smem_limit(gather_rows_kernel, sm);
   for (int first = 0; first < count; first += 65535) {
     const int cnt = count - first < 65535 ? count - first : 65535;
     gather_rows_kernel<<<dim3((max_cols + cb - 1) / cb, cnt), 256, sm, s>>>(b, d + first, cb);
@@ -494,10 +494,10 @@ cudaError_t launch_trsm_batched(const Bases* b, const TrsmDesc* d, int count, in
     dim3 grid((max_cols + TNC - 1) / TNC, cnt);
     const size_t sm = (size_t)(128 * TXS + 2 * 32 * TTS) * sizeof(double);
     if (upper) {
-      cudaFuncSetAttribute(trsm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      raise_smem_limit(trsm_kernel<true>, sm);
       trsm_kernel<true><<<grid, TNC, sm, s>>>(b, d + first);
     } else {
-      cudaFuncSetAttribute(trsm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      raise_smem_limit(trsm_kernel<false>, sm);
       trsm_kernel<false><<<grid, TNC, sm, s>>>(b, d + first);
     }
   }

@@ -240,13 +240,13 @@ cudaError_t launch_lu_fused(const Bases* b, const LuFusedDesc* d, int count, int
     const size_t panel = (size_t)ldp * 32 * sizeof(double);
     const int usc = panel + (size_t)32 * (max_n + max_r) * sizeof(double) <= budget ? max_n + max_r : 0;
     const size_t sm = panel + (size_t)32 * usc * sizeof(double);
-    cudaFuncSetAttribute(lu_fused_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    raise_smem_limit(lu_fused_kernel<32>, sm);
     lu_fused_kernel<32><<<count, FT, sm, s>>>(b, d, ldp, usc);
   } else {
     const size_t panel = (size_t)ldp * 16 * sizeof(double);
     const int usc = panel + (size_t)16 * (max_n + max_r) * sizeof(double) <= budget ? max_n + max_r : 0;
     const size_t sm = panel + (size_t)16 * usc * sizeof(double);
-    cudaFuncSetAttribute(lu_fused_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    raise_smem_limit(lu_fused_kernel<16>, sm);
     lu_fused_kernel<16><<<count, FT, sm, s>>>(b, d, ldp, usc);
   }
   return cudaGetLastError();

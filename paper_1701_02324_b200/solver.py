@@ -167,6 +167,10 @@ def solve_device(f, B):
 
 
 def _solve_block(f, b, in_tree_order):
+    """Host (numpy or torch) or device right-hand sides -> solutions of the
+    same kind.  Host blocks travel as one H2D copy in and one D2H copy into
+    pinned memory out; the tree-order permutation and the (n, k) <-> (k, n)
+    transposes run on the device."""
     t = N.torch()
     host_tensor = isinstance(b, t.Tensor) and not b.is_cuda
     if host_tensor:  # e.g. a pinned host block: asynchronous H2D, host result
@@ -175,23 +179,25 @@ def _solve_block(f, b, in_tree_order):
     vec = b.dim() == 1 if dev else np.ndim(b) == 1
     if dev:
         B = b.to(t.float64).reshape(b.shape[0], -1)
-        if not in_tree_order:
-            B = B[f.tree.device_perm()]
-        B = B.t().contiguous()
     else:
-        bh = np.asarray(b, dtype=np.float64).reshape(np.shape(b)[0], -1)
-        B = N.to_device(np.ascontiguousarray(bh.T))
-        if not in_tree_order:
-            B = B[:, f.tree.device_perm()].contiguous()
-    X = solve_device(f, B)
+        B = N.to_device(np.ascontiguousarray(np.asarray(b, dtype=np.float64).reshape(np.shape(b)[0], -1)))
+    if not in_tree_order:
+        B = B[f.tree.device_perm()]
+    X = solve_device(f, B.t().contiguous())
     if not in_tree_order:
         out = t.empty_like(X)
         out[:, f.tree.device_perm()] = X
         X = out
     if dev and not host_tensor:
         return X[0] if vec else X.t()
-    x = X.cpu().numpy().T
-    return x[:, 0].copy() if vec else np.ascontiguousarray(x)
+    Xn = X.t().contiguous()  # (n, k) on the device, then one copy into pinned host memory
+    xh = t.empty(Xn.shape, dtype=t.float64, pin_memory=True)
+    xh.copy_(Xn, non_blocking=True)
+    t.cuda.current_stream().synchronize()
+    if host_tensor:
+        return xh[:, 0] if vec else xh
+    x = xh.numpy()
+    return x[:, 0] if vec else x
 
 
 def solve(f, b, in_tree_order=False):
