@@ -49,6 +49,17 @@ def parse():
     return p.parse_args()
 
 
+def max_over_ranks(value, world, device):
+    """The slowest rank's value (timings are reported as the max over ranks);
+    NCCL on the GPU box, gloo in the CPU tests."""
+    if world <= 1:
+        return float(value)
+    import torch
+    t = torch.tensor([float(value)], device=device, dtype=torch.float64)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
 # ---------------------------------------------------------------- CPU arm
 
 def oracle_arm(w, n_sample, steps, threads):
@@ -226,10 +237,7 @@ def gpu_arm(args, w, rank, world):
     region_ms = r0.elapsed_time(r1)
     t_fact = [a.elapsed_time(bq) for a, bq, _ in evs]
     t_solve = [bq.elapsed_time(c) for _, bq, c in evs]
-    if world > 1:
-        tt = torch.tensor([region_ms], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        region_ms = float(tt.item())
+    region_ms = max_over_ranks(region_ms, world, dev)
     ms_step = region_ms / args.steps
 
     # parity spot check of the timed solution: residual against Ktilde

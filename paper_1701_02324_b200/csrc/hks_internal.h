@@ -40,7 +40,7 @@ cudaError_t launch_panel_batched(const Bases* b, const PanelDesc* d, int count, 
 cudaError_t launch_swap_batched(const Bases* b, const SwapDesc* d, int count, int max_cols, cudaStream_t s);
 cudaError_t launch_gather_batched(const Bases* b, const GatherDesc* d, int count, int max_rows, int max_cols,
                                   cudaStream_t s);
-cudaError_t launch_trsm_batched(const Bases* b, const TrsmDesc* d, int count, int max_cols, bool upper,
+cudaError_t launch_trsm_batched(const Bases* b, const TrsmDesc* d, int count, int max_cols, int max_k, bool upper,
                                 cudaStream_t s);
 cudaError_t launch_lu_fused(const Bases* b, const LuFusedDesc* d, int count, int max_n, int max_r,
                             cudaStream_t s);

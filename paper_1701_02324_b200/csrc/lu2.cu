@@ -289,64 +289,63 @@ __global__ void swap_kernel(const Bases* __restrict__ bases_ptr, const SwapDesc*
 }
 
 // B := T^-1 B for a k x k triangular block T (unit lower, or non-unit
-// upper), k <= 128, B k x ncols.  A CTA owns 128 columns (one per thread)
-// held in shared memory.  Per 32-row block: the contribution of the
-// already-solved rows is one DMMA product (each warp a 32 x 32 tile), then
-// every thread solves its column against the 32 x 32 diagonal block in
-// registers, column-oriented (axpy) order so the 31 updates of each step are
-// independent (no serial shuffle chain).  All global reads are LDGSTS
-// (cp.async): the 128 x 128 block of B and the first 32 rows of T are in
+// upper), k <= 128, B k x ncols.  A CTA owns NC columns (one per thread,
+// NC = 32/64/128 by the step's widest descriptor) held in shared memory.
+// Per 32-row block: the contribution of the already-solved rows is one DMMA
+// product (each warp a 32 x 32 tile), then every thread solves its column
+// against the 32 x 32 diagonal block in registers, column-oriented (axpy)
+// order so the 31 updates of each step are independent.  All global reads
+// are LDGSTS (cp.async): the block of B and the first 32 rows of T are in
 // flight together, and the next block's rows of T are prefetched into the
-// second buffer while the current block computes -- with one 200 KB CTA per
-// SM, synchronous loads would leave the kernel HBM-latency bound.
-constexpr int TNC = 128;            // columns per CTA (= threads)
-constexpr int TXS = TNC + 4;        // X row stride: == 4 (mod 16), conflict-free DMMA B fragments
-constexpr int TTS = 128 + 4;        // staged T row stride
-
-template <bool UPPER>
-__device__ __forceinline__ void trsm_stage_rows(double* Ts, const double* T, int ldt, int k, int b, int wid,
-                                                int lane) {
+// second buffer while the current block computes.  Shared memory is sized
+// by the step's largest k, so narrow / shallow solves pack several CTAs per
+// SM.
+template <bool UPPER, int NC>
+__device__ __forceinline__ void trsm_stage_rows(double* Ts, int tts, const double* T, int ldt, int k, int b,
+                                                int wid, int lane) {
   const int r0 = b * 32, nr = min(32, k - r0);
   const int klo = UPPER ? r0 : 0, khi = UPPER ? k : r0 + nr;
   const bool ok = lane < nr;
-  for (int cc = klo + wid; cc < khi; cc += TNC / 32)
-    cp_async8(Ts + lane * TTS + cc, ok ? T + (r0 + lane) + (size_t)cc * ldt : T, ok);
+  for (int cc = klo + wid; cc < khi; cc += NC / 32)
+    cp_async8(Ts + lane * tts + cc, ok ? T + (r0 + lane) + (size_t)cc * ldt : T, ok);
 }
 
-template <bool UPPER>
-__global__ void __launch_bounds__(TNC) trsm_kernel(const Bases* __restrict__ bases_ptr,
-                                                  const TrsmDesc* __restrict__ descs) {
+template <bool UPPER, int NC>
+__global__ void __launch_bounds__(NC) trsm_kernel(const Bases* __restrict__ bases_ptr,
+                                                  const TrsmDesc* __restrict__ descs, int kcap, int tts) {
+  constexpr int TXS = NC + 4;  // X row stride: == 4 (mod 16), conflict-free DMMA B fragments
   const Bases& bases = *bases_ptr;
   const TrsmDesc D = descs[blockIdx.y];
-  const int c0 = blockIdx.x * TNC;
+  const int c0 = blockIdx.x * NC;
   if (c0 >= D.ncols) return;
-  const int nc = min(TNC, D.ncols - c0), k = D.k;
+  const int nc = min(NC, D.ncols - c0), k = D.k;
   const double* T = at<const double>(bases, D.T);
   double* B = at<double>(bases, D.B) + (size_t)c0 * D.ldb;
   extern __shared__ double tsm[];
-  double* X = tsm;                    // k x TNC, row-major (ld TXS)
-  double* Tbuf = tsm + 128 * TXS;     // 2 x 32 rows of T, row-major (ld TTS)
+  double* X = tsm;                    // k x NC, row-major (ld TXS)
+  double* Tbuf = tsm + kcap * TXS;    // 2 x 32 rows of T, row-major (ld tts)
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int nblk = (k + 31) / 32;
   // lanes walk a column's rows: 256-byte coalesced LDGSTS
-  for (int c = wid; c < nc; c += TNC / 32)
+  for (int c = wid; c < nc; c += NC / 32)
     for (int i = lane; i < k; i += 32) cp_async8(X + i * TXS + c, B + i + (size_t)c * D.ldb, true);
-  trsm_stage_rows<UPPER>(Tbuf, T, D.ldt, k, UPPER ? nblk - 1 : 0, wid, lane);
+  trsm_stage_rows<UPPER, NC>(Tbuf, tts, T, D.ldt, k, UPPER ? nblk - 1 : 0, wid, lane);
   cp_async_commit();
   const int fr = lane >> 2, fc = lane & 3;
   for (int bb = 0; bb < nblk; ++bb) {
     const int b = UPPER ? nblk - 1 - bb : bb;
     const int r0 = b * 32, nr = min(32, k - r0);
-    double* Ts = Tbuf + (bb & 1) * 32 * TTS;
+    double* Ts = Tbuf + (bb & 1) * 32 * tts;
     cp_async_wait<0>();
     __syncthreads();  // X / this block's rows of T landed; the previous block's solve is complete
     if (bb + 1 < nblk) {
-      trsm_stage_rows<UPPER>(Tbuf + ((bb + 1) & 1) * 32 * TTS, T, D.ldt, k, UPPER ? b - 1 : b + 1, wid, lane);
+      trsm_stage_rows<UPPER, NC>(Tbuf + ((bb + 1) & 1) * 32 * tts, tts, T, D.ldt, k, UPPER ? b - 1 : b + 1, wid,
+                                 lane);
       cp_async_commit();
     }
     // X[r0:r0+nr, :] -= T[r0:r0+nr, u] X[u, :] over the solved rows u (DMMA)
     const int ulo = UPPER ? r0 + nr : 0, uhi = UPPER ? k : r0;
-    if (uhi > ulo) {
+    if (uhi > ulo && wid * 32 < nc) {
       const int cb = wid * 32;  // this warp's 32 columns
       double acc[4][4][2];
 #pragma unroll
@@ -358,7 +357,7 @@ __global__ void __launch_bounds__(TNC) trsm_kernel(const Bases* __restrict__ bas
         const bool kin = kq < uhi;
         double a[4], bv[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = kin ? Ts[(i * 8 + fr) * TTS + kq] : 0.0;
+        for (int i = 0; i < 4; ++i) a[i] = kin ? Ts[(i * 8 + fr) * tts + kq] : 0.0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) bv[j] = kin ? X[kq * TXS + cb + j * 8 + fr] : 0.0;
 #pragma unroll
@@ -386,15 +385,15 @@ __global__ void __launch_bounds__(TNC) trsm_kernel(const Bases* __restrict__ bas
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
 #pragma unroll
-          for (int i = j + 1; i < 32; ++i) x[i] -= Ts[i * TTS + r0 + j] * x[j];
+          for (int i = j + 1; i < 32; ++i) x[i] -= Ts[i * tts + r0 + j] * x[j];
         }
       } else {
 #pragma unroll
         for (int j = 31; j >= 0; --j) {
           if (j < nr) {
-            x[j] /= Ts[j * TTS + r0 + j];  // a true division, as dtrsm (c5 is sensitive to it)
+            x[j] /= Ts[j * tts + r0 + j];  // a true division, as dtrsm (c5 is sensitive to it)
 #pragma unroll
-            for (int i = 0; i < j; ++i) x[i] -= Ts[i * TTS + r0 + j] * x[j];
+            for (int i = 0; i < j; ++i) x[i] -= Ts[i * tts + r0 + j] * x[j];
           }
         }
       }
@@ -404,7 +403,7 @@ __global__ void __launch_bounds__(TNC) trsm_kernel(const Bases* __restrict__ bas
     }
   }
   __syncthreads();
-  for (int c = wid; c < nc; c += TNC / 32)
+  for (int c = wid; c < nc; c += NC / 32)
     for (int i = lane; i < k; i += 32) B[i + (size_t)c * D.ldb] = X[i * TXS + c];
 }
 
@@ -486,22 +485,34 @@ cudaError_t launch_swap_batched(const Bases* b, const SwapDesc* d, int count, in
   return cudaGetLastError();
 }
 
-cudaError_t launch_trsm_batched(const Bases* b, const TrsmDesc* d, int count, int max_cols, bool upper,
-                                cudaStream_t s) {
-  if (count <= 0 || max_cols <= 0) return cudaSuccess;
+template <bool UPPER, int NC>
+static cudaError_t launch_trsm_nc(const Bases* b, const TrsmDesc* d, int count, int max_cols, int max_k,
+                                  cudaStream_t s) {
+  // tts == 4 (mod 16), and > every column r0 + 31 the register diagonal solve touches
+  const int kcap = (max_k + 31) / 32 * 32, tts = kcap + 4;
+  const size_t sm = (size_t)(kcap * (NC + 4) + 2 * 32 * tts) * sizeof(double);
+  raise_smem_limit(trsm_kernel<UPPER, NC>, sm);
   for (int first = 0; first < count; first += 65535) {
     const int cnt = count - first < 65535 ? count - first : 65535;
-    dim3 grid((max_cols + TNC - 1) / TNC, cnt);
-    const size_t sm = (size_t)(128 * TXS + 2 * 32 * TTS) * sizeof(double);
-    if (upper) {
-      raise_smem_limit(trsm_kernel<true>, sm);
-      trsm_kernel<true><<<grid, TNC, sm, s>>>(b, d + first);
-    } else {
-      raise_smem_limit(trsm_kernel<false>, sm);
-      trsm_kernel<false><<<grid, TNC, sm, s>>>(b, d + first);
-    }
+    trsm_kernel<UPPER, NC><<<dim3((max_cols + NC - 1) / NC, cnt), NC, sm, s>>>(b, d + first, kcap, tts);
   }
   return cudaGetLastError();
+}
+
+template <bool UPPER>
+static cudaError_t launch_trsm_t(const Bases* b, const TrsmDesc* d, int count, int max_cols, int max_k,
+                                 cudaStream_t s) {
+  if (max_cols <= 32) return launch_trsm_nc<UPPER, 32>(b, d, count, max_cols, max_k, s);
+  if (max_cols <= 64) return launch_trsm_nc<UPPER, 64>(b, d, count, max_cols, max_k, s);
+  return launch_trsm_nc<UPPER, 128>(b, d, count, max_cols, max_k, s);
+}
+
+cudaError_t launch_trsm_batched(const Bases* b, const TrsmDesc* d, int count, int max_cols, int max_k, bool upper,
+                                cudaStream_t s) {
+  if (count <= 0 || max_cols <= 0 || max_k <= 0) return cudaSuccess;
+  if (max_k > 128) return cudaErrorInvalidValue;
+  return upper ? launch_trsm_t<true>(b, d, count, max_cols, max_k, s)
+               : launch_trsm_t<false>(b, d, count, max_cols, max_k, s);
 }
 
 cudaError_t launch_norm1_batched(const Bases* b, const LuDesc* d, int count, cudaStream_t s) {

@@ -174,7 +174,7 @@ cudaError_t StepList::run(const Bases* b, const double* X, int d, const KernelPa
         break;
       case ST_TRSM_L:
       case ST_TRSM_U:
-        e = launch_trsm_batched(b, (const TrsmDesc*)st.d, st.count, st.p0, st.kind == ST_TRSM_U, s);
+        e = launch_trsm_batched(b, (const TrsmDesc*)st.d, st.count, st.p0, st.p1, st.kind == ST_TRSM_U, s);
         break;
       case ST_NORM1:
         e = launch_norm1_batched(b, (const LuDesc*)st.d, st.count, s);
@@ -474,11 +474,12 @@ struct Swaps {
 
 struct Trsms {
   std::vector<TrsmDesc> v;
-  int mc = 0;
+  int mc = 0, mk = 0;
   void add(Ref T, int ldt, Ref B, int ldb, int k, int ncols) {
     if (k <= 0 || ncols <= 0) return;
     v.push_back(TrsmDesc{T, B, ldt, ldb, k, ncols});
     mc = std::max(mc, ncols);
+    mk = std::max(mk, k);
   }
   void flush(StepList& sl, bool upper) {
     double f = 0, bytes = 0;
@@ -486,9 +487,9 @@ struct Trsms {
       f += (double)d.k * d.k * d.ncols;
       bytes += 8.0 * ((double)d.k * d.k / 2 + 2.0 * d.k * d.ncols);
     }
-    sl.add(upper ? ST_TRSM_U : ST_TRSM_L, v, mc, 0, f, bytes);
+    sl.add(upper ? ST_TRSM_U : ST_TRSM_L, v, mc, mk, f, bytes);
     v.clear();
-    mc = 0;
+    mc = mk = 0;
   }
 };
 

@@ -96,7 +96,7 @@ int main(int argc, char** argv) {
     TrsmDesc* dd;
     CK(cudaMalloc(&dd, B * sizeof(TrsmDesc)));
     CK(cudaMemcpy(dd, hd.data(), B * sizeof(TrsmDesc), cudaMemcpyHostToDevice));
-    float ms = time_it([&] { launch_trsm_batched(db, dd, B, nc, up != 0, 0); }, reps);
+    float ms = time_it([&] { launch_trsm_batched(db, dd, B, nc, k, up != 0, 0); }, reps);
     printf("trsm B=%d k=%d ncols=%d up=%d: %.4f ms  %.2f TF/s\n", B, k, nc, up, ms, (double)B * k * k * nc / ms / 1e9);
   }
   return 0;
