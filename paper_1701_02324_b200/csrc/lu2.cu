@@ -436,8 +436,11 @@ cudaError_t launch_panel_batched(const Bases* b, const PanelDesc* d, int count, 
   // 256 threads, one to four rows each; PB x RPT doubles stay in registers.
   // plan.cu uses pb = 32 only for rows <= 256 (panel32_max_rows).
   const int rpt = (max_rows + 255) / 256;
-  if (pb > 16) {
+  if (pb > 32) {
+    if (rpt == 1) return launch_panel_loop<64, 1, 256, 8>(b, d, count, s);
+  } else if (pb > 16) {
     if (rpt == 1) return launch_panel_loop<32, 1, 256, 8>(b, d, count, s);
+    if (rpt == 2) return launch_panel_loop<32, 2, 256, 8>(b, d, count, s);
   } else {
     switch (rpt) {
       case 1: return launch_panel_loop<16, 1, 256, 8>(b, d, count, s);

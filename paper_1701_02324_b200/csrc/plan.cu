@@ -509,14 +509,21 @@ int fused_lu_max_count() {
   return v;
 }
 
-// Panel width: 32 while a panel's rows fit in registers without spilling
-// (lu2.cu: panel_reg_kernel), else 16.  HKS_PANEL_ROWS32 overrides the cut.
-int panel32_max_rows() {
-  static const int v = [] {
-    const char* e = getenv("HKS_PANEL_ROWS32");
-    return e ? atoi(e) : 256;
+// Panel width by the batch's largest matrix: the register panel kernels
+// (lu2.cu) hold PB x rows/256 doubles per thread without spilling for
+// 64 x 256, 32 x 512 and 16 x 1024.  Wider panels mean fewer in-group
+// interchange / TRSM / GEMM steps per 128-column group.  HKS_PANEL_PB
+// overrides (16, 32 or 64).
+int panel_width(int nmax) {
+  static const int forced = [] {
+    const char* e = getenv("HKS_PANEL_PB");
+    return e ? atoi(e) : 0;
   }();
-  return v;
+  int pb = nmax <= 256 ? 64 : nmax <= 512 ? 32 : 16;
+  if (forced == 16 || forced == 32 || forced == 64) pb = forced;
+  if (pb == 64 && nmax > 256) pb = 32;
+  if (pb == 32 && nmax > 512) pb = 16;
+  return pb;
 }
 
 void add_lu_program(StepList& sl, const std::vector<LuJob>& jobs, bool with_norm) {
@@ -524,7 +531,7 @@ void add_lu_program(StepList& sl, const std::vector<LuJob>& jobs, bool with_norm
   int nmax = 0;
   for (auto& j : jobs) nmax = std::max(nmax, j.n);
   if (nmax == 0) return;
-  const int PB = nmax <= panel32_max_rows() ? 32 : 16;
+  const int PB = panel_width(nmax);
   if (with_norm) {
     std::vector<LuDesc> nd;
     for (auto& j : jobs) nd.push_back(LuDesc{j.A, j.piv, j.info, j.anorm, kNull, j.n, j.lda});
