@@ -219,6 +219,7 @@ def gpu_arm(args, w, rank, world):
     for _ in range(args.steps):
         f, X, ev = step()
         evs.append(ev)
+    f.join_cond()  # the last step's dgecon estimates (condition stream) finish inside the region
     r1.record(stream)
     torch.cuda.synchronize()
     torch.cuda.profiler.stop()

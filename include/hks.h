@@ -136,8 +136,12 @@ int hks_build_operator(hks_plan* plan, void* const* buffers, void* stream);
 int hks_leaf_block(hks_plan* plan, int64_t leaf, double* out, void* stream);
 
 /* factorize, solver.py:111-186.  Reads INTERP, COUP; writes THETA, LEAF_LU,
- * LEAF_PIV, PHI, Z_LU, Z_PIV, PUSH, STATS.  with_cond: run the dgecon
- * estimate of every Z (NodeFactor.z_cond).  On an exactly-zero pivot returns
+ * LEAF_PIV, PHI, Z_LU, Z_PIV, PUSH, STATS.  with_cond: also run the dgecon
+ * estimate of every Z (NodeFactor.z_cond) -- asynchronously, on the
+ * condition stream (hks_set_cond_stream), each level as soon as its LU is
+ * done; Z_LU and STATS must stay allocated until it finishes (hks_cond_wait
+ * / hks_factor_stats).  Returns once the factorization itself is complete.
+ * On an exactly-zero pivot returns
  * HKS_ERR_SINGULAR (leaf, linalg.py:163-168) or HKS_ERR_REDUCED_SINGULAR
  * (Z, solver.py:99-105) with the failing heap index in *bad_node_host. */
 int hks_factorize(hks_plan* plan, void* const* buffers, double lam, int32_t with_cond,
@@ -147,9 +151,16 @@ int hks_factorize(hks_plan* plan, void* const* buffers, double lam, int32_t with
  * level 0..depth; Factorization.level_seconds, solver.py:164-176). */
 int hks_factor_level_ms(hks_plan* plan, double* ms_host);
 
-/* z_cond (1 / dgecon rcond; 0 for leaves) and info per node, host outputs. */
+/* z_cond (1 / dgecon rcond; 0 for leaves) and info per node, host outputs;
+ * waits for the plan's pending dgecon estimates first. */
 int hks_factor_stats(hks_plan* plan, void* const* buffers, double* z_cond_host, int32_t* info_host,
                      void* stream);
+
+/* The stream the dgecon estimates run on (NULL: the plan's own lowest-
+ * priority stream), and a device-side wait of `stream` for the last
+ * factorization's estimates. */
+int hks_set_cond_stream(hks_plan* plan, void* stream);
+int hks_cond_wait(hks_plan* plan, void* stream);
 
 /* solve / solve_multi, solver.py:189-270: x = (Ktilde + lam I)^-1 b for k
  * right-hand sides in tree order; b, x: n x k column-major (ld n); x may

@@ -73,6 +73,8 @@ SIGNATURES = {
     "hks_vaxpys": [_P, _I64, _I64, _P, _D, _P, _I64, _P],
     "hks_profile": [_I32, _DP],
     "hks_factor_level_ms": [_P, _DP],
+    "hks_set_cond_stream": [_P, _P],
+    "hks_cond_wait": [_P, _P],
 }
 
 KIND_NAMES = ("gemm", "copy", "getrf", "getrs", "gecon", "eval", "eval_rm", "ksum", "panel", "swap",

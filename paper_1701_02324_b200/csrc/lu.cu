@@ -280,58 +280,71 @@ __global__ void __launch_bounds__(RS_THREADS) getrs_kernel(const Bases* __restri
 
 // ------------------------------------------------------------------ gecon
 
-// x := op(T)^-1 x for one vector in shared memory; T is the unit-lower (L)
-// or non-unit-upper (U) part of the LU, op = N or T.  32-row blocks: the
-// diagonal block is staged in shared memory (`blk`, 32 x 33) and solved by
-// warp 0 with shuffles, then every thread updates the remaining entries
-// (coalesced column reads for op = N, row reads for op = T).
-__device__ void trsv_block(const double* LU, int lda, int n, double* x, bool upper, bool trans, double* blk) {
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
+// Same solve, latency-lean (gecon only: its result is an estimate, so the
+// diagonal uses a reciprocal computed off the dependency chain).  Warp 0
+// holds the 32 x 32 diagonal block of op(T) in registers (lane i: row i)
+// and solves it with one shuffle per step; the next block's rows are loaded
+// before the block's update so their latency hides behind it; the update of
+// the remaining entries is one thread per entry with 32 independent loads.
+__device__ __forceinline__ void trsv_load_diag(const double* LU, int lda, int n, int b, bool upper, bool trans,
+                                               double (&t)[32], double& rd) {
+  const int lane = threadIdx.x & 31, r0 = b * 32, nr = min(32, n - r0);
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    double v = 0.0;
+    if (lane < nr && j < nr)
+      v = trans ? LU[(r0 + j) + (size_t)(r0 + lane) * lda] : LU[(r0 + lane) + (size_t)(r0 + j) * lda];
+    t[j] = v;
+  }
+  double dg = 1.0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    if (j == lane) dg = t[j];
+  rd = (upper && lane < nr) ? 1.0 / dg : 1.0;
+}
+
+__device__ __noinline__ void trsv_fast(const double* LU, int lda, int n, double* x, bool upper, bool trans) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
   const bool forward = (!upper && !trans) || (upper && trans);
   const int nblk = (n + 31) / 32;
+  double t[32], rd = 1.0;
+  if (tid < 32) trsv_load_diag(LU, lda, n, forward ? 0 : nblk - 1, upper, trans, t, rd);
   for (int bb = 0; bb < nblk; ++bb) {
     const int b = forward ? bb : nblk - 1 - bb;
     const int r0 = b * 32, nr = min(32, n - r0);
-    // stage op(T)[r0.., r0..] (32 x 32): blk[i * 33 + j] = op(T)(r0 + i, r0 + j)
-    for (int j = wid; j < nr; j += nt / 32)
-      if (lane < nr) {
-        const double v = LU[(r0 + lane) + (size_t)(r0 + j) * lda];  // T(r0+lane, r0+j), coalesced
-        if (trans) blk[j * 33 + lane] = v; else blk[lane * 33 + j] = v;
-      }
-    __syncthreads();
     if (tid < 32) {
       double v = lane < nr ? x[r0 + lane] : 0.0;
       if (forward) {
-        for (int j = 0; j < nr; ++j) {
-          double xj = __shfl_sync(0xffffffffu, v, j);
-          if (upper) xj /= blk[j * 33 + j];
-          if (lane == j) v = xj;
-          if (lane > j && lane < nr) v -= blk[lane * 33 + j] * xj;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (lane == j) v *= rd;
+          const double xj = __shfl_sync(0xffffffffu, v, j);
+          if (lane > j) v -= t[j] * xj;
         }
       } else {
-        for (int j = nr - 1; j >= 0; --j) {
-          double xj = __shfl_sync(0xffffffffu, v, j);
-          if (upper) xj /= blk[j * 33 + j];
-          if (lane == j) v = xj;
-          if (lane < j) v -= blk[lane * 33 + j] * xj;
+#pragma unroll
+        for (int j = 31; j >= 0; --j) {
+          if (lane == j) v *= rd;
+          const double xj = __shfl_sync(0xffffffffu, v, j);
+          if (lane < j) v -= t[j] * xj;
         }
       }
       if (lane < nr) x[r0 + lane] = v;
+      if (bb + 1 < nblk) trsv_load_diag(LU, lda, n, forward ? b + 1 : b - 1, upper, trans, t, rd);
     }
     __syncthreads();
     const int lo = forward ? r0 + nr : 0, hi = forward ? n : r0;
-    if (!trans) {
-      for (int i = lo + tid; i < hi; i += nt) {
-        double s = x[i];
+    for (int i = lo + tid; i < hi; i += nt) {
+      double s = x[i];
+      if (!trans) {
+#pragma unroll 8
         for (int j = 0; j < nr; ++j) s -= LU[i + (size_t)(r0 + j) * lda] * x[r0 + j];
-        x[i] = s;
+      } else {
+        const double* col = LU + r0 + (size_t)i * lda;  // op(T)(i, r0 + j) = T(r0 + j, i)
+#pragma unroll 8
+        for (int j = 0; j < nr; ++j) s -= col[j] * x[r0 + j];
       }
-    } else {  // op(T)(i, r0+j) = T(r0+j, i): a warp per output entry, lanes over j
-      for (int i = lo + wid; i < hi; i += nt / 32) {
-        const double t = lane < nr ? LU[(r0 + lane) + (size_t)i * lda] * x[r0 + lane] : 0.0;
-        const double s = warp_sum(t);
-        if (lane == 0) x[i] -= s;
-      }
+      x[i] = s;
     }
     __syncthreads();
   }
@@ -352,7 +365,10 @@ __device__ int block_iamax(const double* x, int n, double* rv, int* ri) {
 // LAPACK dgecon(norm='1') with dlacn2 (Higham's estimator), restated; the
 // dlatrs overflow scaling is not needed at the conditioning the solver
 // admits (documented in DESIGN.md).
-__global__ void __launch_bounds__(256) gecon_kernel(const Bases* __restrict__ bases_ptr,
+#ifndef GECON_THREADS
+#define GECON_THREADS 256
+#endif
+__global__ void __launch_bounds__(GECON_THREADS) gecon_kernel(const Bases* __restrict__ bases_ptr,
                                                      const LuDesc* __restrict__ descs) {
   const Bases& bases = *bases_ptr;
   const LuDesc L = descs[blockIdx.x];
@@ -362,7 +378,7 @@ __global__ void __launch_bounds__(256) gecon_kernel(const Bases* __restrict__ ba
   double* x = sh;        // n
   double* v = sh + n;    // n
   int* isgn = reinterpret_cast<int*>(sh + 2 * n);
-  __shared__ double blk[32 * 33];
+
   __shared__ double red_v[8];
   __shared__ int red_i[8];
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -375,11 +391,11 @@ __global__ void __launch_bounds__(256) gecon_kernel(const Bases* __restrict__ ba
 
   auto apply = [&](int kase) {
     if (kase == 1) {
-      trsv_block(LUa, L.lda, n, x, false, false, blk);
-      trsv_block(LUa, L.lda, n, x, true, false, blk);
+      trsv_fast(LUa, L.lda, n, x, false, false);
+      trsv_fast(LUa, L.lda, n, x, true, false);
     } else {
-      trsv_block(LUa, L.lda, n, x, true, true, blk);
-      trsv_block(LUa, L.lda, n, x, false, true, blk);
+      trsv_fast(LUa, L.lda, n, x, true, true);
+      trsv_fast(LUa, L.lda, n, x, false, true);
     }
   };
 
@@ -499,7 +515,7 @@ cudaError_t launch_gecon_batched(const Bases* b, const LuDesc* d, int count, int
   if (count <= 0) return cudaSuccess;
   const size_t sm = (size_t)(max_n > 0 ? max_n : 1) * (2 * sizeof(double) + sizeof(int));
   raise_smem_limit(gecon_kernel, sm);
-  gecon_kernel<<<count, 256, sm, s>>>(b, d);
+  gecon_kernel<<<count, GECON_THREADS, sm, s>>>(b, d);  // a light co-tenant of the factorization
   return cudaGetLastError();
 }
 

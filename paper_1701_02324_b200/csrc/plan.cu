@@ -85,9 +85,6 @@ void StepList::clear() {
 
 StepList::~StepList() {
   if (dev_) cudaFree(dev_);
-  if (side_) cudaStreamDestroy(side_);
-  if (fork_) cudaEventDestroy(fork_);
-  if (join_) cudaEventDestroy(join_);
 }
 
 cudaError_t DevBuf::ensure(size_t b) {
@@ -112,25 +109,11 @@ cudaError_t StepList::run(const Bases* b, const double* X, int d, const KernelPa
   };
   const bool prof = profiling();
   size_t next_mark = 0;
-  bool forked = false;
   const cudaStream_t main = s;
   for (size_t si = 0; si < steps_.size(); ++si) {
     const Step& st = steps_[si];
     while (ev && next_mark < marks_.size() && marks_[next_mark] == si) record(ev[next_mark++], main);
     s = main;
-    if (st.kind == ST_GECON && side_streams_enabled()) {  // off the critical path: nothing downstream reads z_cond
-      if (!side_) {
-        int lo = 0, hi = 0;
-        cudaDeviceGetStreamPriorityRange(&lo, &hi);
-        cudaStreamCreateWithPriority(&side_, cudaStreamNonBlocking, lo);
-        cudaEventCreateWithFlags(&fork_, cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&join_, cudaEventDisableTiming);
-      }
-      cudaEventRecord(fork_, main);
-      cudaStreamWaitEvent(side_, fork_, 0);
-      s = side_;
-      forked = true;
-    }
     cudaError_t e = cudaSuccess;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (prof) {
@@ -192,10 +175,6 @@ cudaError_t StepList::run(const Bases* b, const double* X, int d, const KernelPa
   s = main;
   while (ev && next_mark < marks_.size()) record(ev[next_mark++], s);
   if (ev) record(ev[marks_.size()], s);
-  if (forked) {
-    cudaEventRecord(join_, side_);
-    cudaStreamWaitEvent(main, join_, 0);
-  }
   return cudaSuccess;
 }
 
@@ -284,13 +263,6 @@ cudaError_t run_graphed(GraphCache& gc, const StepList& sl, const Bases& b, cons
   return cudaGraphLaunch(gc.exec, s);
 }
 
-bool side_streams_enabled() {
-  static const int on = [] {
-    const char* v = getenv("HKS_SIDE_STREAM");
-    return v ? atoi(v) : 1;
-  }();
-  return on != 0;
-}
 void count_launch(int n) { g_launches += n; }
 void profile_step(int kind, double flops, double bytes, cudaEvent_t a, cudaEvent_t b) {
   g_prof.pending.push_back(Pending{kind, flops, bytes, a, b});
@@ -720,7 +692,8 @@ size_t factorize_workspace(const hks_plan& P) {
 
 // ------------------------------------------------------------ factorize
 
-void build_factorize(const hks_plan& P, bool with_cond, StepList& sl) {
+void build_factorize(const hks_plan& P, bool with_cond, StepList& sl,
+                     std::vector<std::unique_ptr<StepList>>* cond_levels, std::vector<int>* cond_wait) {
   const Ctx c(P);
   const Layout& L = P.L;
   sl.mark();
@@ -800,11 +773,13 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl) {
     c_id.flush(sl);
     g_z.flush(sl);
     g_v.flush(sl);
-    add_lu_program(sl, jobs, true);
-    if (with_cond) {
+    add_lu_program(sl, jobs, with_cond);  // with_cond: ||Z||_1 before factoring, for dgecon
+    if (with_cond && cond_levels) {
       double lb = 0;
       for (auto& d : lu) lb += 16.0 * d.n * d.n;
-      sl.add(ST_GECON, lu, maxR, 0, 22.0 * lb / 16.0, 11.0 * lb / 2.0);
+      cond_levels->emplace_back(new StepList());
+      cond_levels->back()->add(ST_GECON, lu, maxR, 0, 22.0 * lb / 16.0, 11.0 * lb / 2.0);
+      cond_wait->push_back((int)sl.marks().size());  // level_ev recorded when this level is done
     }
     if (lev == 0) continue;
     g_f.flush(sl);
@@ -1118,6 +1093,38 @@ extern "C" int hks_leaf_block(hks_plan* P, int64_t leaf, double* out, void* stre
                         0.0, stream);
 }
 
+// dgecon for every internal level on the condition stream, each level as
+// soon as its LU is done (the factorization records level_ev[m] at its
+// level marks); cond_done marks the last one.  Not joined back: the caller
+// reads z_cond through hks_factor_stats, which waits for cond_done.
+static cudaError_t launch_cond(hks_plan* P, const Bases& b) {
+  cudaError_t e = cudaSuccess;
+  if (!P->cond_stream) {
+    if (!P->own_cond_stream) {
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      e = cudaStreamCreateWithPriority(&P->own_cond_stream, cudaStreamNonBlocking, lo);
+      if (e != cudaSuccess) return e;
+    }
+    P->cond_stream = P->own_cond_stream;
+  }
+  if (!P->cond_done) e = cudaEventCreateWithFlags(&P->cond_done, cudaEventDisableTiming);
+  if (e == cudaSuccess && !P->cond_bases) e = cudaMalloc(&P->cond_bases, sizeof(Bases));
+  if (e != cudaSuccess) return e;
+  cudaStream_t cs = P->cond_stream;
+  // pageable source: staged before the call returns; stream order keeps the
+  // previous factorization's estimates reading their own table until done
+  Bases hb = b;
+  e = cudaMemcpyAsync(P->cond_bases, &hb, sizeof(Bases), cudaMemcpyHostToDevice, cs);
+  for (size_t i = 0; i < P->cond_levels.size() && e == cudaSuccess; ++i) {
+    e = cudaStreamWaitEvent(cs, P->level_ev[P->cond_wait[i]], 0);
+    if (e == cudaSuccess) e = P->cond_levels[i]->run(P->cond_bases, P->X, (int)P->d, P->kp, cs);
+  }
+  if (e == cudaSuccess) e = cudaEventRecord(P->cond_done, cs);
+  if (e == cudaSuccess) P->cond_pending = true;
+  return e;
+}
+
 static int check_info(hks_plan* P, void* const* buffers, int64_t* bad_node, cudaStream_t s) {
   const Layout& L = P->L;
   std::vector<int> info(L.nn);
@@ -1148,8 +1155,15 @@ extern "C" int hks_factorize(hks_plan* P, void* const* buffers, double lam, int3
   const int which = with_cond ? 1 : 0;
   if (!P->fact[which]) {
     P->fact[which].reset(new StepList());
-    build_factorize(*P, with_cond != 0, *P->fact[which]);
+    if (which == 1) {
+      P->cond_levels.clear();
+      P->cond_wait.clear();
+    }
+    build_factorize(*P, with_cond != 0, *P->fact[which], which == 1 ? &P->cond_levels : nullptr,
+                    which == 1 ? &P->cond_wait : nullptr);
     cudaError_t e = P->fact[which]->upload(s);
+    for (auto& c : P->cond_levels)
+      if (e == cudaSuccess && which == 1) e = c->upload(s);
     if (e == cudaSuccess) e = P->fws.ensure(std::max<size_t>(factorize_workspace(*P), 1) * sizeof(double));
     if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_factorize: %s", cudaGetErrorString(e));
   }
@@ -1164,6 +1178,7 @@ extern "C" int hks_factorize(hks_plan* P, void* const* buffers, double lam, int3
   }
   cudaError_t e = run_graphed(P->fact_graphs[which], *P->fact[which], b, P->X, (int)P->d, P->kp, s,
                               P->level_ev.data(), buffers[HKS_BUF_STATS], P->L.nn * 3 * sizeof(double));
+  if (e == cudaSuccess && which == 1 && !P->cond_levels.empty()) e = launch_cond(P, b);
   if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_factorize: %s", cudaGetErrorString(e));
   if (bad_node) *bad_node = -1;
   return check_info(P, buffers, bad_node, s);
@@ -1173,6 +1188,10 @@ extern "C" int hks_factor_stats(hks_plan* P, void* const* buffers, double* z_con
   if (!P || !buffers) return set_error(HKS_ERR_INVALID, "hks_factor_stats: null argument");
   cudaStream_t s = as_stream(stream);
   const Layout& L = P->L;
+  if (P->cond_pending) {  // the dgecon estimates run on the condition stream
+    cudaError_t e = cudaEventSynchronize(P->cond_done);
+    if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_factor_stats: %s", cudaGetErrorString(e));
+  }
   std::vector<double> st(3 * L.nn);
   cudaError_t e = cudaMemcpyAsync(st.data(), buffers[HKS_BUF_STATS], st.size() * sizeof(double),
                                   cudaMemcpyDeviceToHost, s);
@@ -1189,6 +1208,25 @@ extern "C" int hks_factor_stats(hks_plan* P, void* const* buffers, double* z_con
       z_cond[i] = rc > 0 ? 1.0 / rc : std::numeric_limits<double>::infinity();
     }
   }
+  return HKS_OK;
+}
+
+// Stream the dgecon estimates run on (default: an internal lowest-priority
+// stream).  A caller that owns the factor storage's allocator passes its
+// own stream so it can mark the storage in use there.
+extern "C" int hks_set_cond_stream(hks_plan* P, void* stream) {
+  if (!P) return set_error(HKS_ERR_INVALID, "hks_set_cond_stream: null plan");
+  if (P->cond_pending && P->cond_done) cudaEventSynchronize(P->cond_done);
+  P->cond_stream = stream ? as_stream(stream) : P->own_cond_stream;
+  return HKS_OK;
+}
+
+// `stream` waits (device-side) for the last factorization's dgecon estimates.
+extern "C" int hks_cond_wait(hks_plan* P, void* stream) {
+  if (!P) return set_error(HKS_ERR_INVALID, "hks_cond_wait: null plan");
+  if (!P->cond_pending) return HKS_OK;
+  const cudaError_t e = cudaStreamWaitEvent(as_stream(stream), P->cond_done, 0);
+  if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_cond_wait: %s", cudaGetErrorString(e));
   return HKS_OK;
 }
 

@@ -53,7 +53,6 @@ constexpr int kNumKinds = 15;
 // Opt-in per-kind CUDA-event timing of every step (hks_profile_*).
 void profile_step(int kind, double flops, double bytes, cudaEvent_t a, cudaEvent_t b);
 bool profiling();
-bool side_streams_enabled();
 void count_launch(int n = 1);
 
 // Accumulates host descriptor arrays, uploads them in one arena.
@@ -88,9 +87,6 @@ class StepList {
   std::vector<size_t> offs_;
   std::vector<Step> steps_;
   std::vector<size_t> marks_;
-  // diagnostic steps (dgecon) run on a low-priority side stream joined at the end
-  mutable cudaStream_t side_ = nullptr;
-  mutable cudaEvent_t fork_ = nullptr, join_ = nullptr;
   char* dev_ = nullptr;
   size_t dev_bytes_ = 0;
 };
@@ -146,8 +142,18 @@ struct hks_plan {
 
   hks::StepList coup_steps;                 // build_operator
   hks::GraphCache coup_exec;
-  std::unique_ptr<hks::StepList> fact[2];   // factorize without / with dgecon
+  std::unique_ptr<hks::StepList> fact[2];   // factorize without / with the anorm steps for dgecon
   hks::GraphCache fact_graphs[2];
+  // dgecon estimates: one step per internal level, run on a side stream as
+  // soon as that level's LU is done (waits on level_ev), never joined into
+  // the factorization -- nothing downstream reads z_cond (solver.py:106).
+  std::vector<std::unique_ptr<hks::StepList>> cond_levels;
+  std::vector<int> cond_wait;               // level_ev index each cond level waits for
+  cudaStream_t cond_stream = nullptr;       // caller's stream (hks_set_cond_stream) or own_cond_stream
+  cudaStream_t own_cond_stream = nullptr;
+  cudaEvent_t cond_done = nullptr;
+  hks::Bases* cond_bases = nullptr;         // device base table of the last cond launch
+  bool cond_pending = false;
   hks::DevBuf fws;                          // factorize level workspace
   std::vector<cudaEvent_t> level_ev;        // per-level factorize timing (leaf level first)
   std::map<int64_t, std::unique_ptr<hks::VecProgram>> solve_prog, mv_prog, up_prog;
@@ -158,6 +164,10 @@ struct hks_plan {
 
   int64_t R(int64_t i) const { return rank[2 * i + 1] + rank[2 * i + 2]; }
   ~hks_plan() {
+    if (cond_done) cudaEventSynchronize(cond_done);
     for (auto e : level_ev) cudaEventDestroy(e);
+    if (cond_done) cudaEventDestroy(cond_done);
+    if (own_cond_stream) cudaStreamDestroy(own_cond_stream);
+    if (cond_bases) cudaFree(cond_bases);
   }
 };

@@ -64,7 +64,7 @@ class Factorization:
     """tree, skeletons, lam, factors, couplings, level_seconds, max_rank,
     solve(), z_cond_per_level() (solver.py:56-83)."""
 
-    def __init__(self, op, lam, bufs, level_seconds, z_cond):
+    def __init__(self, op, lam, bufs, level_seconds, z_cond=None):
         self.op = op
         self.tree = op.tree
         self.skeletons = op.skeletons
@@ -75,8 +75,24 @@ class Factorization:
         self.level_seconds = level_seconds
         ranks = op.skeletons.ranks
         self.max_rank = int(ranks[1:].max()) if ranks.size > 1 else 0
-        self._z_cond = z_cond
+        self._zc = z_cond
         self.factors = _Factors(self)
+
+    @property
+    def _z_cond(self):
+        """Per-node z_cond, read once the asynchronous dgecon estimates of
+        this factorization are done (hks_factor_stats waits for them)."""
+        if self._zc is None:
+            z = np.zeros(self.layout.nn)
+            N.call("hks_factor_stats", self.op.plan.handle, self.buffers(), z.ctypes.data_as(N._DP), None,
+                   N.stream_ptr())
+            self._zc = z
+        return self._zc
+
+    def join_cond(self):
+        """Make the current stream wait (device-side) for the dgecon
+        estimates (they run on op.plan.cond_stream)."""
+        N.call("hks_cond_wait", self.op.plan.handle, N.stream_ptr())
 
     @property
     def n(self):
@@ -147,14 +163,14 @@ def factorize(op, lam, threads=1, with_cond=True):
         raise FactorizationError(N.last_error())
     if rc != N.HKS_OK:
         raise N.HksError(rc, N.last_error())
-    z_cond = np.zeros(lay.nn)
-    N.call("hks_factor_stats", op.plan.handle, op.buffers(bufs), z_cond.ctypes.data_as(N._DP), None,
-           N.stream_ptr())
+    if with_cond:  # the estimates still read Z_LU / STATS on the condition stream
+        for bi in (N.BUF_Z_LU, N.BUF_STATS):
+            bufs[bi].record_stream(op.plan.cond_stream)
     depth = op.tree.depth
     ms = np.zeros(depth + 1)
     N.call("hks_factor_level_ms", op.plan.handle, ms.ctypes.data_as(N._DP))
     level_seconds = {lev: float(ms[lev]) * 1e-3 for lev in range(depth + 1)}  # device time per level
-    return Factorization(op, float(lam), bufs, level_seconds, z_cond)
+    return Factorization(op, float(lam), bufs, level_seconds)
 
 
 def solve_device(f, B):

@@ -31,6 +31,10 @@ class Plan:
         self._x = tree.device_points()
         N.call("hks_plan_create", ctypes.byref(self.handle), N.ptr(self._x), tree.n, tree.d, tree.depth,
                skeletons.layout.max_rank, ranks.ctypes.data_as(N._I64P), ctypes.byref(self.kern))
+        # dgecon estimates run here, off the factorization's critical path;
+        # factor storage they read is marked in use on this stream
+        self.cond_stream = N.torch().cuda.Stream(device=N.device(), priority=0)
+        N.call("hks_set_cond_stream", self.handle, ctypes.c_void_p(self.cond_stream.cuda_stream))
 
     def __del__(self):
         h = getattr(self, "handle", None)

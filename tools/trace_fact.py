@@ -7,6 +7,7 @@ import numpy as np
 import paper_1701_02324_b200 as hk
 from paper_1701_02324_b200 import workloads as W, _native as N
 w = W.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "C2"]
+COND = len(sys.argv) > 2 and sys.argv[2] == "cond"
 x = W.points(w, 0)
 kern = hk.KernelSpec("gaussian", h=w.h, regularization=w.lam)
 cfg = hk.SkeletonConfig(tau=w.tau, max_rank=w.max_rank, samples=w.samples, sample_mode="knn_augmented", seed=0)
@@ -15,10 +16,10 @@ knn = hk.knn_bruteforce(tree.points, w.kappa)
 sk = hk.build_skeletons(tree, kern, cfg, knn=knn)
 op = hk.build_operator(tree, sk, kern)
 for _ in range(3):
-    f = hk.factorize(op, w.lam, with_cond=False)
+    f = hk.factorize(op, w.lam, with_cond=COND)
 torch.cuda.synchronize()
 N.profile(True)
-f = hk.factorize(op, w.lam, with_cond=False)
+f = hk.factorize(op, w.lam, with_cond=COND)
 torch.cuda.synchronize()
 print("MARK", file=sys.stderr, flush=True)
 res = N.profile(False)
