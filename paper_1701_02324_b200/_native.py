@@ -78,13 +78,13 @@ SIGNATURES = {
 }
 
 KIND_NAMES = ("gemm", "copy", "getrf", "getrs", "gecon", "eval", "eval_rm", "ksum", "panel", "swap",
-              "trsm_l", "trsm_u", "norm1", "lu_fused")
+              "trsm_l", "trsm_u", "norm1", "lu_fused", "gather", "getrs_fused")  # plan.h StepKind order (kNumKinds)
 
 
 def profile(enable):
     """Start (True) / stop (False) per-kind CUDA-event timing of plan steps;
     returns {kind: {launches, ms, flops, bytes}} accumulated so far."""
-    out = (ctypes.c_double * (4 * len(KIND_NAMES)))()
+    out = (ctypes.c_double * (4 * 64))()  # >= 4 * kNumKinds (tests/test_cpu_abi.py checks the names)
     call("hks_profile", int(bool(enable)), out)
     return {k: {"launches": out[4 * i], "ms": out[4 * i + 1], "flops": out[4 * i + 2],
                 "bytes": out[4 * i + 3]} for i, k in enumerate(KIND_NAMES)}

@@ -179,6 +179,15 @@ struct PanelDesc {
   int g0, pad;
 };
 
+// B := A^-1 B for an LU (getrf storage, n <= kGetrsFusedMax) and its recorded
+// total row permutation (perm[i] = row of B that lands at i); lower = 0
+// skips the forward sweep (B already forward-substituted).
+constexpr int kGetrsFusedMax = 256;
+struct GetrsDesc {
+  Ref LU, perm, B;
+  int n, lda, ldb, ncols, lower, pad;
+};
+
 // Row gather A[i, c] := A[perm[i], c] for rows [r0, r1) and columns [c0, c1)
 // (perm maps [r0, r1) onto itself): the interchanges of a pivot sequence
 // applied in one parallel pass.

@@ -38,6 +38,8 @@ cudaError_t launch_getrs_batched(const Bases* bases, const LuSolveDesc* d_descs,
 cudaError_t launch_panel_batched(const Bases* b, const PanelDesc* d, int count, int max_rows, int pb,
                                  cudaStream_t s);
 cudaError_t launch_swap_batched(const Bases* b, const SwapDesc* d, int count, int max_cols, cudaStream_t s);
+cudaError_t launch_getrs_fused(const Bases* b, const GetrsDesc* d, int count, int max_n, int max_cols,
+                               cudaStream_t s);
 cudaError_t launch_gather_batched(const Bases* b, const GatherDesc* d, int count, int max_rows, int max_cols,
                                   cudaStream_t s);
 cudaError_t launch_trsm_batched(const Bases* b, const TrsmDesc* d, int count, int max_cols, int max_k, bool upper,

@@ -300,36 +300,28 @@ __global__ void swap_kernel(const Bases* __restrict__ bases_ptr, const SwapDesc*
 // second buffer while the current block computes.  Shared memory is sized
 // by the step's largest k, so narrow / shallow solves pack several CTAs per
 // SM.
-template <bool UPPER, int NC>
+template <bool UPPER, int NW>
 __device__ __forceinline__ void trsm_stage_rows(double* Ts, int tts, const double* T, int ldt, int k, int b,
                                                 int wid, int lane) {
   const int r0 = b * 32, nr = min(32, k - r0);
   const int klo = UPPER ? r0 : 0, khi = UPPER ? k : r0 + nr;
   const bool ok = lane < nr;
-  for (int cc = klo + wid; cc < khi; cc += NC / 32)
+  for (int cc = klo + wid; cc < khi; cc += NW)
     cp_async8(Ts + lane * tts + cc, ok ? T + (r0 + lane) + (size_t)cc * ldt : T, ok);
 }
 
-template <bool UPPER, int NC>
-__global__ void __launch_bounds__(NC) trsm_kernel(const Bases* __restrict__ bases_ptr,
-                                                  const TrsmDesc* __restrict__ descs, int kcap, int tts) {
+// One triangular sweep X := T^-1 X over a k x NC block of right-hand sides
+// already in shared memory (X row-major, ld NC + 4); T is read through the
+// double-buffered 32-row staging area Tbuf (ld tts).  Ends with a barrier.
+template <bool UPPER, int NC, int NT = NC>
+__device__ __forceinline__ void trsm_sweep(double* X, double* Tbuf, int tts, const double* T, int ldt, int k,
+                                           int nc) {
+  static_assert(NT == NC || (NC == 32 && NT == 128), "warp <-> tile mapping");
+  constexpr int NW = NT / 32;
   constexpr int TXS = NC + 4;  // X row stride: == 4 (mod 16), conflict-free DMMA B fragments
-  const Bases& bases = *bases_ptr;
-  const TrsmDesc D = descs[blockIdx.y];
-  const int c0 = blockIdx.x * NC;
-  if (c0 >= D.ncols) return;
-  const int nc = min(NC, D.ncols - c0), k = D.k;
-  const double* T = at<const double>(bases, D.T);
-  double* B = at<double>(bases, D.B) + (size_t)c0 * D.ldb;
-  extern __shared__ double tsm[];
-  double* X = tsm;                    // k x NC, row-major (ld TXS)
-  double* Tbuf = tsm + kcap * TXS;    // 2 x 32 rows of T, row-major (ld tts)
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int nblk = (k + 31) / 32;
-  // lanes walk a column's rows: 256-byte coalesced LDGSTS
-  for (int c = wid; c < nc; c += NC / 32)
-    for (int i = lane; i < k; i += 32) cp_async8(X + i * TXS + c, B + i + (size_t)c * D.ldb, true);
-  trsm_stage_rows<UPPER, NC>(Tbuf, tts, T, D.ldt, k, UPPER ? nblk - 1 : 0, wid, lane);
+  trsm_stage_rows<UPPER, NW>(Tbuf, tts, T, ldt, k, UPPER ? nblk - 1 : 0, wid, lane);
   cp_async_commit();
   const int fr = lane >> 2, fc = lane & 3;
   for (int bb = 0; bb < nblk; ++bb) {
@@ -339,13 +331,35 @@ __global__ void __launch_bounds__(NC) trsm_kernel(const Bases* __restrict__ base
     cp_async_wait<0>();
     __syncthreads();  // X / this block's rows of T landed; the previous block's solve is complete
     if (bb + 1 < nblk) {
-      trsm_stage_rows<UPPER, NC>(Tbuf + ((bb + 1) & 1) * 32 * tts, tts, T, D.ldt, k, UPPER ? b - 1 : b + 1, wid,
+      trsm_stage_rows<UPPER, NW>(Tbuf + ((bb + 1) & 1) * 32 * tts, tts, T, ldt, k, UPPER ? b - 1 : b + 1, wid,
                                  lane);
       cp_async_commit();
     }
     // X[r0:r0+nr, :] -= T[r0:r0+nr, u] X[u, :] over the solved rows u (DMMA)
     const int ulo = UPPER ? r0 + nr : 0, uhi = UPPER ? k : r0;
-    if (uhi > ulo && wid * 32 < nc) {
+    if (NT != NC) {  // 4 warps on one 32-column tile: warp w owns rows 8w .. 8w+7
+      if (uhi > ulo) {
+        double acc[4][2];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
+        for (int kk = ulo; kk < uhi; kk += 4) {
+          const int kq = kk + fc;
+          const bool kin = kq < uhi;
+          const double a = kin ? Ts[(wid * 8 + fr) * tts + kq] : 0.0;
+          double bv[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) bv[j] = kin ? X[kq * TXS + j * 8 + fr] : 0.0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma884(acc[j][0], acc[j][1], a, bv[j]);
+        }
+        const int rr = wid * 8 + fr;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            if (rr < nr) X[(r0 + rr) * TXS + j * 8 + 2 * fc + h] -= acc[j][h];
+      }
+    } else if (uhi > ulo && wid * 32 < nc) {
       const int cb = wid * 32;  // this warp's 32 columns
       double acc[4][4][2];
 #pragma unroll
@@ -403,8 +417,60 @@ __global__ void __launch_bounds__(NC) trsm_kernel(const Bases* __restrict__ base
     }
   }
   __syncthreads();
+}
+
+template <bool UPPER, int NC>
+__global__ void __launch_bounds__(NC) trsm_kernel(const Bases* __restrict__ bases_ptr,
+                                                  const TrsmDesc* __restrict__ descs, int kcap, int tts) {
+  constexpr int TXS = NC + 4;
+  const Bases& bases = *bases_ptr;
+  const TrsmDesc D = descs[blockIdx.y];
+  const int c0 = blockIdx.x * NC;
+  if (c0 >= D.ncols) return;
+  const int nc = min(NC, D.ncols - c0), k = D.k;
+  const double* T = at<const double>(bases, D.T);
+  double* B = at<double>(bases, D.B) + (size_t)c0 * D.ldb;
+  extern __shared__ double tsm[];
+  double* X = tsm;                    // k x NC, row-major (ld TXS)
+  double* Tbuf = tsm + kcap * TXS;    // 2 x 32 rows of T, row-major (ld tts)
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // lanes walk a column's rows: 256-byte coalesced LDGSTS
+  for (int c = wid; c < nc; c += NC / 32)
+    for (int i = lane; i < k; i += 32) cp_async8(X + i * TXS + c, B + i + (size_t)c * D.ldb, true);
+  trsm_sweep<UPPER, NC>(X, Tbuf, tts, T, D.ldt, k, nc);
   for (int c = wid; c < nc; c += NC / 32)
     for (int i = lane; i < k; i += 32) B[i + (size_t)c * D.ldb] = X[i * TXS + c];
+}
+
+// Whole getrs of a small matrix (n <= kGetrsFusedMax) in one CTA per block of
+// NC right-hand-side columns: the recorded total row permutation is applied
+// while B is gathered into shared memory, then the unit-lower and upper
+// sweeps run back to back, one store at the end.  Replaces 2 + 4 n/128
+// level-wide launches of the solve program.
+template <int NC, int NT>
+__global__ void __launch_bounds__(NT) getrs_fused_kernel(const Bases* __restrict__ bases_ptr,
+                                                         const GetrsDesc* __restrict__ descs, int kcap, int tts) {
+  constexpr int TXS = NC + 4;
+  const Bases& bases = *bases_ptr;
+  const GetrsDesc D = descs[blockIdx.y];
+  const int c0 = blockIdx.x * NC;
+  if (c0 >= D.ncols) return;
+  const int nc = min(NC, D.ncols - c0), n = D.n;
+  const double* LU = at<const double>(bases, D.LU);
+  const int* perm = at<const int>(bases, D.perm);
+  double* B = at<double>(bases, D.B) + (size_t)c0 * D.ldb;
+  extern __shared__ double tsm[];
+  double* X = tsm;
+  double* Tbuf = tsm + kcap * TXS;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int i = lane; i < n; i += 32) {
+    const int src = perm[i];
+    for (int c = wid; c < nc; c += NT / 32) cp_async8(X + i * TXS + c, B + src + (size_t)c * D.ldb, true);
+  }
+  if (D.lower) trsm_sweep<false, NC, NT>(X, Tbuf, tts, LU, D.lda, n, nc);
+  trsm_sweep<true, NC, NT>(X, Tbuf, tts, LU, D.lda, n, nc);
+  for (int c = wid; c < nc; c += NT / 32)
+    for (int i = lane; i < n; i += 32) B[i + (size_t)c * D.ldb] = X[i * TXS + c];
 }
 
 // ||A||_1 (max column abs sum) of each n x n matrix, before factoring.
@@ -516,6 +582,21 @@ cudaError_t launch_trsm_batched(const Bases* b, const TrsmDesc* d, int count, in
   if (max_k > 128) return cudaErrorInvalidValue;
   return upper ? launch_trsm_t<true>(b, d, count, max_cols, max_k, s)
                : launch_trsm_t<false>(b, d, count, max_cols, max_k, s);
+}
+
+cudaError_t launch_getrs_fused(const Bases* b, const GetrsDesc* d, int count, int max_n, int max_cols,
+                               cudaStream_t s) {
+  if (count <= 0 || max_n <= 0 || max_cols <= 0) return cudaSuccess;
+  if (max_n > kGetrsFusedMax) return cudaErrorInvalidValue;
+  constexpr int NC = 32;
+  const int kcap = (max_n + 31) / 32 * 32, tts = kcap + 4;
+  const size_t sm = (size_t)(kcap * (NC + 4) + 2 * 32 * tts) * sizeof(double);
+  raise_smem_limit(getrs_fused_kernel<NC, 128>, sm);
+  for (int first = 0; first < count; first += 65535) {
+    const int cnt = count - first < 65535 ? count - first : 65535;
+    getrs_fused_kernel<NC, 128><<<dim3((max_cols + NC - 1) / NC, cnt), 128, sm, s>>>(b, d + first, kcap, tts);
+  }
+  return cudaGetLastError();
 }
 
 cudaError_t launch_norm1_batched(const Bases* b, const LuDesc* d, int count, cudaStream_t s) {

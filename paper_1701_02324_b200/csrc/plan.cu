@@ -76,6 +76,13 @@ cudaError_t StepList::upload(cudaStream_t stream) {
   return e;
 }
 
+StepList::~StepList() {
+  if (dev_) cudaFree(dev_);
+  if (side_) cudaStreamDestroy(side_);
+  if (fork_ev_) cudaEventDestroy(fork_ev_);
+  if (join_ev_) cudaEventDestroy(join_ev_);
+}
+
 void StepList::clear() {
   host_.clear();
   offs_.clear();
@@ -83,9 +90,7 @@ void StepList::clear() {
   marks_.clear();
 }
 
-StepList::~StepList() {
-  if (dev_) cudaFree(dev_);
-}
+
 
 cudaError_t DevBuf::ensure(size_t b) {
   if (b <= bytes) return cudaSuccess;
@@ -113,7 +118,20 @@ cudaError_t StepList::run(const Bases* b, const double* X, int d, const KernelPa
   for (size_t si = 0; si < steps_.size(); ++si) {
     const Step& st = steps_[si];
     while (ev && next_mark < marks_.size() && marks_[next_mark] == si) record(ev[next_mark++], main);
-    s = main;
+    if (st.kind == ST_FORK || st.kind == ST_JOIN) {
+      if (!side_) {
+        cudaError_t e = cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&fork_ev_, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&join_ev_, cudaEventDisableTiming);
+        if (e != cudaSuccess) return e;
+      }
+      cudaError_t e = st.kind == ST_FORK ? cudaEventRecord(fork_ev_, main) : cudaEventRecord(join_ev_, side_);
+      if (e == cudaSuccess)
+        e = st.kind == ST_FORK ? cudaStreamWaitEvent(side_, fork_ev_, 0) : cudaStreamWaitEvent(main, join_ev_, 0);
+      if (e != cudaSuccess) return e;
+      continue;
+    }
+    s = st.stream ? side_ : main;
     cudaError_t e = cudaSuccess;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (prof) {
@@ -154,6 +172,9 @@ cudaError_t StepList::run(const Bases* b, const double* X, int d, const KernelPa
         break;
       case ST_GATHER:
         e = launch_gather_batched(b, (const GatherDesc*)st.d, st.count, st.p0, st.p1, s);
+        break;
+      case ST_GETRS_FUSED:
+        e = launch_getrs_fused(b, (const GetrsDesc*)st.d, st.count, st.p0, st.p1, s);
         break;
       case ST_TRSM_L:
       case ST_TRSM_U:
@@ -547,6 +568,11 @@ void add_lu_program(StepList& sl, const std::vector<LuJob>& jobs, bool with_norm
     else
       ix.sw.add(A, j.piv, lda, r0, r1, c0, c1);
   };
+  static const bool look_ahead = [] {
+    const char* e = getenv("HKS_LOOKAHEAD");
+    return e ? atoi(e) != 0 : false;  // measured neutral: the leaf panels fill the SMs' register files
+  }();
+  bool side_pending = false;
   for (int g0 = 0; g0 < nmax; g0 += kGroup) {
     for (int p0 = g0; p0 < g0 + kGroup && p0 < nmax; p0 += PB) {
       Ix ix;
@@ -582,10 +608,20 @@ void add_lu_program(StepList& sl, const std::vector<LuJob>& jobs, bool with_norm
       gm.flush(sl);
       pn.flush(sl, PB);
     }
-    // the group's interchanges everywhere else, U rows of the group, trailing update
+    // the group's interchanges everywhere else, U rows of the group, trailing
+    // update.  Look-ahead: the next group's 128 columns are updated first on
+    // the main stream, which then goes on to the next group's panels while
+    // the rest of the trailing update (and the right-hand sides) runs on the
+    // side stream; the next group end (whose interchanges touch this group's
+    // L columns) joins it.
+    if (side_pending) {
+      sl.join();
+      side_pending = false;
+    }
+    const bool ahead = look_ahead && g0 + 2 * kGroup < nmax + kGroup && g0 + kGroup < nmax;
     Ix ix;
-    Trsms tr;
-    Gemms gm;
+    Trsms tr, tr_side;
+    Gemms gm, gm_side;
     for (auto& j : jobs) {
       if (g0 >= j.n) continue;
       const int gb = std::min(kGroup, j.n - g0), ge = g0 + gb;
@@ -594,18 +630,36 @@ void add_lu_program(StepList& sl, const std::vector<LuJob>& jobs, bool with_norm
       interchange(ix, j, j.A, j.lda, 1, g0, ge, 0, g0);
       interchange(ix, j, j.A, j.lda, 1, g0, ge, ge, j.n);
       if (j.r > 0) interchange(ix, j, j.B, j.ldb, 1, g0, ge, 0, j.r);
-      tr.add(elem(j.A, g0, g0, j.lda), j.lda, elem(j.A, g0, ge, j.lda), j.lda, gb, j.n - ge);
-      if (j.r > 0) tr.add(elem(j.A, g0, g0, j.lda), j.lda, elem(j.B, g0, 0, j.ldb), j.ldb, gb, j.r);
+      const int split = ahead ? std::min(j.n, ge + kGroup) : j.n;  // columns [ge, split) now, the rest later
+      Trsms& tr2 = ahead ? tr_side : tr;
+      Gemms& gm2 = ahead ? gm_side : gm;
+      tr.add(elem(j.A, g0, g0, j.lda), j.lda, elem(j.A, g0, ge, j.lda), j.lda, gb, split - ge);
       gm.add(elem(j.A, ge, g0, j.lda), j.lda, 0, elem(j.A, g0, ge, j.lda), j.lda, 0, elem(j.A, ge, ge, j.lda), j.lda,
-             j.n - ge, j.n - ge, gb, -1.0, 1.0);
-      if (j.r > 0)
-        gm.add(elem(j.A, ge, g0, j.lda), j.lda, 0, elem(j.B, g0, 0, j.ldb), j.ldb, 0, elem(j.B, ge, 0, j.ldb), j.ldb,
-               j.n - ge, j.r, gb, -1.0, 1.0);
+             j.n - ge, split - ge, gb, -1.0, 1.0);
+      if (split < j.n) {
+        tr2.add(elem(j.A, g0, g0, j.lda), j.lda, elem(j.A, g0, split, j.lda), j.lda, gb, j.n - split);
+        gm2.add(elem(j.A, ge, g0, j.lda), j.lda, 0, elem(j.A, g0, split, j.lda), j.lda, 0,
+                elem(j.A, ge, split, j.lda), j.lda, j.n - ge, j.n - split, gb, -1.0, 1.0);
+      }
+      if (j.r > 0) {
+        tr2.add(elem(j.A, g0, g0, j.lda), j.lda, elem(j.B, g0, 0, j.ldb), j.ldb, gb, j.r);
+        gm2.add(elem(j.A, ge, g0, j.lda), j.lda, 0, elem(j.B, g0, 0, j.ldb), j.ldb, 0, elem(j.B, ge, 0, j.ldb), j.ldb,
+                j.n - ge, j.r, gb, -1.0, 1.0);
+      }
     }
     ix.flush(sl);
+    if (ahead) {
+      sl.fork();
+      sl.side(true);
+      tr_side.flush(sl, false);
+      gm_side.flush(sl);
+      sl.side(false);
+      side_pending = true;
+    }
     tr.flush(sl, false);
     gm.flush(sl);
   }
+  if (side_pending) sl.join();
   // backward: B := U^-1 B, groups from the bottom (right-looking)
   bool any_rhs = false;
   for (auto& j : jobs) any_rhs |= j.r > 0;
@@ -630,6 +684,22 @@ void add_lu_solve_program(StepList& sl, const std::vector<LuJob>& jobs) {
   int nmax = 0;
   for (auto& j : jobs) nmax = std::max(nmax, j.n);
   if (nmax == 0) return;
+  bool fused = nmax <= kGetrsFusedMax && getenv("HKS_GETRS_STEPS") == nullptr;
+  for (auto& j : jobs) fused &= j.r == 0 || j.ws != kNull;
+  if (fused) {  // one launch: gathered load, both sweeps (lu2.cu: getrs_fused_kernel)
+    std::vector<GetrsDesc> v;
+    int mc = 0;
+    double f = 0, bytes = 0;
+    for (auto& j : jobs) {
+      if (j.r <= 0 || j.n <= 0) continue;
+      v.push_back(GetrsDesc{j.A, j.ws, j.B, j.n, j.lda, j.ldb, j.r, 1, 0});
+      mc = std::max(mc, j.r);
+      f += 2.0 * j.n * j.n * (double)j.r;
+      bytes += 8.0 * ((double)j.n * j.n + 2.0 * j.n * j.r);
+    }
+    sl.add(ST_GETRS_FUSED, v, nmax, mc, f, bytes);
+    return;
+  }
   Swaps sw;
   Gathers ga;
   for (auto& j : jobs) {

@@ -36,7 +36,8 @@ Layout make_layout(int64_t n, int64_t depth, int64_t max_rank);
 
 enum StepKind {
   ST_GEMM, ST_COPY, ST_GETRF, ST_GETRS, ST_GECON, ST_EVAL_CM, ST_EVAL_RM, ST_KSUM,
-  ST_PANEL, ST_SWAP, ST_TRSM_L, ST_TRSM_U, ST_NORM1, ST_LU_FUSED, ST_GATHER
+  ST_PANEL, ST_SWAP, ST_TRSM_L, ST_TRSM_U, ST_NORM1, ST_LU_FUSED, ST_GATHER, ST_GETRS_FUSED,
+  ST_FORK, ST_JOIN  // stream control: the side stream waits for / rejoins the main stream
 };
 
 struct Step {
@@ -46,9 +47,10 @@ struct Step {
   int p0, p1;     // grid sizing (max dims)
   double flops;   // algorithmic FP64 flops of the whole step
   double bytes;   // compulsory HBM bytes of the whole step
+  int stream;     // 0 main, 1 side (between ST_FORK and ST_JOIN)
 };
 
-constexpr int kNumKinds = 15;
+constexpr int kNumKinds = 16;
 
 // Opt-in per-kind CUDA-event timing of every step (hks_profile_*).
 void profile_step(int kind, double flops, double bytes, cudaEvent_t a, cudaEvent_t b);
@@ -65,8 +67,14 @@ class StepList {
     host_.resize(at + v.size() * sizeof(D));
     std::memcpy(host_.data() + at, v.data(), v.size() * sizeof(D));
     offs_.push_back(at);
-    steps_.push_back(Step{kind, nullptr, (int)v.size(), p0, p1, flops, bytes});
+    steps_.push_back(Step{kind, nullptr, (int)v.size(), p0, p1, flops, bytes, side_now_ ? 1 : 0});
   }
+  // Steps added between fork() and join() may run on the side stream
+  // (side(true)) concurrently with main-stream steps added meanwhile;
+  // join() makes the main stream wait for everything the side stream has.
+  void fork() { control(ST_FORK); }
+  void join() { control(ST_JOIN); }
+  void side(bool on) { side_now_ = on; }
   cudaError_t upload(cudaStream_t stream);
   // ev (optional): marks().size() + 1 events, recorded before each marked
   // step and after the last step (per-level device timing)
@@ -80,9 +88,20 @@ class StepList {
   StepList& operator=(const StepList&) = delete;
   ~StepList();
   bool empty() const { return steps_.empty(); }
-  size_t launches() const { return steps_.size(); }
+  size_t launches() const {
+    size_t n = 0;
+    for (auto& s : steps_) n += (s.kind != ST_FORK && s.kind != ST_JOIN);
+    return n;
+  }
 
  private:
+  void control(int kind) {
+    offs_.push_back(0);
+    steps_.push_back(Step{kind, nullptr, 0, 0, 0, 0.0, 0.0, 0});
+  }
+  bool side_now_ = false;
+  mutable cudaStream_t side_ = nullptr;
+  mutable cudaEvent_t fork_ev_ = nullptr, join_ev_ = nullptr;
   std::vector<char> host_;
   std::vector<size_t> offs_;
   std::vector<Step> steps_;

@@ -118,3 +118,19 @@ def test_no_cuda_means_loud_failure():
     import paper_1701_02324_b200 as hk
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         hk.eval_block(hk.KernelSpec(), np.zeros((2, 2)), np.zeros((2, 2)))
+
+
+def test_profile_kind_names_match_step_kinds():
+    """KIND_NAMES (hks_profile's per-kind layout) follows plan.h's StepKind
+    enum up to kNumKinds; the stream-control kinds after it are not timed."""
+    import re
+    from pathlib import Path
+    from paper_1701_02324_b200 import _native as N
+    src = (Path(__file__).resolve().parents[1] / "paper_1701_02324_b200" / "csrc" / "plan.h").read_text()
+    body = re.search(r"enum StepKind \{(.*?)\};", src, re.S).group(1)
+    body = re.sub(r"//[^\n]*", "", body)
+    kinds = [k.strip() for k in body.split(",") if k.strip()]
+    nk = int(re.search(r"constexpr int kNumKinds = (\d+);", src).group(1))
+    assert kinds[nk:] == ["ST_FORK", "ST_JOIN"]
+    assert len(N.KIND_NAMES) == nk
+    assert [k[3:].lower() for k in kinds[:nk]] == [{"eval": "eval_cm"}.get(n, n) for n in N.KIND_NAMES]
