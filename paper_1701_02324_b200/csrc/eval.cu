@@ -94,8 +94,14 @@ __global__ void __launch_bounds__(256) eval_kernel(const double* __restrict__ X,
   const double ediag = e.diag ? bases.lam : 0.0;
   const int r0 = (blockIdx.x / tiles_n) * TM, c0 = (blockIdx.x % tiles_n) * TN;
   if (r0 >= e.m || c0 >= e.n) return;
-  __shared__ double Xr[TM * XS];
-  __shared__ double Xc[TN * XS];
+  // K(X_a, X_a): the diff-form distance makes the block exactly symmetric,
+  // so only tiles on / above the diagonal are computed; each off-diagonal
+  // tile also writes its transpose (column-major output only).
+  const bool sym = !ROW_MAJOR && e.rows == kNull && e.cols == kNull && e.row0 == e.col0 && e.m == e.n;
+  if (sym && r0 > c0) return;
+  __shared__ double stage_area[(TM + TN) * XS];
+  double* Xr = stage_area;
+  double* Xc = stage_area + TM * XS;
   const int t = threadIdx.x;
   // ROW_MAJOR: thread owns one column and 16 rows (coalesced row-major store);
   // else one row and 16 columns (coalesced column-major store)
@@ -127,17 +133,29 @@ __global__ void __launch_bounds__(256) eval_kernel(const double* __restrict__ X,
     }
     __syncthreads();
   }
+  const bool mirror = sym && r0 != c0;
+  double* Kt = stage_area;  // 64 x 65 tile for the mirrored store (the staging area is free now)
+  static_assert(TM * (TN + 1) <= (TM + TN) * XS, "tile must fit the staging area");
 #pragma unroll
   for (int q = 0; q < 16; ++q) {
     const int i = ROW_MAJOR ? r0 + grp + q : r0 + own;
     const int j = ROW_MAJOR ? c0 + own : c0 + grp + q;
+    double v = 0.0;
     if (i < e.m && j < e.n) {
-      double v = kernel_value(kp, acc[q]);
+      v = kernel_value(kp, acc[q]);
       if (i == j) v += ediag;
       if (ROW_MAJOR)
         eout[(size_t)i * e.ldo + j] = v;
       else
         eout[i + (size_t)j * e.ldo] = v;
+    }
+    if (mirror) Kt[(grp + q) * (TM + 1) + own] = v;  // Kt[jj][ii]
+  }
+  if (mirror) {  // K[c0 + jj, r0 + ii] = K[r0 + ii, c0 + jj], stored coalesced along jj
+    __syncthreads();
+    for (int ii = t >> 6; ii < TM; ii += 4) {
+      const int jj = t & 63;
+      if (r0 + ii < e.m && c0 + jj < e.n) eout[(c0 + jj) + (size_t)(r0 + ii) * e.ldo] = Kt[jj * (TM + 1) + ii];
     }
   }
 }

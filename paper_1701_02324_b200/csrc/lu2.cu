@@ -419,8 +419,8 @@ __device__ __forceinline__ void trsm_sweep(double* X, double* Tbuf, int tts, con
   __syncthreads();
 }
 
-template <bool UPPER, int NC>
-__global__ void __launch_bounds__(NC) trsm_kernel(const Bases* __restrict__ bases_ptr,
+template <bool UPPER, int NC, int NT>
+__global__ void __launch_bounds__(NT) trsm_kernel(const Bases* __restrict__ bases_ptr,
                                                   const TrsmDesc* __restrict__ descs, int kcap, int tts) {
   constexpr int TXS = NC + 4;
   const Bases& bases = *bases_ptr;
@@ -435,10 +435,10 @@ __global__ void __launch_bounds__(NC) trsm_kernel(const Bases* __restrict__ base
   double* Tbuf = tsm + kcap * TXS;    // 2 x 32 rows of T, row-major (ld tts)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   // lanes walk a column's rows: 256-byte coalesced LDGSTS
-  for (int c = wid; c < nc; c += NC / 32)
+  for (int c = wid; c < nc; c += NT / 32)
     for (int i = lane; i < k; i += 32) cp_async8(X + i * TXS + c, B + i + (size_t)c * D.ldb, true);
-  trsm_sweep<UPPER, NC>(X, Tbuf, tts, T, D.ldt, k, nc);
-  for (int c = wid; c < nc; c += NC / 32)
+  trsm_sweep<UPPER, NC, NT>(X, Tbuf, tts, T, D.ldt, k, nc);
+  for (int c = wid; c < nc; c += NT / 32)
     for (int i = lane; i < k; i += 32) B[i + (size_t)c * D.ldb] = X[i * TXS + c];
 }
 
@@ -554,16 +554,16 @@ cudaError_t launch_swap_batched(const Bases* b, const SwapDesc* d, int count, in
   return cudaGetLastError();
 }
 
-template <bool UPPER, int NC>
+template <bool UPPER, int NC, int NT = NC>
 static cudaError_t launch_trsm_nc(const Bases* b, const TrsmDesc* d, int count, int max_cols, int max_k,
                                   cudaStream_t s) {
   // tts == 4 (mod 16), and > every column r0 + 31 the register diagonal solve touches
   const int kcap = (max_k + 31) / 32 * 32, tts = kcap + 4;
   const size_t sm = (size_t)(kcap * (NC + 4) + 2 * 32 * tts) * sizeof(double);
-  raise_smem_limit(trsm_kernel<UPPER, NC>, sm);
+  raise_smem_limit(trsm_kernel<UPPER, NC, NT>, sm);
   for (int first = 0; first < count; first += 65535) {
     const int cnt = count - first < 65535 ? count - first : 65535;
-    trsm_kernel<UPPER, NC><<<dim3((max_cols + NC - 1) / NC, cnt), NC, sm, s>>>(b, d + first, kcap, tts);
+    trsm_kernel<UPPER, NC, NT><<<dim3((max_cols + NC - 1) / NC, cnt), NT, sm, s>>>(b, d + first, kcap, tts);
   }
   return cudaGetLastError();
 }
@@ -571,7 +571,7 @@ static cudaError_t launch_trsm_nc(const Bases* b, const TrsmDesc* d, int count, 
 template <bool UPPER>
 static cudaError_t launch_trsm_t(const Bases* b, const TrsmDesc* d, int count, int max_cols, int max_k,
                                  cudaStream_t s) {
-  if (max_cols <= 32) return launch_trsm_nc<UPPER, 32>(b, d, count, max_cols, max_k, s);
+  if (max_cols <= 32) return launch_trsm_nc<UPPER, 32, 128>(b, d, count, max_cols, max_k, s);  // 4 warps stage
   if (max_cols <= 64) return launch_trsm_nc<UPPER, 64>(b, d, count, max_cols, max_k, s);
   return launch_trsm_nc<UPPER, 128>(b, d, count, max_cols, max_k, s);
 }
