@@ -128,6 +128,37 @@ int hks_plan_create(hks_plan** plan, const double* X, int64_t n, int64_t d, int6
                     int64_t max_rank, const int64_t* ranks_host, const hks_kernel* kern);
 int hks_plan_destroy(hks_plan* plan);
 
+/* ----- subtree sharding (solver.py:111-259 split at level p) --
+ * A tree sharded over P = 2^p ranks is one subtree plan per rank plus one top
+ * plan, replicated on every rank.
+ *  HKS_PLAN_SUBTREE: the rank's shard, a complete subtree rooted at a level-p
+ *    node of the global tree (X = the shard's first point, n = shard size,
+ *    skeleton indices local to the shard).  Its root keeps a skeleton
+ *    (ranks_host[0] = r_0): factorize also forms the root's Theta and push;
+ *    solve / hmatvec run in two halves around the exchange (hks_solve_part).
+ *  HKS_PLAN_TOP: levels 0..p of the global tree (X = all points, skeleton
+ *    indices global).  Its 2^p leaves are the shard roots: their Theta and
+ *    skeleton indices are written by the caller (the layout puts leaf j's
+ *    s x s Theta at j * s * s and its s indices at j * s, so an all-gather of
+ *    the ranks' blocks lands in place), and factorize starts at level p - 1.
+ * Layout / plan creation take the mode; HKS_PLAN_FULL is the unsharded tree. */
+enum hks_plan_mode { HKS_PLAN_FULL = 0, HKS_PLAN_SUBTREE = 1, HKS_PLAN_TOP = 2 };
+int hks_layout_ex(int64_t n, int64_t depth, int64_t max_rank, int32_t mode, int64_t* sizes, int64_t* offsets);
+int hks_plan_create_ex(hks_plan** plan, const double* X, int64_t n, int64_t d, int64_t depth,
+                       int64_t max_rank, const int64_t* ranks_host, const hks_kernel* kern, int32_t mode);
+
+/* Split solve / hmatvec.  Subtree plans: part 1 = leaf solves and the upward
+ * sweep, leaving the root's psi (solve) or skeleton weights (hmatvec) in
+ * xchg (r_0 x k, ld r_0); part 2 = the downward sweep from the root's
+ * incoming correction / accumulator read from xchg.  x (u) must be the same
+ * buffer in both halves.  Top plans and full plans: part 0.  For top plans
+ * b (w) holds the shard roots' psi and x (u) receives their corrections,
+ * shard j's r_j x k block at j * max_rank * k (ld r_j). */
+int hks_solve_part(hks_plan* plan, void* const* buffers, const double* b, double* x, int64_t k, int32_t part,
+                   double* xchg, void* stream);
+int hks_hmatvec_part(hks_plan* plan, void* const* buffers, const double* w, double* u, int64_t k, double lam,
+                     int32_t part, double* xchg, void* stream);
+
 /* build_operator, treecode.py:41-62: the sibling couplings K(q_l, q_r) from
  * HKS_BUF_SKEL into HKS_BUF_COUP.  Leaf blocks are never stored (they are
  * re-evaluated inside factorize and the fused hmatvec; hks_leaf_block gives
@@ -201,6 +232,10 @@ int hks_build_tree(const double* X_in, int64_t n, int64_t d, int64_t depth, int6
 
 /* knn_bruteforce, tree.py:163-188: out[n x k] int64, (d^2, index) order, k <= 32. */
 int hks_knn(const double* X, int64_t n, int64_t d, int64_t k, int64_t* out, void* stream);
+/* The same lists for the query rows [q0, q0 + nq) only (a shard's points
+ * against all n): out[nq x k]. */
+int hks_knn_rows(const double* X, int64_t n, int64_t d, int64_t k, int64_t q0, int64_t nq, int64_t* out,
+                 void* stream);
 
 /* sample_rows(knn_augmented), skeleton.py:111-121, for every node of one
  * level: mark = per-node bitmap of neighbours outside the node (counts to
@@ -211,6 +246,16 @@ int hks_knn_rows_mark(const int64_t* knn, int64_t n, int64_t kappa, int64_t leve
 int hks_knn_rows_fill(int64_t n, int64_t level, int64_t depth, int32_t* bitmap, const int64_t* extra,
                       const int64_t* extra_off_host, int64_t* rows, const int64_t* row_off_host,
                       void* stream);
+/* Sharded variants: the nodes [node0, node0 + count) of `level` only, and
+ * kNN lists of the points [row0, row0 + nrows) only (a shard's rows; global
+ * indices).  A node spanning several shards gets the OR of the ranks'
+ * bitmaps (the caller's all-gather) and its counts from hks_bitmap_count. */
+int hks_knn_rows_mark_ex(const int64_t* knn, int64_t row0, int64_t nrows, int64_t n, int64_t kappa, int64_t level,
+                         int64_t node0, int64_t count, int32_t* bitmap, int64_t* counts_host, void* stream);
+int hks_bitmap_count(const int32_t* bitmap, int64_t n, int64_t count, int64_t* counts_host, void* stream);
+int hks_knn_rows_fill_ex(int64_t n, int64_t level, int64_t node0, int64_t count, int32_t* bitmap,
+                         const int64_t* extra, const int64_t* extra_off_host, int64_t* rows,
+                         const int64_t* row_off_host, void* stream);
 
 /* build_skeletons for one level, skeleton.py:125-182: sampled block eval +
  * truncated column-pivoted QR + ID for `count` nodes (first heap index

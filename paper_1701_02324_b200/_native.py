@@ -75,7 +75,18 @@ SIGNATURES = {
     "hks_factor_level_ms": [_P, _DP],
     "hks_set_cond_stream": [_P, _P],
     "hks_cond_wait": [_P, _P],
+    # subtree sharding (include/hks.h, "subtree sharding")
+    "hks_layout_ex": [_I64, _I64, _I64, _I32, _I64P, _I64P],
+    "hks_plan_create_ex": [ctypes.POINTER(_P), _P, _I64, _I64, _I64, _I64, _I64P, _KP, _I32],
+    "hks_solve_part": [_P, _BUFS, _P, _P, _I64, _I32, _P, _P],
+    "hks_hmatvec_part": [_P, _BUFS, _P, _P, _I64, _D, _I32, _P, _P],
+    "hks_knn_rows": [_P, _I64, _I64, _I64, _I64, _I64, _P, _P],
+    "hks_knn_rows_mark_ex": [_P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _P, _I64P, _P],
+    "hks_bitmap_count": [_P, _I64, _I64, _I64P, _P],
+    "hks_knn_rows_fill_ex": [_I64, _I64, _I64, _I64, _P, _P, _I64P, _P, _I64P, _P],
 }
+
+PLAN_FULL, PLAN_SUBTREE, PLAN_TOP = 0, 1, 2
 
 KIND_NAMES = ("gemm", "copy", "getrf", "getrs", "gecon", "eval", "eval_rm", "ksum", "panel", "swap",
               "trsm_l", "trsm_u", "norm1", "lu_fused", "gather", "getrs_fused")  # plan.h StepKind order (kNumKinds)
@@ -181,6 +192,8 @@ def to_device(a, dtype=None):
         out = a.to(device=device(), dtype=dtype or a.dtype)
         return out.contiguous()
     arr = np.ascontiguousarray(a, dtype=dtype and _np_dtype(dtype))
+    if not arr.flags.writeable:  # e.g. tree.perm: torch wants a writable source
+        arr = arr.copy()
     return t.from_numpy(arr).to(device())
 
 
@@ -219,19 +232,20 @@ def col_major(mat):
 
 
 class Layout:
-    """Flat per-node buffer layout of a complete tree (hks_layout)."""
+    """Flat per-node buffer layout of a complete tree (hks_layout_ex); mode
+    PLAN_SUBTREE / PLAN_TOP for the two halves of a sharded tree."""
 
-    def __init__(self, n, depth, max_rank):
-        self.n, self.depth, self.max_rank = int(n), int(depth), int(max_rank)
+    def __init__(self, n, depth, max_rank, mode=PLAN_FULL):
+        self.n, self.depth, self.max_rank, self.mode = int(n), int(depth), int(max_rank), int(mode)
         self.nn = (1 << (self.depth + 1)) - 1
         sizes = (ctypes.c_int64 * NBUF)()
         offs = np.zeros(NBUF * self.nn, dtype=np.int64)
-        call("hks_layout", self.n, self.depth, self.max_rank, sizes,
+        call("hks_layout_ex", self.n, self.depth, self.max_rank, self.mode, sizes,
              offs.ctypes.data_as(_I64P))
         self.sizes = np.array(list(sizes), dtype=np.int64)
         self.off = offs.reshape(NBUF, self.nn)
 
-    def alloc(self, buf):
+    def alloc(self, buf, min_elems=1):
         t = torch()
         dt = {np.int64: t.int64, np.int32: t.int32}.get(BUF_DTYPE.get(buf), t.float64)
-        return t.empty(max(int(self.sizes[buf]), 1), dtype=dt, device=device())
+        return t.empty(max(int(self.sizes[buf]), int(min_elems), 1), dtype=dt, device=device())

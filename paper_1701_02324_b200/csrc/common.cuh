@@ -105,17 +105,17 @@ __device__ inline double block_sum(double v, double* sv) {
 // 56 bits are a byte offset.  One uploaded descriptor program therefore
 // serves every factorization of an operator and every right-hand-side
 // buffer; a call only supplies its base pointers.
-// Buffer id kAbs (= 15) has base 0, i.e. the offset is a raw address.
+// Buffer id kAbs (= 17) has base 0, i.e. the offset is a raw address.
 using Ref = uint64_t;
-constexpr int kNumBases = 16;
-constexpr int kAbs = 15;
+constexpr int kNumBases = 18;
+constexpr int kAbs = 17;
 constexpr uint64_t kOffMask = (uint64_t(1) << 56) - 1;
 constexpr uint64_t kNull = ~uint64_t(0);  // "no operand"
 
 struct Bases {
   char* p[kNumBases];
   double lam;  // regularization for eval/ksum descriptors flagged `diag`
-  double pad[3];
+  double pad[1];
 };
 
 __host__ __device__ inline Ref make_ref(int buf, uint64_t byte_off) {

@@ -30,12 +30,13 @@ __device__ __forceinline__ bool lex_less(double a, int ia, double b, int ib) {
 }
 
 __global__ void __launch_bounds__(KT) knn_kernel(const double* __restrict__ X, const double* __restrict__ sq,
-                                                 int n, int d, int kk, int64_t* __restrict__ out) {
+                                                 int n, int d, int kk, int qlo, int qhi,
+                                                 int64_t* __restrict__ out) {
   extern __shared__ double smem[];
   double* Qs = smem;                 // QB x DS
   double* Cs = smem + QB * DS;       // CB x DS
   double* Dt = smem + 2 * QB * DS;   // QB x (CB + 1)
-  const int q0 = blockIdx.x * QB;
+  const int q0 = qlo + blockIdx.x * QB;  // queries [qlo, qhi) against all n points
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int fr = lane >> 2, fc = lane & 3;
   const int wm = (wid >> 1) * 32, wn = (wid & 1) * 32;
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(KT) knn_kernel(const double* __restrict__ X, c
 #pragma unroll
     for (int qi = 0; qi < 16; ++qi) {
       const int ql = wid * 16 + qi, q = q0 + ql;
-      if (q >= n) continue;
+      if (q >= qhi) continue;
       double tv = __shfl_sync(0xffffffffu, lv[qi], kk - 1);
       int ti = __shfl_sync(0xffffffffu, li[qi], kk - 1);
       double cv[2];
@@ -143,7 +144,7 @@ __global__ void __launch_bounds__(KT) knn_kernel(const double* __restrict__ X, c
 #pragma unroll
   for (int qi = 0; qi < 16; ++qi) {
     const int q = q0 + wid * 16 + qi;
-    if (q < n && lane < kk) out[(size_t)q * kk + lane] = li[qi];
+    if (q < qhi && lane < kk) out[(size_t)(q - qlo) * kk + lane] = li[qi];
   }
 }
 
@@ -153,11 +154,13 @@ __global__ void __launch_bounds__(KT) knn_kernel(const double* __restrict__ X, c
 using namespace hks;
 
 // knn_bruteforce (tree.py:163-188): out[n x k] int64, k <= 32.
-extern "C" int hks_knn(const double* X, int64_t n, int64_t d, int64_t k, int64_t* out, void* stream) {
-  if (!X || !out || n < 2 || d < 1 || k < 1 || k > n - 1)
-    return set_error(HKS_ERR_INVALID, "need 1 <= k <= n - 1");
+extern "C" int hks_knn_rows(const double* X, int64_t n, int64_t d, int64_t k, int64_t q0, int64_t nq, int64_t* out,
+                            void* stream) {
+  if (!X || !out || n < 2 || d < 1 || k < 1 || k > n - 1 || q0 < 0 || nq < 0 || q0 + nq > n)
+    return set_error(HKS_ERR_INVALID, "need 1 <= k <= n - 1 and a query range inside [0, n)");
   if (k > 32) return set_error(HKS_ERR_NOT_SUPPORTED, "hks_knn: k <= 32 supported (got %lld)", (long long)k);
   if (n > 0x7ffffffe) return set_error(HKS_ERR_NOT_SUPPORTED, "hks_knn: n too large");
+  if (nq == 0) return HKS_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   double* sq = nullptr;
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&sq), n * sizeof(double), s);
@@ -165,10 +168,15 @@ extern "C" int hks_knn(const double* X, int64_t n, int64_t d, int64_t k, int64_t
     sqnorm_kernel<<<592, 256, 0, s>>>(X, n, (int)d, sq);
     const size_t sm = (size_t)(2 * QB * DS + QB * (CB + 1)) * sizeof(double);
     raise_smem_limit(knn_kernel, sm);
-    knn_kernel<<<(unsigned)((n + QB - 1) / QB), KT, sm, s>>>(X, sq, (int)n, (int)d, (int)k, out);
+    knn_kernel<<<(unsigned)((nq + QB - 1) / QB), KT, sm, s>>>(X, sq, (int)n, (int)d, (int)k, (int)q0, (int)(q0 + nq),
+                                                             out);
     e = cudaGetLastError();
     cudaFreeAsync(sq, s);
   }
   if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_knn: %s", cudaGetErrorString(e));
   return HKS_OK;
+}
+
+extern "C" int hks_knn(const double* X, int64_t n, int64_t d, int64_t k, int64_t* out, void* stream) {
+  return hks_knn_rows(X, n, d, k, 0, n, out, stream);
 }

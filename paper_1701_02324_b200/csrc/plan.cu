@@ -11,11 +11,12 @@
 
 namespace hks {
 
-Layout make_layout(int64_t n, int64_t depth, int64_t s) {
+Layout make_layout(int64_t n, int64_t depth, int64_t s, int mode) {
   Layout L;
   L.n = n;
   L.depth = depth;
   L.s = s;
+  L.mode = mode;
   L.nn = ((int64_t)1 << (depth + 1)) - 1;
   L.begin.assign(L.nn, 0);
   L.size.assign(L.nn, 0);
@@ -31,16 +32,24 @@ Layout make_layout(int64_t n, int64_t depth, int64_t s) {
   }
   for (int64_t i = L.nn - 1; i >= 0; --i) {
     L.ccap[i] = L.is_leaf(i) ? L.size[i] : L.rcap[2 * i + 1] + L.rcap[2 * i + 2];
-    L.rcap[i] = i == 0 ? 0 : std::min<int64_t>(s, L.ccap[i]);
+    if (L.external(i)) L.rcap[i] = s;  // a shard root: rank <= s
+    else L.rcap[i] = L.has_up(i) ? std::min<int64_t>(s, L.ccap[i]) : 0;
   }
   for (int b = 0; b < HKS_NBUF; ++b) L.off[b].assign(L.nn, -1);
   auto put = [&](int b, int64_t i, int64_t elems) {
     L.off[b][i] = L.total[b];
     L.total[b] += elems;
   };
+  if (mode == PM_TOP)  // shard roots first, s x s / s apart: the exchange gathers straight into them
+    for (int64_t i = L.first(depth); i < L.nn; ++i) {
+      put(HKS_BUF_THETA, i, s * s);
+      put(HKS_BUF_SKEL, i, s);
+    }
   for (int64_t i = 0; i < L.nn; ++i) {
-    const bool leaf = L.is_leaf(i);
-    if (i > 0) {
+    L.off[HKS_BUF_STATS][i] = i;
+    if (L.external(i)) continue;
+    const bool leaf = L.is_leaf(i), up = L.has_up(i);
+    if (up) {
       put(HKS_BUF_INTERP, i, L.rcap[i] * L.ccap[i]);
       put(HKS_BUF_SKEL, i, L.rcap[i]);
       put(HKS_BUF_THETA, i, L.rcap[i] * L.rcap[i]);
@@ -48,14 +57,13 @@ Layout make_layout(int64_t n, int64_t depth, int64_t s) {
     if (leaf) {
       put(HKS_BUF_LEAF_LU, i, L.size[i] * L.size[i]);
       put(HKS_BUF_LEAF_PIV, i, 4 * L.size[i]);  // pivots | total perm | panel perm | group perm
-      if (i > 0) put(HKS_BUF_PHI, i, L.size[i] * L.rcap[i]);
+      if (up) put(HKS_BUF_PHI, i, L.size[i] * L.rcap[i]);
     } else {
       put(HKS_BUF_Z_LU, i, L.ccap[i] * L.ccap[i]);
       put(HKS_BUF_Z_PIV, i, 4 * L.ccap[i]);  // pivots | total perm | panel perm | group perm
-      if (i > 0) put(HKS_BUF_PUSH, i, L.ccap[i] * L.rcap[i]);
+      if (up) put(HKS_BUF_PUSH, i, L.ccap[i] * L.rcap[i]);
       put(HKS_BUF_COUP, i, L.rcap[2 * i + 1] * L.rcap[2 * i + 2]);
     }
-    L.off[HKS_BUF_STATS][i] = i;
   }
   L.total[HKS_BUF_STATS] = 3 * L.nn;
   return L;
@@ -386,6 +394,10 @@ struct Ctx {
   int r(int64_t i) const { return (int)P.rank[i]; }
   // stacked slot of node i inside its parent's R_p x k block (buffer `buf`, base element `at`)
   Ref slot(int buf, int64_t at, int64_t i, int64_t k, int* ld) const {
+    if (i == 0) {  // root of a subtree plan: its own r_0 rows behind the internal nodes' blocks
+      *ld = r(0);
+      return D(buf, at + P.root_slot * k);
+    }
     const int64_t p = (i - 1) / 2;
     *ld = (int)P.R(p);
     const int64_t row = (i == 2 * p + 1) ? 0 : P.rank[2 * p + 1];
@@ -749,7 +761,7 @@ void add_theta_hat(Copies& cp, const Ctx& c, int64_t i, Ref Y) {
 
 size_t factorize_workspace(const hks_plan& P) {
   size_t need = 0;
-  for (int64_t lev = 1; lev < P.L.depth; ++lev) {
+  for (int64_t lev = P.L.has_up(0) ? 0 : 1; lev < P.L.depth; ++lev) {
     size_t lv = 0;
     for (int64_t i = P.L.first(lev); i < P.L.first(lev) + P.L.count(lev); ++i) {
       const int64_t R = P.R(i);
@@ -767,14 +779,14 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl,
   const Ctx c(P);
   const Layout& L = P.L;
   sl.mark();
-  {  // leaf level (solver.py:128-137): A = K + lam I, LU with P^T carried -> phi, theta = P phi
+  if (L.mode != PM_TOP) {  // leaf level (solver.py:128-137): A = K + lam I, LU with P^T carried -> phi, theta = P phi
     std::vector<EvalDesc> ev;
     std::vector<LuJob> jobs;
     Copies cp;
     Gemms gm;
     int mx = 0;
     for (int64_t i = L.first(L.depth); i < L.nn; ++i) {
-      const int m = (int)L.size[i], r = i > 0 ? c.r(i) : 0;
+      const int m = (int)L.size[i], r = L.has_up(i) ? c.r(i) : 0;
       ev.push_back(EvalDesc{kNull, kNull, L.begin[i], L.begin[i], m, m, c.leaf_lu(i), m, 1});
       mx = std::max(mx, m);
       if (r > 0) cp.copy(c.interp(i), r, 1, c.phi(i), m, m, r);  // phi = P^T, then A^-1 P^T
@@ -813,7 +825,7 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl,
       g_z.add(c.theta(a), rl, 0, C, rl, 0, adv(Z, (int64_t)rl * R), R, rl, rr, rl, 1.0, 1.0);
       g_z.add(c.theta(b), rr, 0, C, rl, 1, adv(Z, rl), R, rr, rl, rr, 1.0, 1.0);
       lu.push_back(LuDesc{Z, c.z_piv(i), c.info(i), c.anorm(i), with_cond ? c.rcond(i) : kNull, R, R});
-      if (lev == 0) {
+      if (!L.has_up(i)) {
         jobs.push_back(LuJob{Z, R, R, c.z_piv(i), c.info(i), c.anorm(i), kNull, 0, R, c.z_ws(i), (int)L.ccap[i]});
         continue;
       }
@@ -851,7 +863,7 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl,
       cond_levels->back()->add(ST_GECON, lu, maxR, 0, 22.0 * lb / 16.0, 11.0 * lb / 2.0);
       cond_wait->push_back((int)sl.marks().size());  // level_ev recorded when this level is done
     }
-    if (lev == 0) continue;
+    if (lev == 0 && !L.has_up(0)) continue;
     g_f.flush(sl);
     c_t.flush(sl);
     c_p.flush(sl);
@@ -862,61 +874,92 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl,
 
 // ------------------------------------------------------------ solve
 
-void build_solve(const hks_plan& P, int64_t kk, StepList& sl) {
+// part: 0 the whole solve; subtree plans run it in two halves around the
+// shard-root exchange -- 1 upward (psi of the root into B_XOUT), 2 downward
+// (the root's incoming correction from B_XIN).  Top plans read the shard
+// roots' psi from B_VIN and write their corrections to B_VOUT, shard j's
+// r_j x k block at j * s * k (ld r_j).
+void build_solve(const hks_plan& P, int64_t kk, int part, StepList& sl) {
   const Ctx c(P);
   const Layout& L = P.L;
   const int k = (int)kk, n = (int)L.n;
   const int64_t stk = P.stack_total * kk;
   const int64_t S = 0, G = stk, Gb = 2 * stk;  // element bases inside B_VWS
-  {  // upward, leaves (solver.py:215-218)
-    Gemms gp;
-    Copies cp;
-    std::vector<LuJob> jobs;
-    int mx = 0;
-    for (int64_t i = L.first(L.depth); i < L.nn; ++i) {
-      const int m = (int)L.size[i], r = c.r(i);
-      mx = std::max(mx, m);
-      if (i > 0 && r > 0) {
+  const int64_t xs = L.s * kk;                  // top plans: shard-root block stride
+  const bool sub = L.mode == PM_SUBTREE;
+  if (part != 2) {
+    if (L.mode == PM_TOP) {  // shard roots: their psi arrive from the subtree plans
+      Copies cp;
+      for (int64_t i = L.first(L.depth); i < L.nn; ++i) {
         int ld;
         const Ref dst = c.slot(B_VWS, S, i, k, &ld);
-        gp.add(c.phi(i), m, 1, D(B_VIN, L.begin[i]), n, 0, dst, ld, r, k, m, 1.0, 0.0);
+        cp.copy(D(B_VIN, (i - L.first(L.depth)) * xs), c.r(i), 0, dst, ld, c.r(i), k);
       }
-      cp.copy(D(B_VIN, L.begin[i]), n, 0, D(B_VOUT, L.begin[i]), n, m, k);
-      jobs.push_back(LuJob{c.leaf_lu(i), m, m, c.leaf_piv(i), kNull, kNull, D(B_VOUT, L.begin[i]), k, n, c.leaf_ws(i), m});
+      cp.flush(sl);
+    } else {  // upward, leaves (solver.py:215-218)
+      Gemms gp;
+      Copies cp;
+      std::vector<LuJob> jobs;
+      int mx = 0;
+      for (int64_t i = L.first(L.depth); i < L.nn; ++i) {
+        const int m = (int)L.size[i], r = c.r(i);
+        mx = std::max(mx, m);
+        if (L.has_up(i) && r > 0) {
+          int ld;
+          const Ref dst = c.slot(B_VWS, S, i, k, &ld);
+          gp.add(c.phi(i), m, 1, D(B_VIN, L.begin[i]), n, 0, dst, ld, r, k, m, 1.0, 0.0);
+        }
+        cp.copy(D(B_VIN, L.begin[i]), n, 0, D(B_VOUT, L.begin[i]), n, m, k);
+        jobs.push_back(LuJob{c.leaf_lu(i), m, m, c.leaf_piv(i), kNull, kNull, D(B_VOUT, L.begin[i]), k, n,
+                             c.leaf_ws(i), m});
+      }
+      gp.flush(sl);
+      cp.flush(sl);
+      add_lu_solve_program(sl, jobs);
     }
-    gp.flush(sl);
-    cp.flush(sl);
-    add_lu_solve_program(sl, jobs);
-  }
-  for (int64_t lev = L.depth - 1; lev >= 0; --lev) {  // upward, internal (solver.py:219-233)
-    Copies cp;
-    std::vector<LuJob> jobs;
-    Gemms g1, g2, g3;
-    int maxR = 0;
-    for (int64_t i = L.first(lev); i < L.first(lev) + L.count(lev); ++i) {
-      const int64_t a = 2 * i + 1, bb = 2 * i + 2;
-      const int rl = c.r(a), rr = c.r(bb), R = rl + rr, r = c.r(i);
-      maxR = std::max(maxR, R);
-      const Ref Si = c.block(B_VWS, S, i, k), Gi = c.block(B_VWS, G, i, k), Gbi = c.block(B_VWS, Gb, i, k);
-      const Ref C = c.coup(i);
-      cp.copy(Si, R, 0, Gi, R, R, k);
-      jobs.push_back(LuJob{c.z_lu(i), R, R, c.z_piv(i), kNull, kNull, Gi, k, R, c.z_ws(i), (int)L.ccap[i]});
-      g1.add(C, rl, 0, adv(Gi, rl), R, 0, Gbi, R, rl, k, rr, 1.0, 0.0);
-      g1.add(C, rl, 1, Gi, R, 0, adv(Gbi, rl), R, rr, k, rl, 1.0, 0.0);
-      if (lev == 0) continue;
-      g2.add(c.theta(a), rl, 0, Gbi, R, 0, Si, R, rl, k, rl, -1.0, 1.0);
-      g2.add(c.theta(bb), rr, 0, adv(Gbi, rl), R, 0, adv(Si, rl), R, rr, k, rr, -1.0, 1.0);
+    for (int64_t lev = L.depth - 1; lev >= 0; --lev) {  // upward, internal (solver.py:219-233)
+      Copies cp;
+      std::vector<LuJob> jobs;
+      Gemms g1, g2, g3;
+      for (int64_t i = L.first(lev); i < L.first(lev) + L.count(lev); ++i) {
+        const int64_t a = 2 * i + 1, bb = 2 * i + 2;
+        const int rl = c.r(a), rr = c.r(bb), R = rl + rr, r = c.r(i);
+        const Ref Si = c.block(B_VWS, S, i, k), Gi = c.block(B_VWS, G, i, k), Gbi = c.block(B_VWS, Gb, i, k);
+        const Ref C = c.coup(i);
+        cp.copy(Si, R, 0, Gi, R, R, k);
+        jobs.push_back(LuJob{c.z_lu(i), R, R, c.z_piv(i), kNull, kNull, Gi, k, R, c.z_ws(i), (int)L.ccap[i]});
+        g1.add(C, rl, 0, adv(Gi, rl), R, 0, Gbi, R, rl, k, rr, 1.0, 0.0);
+        g1.add(C, rl, 1, Gi, R, 0, adv(Gbi, rl), R, rr, k, rl, 1.0, 0.0);
+        if (!L.has_up(i)) continue;
+        g2.add(c.theta(a), rl, 0, Gbi, R, 0, Si, R, rl, k, rl, -1.0, 1.0);
+        g2.add(c.theta(bb), rr, 0, adv(Gbi, rl), R, 0, adv(Si, rl), R, rr, k, rr, -1.0, 1.0);
+        int ld;
+        const Ref dst = c.slot(B_VWS, S, i, k, &ld);
+        g3.add(c.interp(i), r, 0, Si, R, 0, dst, ld, r, k, R, 1.0, 0.0);
+      }
+      cp.flush(sl);
+      add_lu_solve_program(sl, jobs);
+      g1.flush(sl);
+      g2.flush(sl);
+      g3.flush(sl);
+    }
+    if (sub) {  // psi of the shard root, for the top plan
+      Copies cp;
       int ld;
-      const Ref dst = c.slot(B_VWS, S, i, k, &ld);
-      g3.add(c.interp(i), r, 0, Si, R, 0, dst, ld, r, k, R, 1.0, 0.0);
+      const Ref src_ = c.slot(B_VWS, S, 0, k, &ld);
+      cp.copy(src_, ld, 0, D(B_XOUT, 0), c.r(0), c.r(0), k);
+      cp.flush(sl);
     }
-    cp.flush(sl);
-    add_lu_solve_program(sl, jobs);
-    g1.flush(sl);
-    g2.flush(sl);
-    g3.flush(sl);
   }
-  for (int64_t lev = 1; lev < L.depth; ++lev) {  // downward (solver.py:235-253)
+  if (part == 1) return;
+  if (sub) {  // the shard root's correction, from the top plan
+    Copies cp;
+    int ld;
+    const Ref dst_ = c.slot(B_VWS, Gb, 0, k, &ld);
+    cp.copy(D(B_XIN, 0), c.r(0), 0, dst_, ld, c.r(0), k);
+    cp.flush(sl);
+  }
+  for (int64_t lev = sub ? 0 : 1; lev < L.depth; ++lev) {  // downward (solver.py:235-253)
     Gemms g;
     for (int64_t i = L.first(lev); i < L.first(lev) + L.count(lev); ++i) {
       const int R = (int)P.R(i), r = c.r(i);
@@ -927,7 +970,15 @@ void build_solve(const hks_plan& P, int64_t kk, StepList& sl) {
     }
     g.flush(sl);
   }
-  if (L.depth > 0) {
+  if (L.mode == PM_TOP) {  // corrections of the shard roots, for the subtree plans
+    Copies cp;
+    for (int64_t i = L.first(L.depth); i < L.nn; ++i) {
+      int ld;
+      const Ref src_ = c.slot(B_VWS, Gb, i, k, &ld);
+      cp.copy(src_, ld, 0, D(B_VOUT, (i - L.first(L.depth)) * xs), c.r(i), c.r(i), k);
+    }
+    cp.flush(sl);
+  } else if (L.depth > 0 || sub) {
     Gemms g;
     for (int64_t i = L.first(L.depth); i < L.nn; ++i) {
       const int m = (int)L.size[i], r = c.r(i);
@@ -946,15 +997,20 @@ void build_upward(const hks_plan& P, int64_t kk, int64_t S, StepList& sl) {
   const Ctx c(P);
   const Layout& L = P.L;
   const int k = (int)kk, n = (int)L.n;
-  if (L.depth == 0) return;
+  if (L.depth == 0 && !L.has_up(0)) return;
   Gemms g;
+  Copies cp;
   for (int64_t i = L.first(L.depth); i < L.nn; ++i) {  // treecode.py:81-82
     int ld;
     const Ref dst = c.slot(B_VWS, S, i, k, &ld);
-    g.add(c.interp(i), c.r(i), 0, D(B_VIN, L.begin[i]), n, 0, dst, ld, c.r(i), k, (int)L.size[i], 1.0, 0.0);
+    if (L.external(i))  // a top plan's shard root: skeleton weights from its subtree plan
+      cp.copy(D(B_VIN, (i - L.first(L.depth)) * L.s * kk), c.r(i), 0, dst, ld, c.r(i), k);
+    else
+      g.add(c.interp(i), c.r(i), 0, D(B_VIN, L.begin[i]), n, 0, dst, ld, c.r(i), k, (int)L.size[i], 1.0, 0.0);
   }
   g.flush(sl);
-  for (int64_t lev = L.depth - 1; lev >= 1; --lev) {  // treecode.py:83-88
+  cp.flush(sl);
+  for (int64_t lev = L.depth - 1; lev >= (L.has_up(0) ? 0 : 1); --lev) {  // treecode.py:83-88
     Gemms g2;
     for (int64_t i = L.first(lev); i < L.first(lev) + L.count(lev); ++i) {
       int ld;
@@ -966,37 +1022,58 @@ void build_upward(const hks_plan& P, int64_t kk, int64_t S, StepList& sl) {
   }
 }
 
-void build_matvec(const hks_plan& P, int64_t kk, StepList& sl) {
+// part as in build_solve: subtree plans send the root's skeleton weights
+// (B_XOUT) and receive its incoming accumulator (B_XIN); top plans read the
+// shard roots' weights from B_VIN and write their accumulators to B_VOUT.
+void build_matvec(const hks_plan& P, int64_t kk, int part, StepList& sl) {
   const Ctx c(P);
   const Layout& L = P.L;
   const int k = (int)kk, n = (int)L.n;
   const int64_t stk = P.stack_total * kk;
   const int64_t S = 0, A = stk;
-  {  // leaves: u = K w + lam w, K never stored (treecode.py:99-101)
-    std::vector<SumDesc> ks;
-    int mx = 0;
-    for (int64_t i = L.first(L.depth); i < L.nn; ++i) {
-      const int m = (int)L.size[i];
-      mx = std::max(mx, m);
-      ks.push_back(SumDesc{kNull, kNull, L.begin[i], L.begin[i], m, m, k, D(B_VIN, L.begin[i]), n,
-                           D(B_VOUT, L.begin[i]), n, 0.0, 1});
+  const bool sub = L.mode == PM_SUBTREE;
+  if (part != 2) {
+    if (L.mode != PM_TOP) {  // leaves: u = K w + lam w, K never stored (treecode.py:99-101)
+      std::vector<SumDesc> ks;
+      int mx = 0;
+      for (int64_t i = L.first(L.depth); i < L.nn; ++i) {
+        const int m = (int)L.size[i];
+        mx = std::max(mx, m);
+        ks.push_back(SumDesc{kNull, kNull, L.begin[i], L.begin[i], m, m, k, D(B_VIN, L.begin[i]), n,
+                             D(B_VOUT, L.begin[i]), n, 0.0, 1});
+      }
+      double kf = 0, kb = 0;
+      for (auto& q : ks) {
+        kf += (double)q.m * q.n * (2.0 * P.d + 5.0) + 2.0 * q.m * q.n * q.k;
+        kb += 8.0 * ((double)q.n * q.k + (double)q.m * q.k);
+      }
+      sl.add(ST_KSUM, ks, mx, 0, kf, kb);
     }
-    double kf = 0, kb = 0;
-    for (auto& q : ks) {
-      kf += (double)q.m * q.n * (2.0 * P.d + 5.0) + 2.0 * q.m * q.n * q.k;
-      kb += 8.0 * ((double)q.n * q.k + (double)q.m * q.k);
+    if (L.depth == 0 && !sub) return;
+    build_upward(P, kk, S, sl);
+    if (sub) {
+      Copies cp;
+      int ld;
+      const Ref src_ = c.slot(B_VWS, S, 0, k, &ld);
+      cp.copy(src_, ld, 0, D(B_XOUT, 0), c.r(0), c.r(0), k);
+      cp.flush(sl);
     }
-    sl.add(ST_KSUM, ks, mx, 0, kf, kb);
   }
-  if (L.depth == 0) return;
-  build_upward(P, kk, S, sl);
+  if (part == 1) return;
+  if (sub) {
+    Copies cp;
+    int ld;
+    const Ref dst_ = c.slot(B_VWS, A, 0, k, &ld);
+    cp.copy(D(B_XIN, 0), c.r(0), 0, dst_, ld, c.r(0), k);
+    cp.flush(sl);
+  }
   for (int64_t lev = 0; lev < L.depth; ++lev) {  // downward (treecode.py:109-123)
     Gemms gp, gc;
     for (int64_t i = L.first(lev); i < L.first(lev) + L.count(lev); ++i) {
       const int64_t a = 2 * i + 1, bb = 2 * i + 2;
       const int rl = c.r(a), rr = c.r(bb), R = rl + rr, r = c.r(i);
       const Ref Ai = c.block(B_VWS, A, i, k), Si = c.block(B_VWS, S, i, k), C = c.coup(i);
-      const bool has_acc = lev > 0;
+      const bool has_acc = L.has_up(i);
       if (has_acc) {
         int ld;
         const Ref acc = c.slot(B_VWS, A, i, k, &ld);
@@ -1008,6 +1085,16 @@ void build_matvec(const hks_plan& P, int64_t kk, StepList& sl) {
     }
     gp.flush(sl);
     gc.flush(sl);
+  }
+  if (L.mode == PM_TOP) {
+    Copies cp;
+    for (int64_t i = L.first(L.depth); i < L.nn; ++i) {
+      int ld;
+      const Ref src_ = c.slot(B_VWS, A, i, k, &ld);
+      cp.copy(src_, ld, 0, D(B_VOUT, (i - L.first(L.depth)) * L.s * kk), c.r(i), c.r(i), k);
+    }
+    cp.flush(sl);
+    return;
   }
   Gemms g;  // leaves (treecode.py:124-127)
   for (int64_t i = L.first(L.depth); i < L.nn; ++i) {
@@ -1096,19 +1183,22 @@ extern "C" int hks_lu_solve(const double* LU, const int32_t* piv, int64_t n, int
   return HKS_OK;
 }
 
-extern "C" int hks_plan_create(hks_plan** out, const double* X, int64_t n, int64_t d, int64_t depth,
-                               int64_t max_rank, const int64_t* ranks_host, const hks_kernel* kern) {
-  if (!out || !X || !ranks_host || !kern || n < 1 || d < 1 || depth < 0 || max_rank < 1)
+extern "C" int hks_plan_create_ex(hks_plan** out, const double* X, int64_t n, int64_t d, int64_t depth,
+                                  int64_t max_rank, const int64_t* ranks_host, const hks_kernel* kern, int32_t mode) {
+  if (!out || !X || !ranks_host || !kern || n < 1 || d < 1 || depth < 0 || max_rank < 1 ||
+      (mode != PM_FULL && mode != PM_SUBTREE && mode != PM_TOP) || (mode == PM_TOP && depth < 1))
     return set_error(HKS_ERR_INVALID, "hks_plan_create: bad arguments");
   std::unique_ptr<hks_plan> P(new hks_plan());
-  P->L = make_layout(n, depth, max_rank);
+  P->L = make_layout(n, depth, max_rank, mode);
   P->X = X;
   P->d = d;
   P->rank.assign(ranks_host, ranks_host + P->L.nn);
-  P->rank[0] = 0;
-  for (int64_t i = 1; i < P->L.nn; ++i) {
-    const int64_t cap = P->L.is_leaf(i) ? std::min<int64_t>(max_rank, P->L.size[i])
-                                        : std::min<int64_t>(max_rank, P->R(i));
+  if (!P->L.has_up(0)) P->rank[0] = 0;
+  for (int64_t i = 0; i < P->L.nn; ++i) {
+    if (!P->L.has_up(i)) continue;
+    const int64_t cap = P->L.external(i) ? max_rank
+                        : P->L.is_leaf(i) ? std::min<int64_t>(max_rank, P->L.size[i])
+                                          : std::min<int64_t>(max_rank, P->R(i));
     if (P->rank[i] < 0 || P->rank[i] > cap)
       return set_error(HKS_ERR_INVALID, "hks_plan_create: rank %lld of node %lld outside [0, %lld]",
                        (long long)P->rank[i], (long long)i, (long long)cap);
@@ -1120,7 +1210,30 @@ extern "C" int hks_plan_create(hks_plan** out, const double* X, int64_t n, int64
     P->stack_off[i] = P->stack_total;
     P->stack_total += P->R(i);
   }
+  if (mode == PM_SUBTREE) {
+    P->root_slot = P->stack_total;
+    P->stack_total += P->rank[0];
+  }
   *out = P.release();
+  return HKS_OK;
+}
+
+extern "C" int hks_plan_create(hks_plan** out, const double* X, int64_t n, int64_t d, int64_t depth,
+                               int64_t max_rank, const int64_t* ranks_host, const hks_kernel* kern) {
+  return hks_plan_create_ex(out, X, n, d, depth, max_rank, ranks_host, kern, PM_FULL);
+}
+
+extern "C" int hks_layout_ex(int64_t n, int64_t depth, int64_t max_rank, int32_t mode, int64_t* sizes,
+                             int64_t* offsets) {
+  if (n < 1 || depth < 0 || depth > 40 || max_rank < 1 || mode < PM_FULL || mode > PM_TOP ||
+      (mode == PM_TOP && depth < 1))
+    return set_error(HKS_ERR_INVALID, "hks_layout: bad arguments n=%lld depth=%lld max_rank=%lld mode=%d",
+                     (long long)n, (long long)depth, (long long)max_rank, (int)mode);
+  Layout L = make_layout(n, depth, max_rank, mode);
+  for (int b = 0; b < HKS_NBUF; ++b) {
+    if (sizes) sizes[b] = L.total[b];
+    if (offsets) std::memcpy(offsets + b * L.nn, L.off[b].data(), L.nn * sizeof(int64_t));
+  }
   return HKS_OK;
 }
 
@@ -1204,7 +1317,7 @@ static int check_info(hks_plan* P, void* const* buffers, int64_t* bad_node, cuda
   if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_factorize: %s", cudaGetErrorString(e));
   for (int64_t lev = L.depth; lev >= 0; --lev) {
     for (int64_t i = L.first(lev); i < L.first(lev) + L.count(lev); ++i) {
-      if (info[i] == 0) continue;
+      if (info[i] == 0 || L.external(i)) continue;
       if (bad_node) *bad_node = i;
       if (lev == L.depth)
         return set_error(HKS_ERR_SINGULAR, "singular matrix: zero pivot at elimination step %d", info[i] - 1);
@@ -1308,46 +1421,82 @@ static VecProgram* get_prog(std::map<int64_t, std::unique_ptr<VecProgram>>& m, i
   return v;
 }
 
-extern "C" int hks_solve(hks_plan* P, void* const* buffers, const double* b, double* x, int64_t k, void* stream) {
+// One program half (part 0 whole, 1 up, 2 down; see build_solve) with its
+// own graph; both halves of a subtree plan share the workspace.
+static cudaError_t run_vec_part(hks_plan* P, VecProgram* v, int part, Bases& bb, const void* xin, void* xout,
+                                cudaStream_t s) {
+  bb.p[B_VWS] = (char*)v->ws.p;
+  bb.p[B_XIN] = (char*)xin;
+  bb.p[B_XOUT] = (char*)xout;
+  StepList& sl = part == 2 ? v->down : v->steps;
+  GraphCache& gc = part == 2 ? v->down_graphs : v->graphs;
+  return run_graphed(gc, sl, bb, P->X, (int)P->d, P->kp, s, nullptr, nullptr, 0);
+}
+
+static int check_part(hks_plan* P, int part, const void* xchg, const char* who) {
+  const bool sub = P->L.mode == PM_SUBTREE;
+  if (part < 0 || part > 2 || (sub && part == 0) || (!sub && part != 0))
+    return set_error(HKS_ERR_INVALID, "%s: part %d does not fit a mode-%d plan", who, part, P->L.mode);
+  if (sub && !xchg && P->rank[0] > 0) return set_error(HKS_ERR_INVALID, "%s: subtree plans need the exchange block", who);
+  return HKS_OK;
+}
+
+extern "C" int hks_solve_part(hks_plan* P, void* const* buffers, const double* b, double* x, int64_t k, int32_t part,
+                              double* xchg, void* stream) {
   if (!P || !buffers || !b || !x || k < 0) return set_error(HKS_ERR_INVALID, "hks_solve: bad arguments");
+  if (int rc = check_part(P, part, xchg, "hks_solve")) return rc;
   if (k == 0) return HKS_OK;
   cudaStream_t s = as_stream(stream);
   VecProgram* v = get_prog(P->solve_prog, k);
-  if (v->steps.empty()) {
-    build_solve(*P, k, v->steps);
+  if (v->steps.empty() && v->down.empty()) {
+    const bool sub = P->L.mode == PM_SUBTREE;
+    build_solve(*P, k, sub ? 1 : 0, v->steps);
+    if (sub) build_solve(*P, k, 2, v->down);
     cudaError_t e = v->steps.upload(s);
+    if (e == cudaSuccess) e = v->down.upload(s);
     if (e == cudaSuccess) e = v->ws.ensure(std::max<size_t>(3 * P->stack_total * k, 1) * sizeof(double));
     if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_solve: %s", cudaGetErrorString(e));
   }
   Bases bb = make_bases(buffers);
   bb.p[B_VIN] = (char*)b;
   bb.p[B_VOUT] = (char*)x;
-  bb.p[B_VWS] = (char*)v->ws.p;
-  cudaError_t e = run_graphed(v->graphs, v->steps, bb, P->X, (int)P->d, P->kp, s, nullptr, nullptr, 0);
+  cudaError_t e = run_vec_part(P, v, part, bb, xchg, xchg, s);
   if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_solve: %s", cudaGetErrorString(e));
   return HKS_OK;
 }
 
-extern "C" int hks_hmatvec(hks_plan* P, void* const* buffers, const double* w, double* u, int64_t k, double lam,
-                           void* stream) {
+extern "C" int hks_solve(hks_plan* P, void* const* buffers, const double* b, double* x, int64_t k, void* stream) {
+  return hks_solve_part(P, buffers, b, x, k, 0, nullptr, stream);
+}
+
+extern "C" int hks_hmatvec_part(hks_plan* P, void* const* buffers, const double* w, double* u, int64_t k, double lam,
+                                int32_t part, double* xchg, void* stream) {
   if (!P || !buffers || !w || !u || k < 0 || w == u) return set_error(HKS_ERR_INVALID, "hks_hmatvec: bad arguments");
+  if (int rc = check_part(P, part, xchg, "hks_hmatvec")) return rc;
   if (k == 0) return HKS_OK;
   cudaStream_t s = as_stream(stream);
   VecProgram* v = get_prog(P->mv_prog, k);
-  if (v->steps.empty()) {
-    build_matvec(*P, k, v->steps);
+  if (v->steps.empty() && v->down.empty()) {
+    const bool sub = P->L.mode == PM_SUBTREE;
+    build_matvec(*P, k, sub ? 1 : 0, v->steps);
+    if (sub) build_matvec(*P, k, 2, v->down);
     cudaError_t e = v->steps.upload(s);
+    if (e == cudaSuccess) e = v->down.upload(s);
     if (e == cudaSuccess) e = v->ws.ensure(std::max<size_t>(2 * P->stack_total * k, 1) * sizeof(double));
     if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_hmatvec: %s", cudaGetErrorString(e));
   }
   Bases bb = make_bases(buffers);
   bb.p[B_VIN] = (char*)w;
   bb.p[B_VOUT] = (char*)u;
-  bb.p[B_VWS] = (char*)v->ws.p;
   bb.lam = lam;
-  cudaError_t e = run_graphed(v->graphs, v->steps, bb, P->X, (int)P->d, P->kp, s, nullptr, nullptr, 0);
+  cudaError_t e = run_vec_part(P, v, part, bb, xchg, xchg, s);
   if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_hmatvec: %s", cudaGetErrorString(e));
   return HKS_OK;
+}
+
+extern "C" int hks_hmatvec(hks_plan* P, void* const* buffers, const double* w, double* u, int64_t k, double lam,
+                           void* stream) {
+  return hks_hmatvec_part(P, buffers, w, u, k, lam, 0, nullptr, stream);
 }
 
 extern "C" int hks_upward_offsets(hks_plan* P, int64_t k, int64_t* offsets, int64_t* lds, int64_t* total) {

@@ -18,11 +18,26 @@
 namespace hks {
 
 // Base-table slots beyond the HKS_BUF_* ids.
-enum BaseSlot { B_FWS = HKS_NBUF, B_VIN, B_VOUT, B_VWS };
-static_assert(B_VWS < kAbs, "base slots overflow");
+// B_XIN / B_XOUT: the shard-root exchange vectors of a sharded tree's
+// subtree plan (HKS_PLAN_SUBTREE): r_0 x k blocks, ld r_0.
+enum BaseSlot { B_FWS = HKS_NBUF, B_VIN, B_VOUT, B_VWS, B_XIN, B_XOUT };
+static_assert(B_XOUT < kAbs, "base slots overflow");
+
+// Plan modes (hks_plan_create_ex).  A sharded tree is one subtree plan per
+// rank (the rank's shard, rooted at a level-p node that still has a
+// skeleton, Theta and a push) plus a top plan over levels 0..p whose leaves
+// are the 2^p shard roots, supplied from outside (Theta, skeleton indices,
+// up-pass vectors) instead of being factored.
+enum PlanMode { PM_FULL = 0, PM_SUBTREE = 1, PM_TOP = 2 };
 
 struct Layout {
   int64_t n = 0, depth = 0, nn = 0, s = 0;
+  int mode = PM_FULL;
+  // node i carries a skeleton (interp, Theta, push / phi): every node but
+  // the root of a full or top tree
+  bool has_up(int64_t i) const { return i > 0 || mode == PM_SUBTREE; }
+  // leaves of a top plan are shard roots owned by other plans
+  bool external(int64_t i) const { return mode == PM_TOP && is_leaf(i); }
   std::vector<int64_t> begin, size, rcap, ccap;
   std::vector<int64_t> off[HKS_NBUF];
   int64_t total[HKS_NBUF] = {0};
@@ -32,7 +47,7 @@ struct Layout {
   int64_t count(int64_t level) const { return (int64_t)1 << level; }
 };
 
-Layout make_layout(int64_t n, int64_t depth, int64_t max_rank);
+Layout make_layout(int64_t n, int64_t depth, int64_t max_rank, int mode = PM_FULL);
 
 enum StepKind {
   ST_GEMM, ST_COPY, ST_GETRF, ST_GETRS, ST_GECON, ST_EVAL_CM, ST_EVAL_RM, ST_KSUM,
@@ -147,6 +162,10 @@ struct VecProgram {
   StepList steps;
   DevBuf ws;
   GraphCache graphs;
+  // subtree plans: the downward half (after the shard-root exchange),
+  // sharing `ws` with the upward half in `steps`
+  StepList down;
+  GraphCache down_graphs;
 };
 
 }  // namespace hks
@@ -177,9 +196,11 @@ struct hks_plan {
   std::vector<cudaEvent_t> level_ev;        // per-level factorize timing (leaf level first)
   std::map<int64_t, std::unique_ptr<hks::VecProgram>> solve_prog, mv_prog, up_prog;
 
-  // stacked per-internal-node slots: node p owns R_p rows (x k columns)
+  // stacked per-internal-node slots: node p owns R_p rows (x k columns);
+  // a subtree plan's root owns r_0 more rows at root_slot
   std::vector<int64_t> stack_off;
   int64_t stack_total = 0;
+  int64_t root_slot = -1;
 
   int64_t R(int64_t i) const { return rank[2 * i + 1] + rank[2 * i + 2]; }
   ~hks_plan() {

@@ -40,11 +40,16 @@ __device__ __forceinline__ int node_of(const int64_t* beg, int count, int64_t p)
   return lo;
 }
 
-__global__ void mark_kernel(const int64_t* __restrict__ knn, int64_t n, int kappa, const int64_t* __restrict__ beg,
-                            const int64_t* __restrict__ sz, int count, int64_t words, unsigned* __restrict__ bm) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * kappa;
+// knn holds the lists of the points [row0, row0 + nrows) (global indices);
+// the bitmaps belong to `count` consecutive nodes of one level
+__global__ void mark_kernel(const int64_t* __restrict__ knn, int64_t row0, int64_t nrows, int kappa,
+                            const int64_t* __restrict__ beg, const int64_t* __restrict__ sz, int count, int64_t words,
+                            unsigned* __restrict__ bm) {
+  const int64_t lo = beg[0], hi = beg[count - 1] + sz[count - 1];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nrows * kappa;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p = e / kappa;
+    const int64_t p = row0 + e / kappa;
+    if (p < lo || p >= hi) continue;
     const int j = node_of(beg, count, p);
     const int64_t q = knn[e];
     if (q >= beg[j] && q < beg[j] + sz[j]) continue;
@@ -156,13 +161,25 @@ __global__ void compact_kernel(const unsigned* __restrict__ bm, int64_t words, c
 
 using namespace hks;
 
-extern "C" int hks_knn_rows_mark(const int64_t* knn, int64_t n, int64_t kappa, int64_t level, int64_t depth,
-                                 int32_t* bitmap, int64_t* counts_host, void* stream) {
-  if (!knn || !bitmap || !counts_host || level < 1 || level > depth)
+namespace {
+int subset_ranges(int64_t n, int64_t level, int64_t node0, int64_t count, std::vector<int64_t>& beg,
+                  std::vector<int64_t>& sz) {
+  if (level < 0 || level > 40 || node0 < 0 || count < 1 || node0 + count > ((int64_t)1 << level)) return -1;
+  level_ranges(n, level, beg, sz);
+  beg = std::vector<int64_t>(beg.begin() + node0, beg.begin() + node0 + count);
+  sz = std::vector<int64_t>(sz.begin() + node0, sz.begin() + node0 + count);
+  return 0;
+}
+}  // namespace
+
+extern "C" int hks_knn_rows_mark_ex(const int64_t* knn, int64_t row0, int64_t nrows, int64_t n, int64_t kappa,
+                                    int64_t level, int64_t node0, int64_t count_, int32_t* bitmap,
+                                    int64_t* counts_host, void* stream) {
+  std::vector<int64_t> beg, sz;
+  if ((!knn && nrows > 0) || !bitmap || !counts_host || level < 1 || row0 < 0 || nrows < 0 || row0 + nrows > n ||
+      subset_ranges(n, level, node0, count_, beg, sz))
     return set_error(HKS_ERR_INVALID, "hks_knn_rows_mark: bad arguments");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  std::vector<int64_t> beg, sz;
-  level_ranges(n, level, beg, sz);
   const int count = (int)beg.size();
   const int64_t words = (n + 31) / 32;
   int64_t *dbeg = nullptr, *dsz = nullptr, *dcnt = nullptr;
@@ -173,7 +190,9 @@ extern "C" int hks_knn_rows_mark(const int64_t* knn, int64_t n, int64_t kappa, i
     cudaMemcpyAsync(dbeg, beg.data(), count * sizeof(int64_t), cudaMemcpyHostToDevice, s);
     cudaMemcpyAsync(dsz, sz.data(), count * sizeof(int64_t), cudaMemcpyHostToDevice, s);
     cudaMemsetAsync(bitmap, 0, (size_t)count * words * sizeof(unsigned), s);
-    mark_kernel<<<1184, 256, 0, s>>>(knn, n, (int)kappa, dbeg, dsz, count, words, reinterpret_cast<unsigned*>(bitmap));
+    if (nrows > 0)
+      mark_kernel<<<1184, 256, 0, s>>>(knn, row0, nrows, (int)kappa, dbeg, dsz, count, words,
+                                       reinterpret_cast<unsigned*>(bitmap));
     count_kernel<<<count, 256, 0, s>>>(reinterpret_cast<unsigned*>(bitmap), words, dcnt);
     e = cudaMemcpyAsync(counts_host, dcnt, count * sizeof(int64_t), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
@@ -185,14 +204,36 @@ extern "C" int hks_knn_rows_mark(const int64_t* knn, int64_t n, int64_t kappa, i
   return HKS_OK;
 }
 
-extern "C" int hks_knn_rows_fill(int64_t n, int64_t level, int64_t depth, int32_t* bitmap, const int64_t* extra,
-                                 const int64_t* extra_off_host, int64_t* rows, const int64_t* row_off_host,
-                                 void* stream) {
-  if (!bitmap || !rows || !extra_off_host || !row_off_host || level < 1 || level > depth)
+extern "C" int hks_knn_rows_mark(const int64_t* knn, int64_t n, int64_t kappa, int64_t level, int64_t depth,
+                                 int32_t* bitmap, int64_t* counts_host, void* stream) {
+  if (level > depth) return set_error(HKS_ERR_INVALID, "hks_knn_rows_mark: bad arguments");
+  return hks_knn_rows_mark_ex(knn, 0, n, n, kappa, level, 0, (int64_t)1 << level, bitmap, counts_host, stream);
+}
+
+extern "C" int hks_bitmap_count(const int32_t* bitmap, int64_t n, int64_t count, int64_t* counts_host, void* stream) {
+  if (!bitmap || !counts_host || n < 1 || count < 1) return set_error(HKS_ERR_INVALID, "hks_bitmap_count: bad arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t words = (n + 31) / 32;
+  int64_t* dcnt = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&dcnt), count * sizeof(int64_t), s);
+  if (e == cudaSuccess) {
+    count_kernel<<<(unsigned)count, 256, 0, s>>>(reinterpret_cast<const unsigned*>(bitmap), words, dcnt);
+    e = cudaMemcpyAsync(counts_host, dcnt, count * sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFreeAsync(dcnt, s);
+  }
+  if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_bitmap_count: %s", cudaGetErrorString(e));
+  return HKS_OK;
+}
+
+extern "C" int hks_knn_rows_fill_ex(int64_t n, int64_t level, int64_t node0, int64_t count_, int32_t* bitmap,
+                                    const int64_t* extra, const int64_t* extra_off_host, int64_t* rows,
+                                    const int64_t* row_off_host, void* stream) {
+  std::vector<int64_t> beg, sz;
+  if (!bitmap || !rows || !extra_off_host || !row_off_host || level < 1 ||
+      subset_ranges(n, level, node0, count_, beg, sz))
     return set_error(HKS_ERR_INVALID, "hks_knn_rows_fill: bad arguments");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  std::vector<int64_t> beg, sz;
-  level_ranges(n, level, beg, sz);
   const int count = (int)beg.size();
   const int64_t words = (n + 31) / 32;
   std::vector<int> topup;
@@ -245,4 +286,12 @@ extern "C" int hks_knn_rows_fill(int64_t n, int64_t level, int64_t depth, int32_
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_knn_rows_fill: %s", cudaGetErrorString(e));
   return HKS_OK;
+}
+
+extern "C" int hks_knn_rows_fill(int64_t n, int64_t level, int64_t depth, int32_t* bitmap, const int64_t* extra,
+                                 const int64_t* extra_off_host, int64_t* rows, const int64_t* row_off_host,
+                                 void* stream) {
+  if (level > depth) return set_error(HKS_ERR_INVALID, "hks_knn_rows_fill: bad arguments");
+  return hks_knn_rows_fill_ex(n, level, 0, (int64_t)1 << level, bitmap, extra, extra_off_host, rows, row_off_host,
+                              stream);
 }
