@@ -41,7 +41,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["hks", "reference"], default="hks")
     p.add_argument("--config", default="C2")
-    p.add_argument("--n", type=int, default=None, help="override N (same generator / kernel / ranks)")
+    p.add_argument("--points", type=int, default=None, help="override N per GPU (same generator / kernel / ranks)")
     p.add_argument("--cpu-sample-n", type=int, default=16384)
     p.add_argument("--cpu-steps", type=int, default=2)
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -157,47 +157,145 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- GPU arm
 
+class SingleRunner:
+    """One GPU: the whole workload through the public API (N=1 line, and
+    the replicas fallback)."""
+
+    def __init__(self, w, seed):
+        import torch
+        import paper_1701_02324_b200 as hk
+        from paper_1701_02324_b200 import _native as N
+        from paper_1701_02324_b200 import workloads as W
+        self.hk, self.N, self.w = hk, N, w
+        x = W.points(w, seed)
+        self.b = W.rhs(w, seed)
+        kern = hk.KernelSpec("gaussian", h=w.h, regularization=w.lam)
+        cfg = hk.SkeletonConfig(tau=w.tau, max_rank=w.max_rank, samples=w.samples,
+                                sample_mode="knn_augmented", seed=seed)
+        setup = {}
+        ps = hk.PointSet(x)
+        _, setup["h2d_points"] = timed(ps.device)
+        tree, setup["build_tree"] = timed(lambda: hk.build_tree(ps, w.leaf_size, seed=seed))
+        knn, setup["knn"] = timed(lambda: hk.knn_bruteforce(tree.points, w.kappa))
+        skels, setup["skeletonize"] = timed(lambda: hk.build_skeletons(tree, kern, cfg, knn=knn))
+        self.op, setup["assemble"] = timed(lambda: hk.build_operator(tree, skels, kern))
+        self.setup = {k: round(v, 4) for k, v in setup.items()}
+        self.tree = tree
+        # right-hand sides resident in tree order, column-major (k, n)
+        self.B = N.to_device(np.ascontiguousarray(self.b[np.asarray(tree.perm)].T))
+        self.n_job = w.n
+        self.Bh = torch.from_numpy(np.ascontiguousarray(self.b)).pin_memory()
+
+    def factorize(self):
+        return self.hk.factorize(self.op, self.w.lam)
+
+    def solve(self, f):
+        from paper_1701_02324_b200.solver import solve_device
+        return solve_device(f, self.B)
+
+    def relres(self, X):
+        import torch
+        res = self.hk.treecode.hmatvec_device(self.op, X[:1].contiguous(), self.w.lam)[0] - self.B[0]
+        return float(torch.linalg.vector_norm(res) / torch.linalg.vector_norm(self.B[0]))
+
+    def e2e(self):
+        """pinned host B (input order) -> host x through the public API."""
+        f = self.hk.factorize(self.op, self.w.lam)
+        xh = self.hk.solve_multi(f, self.Bh, in_tree_order=False)
+        return xh.cpu().numpy() if hasattr(xh, "cpu") else xh
+
+    @property
+    def io_bytes(self):
+        return int(self.b.nbytes), int(self.b.nbytes)
+
+
+class ShardedRunner:
+    """P = 2^p GPUs: one global instance of P x N points (weak scaling: every
+    rank's shard has the single-GPU workload's N), subtree-sharded
+    (paper_1701_02324_b200/sharded.py; NCCL only for the shard-root
+    exchange)."""
+
+    def __init__(self, w, world, rank):
+        import torch
+        import paper_1701_02324_b200 as hk
+        from paper_1701_02324_b200 import _native as N
+        from paper_1701_02324_b200 import sharded as S
+        from paper_1701_02324_b200 import workloads as W
+        self.hk, self.N, self.S, self.w = hk, N, S, w
+        wg = w.scaled(w.n * world)
+        x = W.points(wg, 0)
+        b = W.rhs(wg, 0)
+        kern = hk.KernelSpec("gaussian", h=w.h, regularization=w.lam)
+        cfg = hk.SkeletonConfig(tau=w.tau, max_rank=w.max_rank, samples=w.samples,
+                                sample_mode="knn_augmented", seed=0)
+        self.comm = S.ShardComm()
+        setup = {}
+        ps = hk.PointSet(x)
+        _, setup["h2d_points"] = timed(ps.device)
+        tree, setup["build_tree"] = timed(lambda: hk.build_tree(ps, w.leaf_size, seed=0))
+        self.spec = spec = S.ShardSpec(wg.n, tree.depth, world, rank)
+        knn, setup["knn"] = timed(lambda: S.knn_shard(tree, w.kappa, spec))
+        sk, setup["skeletonize"] = timed(lambda: S.build_skeletons_sharded(tree, kern, cfg, knn, spec, self.comm))
+        self.op, setup["assemble"] = timed(lambda: S.build_operator_sharded(tree, sk, kern, self.comm))
+        self.setup = {k: round(v, 4) for k, v in setup.items()}
+        bl = np.ascontiguousarray(b[np.asarray(tree.perm)][spec.begin: spec.end].T)  # (k, n_shard)
+        self.b_local = bl
+        self.B = N.to_device(bl)
+        self.Bh = torch.from_numpy(bl).pin_memory()
+        self.n_job = wg.n
+
+    def factorize(self):
+        return self.S.factorize_sharded(self.op, self.w.lam)
+
+    def solve(self, f):
+        return self.S.solve_sharded(f, self.B)
+
+    def relres(self, X):
+        import torch
+        U = self.S.hmatvec_sharded(self.op, X[:1].contiguous(), self.w.lam)
+        num = torch.stack([torch.sum((U[0] - self.B[0]) ** 2), torch.sum(self.B[0] ** 2)])
+        self.comm.all_reduce_sum_(num)
+        return float(torch.sqrt(num[0] / num[1]))
+
+    def e2e(self):
+        """pinned host block of the shard's right-hand sides -> host x rows."""
+        import torch
+        B = self.Bh.to(self.N.device(), non_blocking=True)
+        f = self.S.factorize_sharded(self.op, self.w.lam)
+        X = self.S.solve_sharded(f, B)
+        xh = torch.empty(X.shape, dtype=torch.float64, pin_memory=True)
+        xh.copy_(X, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return xh
+
+    @property
+    def io_bytes(self):
+        return int(self.b_local.nbytes), int(self.b_local.nbytes)
+
+
+def timed(fn):
+    import torch
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    out = fn()
+    torch.cuda.synchronize()
+    return out, time.perf_counter() - t0
+
+
 def gpu_arm(args, w, rank, world):
     import torch
-    import paper_1701_02324_b200 as hk
     from paper_1701_02324_b200 import _native as N
-    from paper_1701_02324_b200 import workloads as W
-    from paper_1701_02324_b200.solver import solve_device
 
     dev = torch.device("cuda", torch.cuda.current_device())
-    seed = rank  # replicas: every rank owns an independent instance (multi-GPU)
-    x = W.points(w, seed)
-    b = W.rhs(w, seed)
-    kern = hk.KernelSpec("gaussian", h=w.h, regularization=w.lam)
-    cfg = hk.SkeletonConfig(tau=w.tau, max_rank=w.max_rank, samples=w.samples,
-                            sample_mode="knn_augmented", seed=seed)
-
-    def timed(fn):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        out = fn()
-        torch.cuda.synchronize()
-        return out, time.perf_counter() - t0
-
-    setup = {}
-    ps = hk.PointSet(x)
-    _, setup["h2d_points"] = timed(ps.device)
-    tree, setup["build_tree"] = timed(lambda: hk.build_tree(ps, w.leaf_size, seed=seed))
-    knn, setup["knn"] = timed(lambda: hk.knn_bruteforce(tree.points, w.kappa))
-    skels, setup["skeletonize"] = timed(lambda: hk.build_skeletons(tree, kern, cfg, knn=knn))
-    op, setup["assemble"] = timed(lambda: hk.build_operator(tree, skels, kern))
-    setup = {k: round(v, 4) for k, v in setup.items()}
-
-    # right-hand sides resident in tree order, column-major (k, n)
-    B = N.to_device(np.ascontiguousarray(b[np.asarray(tree.perm)].T))
+    run = ShardedRunner(w, world, rank) if world > 1 else SingleRunner(w, 0)
     stream = torch.cuda.current_stream()
 
     def step():
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record(stream)
-        f = hk.factorize(op, w.lam)
+        f = run.factorize()
         e1.record(stream)
-        X = solve_device(f, B)
+        X = run.solve(f)
         e2.record(stream)
         return f, X, (e0, e1, e2)
 
@@ -242,22 +340,21 @@ def gpu_arm(args, w, rank, world):
     ms_step = region_ms / args.steps
 
     # parity spot check of the timed solution: residual against Ktilde
-    xs = X[0]
-    res = hk.treecode.hmatvec_device(op, xs.reshape(1, -1).contiguous(), w.lam)[0] - B[0]
-    relres = float(torch.linalg.vector_norm(res) / torch.linalg.vector_norm(B[0]))
+    relres = run.relres(X)
 
-    # e2e through the public API: pinned host B (input order) -> host x
-    Bh = torch.from_numpy(np.ascontiguousarray(b)).pin_memory()
+    # e2e through the public API: pinned host B -> host x, H2D + D2H inside
     e2e_ms = []
     for i in range(max(2, min(args.steps, 5))):
         torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
         t0 = time.perf_counter()
-        f = hk.factorize(op, w.lam)
-        xh = hk.solve_multi(f, Bh, in_tree_order=False)
-        xh = xh.cpu().numpy() if hasattr(xh, "cpu") else xh
+        run.e2e()
         torch.cuda.synchronize()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
-    e2e_step = statistics.median(e2e_ms)
+    e2e_step = max_over_ranks(statistics.median(e2e_ms), world, dev)
+    w_name = w.name
+    setup = run.setup
 
     # roofline of the dominant kernel kind (algorithmic flops / event time)
     tensor_kinds = {"gemm", "getrf", "getrs", "gecon"}
@@ -287,7 +384,8 @@ def gpu_arm(args, w, rank, world):
                    "tflops": round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 3) if v["flops"] else None,
                    "gbs": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1)}
                for k, v in kinds.items() if v["launches"]}
-    n_total = w.n * world
+    n_total = run.n_job
+    h2d, d2h = run.io_bytes
     result = {
         "metric": "factorize+solve points/s",
         "value": round(n_total / (ms_step * 1e-3), 1),
@@ -300,25 +398,28 @@ def gpu_arm(args, w, rank, world):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic: seeded BASELINE generator (BASELINE.md 4.4), seed = rank",
+        "data": ("synthetic: seeded BASELINE generator (BASELINE.md 4.4), seed 0" if world == 1 else
+                 f"synthetic: one seeded instance of {world} x {w.n} points (BASELINE.md 4.4), subtree-sharded"),
         "config": {"workload": w.name, "n": w.n, "d": w.d, "leaf": w.leaf_size, "max_rank": w.max_rank,
                    "tau": w.tau, "kappa": w.kappa, "samples": w.samples, "sample_mode": "knn_augmented",
                    "h": w.h, "lambda": w.lam, "nrhs": w.nrhs,
-                   "parallelism": "replicas" if world > 1 else "single",
+                   "parallelism": f"subtree-sharded x{world} (NCCL shard-root exchange)" if world > 1 else "single",
+                   "n_global": n_total,
                    "l2": "no flush: per-step working set (factor storage) exceeds the 126 MB L2"},
-        "factorize_points_per_s": round(w.n / (statistics.mean(t_fact) * 1e-3), 1),
+        "factorize_points_per_s": round(n_total / (max_over_ranks(statistics.mean(t_fact), world, dev) * 1e-3), 1),
         "solve_rhs_per_s": round(w.nrhs / (statistics.mean(t_solve) * 1e-3), 1),
         "factorize_ms": round(statistics.mean(t_fact), 4),
         "solve_ms": round(statistics.mean(t_solve), 4),
         "step_tflops": round(total_flops / (ms_step * 1e-3) / 1e12, 3),
         "setup_s": setup,
-        "setup_points_per_s": round(w.n / sum(v for k, v in setup.items() if k != "h2d_points"), 1),
+        "setup_points_per_s": round(n_total / max_over_ranks(sum(v for k, v in setup.items() if k != "h2d_points"),
+                                                             world, dev), 1),
         "relres_vs_ktilde": relres,
         "roofline": roof,
         "kernels": kernels,
         "e2e": {"value": round(n_total / (e2e_step * 1e-3), 1), "unit": "points/s",
-                "ms_per_step": round(e2e_step, 4), "h2d_bytes_per_step": int(b.nbytes),
-                "d2h_bytes_per_step": int(b.nbytes)},
+                "ms_per_step": round(e2e_step, 4), "h2d_bytes_per_step": h2d * world,
+                "d2h_bytes_per_step": d2h * world},
         "clocks": clk,
         "gpu_launches": int(launches),
     }
@@ -329,8 +430,8 @@ def main():
     args = parse()
     from paper_1701_02324_b200 import workloads as W
     w = W.CONFIGS[args.config]
-    if args.n:
-        w = w.scaled(args.n)
+    if args.points:
+        w = w.scaled(args.points)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
@@ -356,9 +457,13 @@ def main():
 
     import torch
     if world > 1:
-        local = int(os.environ.get("LOCAL_RANK", "0"))
+        local = int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count()
         torch.cuda.set_device(local)
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("HKS_BENCH_BACKEND", "nccl")  # gloo: functional runs of P ranks on one GPU
+        if backend == "nccl":
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            torch.distributed.init_process_group(backend)
     result = gpu_arm(args, w, rank, world)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         r = oracle_arm(w, min(args.cpu_sample_n, w.n), args.cpu_steps, cores)

@@ -485,6 +485,11 @@ class ShardedFactorization:
     def solve_local(self, B):
         return solve_sharded(self, B)
 
+    def join_cond(self):
+        """The current stream waits for both plans' dgecon estimates."""
+        N.call("hks_cond_wait", self.op.local.handle, N.stream_ptr())
+        N.call("hks_cond_wait", self.op.top.handle, N.stream_ptr())
+
 
 def factorize_sharded(op, lam, with_cond=True):
     """Shard levels on this rank, shard-root Theta all-gathered, top levels
