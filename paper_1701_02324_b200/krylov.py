@@ -41,18 +41,25 @@ class KrylovReport:
 
 
 class _Vec:
-    """Device BLAS-1 helpers over libhks."""
+    """Device BLAS-1 helpers over libhks.  With a ShardComm of several ranks
+    the vectors are the ranks' row blocks and every inner product is summed
+    over the ranks (one all-reduce of m doubles per call)."""
 
-    def __init__(self, n, cap):
+    def __init__(self, n, cap, comm=None):
         t = N.torch()
         self.n = n
+        self.comm = comm if comm is not None and comm.world > 1 else None
         self.part = t.empty(max(cap, 1) * _VG, dtype=t.float64, device=N.device())
         self.scal = t.empty(max(cap, 1), dtype=t.float64, device=N.device())
 
     def dots(self, V, m, w, out=None, scale=1.0, accumulate=False):
         out = self.scal if out is None else out
+        if accumulate and self.comm is not None:
+            raise ValueError("accumulating dots are not supported over several ranks")
         N.call("hks_vdots", N.ptr(V), V.stride(0), m, N.ptr(w), self.n, N.ptr(out), float(scale),
                int(accumulate), N.ptr(self.part), N.stream_ptr())
+        if self.comm is not None:
+            self.comm.all_reduce_sum_(out[:m])
         return out
 
     def norm(self, w):
@@ -84,10 +91,13 @@ def _device_op(fn, n, host_callable, check):
     return apply
 
 
-def gmres(apply_a, apply_minv, b, tol=1e-8, max_iter=500, restart=50):
+def gmres(apply_a, apply_minv, b, tol=1e-8, max_iter=500, restart=50, comm=None):
     """Solve A x = b with right-preconditioned restarted GMRES; x = M^-1 y
     (krylov.py:40-143).  b may be a numpy array (callables then receive and
-    return numpy) or a CUDA tensor (callables see CUDA tensors)."""
+    return numpy) or a CUDA tensor (callables see CUDA tensors).  comm (a
+    sharded.ShardComm): b, x and the callables' vectors are this rank's
+    rows of distributed vectors; inner products are all-reduced, so every
+    rank takes the same Givens / restart / convergence decisions."""
     if tol <= 0:
         raise ValueError("tol must be positive")
     if restart < 1:
@@ -100,7 +110,7 @@ def gmres(apply_a, apply_minv, b, tol=1e-8, max_iter=500, restart=50):
     M = _device_op(apply_minv, n, host, False)
     t0 = time.perf_counter()
     rep = KrylovReport()
-    vec = _Vec(n, restart + 2)
+    vec = _Vec(n, restart + 2, comm)
     bnorm = vec.norm(bd)
     out_of = (lambda x: x.cpu().numpy()) if host else (lambda x: x)
     if bnorm == 0.0:
@@ -216,4 +226,30 @@ def hybrid_solve(op, f, b, tol=1e-8, max_iter=500, restart=50, operator_mode="co
     host = not (isinstance(b, t.Tensor) and b.is_cuda)
     bd = N.to_device(np.asarray(b, dtype=np.float64)) if host else b
     x, rep = gmres(apply_a, apply_minv, bd, tol=tol, max_iter=max_iter, restart=restart)
+    return (x.cpu().numpy() if host else x), rep
+
+
+def hybrid_solve_sharded(op, f, b, tol=1e-8, max_iter=500, restart=50):
+    """hybrid_solve (krylov.py:155-188) on a subtree-sharded operator
+    (sharded.py): b is this rank's rows (tree order, device or host), A the
+    sharded hmatvec, M^-1 the sharded solve, inner products all-reduced over
+    the ranks.  Returns this rank's rows of x and the (rank-identical)
+    report."""
+    from . import sharded as S
+    lam = f.lam
+    if op.kernel.regularization != lam:
+        raise ValueError(f"factorization lambda {lam} does not match operator lambda {op.kernel.regularization}")
+    t = N.torch()
+    if (tuple(b.shape) if isinstance(b, t.Tensor) else np.shape(b)) != (op.spec.size,):
+        raise ValueError(f"right-hand side must have this shard's {op.spec.size} rows")
+    host = not (isinstance(b, t.Tensor) and b.is_cuda)
+    bd = N.to_device(np.asarray(b, dtype=np.float64)) if host else b
+
+    def apply_a(v):
+        return S.hmatvec_sharded(op, v.reshape(1, -1), lam)[0]
+
+    def apply_minv(v):
+        return S.solve_sharded(f, v.reshape(1, -1))[0]
+
+    x, rep = gmres(apply_a, apply_minv, bd, tol=tol, max_iter=max_iter, restart=restart, comm=op.comm)
     return (x.cpu().numpy() if host else x), rep

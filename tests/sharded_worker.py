@@ -67,6 +67,10 @@ def main():
     X2 = S.solve_sharded(f, B)  # graph replay
     U = S.hmatvec_sharded(op, B, a.lam)
     full = S.gather_rows(comm, spec, X)
+    from paper_1701_02324_b200.krylov import hybrid_solve_sharded
+    xh, rep = hybrid_solve_sharded(op, f, B[0], tol=1e-9, max_iter=40, restart=5)
+    res.update(xh=xh.cpu().numpy(), h_iters=rep.iterations, h_res=np.array(rep.residuals),
+               h_final=rep.final_residual)
     res.update(x=X.cpu().numpy(), x2=X2.cpu().numpy(), u=U.cpu().numpy(), xfull=full.cpu().numpy())
     for i in range(1, (1 << (tree.depth + 1)) - 1):
         if i in sk:

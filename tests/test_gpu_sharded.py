@@ -67,7 +67,8 @@ def _reference(n, d, leaf, s, kappa, tau, h, lam, seed):
     bt = b[np.asarray(tree.perm)]
     xs = hk.solve_multi(f, bt, in_tree_order=True)
     u = np.stack([hk.hmatvec(op, bt[:, j], lam) for j in range(bt.shape[1])], axis=1)
-    return dict(tree=tree, knn=np.asarray(knn), sk=sk, x=xs, u=u, zc=f.z_cond_per_level())
+    xh, rep = hk.hybrid_solve(op, f, bt[:, 0], tol=1e-9, max_iter=40, restart=5)
+    return dict(tree=tree, knn=np.asarray(knn), sk=sk, x=xs, u=u, zc=f.z_cond_per_level(), xh=xh, rep=rep)
 
 
 CASES = {
@@ -108,6 +109,10 @@ def test_sharded_matches_unsharded(tmp_path, case):
         np.testing.assert_array_equal(res["x"], res["x2"])
         np.testing.assert_allclose(res["u"], ref["u"][b:e].T, rtol=0, atol=1e-12 * np.abs(ref["u"]).max())
         np.testing.assert_allclose(res["xfull"], ref["x"].T, rtol=0, atol=1e-11 * np.abs(ref["x"]).max())
+        # hybrid GMRES over the shards: same iterations, same solution
+        assert int(res["h_iters"]) == ref["rep"].iterations
+        np.testing.assert_allclose(res["h_res"], ref["rep"].residuals, rtol=0.5, atol=1e-13)
+        np.testing.assert_allclose(res["xh"], ref["xh"][b:e], rtol=0, atol=1e-10 * np.abs(ref["xh"]).max())
         # per-level z_cond: top levels identical on every rank, shard levels bounded by the global max
         for lev, z in zip(res["zc_levels"], res["zc"]):
             assert z <= ref["zc"][int(lev)] * (1 + 1e-8) + 1e-12
