@@ -99,6 +99,17 @@ int hks_kernel_sum(const double* X, int64_t d, const hks_kernel* kern, const int
                    const double* W, int64_t ldw, int64_t k, double* U, int64_t ldu, double beta,
                    double diag, void* stream);
 
+/* Cross kernel summation U = beta U + K(Xq[rows], Xs) W for nq query points
+ * (rows: device int64 indices into Xq, or NULL for Xq[0..nq)) against ns
+ * source points, both row-major n x d, W ns x k (ldw), U nq x k (ldu).  The
+ * sources are split into column chunks so few queries still fill the GPU;
+ * the chunks' partial sums are added in a fixed order (deterministic).
+ * KRR prediction (cli.py:415-422 _cross_predict) and the sampled-row error
+ * metrics.  Synchronous (returns when U is written). */
+int hks_cross_sum(const double* Xq, int64_t nq, const double* Xs, int64_t ns, int64_t d, const hks_kernel* kern,
+                  const int64_t* rows, const double* W, int64_t ldw, int64_t k, double* U, int64_t ldu,
+                  double beta, void* stream);
+
 /* factor_dense, linalg.py:151-169: in-place LU with partial pivoting of an
  * n x n matrix; piv 0-based (scipy lu_factor); *info_host = 0 or the 1-based
  * step of the first exactly-zero pivot. */

@@ -65,7 +65,7 @@ __device__ __forceinline__ void accumulate16(const double* xa, const double* xb1
 
 // Stage rows [r0, r0+TM) of the row set and [c0, c0+TN) of the column set
 // for dims [k0, k0+dc) into shared memory.
-__device__ __forceinline__ void stage(const double* X, int d, const int64_t* rows, int64_t row0,
+__device__ __forceinline__ void stage(const double* X, const double* XC, int d, const int64_t* rows, int64_t row0,
                                       int m, int r0, const int64_t* cols, int64_t col0, int n,
                                       int c0, int k0, int dc, double* Xr, double* Xc) {
   // one point per warp iteration, lanes over its (contiguous) coordinates
@@ -77,7 +77,7 @@ __device__ __forceinline__ void stage(const double* X, int d, const int64_t* row
   }
   for (int j = wid; j < TN; j += nw) {
     const bool ok = c0 + j < n;
-    const double* src = ok ? X + row_id(cols, col0, c0 + j) * d + k0 : X;
+    const double* src = ok ? XC + row_id(cols, col0, c0 + j) * d + k0 : XC;
     for (int k = lane; k < dc; k += 32) Xc[j * XS + k] = ok ? src[k] : 0.0;
   }
 }
@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(256) eval_kernel(const double* __restrict__ X,
   const bool poly = kp.family == HKS_POLYNOMIAL;
   for (int k0 = 0; k0 < d; k0 += DC) {
     const int dc = min(DC, d - k0);
-    stage(X, d, erows, e.row0, e.m, r0, ecols, e.col0, e.n, c0, k0, dc, Xr, Xc);
+    stage(X, X, d, erows, e.row0, e.m, r0, ecols, e.col0, e.n, c0, k0, dc, Xr, Xc);
     __syncthreads();
     const double* mine = ROW_MAJOR ? Xc + own * XS : Xr + own * XS;
     const double* other = ROW_MAJOR ? Xr + grp * XS : Xc + grp * XS;
@@ -162,7 +162,9 @@ __global__ void __launch_bounds__(256) eval_kernel(const double* __restrict__ X,
 
 constexpr int KC = 16;  // right-hand sides per pass
 
-__global__ void __launch_bounds__(256) ksum_kernel(const double* __restrict__ X, int d, KernelParams kp,
+// XC: the column points (X itself except in cross sums, hks_cross_sum).
+__global__ void __launch_bounds__(256) ksum_kernel(const double* __restrict__ X, const double* __restrict__ XC,
+                                                   int d, KernelParams kp,
                                                    const Bases* __restrict__ bases_ptr,
                                                    const SumDesc* __restrict__ descs) {
   const Bases& bases = *bases_ptr;
@@ -194,7 +196,7 @@ __global__ void __launch_bounds__(256) ksum_kernel(const double* __restrict__ X,
       for (int q = 0; q < 16; ++q) acc[q] = 0.0;
       for (int k0 = 0; k0 < d; k0 += DC) {
         const int dc = min(DC, d - k0);
-        stage(X, d, srows, s.row0, s.m, r0, scols, s.col0, s.n, c0, k0, dc, Xr, Xc);
+        stage(X, XC, d, srows, s.row0, s.m, r0, scols, s.col0, s.n, c0, k0, dc, Xr, Xc);
         __syncthreads();
         if (poly)
           accumulate16<true>(Xr + own * XS, Xc + grp * XS, XS, dc, acc);
@@ -254,12 +256,12 @@ cudaError_t launch_eval_batched(const double* X, int d, KernelParams kp, const B
 }
 
 cudaError_t launch_ksum_batched(const double* X, int d, KernelParams kp, const Bases* bases,
-                                const SumDesc* d_descs, int count, int max_m, cudaStream_t stream) {
+                                const SumDesc* d_descs, int count, int max_m, cudaStream_t stream, const double* XC) {
   if (count <= 0 || max_m <= 0) return cudaSuccess;
   for (int first = 0; first < count; first += 65535) {
     const int cnt = count - first < 65535 ? count - first : 65535;
     dim3 grid((max_m + TM - 1) / TM, cnt);
-    ksum_kernel<<<grid, 256, 0, stream>>>(X, d, kp, bases, d_descs + first);
+    ksum_kernel<<<grid, 256, 0, stream>>>(X, XC ? XC : X, d, kp, bases, d_descs + first);
   }
   return cudaGetLastError();
 }

@@ -94,6 +94,7 @@ struct SumDesc {
 };
 
 cudaError_t launch_ksum_batched(const double* X, int d, KernelParams kp, const Bases* bases,
-                                const SumDesc* d_descs, int count, int max_m, cudaStream_t stream);
+                                const SumDesc* d_descs, int count, int max_m, cudaStream_t stream,
+                                const double* XC = nullptr);
 
 }  // namespace hks

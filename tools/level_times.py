@@ -33,3 +33,25 @@ f = hk.factorize(op, w.lam, with_cond=True)
 torch.cuda.synchronize()
 res = N.profile(False)
 print({k: round(v["ms"], 3) for k, v in res.items() if v["launches"]})
+
+# the bench step's solve (nrhs device-resident right-hand sides), per step
+from paper_1701_02324_b200 import solver as S
+B = torch.from_numpy(np.ascontiguousarray(W.rhs(w, 0).T)).cuda()
+for _ in range(3):
+    S.solve_device(f, B)
+torch.cuda.synchronize()
+ts = []
+for _ in range(5):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    S.solve_device(f, B)
+    e1.record()
+    torch.cuda.synchronize()
+    ts.append(e0.elapsed_time(e1))
+print("solve ms (graph)", np.round(ts, 3))
+print("MARK SOLVE", file=sys.stderr, flush=True)
+N.profile(True)
+S.solve_device(f, B)
+torch.cuda.synchronize()
+res = N.profile(False)
+print("solve", {k: round(v["ms"], 3) for k, v in res.items() if v["launches"]})
