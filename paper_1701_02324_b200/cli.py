@@ -1,0 +1,393 @@
+"""``hikersolve``-compatible command line on the GPU path (cli.py of the
+reference).
+
+Subcommands gen / build / matvec / factor / solve / krr / verify take the
+reference's flags and config file (``key = value`` lines, ``#`` comments,
+``lambda`` alias; precedence flags > file > defaults, config.py:17-120) and
+print one JSON report of schema ``hikersolve-report-1`` ({version,
+config_echo, timings, ranks, errors, krylov}; absent sections omitted,
+cli.py:24,215-232).  Failures print one ``ERROR: ...`` line on stderr and
+exit 1.  Every numerical stage runs in libhks; ``verify`` reports the
+GPU-scale sampled-row metrics (metrics.sampled_error_report) instead of the
+reference's dense oracle (limited to n <= 8192 there).
+
+    python -m paper_1701_02324_b200 solve --points x.pts --rhs b.pts --lambda 1e-2
+"""
+
+from __future__ import annotations
+
+import argparse
+import dataclasses
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+REPORT_VERSION = "hikersolve-report-1"
+SHAPE_ALIASES = {"cube": "uniform_cube", "sphere": "sphere_surface", "mixture": "gaussian_mixture"}
+
+
+@dataclasses.dataclass(frozen=True)
+class RunConfig:
+    """Defaults of the reference's Config (config.py:17-37)."""
+    kernel: str = "gaussian"
+    h: float = 0.5
+    degree: int = 2
+    shift: float = 1.0
+    lam: float = 1e-3
+    leaf: int = 256
+    tau: float = 1e-5
+    max_rank: int = 64
+    samples: int = 256
+    sample_mode: str = "uniform"
+    knn: int = 8
+    restart: int = 50
+    tol: float = 1e-8
+    maxiter: int = 500
+    threads: int = 0
+    seed: int = 0
+
+    def kernel_spec(self):
+        from .kernels import KernelSpec
+        return KernelSpec(self.kernel, h=self.h, degree=self.degree, shift=self.shift, regularization=self.lam)
+
+    def skeleton_config(self):
+        from .skeleton import SkeletonConfig
+        return SkeletonConfig(tau=self.tau, max_rank=self.max_rank, samples=self.samples,
+                              sample_mode=self.sample_mode, seed=self.seed)
+
+    def echo(self):
+        out = {f.name: getattr(self, f.name) for f in dataclasses.fields(self)}
+        out["lambda"] = out.pop("lam")
+        out["threads"] = self.threads if self.threads > 0 else (os.cpu_count() or 1)
+        return out
+
+
+_TYPES = {f.name: f.type for f in dataclasses.fields(RunConfig)}
+
+
+def read_config(path, base=None):
+    """Overlay a key = value file (config.py:93-114 semantics)."""
+    base = base or RunConfig()
+    upd = {}
+    with open(path) as fh:
+        for lineno, line in enumerate(fh, start=1):
+            text = line.split("#", 1)[0].strip()
+            if not text:
+                continue
+            if "=" not in text:
+                raise ValueError(f"{path}: line {lineno}: expected key = value")
+            key, raw = (p.strip() for p in text.split("=", 1))
+            key = "lam" if key == "lambda" else key
+            if key not in _TYPES:
+                raise ValueError(f"{path}: line {lineno}: unknown key {key!r}")
+            conv = {"int": int, "float": float}.get(str(_TYPES[key]), str)
+            try:
+                upd[key] = conv(raw)
+            except ValueError:
+                raise ValueError(f"{path}: line {lineno}: bad value {raw!r} for {key}") from None
+    return dataclasses.replace(base, **upd)
+
+
+class _Parser(argparse.ArgumentParser):
+    def error(self, message):
+        self.exit(1, f"ERROR: {message}\n")
+
+
+def _flags(p, *groups):
+    if "points" in groups:
+        p.add_argument("--points", required=True)
+        p.add_argument("--normalize", choices=("unit-box",))
+    if "build" in groups:
+        p.add_argument("--leaf", type=int)
+        p.add_argument("--tau", type=float)
+        p.add_argument("--max-rank", dest="max_rank", type=int)
+        p.add_argument("--samples", type=int)
+        p.add_argument("--sample-mode", dest="sample_mode", choices=("uniform", "knn_augmented", "exact"))
+        p.add_argument("--knn", type=int)
+        p.add_argument("--kernel", choices=("gaussian", "laplace3d", "polynomial"))
+        p.add_argument("--h", type=float)
+        p.add_argument("--degree", type=int)
+        p.add_argument("--shift", type=float)
+        p.add_argument("--lambda", dest="lam", type=float)
+    if "krylov" in groups:
+        p.add_argument("--tol", type=float)
+        p.add_argument("--maxiter", type=int)
+        p.add_argument("--restart", type=int)
+    p.add_argument("--config")
+    p.add_argument("--threads", type=int)
+    p.add_argument("--seed", type=int)
+    if "gen" not in groups:
+        p.add_argument("--out-stats")
+
+
+def build_parser():
+    from .data import SHAPES
+    parser = _Parser(prog="hikersolve")
+    sub = parser.add_subparsers(dest="command", required=True)
+    p = sub.add_parser("gen", help="generate a synthetic point set")
+    p.add_argument("--shape", required=True, choices=sorted(set(SHAPE_ALIASES) | set(SHAPES)))
+    p.add_argument("--n", type=int, required=True)
+    p.add_argument("--d", type=int, default=3)
+    p.add_argument("--clusters", type=int, default=4)
+    p.add_argument("--out", required=True)
+    p.add_argument("--format", choices=("binary", "csv"), default="binary")
+    _flags(p, "gen")
+    p = sub.add_parser("build", help="tree + skeletons, emit statistics")
+    _flags(p, "points", "build")
+    p = sub.add_parser("matvec", help="fast kernel summation")
+    p.add_argument("--weights", required=True)
+    p.add_argument("--out")
+    p.add_argument("--verify", action="store_true", help="sampled-row error against the true kernel")
+    _flags(p, "points", "build")
+    p = sub.add_parser("factor", help="factorize and emit statistics")
+    _flags(p, "points", "build")
+    for name in ("solve", "krr"):
+        p = sub.add_parser(name, help="solve (Ktilde + lambda I) x = b" if name == "solve" else
+                           "kernel ridge regression")
+        if name == "solve":
+            _flags(p, "points", "build", "krylov")
+            p.add_argument("--rhs", required=True)
+            p.add_argument("--out")
+        else:
+            _flags(p, "build", "krylov")
+            p.add_argument("--train", required=True)
+            p.add_argument("--labels", required=True)
+            p.add_argument("--test")
+            p.add_argument("--test-labels", dest="test_labels")
+            p.add_argument("--normalize", choices=("unit-box",))
+            p.add_argument("--out-weights", dest="out_weights")
+            p.add_argument("--out-pred", dest="out_pred")
+        p.add_argument("--method", choices=("direct", "hybrid"), default="direct")
+        p.add_argument("--operator", choices=("compressed", "dense"), default="compressed")
+    p = sub.add_parser("verify", help="sampled-row error metrics on a standard instance")
+    p.add_argument("--n", type=int, required=True)
+    p.add_argument("--d", type=int, default=3)
+    p.add_argument("--rows", type=int, default=256)
+    _flags(p, "build")
+    return parser
+
+
+def _config(args, base=None):
+    cfg = read_config(args.config, base) if getattr(args, "config", None) else (base or RunConfig())
+    known = {k: v for k, v in vars(args).items() if v is not None and k in _TYPES}
+    return dataclasses.replace(cfg, **known) if known else cfg
+
+
+def _sync():
+    from . import _native as N
+    N.torch().cuda.synchronize()
+
+
+class _Clock:
+    def __init__(self):
+        self.t = {}
+
+    def __call__(self, name, fn):
+        _sync()
+        t0 = time.perf_counter()
+        out = fn()
+        _sync()
+        self.t[name] = time.perf_counter() - t0
+        return out
+
+
+def _points(path, normalize):
+    from .pointio import load_points, normalize_unit_box
+    ps = load_points(path)
+    return normalize_unit_box(ps) if normalize == "unit-box" else ps
+
+
+def _build(cfg, ps, clock):
+    from . import build_operator, build_skeletons, build_tree, knn_bruteforce
+    tr = clock("build", lambda: build_tree(ps, cfg.leaf, seed=cfg.seed))
+    knn = None
+    if cfg.sample_mode == "knn_augmented":
+        knn = clock("knn", lambda: knn_bruteforce(tr.points, min(cfg.knn, tr.n - 1)))
+    sk = clock("skeletonize", lambda: build_skeletons(tr, cfg.kernel_spec(), cfg.skeleton_config(), knn=knn))
+    op = clock("assemble", lambda: build_operator(tr, sk, cfg.kernel_spec()))
+    return tr, sk, op
+
+
+def _report(cfg, command, extra=None, timings=None, ranks=None, errors=None, kr=None):
+    echo = {"command": command, **cfg.echo(), **(extra or {})}
+    rep = {"version": REPORT_VERSION, "config_echo": echo}
+    if timings:
+        rep["timings"] = {k: float(v) for k, v in timings.items()}
+    if ranks:
+        rep["ranks"] = {str(k): int(v) for k, v in ranks.items()}
+    if errors:
+        rep["errors"] = {k: float(v) for k, v in errors.items()}
+    if kr is not None:
+        rep["krylov"] = {"iterations": int(kr.iterations), "residuals": [float(r) for r in kr.residuals]}
+    return rep
+
+
+def _solve_tree(cfg, op, f, b_tree, method, operator):
+    from . import hybrid_solve, solve
+    if method == "direct":
+        return solve(f, b_tree, in_tree_order=True), None
+    mode = "dense_oracle" if operator == "dense" else "compressed"
+    return hybrid_solve(op, f, b_tree, tol=cfg.tol, max_iter=cfg.maxiter, restart=cfg.restart, operator_mode=mode)
+
+
+def cmd_gen(args):
+    from .data import generate
+    from .pointio import save_points
+    cfg = _config(args)
+    shape = SHAPE_ALIASES.get(args.shape, args.shape)
+    t0 = time.perf_counter()
+    save_points(generate(shape, args.n, cfg.seed, d=args.d, k_clusters=args.clusters), args.out, format=args.format)
+    return _report(cfg, "gen", {"shape": shape, "n": args.n, "d": args.d, "out": args.out},
+                   {"generate": time.perf_counter() - t0})
+
+
+def cmd_build(args):
+    cfg = _config(args)
+    ps = _points(args.points, args.normalize)
+    clock = _Clock()
+    tr, sk, _ = _build(cfg, ps, clock)
+    return _report(cfg, "build", {"points": args.points, "n": ps.n, "d": ps.d}, clock.t, sk.max_rank_per_level(tr))
+
+
+def cmd_matvec(args):
+    from . import hmatvec, sampled_error_report
+    from .pointio import load_vector, save_vector
+    cfg = _config(args)
+    ps = _points(args.points, args.normalize)
+    w = load_vector(args.weights)
+    if w.shape[0] != ps.n:
+        raise ValueError(f"weights length {w.shape[0]} does not match n={ps.n}")
+    clock = _Clock()
+    tr, sk, op = _build(cfg, ps, clock)
+    perm = np.asarray(tr.perm)
+    u_tree = clock("matvec", lambda: hmatvec(op, w[perm], cfg.lam))
+    u = np.empty_like(u_tree)
+    u[perm] = u_tree
+    if args.out:
+        save_vector(u, args.out)
+    errors = None
+    if args.verify:
+        from .metrics import cross_sum, sample_rows
+        from . import _native as N
+        R = sample_rows(tr.n, 256, cfg.seed)
+        x = tr.device_points()
+        ref = cross_sum(op.kernel, x, x, N.to_device(w[perm]).reshape(1, -1), rows=N.to_device(R))[0].cpu().numpy()
+        ref += cfg.lam * w[perm][R]
+        errors = {"matvec_relerr": np.linalg.norm(u_tree[R] - ref) / np.linalg.norm(ref)}
+    return _report(cfg, "matvec", {"points": args.points, "n": ps.n, "d": ps.d}, clock.t,
+                   sk.max_rank_per_level(tr), errors)
+
+
+def cmd_factor(args):
+    from . import factorize
+    cfg = _config(args)
+    ps = _points(args.points, args.normalize)
+    clock = _Clock()
+    tr, sk, op = _build(cfg, ps, clock)
+    f = clock("factorize", lambda: factorize(op, cfg.lam))
+    for level, secs in f.level_seconds.items():
+        clock.t[f"factorize_level{level}"] = secs
+    errors = {f"z_cond_L{lev}": c for lev, c in f.z_cond_per_level().items()}
+    return _report(cfg, "factor", {"points": args.points, "n": ps.n, "d": ps.d}, clock.t,
+                   sk.max_rank_per_level(tr), errors or None)
+
+
+def cmd_solve(args):
+    from . import factorize, hmatvec
+    from .pointio import load_vector, save_vector
+    cfg = _config(args)
+    ps = _points(args.points, args.normalize)
+    b = load_vector(args.rhs)
+    if b.shape[0] != ps.n:
+        raise ValueError(f"rhs length {b.shape[0]} does not match n={ps.n}")
+    clock = _Clock()
+    tr, sk, op = _build(cfg, ps, clock)
+    f = clock("factorize", lambda: factorize(op, cfg.lam))
+    perm = np.asarray(tr.perm)
+    x_tree, kr = clock("solve", lambda: _solve_tree(cfg, op, f, b[perm], args.method, args.operator))
+    x = np.empty_like(x_tree)
+    x[perm] = x_tree
+    if args.out:
+        save_vector(x, args.out)
+    resid = hmatvec(op, x_tree, cfg.lam) - b[perm]
+    errors = {"residual_vs_Ktilde": np.linalg.norm(resid) / np.linalg.norm(b)}
+    if kr is not None:
+        errors["final_residual"] = kr.final_residual
+    return _report(cfg, "solve", {"points": args.points, "n": ps.n, "d": ps.d, "method": args.method}, clock.t,
+                   sk.max_rank_per_level(tr), errors, kr)
+
+
+def cmd_krr(args):
+    from . import cross_predict, factorize, hmatvec
+    from .pointio import load_vector, save_vector
+    cfg = _config(args)
+    train = _points(args.train, args.normalize)
+    y = load_vector(args.labels)
+    if y.shape[0] != train.n:
+        raise ValueError(f"labels length {y.shape[0]} does not match n={train.n}")
+    clock = _Clock()
+    tr, sk, op = _build(cfg, train, clock)
+    f = clock("factorize", lambda: factorize(op, cfg.lam))
+    perm = np.asarray(tr.perm)
+    w_tree, kr = clock("fit", lambda: _solve_tree(cfg, op, f, y[perm], args.method, args.operator))
+    if args.out_weights:
+        w = np.empty_like(w_tree)
+        w[perm] = w_tree
+        save_vector(w, args.out_weights)
+    pred_train = hmatvec(op, w_tree, 0.0)
+    errors = {"rmse_train": float(np.sqrt(np.mean((pred_train - y[perm]) ** 2)))}
+    if args.test:
+        test = _points(args.test, args.normalize)
+        pred = clock("predict", lambda: cross_predict(cfg.kernel_spec(), test, tr.points, w_tree))
+        if args.out_pred:
+            save_vector(pred, args.out_pred)
+        if args.test_labels:
+            yt = load_vector(args.test_labels)
+            if yt.shape[0] != test.n:
+                raise ValueError(f"test labels length {yt.shape[0]} does not match n={test.n}")
+            errors["rmse_test"] = float(np.sqrt(np.mean((pred - yt) ** 2)))
+    return _report(cfg, "krr", {"train": args.train, "n": train.n, "d": train.d, "method": args.method}, clock.t,
+                   sk.max_rank_per_level(tr), errors, kr)
+
+
+VERIFY_DEFAULTS = dict(kernel="gaussian", h=0.3, lam=1e-2, tau=1e-7, sample_mode="exact", max_rank=384)
+
+
+def cmd_verify(args):
+    from . import factorize, sampled_error_report
+    from .data import generate
+    cfg = _config(args, RunConfig(**VERIFY_DEFAULTS))
+    ps = generate("uniform_cube", args.n, cfg.seed, d=args.d)
+    clock = _Clock()
+    tr, sk, op = _build(cfg, ps, clock)
+    f = clock("factorize", lambda: factorize(op, cfg.lam))
+    rep = clock("verify", lambda: sampled_error_report(op, f, rows=args.rows, seed=cfg.seed))
+    errors = {f"sampled_{k}": v for k, v in rep.items() if k != "rows"}
+    return _report(cfg, "verify", {"n": args.n, "d": args.d, "rows": rep["rows"]}, clock.t,
+                   sk.max_rank_per_level(tr), errors)
+
+
+COMMANDS = {"gen": cmd_gen, "build": cmd_build, "matvec": cmd_matvec, "factor": cmd_factor, "solve": cmd_solve,
+            "krr": cmd_krr, "verify": cmd_verify}
+
+
+def run(argv=None):
+    args = build_parser().parse_args(argv)
+    try:
+        report = COMMANDS[args.command](args)
+    except Exception as exc:  # noqa: BLE001 -- the reference's ERROR: convention (cli.py:524-530)
+        print(f"ERROR: {exc}", file=sys.stderr)
+        return 1
+    text = json.dumps(report, indent=2)
+    print(text)
+    if getattr(args, "out_stats", None):
+        with open(args.out_stats, "w") as fh:
+            fh.write(text + "\n")
+    return 0
+
+
+def main():
+    sys.exit(run())
