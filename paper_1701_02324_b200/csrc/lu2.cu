@@ -98,8 +98,9 @@ __global__ void __launch_bounds__(PT) panel_kernel(const Bases* __restrict__ bas
 // unsigned bit order; bit 63 marks a live row) reduced with three 32-bit
 // warp reductions (max high word, max low word among the high-word winners,
 // min row label among the key winners -- the lowest current row wins ties,
-// as idamax); per-warp winners publish key + working row into a
-// parity-double-buffered slot, so one barrier per column suffices.
+// as idamax); per-warp winners publish their keys, every thread reduces
+// them after a barrier, and only the thread holding the pivot row publishes
+// it (a second barrier) -- one row store per column instead of one per warp.
 template <int PB, int RPT, int NT, int U>
 __global__ void __launch_bounds__(NT) panel_loop_kernel(const Bases* __restrict__ bases_ptr,
                                                         const PanelDesc* __restrict__ descs) {
@@ -144,7 +145,7 @@ __global__ void __launch_bounds__(NT) panel_loop_kernel(const Bases* __restrict_
       if (jj < pb) {
         const int par = jj & 1;
         unsigned long long key = 0;
-        int ai = 0x7fffffff, aq = 0;
+        int ai = 0x7fffffff;
 #pragma unroll
         for (int q = 0; q < RPT; ++q) {
           if (lab[q] >= jj && lab[q] < mr) {
@@ -152,7 +153,6 @@ __global__ void __launch_bounds__(NT) panel_loop_kernel(const Bases* __restrict_
             if (k > key || (k == key && lab[q] < ai)) {
               key = k;
               ai = lab[q];
-              aq = q;
             }
           }
         }
@@ -160,15 +160,6 @@ __global__ void __launch_bounds__(NT) panel_loop_kernel(const Bases* __restrict_
         const unsigned m1 = __reduce_max_sync(0xffffffffu, hi);
         const unsigned m2 = __reduce_max_sync(0xffffffffu, hi == m1 ? lo : 0u);
         const unsigned id = __reduce_min_sync(0xffffffffu, (hi == m1 && lo == m2) ? (unsigned)ai : 0xffffffffu);
-        double* mine = cand + (par * NW + wid) * PB;
-        if (m1 != 0u && (unsigned)ai == id) {  // this lane holds the warp's candidate row
-#pragma unroll
-          for (int q = 0; q < RPT; ++q)
-            if (q == aq)
-#pragma unroll
-              for (int c = (u & ~1); c < PB; c += 2)
-                *reinterpret_cast<double2*>(mine + c) = make_double2(w[q][c], w[q][c + 1]);
-        }
         if (lane == 0) {
           khi[par][wid] = m1;
           klo[par][wid] = m2;
@@ -180,10 +171,17 @@ __global__ void __launch_bounds__(NT) panel_loop_kernel(const Bases* __restrict_
         const unsigned g1 = __reduce_max_sync(0xffffffffu, h2);
         const unsigned g2 = __reduce_max_sync(0xffffffffu, h2 == g1 ? l2 : 0u);
         const unsigned gi = __reduce_min_sync(0xffffffffu, (h2 == g1 && l2 == g2) ? i2 : 0xffffffffu);
-        const unsigned win = __ballot_sync(0xffffffffu, lane < NW && h2 == g1 && l2 == g2 && i2 == gi);
-        const int gw = win ? __ffs(win) - 1 : 0;
         const int p = g1 != 0u ? (int)gi : jj;
-        const double* pr = cand + (par * NW + gw) * PB;
+        // only the pivot row is published (one thread), then a second barrier
+        double* pr_w = cand + par * PB;
+#pragma unroll
+        for (int q = 0; q < RPT; ++q)
+          if (lab[q] == p)
+#pragma unroll
+            for (int c = (u & ~1); c < PB; c += 2)
+              *reinterpret_cast<double2*>(pr_w + c) = make_double2(w[q][c], w[q][c + 1]);
+        __syncthreads();
+        const double* pr = pr_w;
         const double pv = pr[u];
         if (tid == 0) {
           piv[p0 + jj] = p0 + p;
@@ -502,8 +500,15 @@ cudaError_t launch_panel_batched(const Bases* b, const PanelDesc* d, int count, 
   // 256 threads, one to four rows each; PB x RPT doubles stay in registers.
   // plan.cu uses pb = 32 only for rows <= 256 (panel32_max_rows).
   const int rpt = (max_rows + 255) / 256;
+  // 257..512 rows (leaf blocks): 512 threads, one row each -- twice the
+  // warps of the 256 x 2 layout hide more of the per-column latency chain
+  if (max_rows > 256 && max_rows <= 512 && pb > 16 && pb <= 32)
+    return launch_panel_loop<32, 1, 512, 8>(b, d, count, s);
+  static const bool narrow1024 = getenv("HKS_PANEL_NARROW") != nullptr;  // development knob
+  if (!narrow1024 && max_rows > 512 && max_rows <= 1024 && pb <= 16)
+    return launch_panel_loop<16, 2, 512, 8>(b, d, count, s);
   if (pb > 32) {
-    if (rpt == 1) return launch_panel_loop<64, 1, 256, 8>(b, d, count, s);
+    if (rpt == 1) return launch_panel_loop<64, 1, 256, 16>(b, d, count, s);
   } else if (pb > 16) {
     if (rpt == 1) return launch_panel_loop<32, 1, 256, 8>(b, d, count, s);
     if (rpt == 2) return launch_panel_loop<32, 2, 256, 8>(b, d, count, s);
