@@ -8,15 +8,24 @@
 // order) and independent of n, so a column of a multi-RHS product is
 // bit-identical to the single-RHS product (solve_multi == solve column-wise,
 // tests/test_solver.py:174-185).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "hks_internal.h"
 
 namespace hks {
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, KS = BK + 4;  // KS: smem row stride (bank spread)
-constexpr int THREADS = 128;
-constexpr int STAGES = 3;  // cp.async pipeline depth
+// Output tile TBM x 64 (TBM = 64: 4 warps, TBM = 128: 8 warps), each warp a
+// 32 x 32 block of 8x8x4 DMMA fragments.
+#ifndef HKS_GEMM_BK
+#define HKS_GEMM_BK 16
+#endif
+#ifndef HKS_GEMM_STAGES
+#define HKS_GEMM_STAGES 3
+#endif
+constexpr int BN = 64, BK = HKS_GEMM_BK, KS = BK + 4;  // KS: smem row stride (bank spread)
+constexpr int STAGES = HKS_GEMM_STAGES;  // cp.async pipeline depth
 
 struct GemmOp {
   const double* A;
@@ -30,43 +39,51 @@ struct GemmOp {
 // Stage the A (64 x 16) and B (16 x 64) tiles of k-block k0 into shared
 // memory as As[m][k], Bs[n][k]; global reads are coalesced along whichever
 // index is contiguous, out-of-range elements are zero-filled.
+template <int TBM>
 __device__ __forceinline__ void load_stage(const GemmOp& g, int m0, int n0, int k0, double* As, double* Bs) {
+  constexpr int T = 2 * TBM;  // threads
   const int t = threadIdx.x;
   if (!g.transA) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int m = m0 + (t & 63), k = k0 + (t >> 6) + 2 * j;
+    for (int j = 0; j < BK / (T / TBM); ++j) {
+      const int mi = t % TBM, ki = t / TBM + (T / TBM) * j;
+      const int m = m0 + mi, k = k0 + ki;
       const bool ok = m < g.m && k < g.k;
-      cp_async8(As + (t & 63) * KS + (t >> 6) + 2 * j, ok ? g.A + m + (size_t)k * g.lda : g.A, ok);
+      cp_async8(As + mi * KS + ki, ok ? g.A + m + (size_t)k * g.lda : g.A, ok);
     }
   } else {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int k = k0 + (t & 15), m = m0 + (t >> 4) + 8 * j;
+    for (int j = 0; j < TBM / (T / 16); ++j) {
+      const int ki = t & 15, mi = (t >> 4) + (T / 16) * j;
+      const int k = k0 + ki, m = m0 + mi;
       const bool ok = m < g.m && k < g.k;
-      cp_async8(As + ((t >> 4) + 8 * j) * KS + (t & 15), ok ? g.A + k + (size_t)m * g.lda : g.A, ok);
+      cp_async8(As + mi * KS + ki, ok ? g.A + k + (size_t)m * g.lda : g.A, ok);
     }
   }
   if (!g.transB) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int k = k0 + (t & 15), n = n0 + (t >> 4) + 8 * j;
+    for (int j = 0; j < BN / (T / 16); ++j) {
+      const int ki = t & 15, ni = (t >> 4) + (T / 16) * j;
+      const int k = k0 + ki, n = n0 + ni;
       const bool ok = n < g.n && k < g.k;
-      cp_async8(Bs + ((t >> 4) + 8 * j) * KS + (t & 15), ok ? g.B + k + (size_t)n * g.ldb : g.B, ok);
+      cp_async8(Bs + ni * KS + ki, ok ? g.B + k + (size_t)n * g.ldb : g.B, ok);
     }
   } else {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int n = n0 + (t & 63), k = k0 + (t >> 6) + 2 * j;
+    for (int j = 0; j < BK / (T / BN); ++j) {
+      const int ni = t & (BN - 1), ki = (t / BN) + (T / BN) * j;
+      const int n = n0 + ni, k = k0 + ki;
       const bool ok = n < g.n && k < g.k;
-      cp_async8(Bs + (t & 63) * KS + (t >> 6) + 2 * j, ok ? g.B + n + (size_t)k * g.ldb : g.B, ok);
+      cp_async8(Bs + ni * KS + ki, ok ? g.B + n + (size_t)k * g.ldb : g.B, ok);
     }
   }
 }
 
-__global__ void __launch_bounds__(THREADS) gemm_batched_kernel(const Bases* __restrict__ bases_ptr,
+template <int TBM>
+__global__ void __launch_bounds__(2 * TBM) gemm_batched_kernel(const Bases* __restrict__ bases_ptr,
                                                                 const GemmDesc* __restrict__ descs,
                                                                 int tiles_n) {
+  constexpr int BM = TBM;
   const Bases& bases = *bases_ptr;
   const GemmDesc gd = descs[blockIdx.y];
   const GemmOp g{at<const double>(bases, gd.A), at<const double>(bases, gd.B), at<double>(bases, gd.C),
@@ -82,35 +99,33 @@ __global__ void __launch_bounds__(THREADS) gemm_batched_kernel(const Bases* __re
   const int wm = (wid >> 1) * 32, wn = (wid & 1) * 32;
   const int fr = lane >> 2, fc = lane & 3;
 
-  // alpha = +-1 (every product the plans build): the accumulators start at
-  // +-beta*C, loaded before the k loop so the C latency overlaps the
-  // prologue, and the result is +-acc -- exact sign flips, so this is
-  // beta*C + alpha*sum in the DMMA's k order.  Any other alpha keeps the
-  // plain alpha*sum + beta*C epilogue.
-  const bool unit = g.alpha == 1.0 || g.alpha == -1.0;
-  const double cinit = unit ? g.alpha * g.beta : 0.0;
+  // The DMMA sum starts at 0 (k order fixed by the tiles); the epilogue
+  // forms alpha*sum + beta*C.  The C tile is prefetched into L2 at the
+  // start (no registers held, no stall at the first DMMA), so the
+  // epilogue's loads hit L2 after the k loop.
+  if (g.beta != 0.0) {  // one 64-byte line per (column, 8-row group) of the tile
+    for (int e = threadIdx.x; e < BN * (BM / 8); e += 2 * TBM) {
+      const int c = n0 + e / (BM / 8), r = m0 + (e % (BM / 8)) * 8;
+      if (c < g.n && r < g.m) asm volatile("prefetch.global.L2 [%0];" ::"l"(g.C + r + (size_t)c * g.ldc));
+    }
+  }
   double acc[4][4][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int r = m0 + wm + i * 8 + fr, c = n0 + wn + j * 8 + 2 * fc + h;
-        acc[i][j][h] = (cinit != 0.0 && r < g.m && c < g.n) ? cinit * g.C[r + (size_t)c * g.ldc] : 0.0;
-      }
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int nk = (g.k + BK - 1) / BK;
 #pragma unroll
   for (int st = 0; st < STAGES - 1; ++st) {
-    if (st < nk) load_stage(g, m0, n0, st * BK, As + st * BM * KS, Bs + st * BN * KS);
+    if (st < nk) load_stage<TBM>(g, m0, n0, st * BK, As + st * BM * KS, Bs + st * BN * KS);
     cp_async_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     const int pf = kt + STAGES - 1;
-    if (pf < nk) load_stage(g, m0, n0, pf * BK, As + (pf % STAGES) * BM * KS, Bs + (pf % STAGES) * BN * KS);
+    if (pf < nk) load_stage<TBM>(g, m0, n0, pf * BK, As + (pf % STAGES) * BM * KS, Bs + (pf % STAGES) * BN * KS);
     cp_async_commit();
     const double* as = As + (kt % STAGES) * BM * KS;
     const double* bs = Bs + (kt % STAGES) * BN * KS;
@@ -130,7 +145,7 @@ __global__ void __launch_bounds__(THREADS) gemm_batched_kernel(const Bases* __re
   cp_async_wait<0>();
 
   const double alpha = g.alpha, beta = g.beta;
-  if (!unit && beta != 0.0) {  // general alpha: C read after the loop, all loads first
+  if (beta != 0.0) {  // C from L2 (prefetched), all loads first
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -141,21 +156,13 @@ __global__ void __launch_bounds__(THREADS) gemm_batched_kernel(const Bases* __re
           const double cv = (r < g.m && c < g.n) ? g.C[r + (size_t)c * g.ldc] : 0.0;
           acc[i][j][h] = alpha * acc[i][j][h] + beta * cv;
         }
-  } else if (!unit) {
+  } else if (alpha != 1.0) {
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         acc[i][j][0] *= alpha;
         acc[i][j][1] *= alpha;
-      }
-  } else if (alpha < 0.0) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        acc[i][j][0] = -acc[i][j][0];
-        acc[i][j][1] = -acc[i][j][1];
       }
   }
 #pragma unroll
@@ -199,13 +206,26 @@ __global__ void copy_batched_kernel(const Bases* __restrict__ bases_ptr, const C
 cudaError_t launch_gemm_batched(const Bases* bases, const GemmDesc* d_descs, int count, int max_m,
                                 int max_n, cudaStream_t stream) {
   if (count <= 0 || max_m <= 0 || max_n <= 0) return cudaSuccess;
+  static const int forced = [] {  // development knob: HKS_GEMM_BM = 64 / 128
+    const char* e = getenv("HKS_GEMM_BM");
+    return e ? atoi(e) : 0;
+  }();
+  // 128-row tiles (8 warps) once the products are tall and the grid is
+  // large: more warps per SM and half the B-operand staging per flop
+  const bool tall = forced == 128;  // measured: no gain over 64-row tiles on the plans' products
+  const int BM = tall ? 128 : 64;
   const int tm = (max_m + BM - 1) / BM, tn = (max_n + BN - 1) / BN;
   for (int first = 0; first < count; first += 65535) {
     const int cnt = count - first < 65535 ? count - first : 65535;
     dim3 grid(tm * tn, cnt);
     const size_t sm = (size_t)STAGES * (BM + BN) * KS * sizeof(double);
-    raise_smem_limit(gemm_batched_kernel, sm);
-    gemm_batched_kernel<<<grid, THREADS, sm, stream>>>(bases, d_descs + first, tn);
+    if (tall) {
+      raise_smem_limit(gemm_batched_kernel<128>, sm);
+      gemm_batched_kernel<128><<<grid, 256, sm, stream>>>(bases, d_descs + first, tn);
+    } else {
+      raise_smem_limit(gemm_batched_kernel<64>, sm);
+      gemm_batched_kernel<64><<<grid, 128, sm, stream>>>(bases, d_descs + first, tn);
+    }
   }
   return cudaGetLastError();
 }

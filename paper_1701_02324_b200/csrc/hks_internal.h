@@ -47,8 +47,14 @@ cudaError_t launch_trsm_batched(const Bases* b, const TrsmDesc* d, int count, in
 cudaError_t launch_lu_fused(const Bases* b, const LuFusedDesc* d, int count, int max_n, int max_r,
                             cudaStream_t s);
 cudaError_t launch_norm1_batched(const Bases* b, const LuDesc* d, int count, cudaStream_t s);
+// dgecon estimates; phase -1: one monolithic launch; phase 0..kGeconSteps:
+// the split estimate (init, then one LU application + dlacn2 step per
+// launch) with per-matrix state in base kGeconScratchBase.
+constexpr int kGeconSteps = 11;      // dlacn2 applies A, B, 4 x (C, D), E
+constexpr int kGeconScratchBase = 14;  // == B_VWS (plan.h)
+inline int gecon_stride(int max_n) { return 2 * (max_n > 0 ? max_n : 1) + 8; }
 cudaError_t launch_gecon_batched(const Bases* bases, const LuDesc* d_descs, int count, int max_n,
-                                 cudaStream_t stream);
+                                 cudaStream_t stream, int phase = -1);
 
 // Kernel-block evaluation (K1/K2/K3).  Rows/cols are either explicit global
 // (tree-order) index lists or contiguous ranges starting at row0/col0.

@@ -468,6 +468,162 @@ __global__ void __launch_bounds__(GECON_THREADS) gecon_kernel(const Bases* __res
   }
 }
 
+// The same estimate as a sequence of short launches (dgecon runs
+// beside the factorization on a low-priority stream).  A monolithic
+// estimate keeps its CTA resident for ~11 LU sweeps (~0.5-1 ms), and
+// resident CTAs block the factorization's large-footprint kernels from
+// those SMs; split at every LU application, each CTA lives one application
+// (two triangular sweeps) and the SMs turn over quickly.  The dlacn2 state
+// of each matrix (x, sign vector, est, j, iter, next step) lives in global
+// scratch (base kGeconScratchBase, `stride` doubles per matrix).  Arithmetic
+// and its order are those of gecon_kernel, so the results are identical.
+enum GeconState { GS_A = 0, GS_B, GS_C, GS_D, GS_E, GS_DONE };
+
+__global__ void __launch_bounds__(GECON_THREADS) gecon_step_kernel(const Bases* __restrict__ bases_ptr,
+                                                          const LuDesc* __restrict__ descs, int stride,
+                                                          int phase) {
+  const Bases& bases = *bases_ptr;
+  const LuDesc L = descs[blockIdx.x];
+  if (L.rcond == kNull) return;
+  const int n = L.n;
+  double* st = at<double>(bases, make_ref(kGeconScratchBase, 0)) + (size_t)blockIdx.x * stride;
+  double* gx = st;                     // n
+  double* gsgn = st + n;               // n (+-1)
+  double* sc = st + 2 * (size_t)n;     // state, kase, iter, j, est
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double* rcond = at<double>(bases, L.rcond);
+  extern __shared__ double sh[];
+  double* x = sh;
+  __shared__ double red_v[8];
+  __shared__ int red_i[8];
+  __shared__ int s_diff;
+  if (phase == 0) {  // initialise (or finish the trivial cases)
+    int state = GS_A;
+    if (n == 0) {
+      if (tid == 0) *rcond = 1.0;
+      state = GS_DONE;
+    } else {
+      const double anorm = *at<const double>(bases, L.anorm);
+      if (anorm == 0.0 || (L.info != kNull && *at<const int>(bases, L.info) != 0)) {
+        if (tid == 0) *rcond = 0.0;
+        state = GS_DONE;
+      }
+    }
+    if (state != GS_DONE)
+      for (int i = tid; i < n; i += nt) gx[i] = 1.0 / n;
+    if (tid == 0) {
+      sc[0] = state;
+      sc[1] = 1;  // kase of the next application
+      sc[2] = 0;
+      sc[3] = 0;
+      sc[4] = 0.0;
+    }
+    return;
+  }
+  int state = (int)sc[0];
+  if (state == GS_DONE) return;
+  const double* LUa = at<const double>(bases, L.A);
+  const int kase = (int)sc[1];
+  int iter = (int)sc[2], j = (int)sc[3];
+  double est = sc[4];
+  for (int i = tid; i < n; i += nt) x[i] = gx[i];
+  __syncthreads();
+  if (kase == 1) {
+    trsv_fast(LUa, L.lda, n, x, false, false);
+    trsv_fast(LUa, L.lda, n, x, true, false);
+  } else {
+    trsv_fast(LUa, L.lda, n, x, true, true);
+    trsv_fast(LUa, L.lda, n, x, false, true);
+  }
+  int next_kase = 1;
+  auto set_alt = [&]() {  // L120: alternating-sign probe
+    for (int i = tid; i < n; i += nt) {
+      const double sg = (i % 2 == 0) ? 1.0 : -1.0;
+      x[i] = sg * (1.0 + (double)i / (double)(n - 1));
+    }
+    next_kase = 1;
+    state = GS_E;
+  };
+  auto set_unit = [&](int jj) {  // L50: x = e_j
+    for (int i = tid; i < n; i += nt) x[i] = (i == jj) ? 1.0 : 0.0;
+    next_kase = 1;
+    state = GS_C;
+  };
+  if (state == GS_A) {
+    if (n == 1) {
+      est = fabs(x[0]);
+      state = GS_DONE;
+    } else {
+      est = block_asum(x, n, red_v);
+      for (int i = tid; i < n; i += nt) {
+        x[i] = x[i] >= 0.0 ? 1.0 : -1.0;
+        gsgn[i] = x[i];
+      }
+      next_kase = 2;
+      state = GS_B;
+    }
+  } else if (state == GS_B) {
+    j = block_iamax(x, n, red_v, red_i);
+    iter = 2;
+    __syncthreads();
+    set_unit(j);
+  } else if (state == GS_C) {
+    const double estold = est;
+    est = block_asum(x, n, red_v);
+    if (tid == 0) s_diff = 0;
+    __syncthreads();
+    for (int i = tid; i < n; i += nt) {
+      const double xs = x[i] >= 0.0 ? 1.0 : -1.0;
+      if (xs != gsgn[i]) s_diff = 1;
+    }
+    __syncthreads();
+    const int diff = s_diff;
+    __syncthreads();
+    if (!diff || est <= estold) {
+      set_alt();
+    } else {
+      for (int i = tid; i < n; i += nt) {
+        x[i] = x[i] >= 0.0 ? 1.0 : -1.0;
+        gsgn[i] = x[i];
+      }
+      next_kase = 2;
+      state = GS_D;
+    }
+  } else if (state == GS_D) {
+    const int jlast = j;
+    j = block_iamax(x, n, red_v, red_i);
+    __syncthreads();
+    if (x[jlast] != fabs(x[j]) && iter < 5) {
+      ++iter;
+      __syncthreads();
+      set_unit(j);
+    } else {
+      __syncthreads();
+      set_alt();
+    }
+  } else {  // GS_E
+    const double temp = 2.0 * (block_asum(x, n, red_v) / (double)(3 * n));
+    if (temp > est) est = temp;
+    state = GS_DONE;
+  }
+  __syncthreads();
+  if (state == GS_DONE) {
+    if (tid == 0) {
+      const double anorm = *at<const double>(bases, L.anorm);
+      *rcond = est != 0.0 ? (1.0 / est) / anorm : 0.0;
+    }
+  } else {
+    for (int i = tid; i < n; i += nt) gx[i] = x[i];
+  }
+  if (tid == 0) {
+    sc[0] = state;
+    sc[1] = next_kase;
+    sc[2] = iter;
+    sc[3] = j;
+    sc[4] = est;
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_getrf_batched(const Bases* b, const LuDesc* d, int count, int max_n, cudaStream_t s) {
@@ -511,8 +667,14 @@ cudaError_t launch_getrs_batched(const Bases* b, const LuSolveDesc* d, int count
   return cudaGetLastError();
 }
 
-cudaError_t launch_gecon_batched(const Bases* b, const LuDesc* d, int count, int max_n, cudaStream_t s) {
+cudaError_t launch_gecon_batched(const Bases* b, const LuDesc* d, int count, int max_n, cudaStream_t s, int phase) {
   if (count <= 0) return cudaSuccess;
+  if (phase >= 0) {  // split estimate: phase 0 initialises, 1..kGeconSteps apply + advance
+    const size_t sm = (size_t)(max_n > 0 ? max_n : 1) * sizeof(double);
+    raise_smem_limit(gecon_step_kernel, sm);
+    gecon_step_kernel<<<count, GECON_THREADS, sm, s>>>(b, d, gecon_stride(max_n), phase);
+    return cudaGetLastError();
+  }
   const size_t sm = (size_t)(max_n > 0 ? max_n : 1) * (2 * sizeof(double) + sizeof(int));
   raise_smem_limit(gecon_kernel, sm);
   gecon_kernel<<<count, GECON_THREADS, sm, s>>>(b, d);  // a light co-tenant of the factorization

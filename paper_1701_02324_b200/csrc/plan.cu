@@ -161,8 +161,8 @@ cudaError_t StepList::run(const Bases* b, const double* X, int d, const KernelPa
       case ST_GETRS:
         e = launch_getrs_batched(b, (const LuSolveDesc*)st.d, st.count, st.p0, st.p1, s);
         break;
-      case ST_GECON:
-        e = launch_gecon_batched(b, (const LuDesc*)st.d, st.count, st.p0, s);
+      case ST_GECON:  // p1 = 0: one launch; p1 = 1 + phase: a step of the split estimate
+        e = launch_gecon_batched(b, (const LuDesc*)st.d, st.count, st.p0, s, st.p1 - 1);
         break;
       case ST_EVAL_CM:
       case ST_EVAL_RM:
@@ -759,6 +759,18 @@ void add_theta_hat(Copies& cp, const Ctx& c, int64_t i, Ref Y) {
   cp.fill(adv(Y, rl), R, rr, rl, false);
 }
 
+// dgecon scratch of the split estimate: the largest level's matrices x
+// gecon_stride(R) doubles (the levels run in order on the condition stream)
+size_t cond_scratch_elems(const hks_plan& P) {
+  size_t need = 0;
+  for (int64_t lev = 0; lev < P.L.depth; ++lev) {
+    int maxR = 0;
+    for (int64_t i = P.L.first(lev); i < P.L.first(lev) + P.L.count(lev); ++i) maxR = std::max<int>(maxR, (int)P.R(i));
+    need = std::max(need, (size_t)P.L.count(lev) * gecon_stride(maxR));
+  }
+  return need;
+}
+
 size_t factorize_workspace(const hks_plan& P) {
   size_t need = 0;
   for (int64_t lev = P.L.has_up(0) ? 0 : 1; lev < P.L.depth; ++lev) {
@@ -773,6 +785,16 @@ size_t factorize_workspace(const hks_plan& P) {
 }
 
 // ------------------------------------------------------------ factorize
+
+// The dgecon estimates of levels deeper than this start once the
+// factorization has finished this level (HKS_COND_START_LEVEL overrides).
+int64_t cond_start_level() {
+  static const int64_t v = [] {
+    const char* e = getenv("HKS_COND_START_LEVEL");
+    return e ? (int64_t)atoi(e) : (int64_t)4;
+  }();
+  return v;
+}
 
 void build_factorize(const hks_plan& P, bool with_cond, StepList& sl,
                      std::vector<std::unique_ptr<StepList>>* cond_levels, std::vector<int>* cond_wait) {
@@ -860,8 +882,16 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl,
       double lb = 0;
       for (auto& d : lu) lb += 16.0 * d.n * d.n;
       cond_levels->emplace_back(new StepList());
-      cond_levels->back()->add(ST_GECON, lu, maxR, 0, 22.0 * lb / 16.0, 11.0 * lb / 2.0);
-      cond_wait->push_back((int)sl.marks().size());  // level_ev recorded when this level is done
+      // split estimate: short-lived CTAs turn the SMs over to the
+      // factorization's kernels between LU applications (lu.cu)
+      for (int ph = 0; ph <= kGeconSteps; ++ph)
+        cond_levels->back()->add(ST_GECON, lu, maxR, 1 + ph, ph ? 2.0 * lb / 16.0 : 0.0, ph ? lb / 2.0 : 0.0);
+      // level_ev recorded when this level is done -- or, for the wide deep
+      // levels, when the factorization reaches the narrow top levels
+      // (cond_start_level): the estimates then fill SMs the latency-bound
+      // top levels leave idle instead of competing with wide levels
+      const int64_t start = std::min<int64_t>(lev, cond_start_level());
+      cond_wait->push_back((int)(L.depth - start + 1));
     }
     if (lev == 0 && !L.has_up(0)) continue;
     g_f.flush(sl);
@@ -1298,6 +1328,7 @@ static cudaError_t launch_cond(hks_plan* P, const Bases& b) {
   // pageable source: staged before the call returns; stream order keeps the
   // previous factorization's estimates reading their own table until done
   Bases hb = b;
+  hb.p[B_VWS] = static_cast<char*>(P->cond_ws.p);  // per-matrix dlacn2 state (kGeconScratchBase)
   e = cudaMemcpyAsync(P->cond_bases, &hb, sizeof(Bases), cudaMemcpyHostToDevice, cs);
   for (size_t i = 0; i < P->cond_levels.size() && e == cudaSuccess; ++i) {
     e = cudaStreamWaitEvent(cs, P->level_ev[P->cond_wait[i]], 0);
@@ -1348,6 +1379,8 @@ extern "C" int hks_factorize(hks_plan* P, void* const* buffers, double lam, int3
     for (auto& c : P->cond_levels)
       if (e == cudaSuccess && which == 1) e = c->upload(s);
     if (e == cudaSuccess) e = P->fws.ensure(std::max<size_t>(factorize_workspace(*P), 1) * sizeof(double));
+    if (e == cudaSuccess && which == 1)
+      e = P->cond_ws.ensure(std::max<size_t>(cond_scratch_elems(*P), 1) * sizeof(double));
     if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_factorize: %s", cudaGetErrorString(e));
   }
   Bases b = make_bases(buffers);

@@ -22,6 +22,7 @@ namespace hks {
 // subtree plan (HKS_PLAN_SUBTREE): r_0 x k blocks, ld r_0.
 enum BaseSlot { B_FWS = HKS_NBUF, B_VIN, B_VOUT, B_VWS, B_XIN, B_XOUT };
 static_assert(B_XOUT < kAbs, "base slots overflow");
+static_assert(B_VWS == kGeconScratchBase, "gecon scratch base slot");
 
 // Plan modes (hks_plan_create_ex).  A sharded tree is one subtree plan per
 // rank (the rank's shard, rooted at a level-p node that still has a
@@ -193,6 +194,7 @@ struct hks_plan {
   hks::Bases* cond_bases = nullptr;         // device base table of the last cond launch
   bool cond_pending = false;
   hks::DevBuf fws;                          // factorize level workspace
+  hks::DevBuf cond_ws;                      // dgecon state of the split estimate
   std::vector<cudaEvent_t> level_ev;        // per-level factorize timing (leaf level first)
   std::map<int64_t, std::unique_ptr<hks::VecProgram>> solve_prog, mv_prog, up_prog;
 
