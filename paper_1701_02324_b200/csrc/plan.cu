@@ -917,6 +917,7 @@ void build_solve(const hks_plan& P, int64_t kk, int part, StepList& sl) {
   const int64_t S = 0, G = stk, Gb = 2 * stk;  // element bases inside B_VWS
   const int64_t xs = L.s * kk;                  // top plans: shard-root block stride
   const bool sub = L.mode == PM_SUBTREE;
+  bool forked = false;
   if (part != 2) {
     if (L.mode == PM_TOP) {  // shard roots: their psi arrive from the subtree plans
       Copies cp;
@@ -944,8 +945,17 @@ void build_solve(const hks_plan& P, int64_t kk, int part, StepList& sl) {
                              c.leaf_ws(i), m});
       }
       gp.flush(sl);
+      // The leaf solves x = A^-1 b feed nothing until the final x -= phi c
+      // (solver.py:215-217, 247-250): they run on the side stream while the
+      // latency-bound internal levels run on the main one.
+      forked = L.depth > 0 || sub;
+      if (forked) {
+        sl.fork();
+        sl.side(true);
+      }
       cp.flush(sl);
       add_lu_solve_program(sl, jobs);
+      if (forked) sl.side(false);
     }
     for (int64_t lev = L.depth - 1; lev >= 0; --lev) {  // upward, internal (solver.py:219-233)
       Copies cp;
@@ -981,7 +991,10 @@ void build_solve(const hks_plan& P, int64_t kk, int part, StepList& sl) {
       cp.flush(sl);
     }
   }
-  if (part == 1) return;
+  if (part == 1) {
+    if (forked) sl.join();  // the down half is another program
+    return;
+  }
   if (sub) {  // the shard root's correction, from the top plan
     Copies cp;
     int ld;
@@ -1009,6 +1022,7 @@ void build_solve(const hks_plan& P, int64_t kk, int part, StepList& sl) {
     }
     cp.flush(sl);
   } else if (L.depth > 0 || sub) {
+    if (forked) sl.join();
     Gemms g;
     for (int64_t i = L.first(L.depth); i < L.nn; ++i) {
       const int m = (int)L.size[i], r = c.r(i);
