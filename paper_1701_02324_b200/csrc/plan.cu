@@ -531,17 +531,24 @@ int panel_width(int nmax) {
   return pb;
 }
 
+// ||A||_1 of every matrix before it is factored (dgecon's anorm, solver.py:98).
+void add_norm_step(StepList& sl, const std::vector<LuJob>& jobs) {
+  std::vector<LuDesc> nd;
+  int nmax = 0;
+  for (auto& j : jobs) {
+    nd.push_back(LuDesc{j.A, j.piv, j.info, j.anorm, kNull, j.n, j.lda});
+    nmax = std::max(nmax, j.n);
+  }
+  sl.add(ST_NORM1, nd, nmax);
+}
+
 void add_lu_program(StepList& sl, const std::vector<LuJob>& jobs, bool with_norm) {
   if (jobs.empty()) return;
   int nmax = 0;
   for (auto& j : jobs) nmax = std::max(nmax, j.n);
   if (nmax == 0) return;
   const int PB = panel_width(nmax);
-  if (with_norm) {
-    std::vector<LuDesc> nd;
-    for (auto& j : jobs) nd.push_back(LuDesc{j.A, j.piv, j.info, j.anorm, kNull, j.n, j.lda});
-    sl.add(ST_NORM1, nd, nmax);
-  }
+  if (with_norm) add_norm_step(sl, jobs);
   if ((int)jobs.size() <= fused_lu_max_count()) {
     std::vector<LuFusedDesc> fd;
     double f = 0, bytes = 0;
@@ -826,8 +833,13 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl,
     add_lu_program(sl, jobs, false);
     gm.flush(sl);
   }
+  bool push_pending = false;
   for (int64_t lev = L.depth - 1; lev >= 0; --lev) {  // internal levels (solver.py:139-161)
     sl.mark();
+    if (push_pending) {
+      sl.join();
+      push_pending = false;
+    }
     // Algebraically identical to solver.py:145-158 with the interpolation
     // folded in before the reduced solve: V = thhat P^T (R x r), Y = Z^-1 V,
     // F = B Y (= folded P^T), push = P^T - F, theta = P (V - thhat F).
@@ -876,8 +888,15 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl,
     }
     c_id.flush(sl);
     g_z.flush(sl);
+    if (with_cond) {  // ||Z||_1 for dgecon (solver.py:98) beside V = thhat P^T, before Z is overwritten
+      sl.fork();
+      sl.side(true);
+      add_norm_step(sl, jobs);
+      sl.side(false);
+    }
     g_v.flush(sl);
-    add_lu_program(sl, jobs, with_cond);  // with_cond: ||Z||_1 before factoring, for dgecon
+    if (with_cond) sl.join();
+    add_lu_program(sl, jobs, false);
     if (with_cond && cond_levels) {
       double lb = 0;
       for (auto& d : lu) lb += 16.0 * d.n * d.n;
@@ -895,11 +914,18 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl,
     }
     if (lev == 0 && !L.has_up(0)) continue;
     g_f.flush(sl);
+    // push = P^T - F feeds only the solve: side stream, joined before the
+    // next level reuses the workspace holding F
+    sl.fork();
+    sl.side(true);
     c_t.flush(sl);
     c_p.flush(sl);
+    sl.side(false);
+    push_pending = true;
     g_tf.flush(sl);
     g_out.flush(sl);
   }
+  if (push_pending) sl.join();
 }
 
 // ------------------------------------------------------------ solve
