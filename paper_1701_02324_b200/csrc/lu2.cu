@@ -576,7 +576,16 @@ static cudaError_t launch_trsm_nc(const Bases* b, const TrsmDesc* d, int count, 
 template <bool UPPER>
 static cudaError_t launch_trsm_t(const Bases* b, const TrsmDesc* d, int count, int max_cols, int max_k,
                                  cudaStream_t s) {
-  if (max_cols <= 32) return launch_trsm_nc<UPPER, 32, 128>(b, d, count, max_cols, max_k, s);  // 4 warps stage
+  static const int cap = [] {  // development knob: widest column block per CTA
+    const char* e = getenv("HKS_TRSM_NC");
+    return e ? atoi(e) : 128;
+  }();
+  // few matrices (the narrow top levels): 32-column blocks, 4x the CTAs for
+  // the latency-bound sweeps; wide batches keep 128 (more reuse of T)
+  const bool narrow_batch = (long long)count * ((max_cols + 127) / 128) < 96;
+  if (max_cols <= 32 || cap == 32 || (narrow_batch && cap == 128))
+    return launch_trsm_nc<UPPER, 32, 128>(b, d, count, max_cols, max_k, s);
+  if (cap == 64) return launch_trsm_nc<UPPER, 64>(b, d, count, max_cols, max_k, s);
   if (max_cols <= 64) return launch_trsm_nc<UPPER, 64>(b, d, count, max_cols, max_k, s);
   return launch_trsm_nc<UPPER, 128>(b, d, count, max_cols, max_k, s);
 }
