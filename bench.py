@@ -411,6 +411,7 @@ def gpu_arm(args, w, rank, world):
         "factorize_points_per_s": round(n_total / (max_over_ranks(statistics.mean(t_fact), world, dev) * 1e-3), 1),
         "solve_rhs_per_s": round(w.nrhs / (statistics.mean(t_solve) * 1e-3), 1),
         "factorize_ms": round(statistics.mean(t_fact), 4),
+        "step_ms_each": [round(a + b2, 3) for a, b2 in zip(t_fact, t_solve)],
         "solve_ms": round(statistics.mean(t_solve), 4),
         "step_tflops": round(total_flops / (ms_step * 1e-3) / 1e12, 3),
         "setup_s": setup,

@@ -566,12 +566,18 @@ void add_lu_program(StepList& sl, const std::vector<LuJob>& jobs, bool with_norm
   // (the panel kernel records where every row went); otherwise LAPACK-style
   // sequential sweeps.  kind 0: this panel's pivots (rows from the panel's
   // first column), 1: the group's pivots so far (rows from g0).
-  // Gathers over the panel/group permutations were measured slower than the
-  // pivot sweeps inside the factorization (many short CTAs); the panels
-  // still record the total permutation (tperm) for the solves.
+  // Gathers over the panel/group permutations are slower than the pivot
+  // sweeps on wide levels (many short CTAs) and faster on narrow ones; the
+  // panels always record the total permutation (tperm) for the solves.
   bool track = nmax <= kPermMaxRows;
   for (auto& j : jobs) track &= j.ws != kNull;
-  const bool use_perm = track && getenv("HKS_LU_GATHER") != nullptr;
+  // measured (C2): gathers win for batches of <= 64 matrices (levels <= 6),
+  // sweeps for the wide levels; HKS_LU_GATHER=0/1 forces either
+  static const int gather_env = [] {
+    const char* e = getenv("HKS_LU_GATHER");
+    return e ? atoi(e) : -1;
+  }();
+  const bool use_perm = track && (gather_env >= 0 ? gather_env != 0 : jobs.size() <= 64);
   auto ws_perm = [](const LuJob& j, int which) { return j.ws + (uint64_t)which * j.cap * 4; };  // 0 total, 1 panel, 2 group
   struct Ix {
     Swaps sw;
@@ -1379,6 +1385,41 @@ static cudaError_t launch_cond(hks_plan* P, const Bases& b) {
   return e;
 }
 
+// The caller's stream hands over to the plan's high-priority stream and
+// back (HKS_HIPRI=0: run on the caller's stream).
+static bool hipri_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("HKS_HIPRI");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return on;
+}
+
+static cudaError_t enter_hi(hks_plan* P, cudaStream_t s, cudaStream_t* run) {
+  *run = s;
+  if (!hipri_enabled()) return cudaSuccess;
+  cudaError_t e = cudaSuccess;
+  if (!P->hi) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    e = cudaStreamCreateWithPriority(&P->hi, cudaStreamNonBlocking, hi);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&P->hi_in, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&P->hi_out, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  }
+  e = cudaEventRecord(P->hi_in, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(P->hi, P->hi_in, 0);
+  if (e == cudaSuccess) *run = P->hi;
+  return e;
+}
+
+static cudaError_t leave_hi(hks_plan* P, cudaStream_t s, cudaStream_t run) {
+  if (run == s) return cudaSuccess;
+  cudaError_t e = cudaEventRecord(P->hi_out, run);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(s, P->hi_out, 0);
+  return e;
+}
+
 static int check_info(hks_plan* P, void* const* buffers, int64_t* bad_node, cudaStream_t s) {
   const Layout& L = P->L;
   std::vector<int> info(L.nn);
@@ -1432,8 +1473,12 @@ extern "C" int hks_factorize(hks_plan* P, void* const* buffers, double lam, int3
     cudaEventCreate(&ev);
     P->level_ev.push_back(ev);
   }
-  cudaError_t e = run_graphed(P->fact_graphs[which], *P->fact[which], b, P->X, (int)P->d, P->kp, s,
-                              P->level_ev.data(), buffers[HKS_BUF_STATS], P->L.nn * 3 * sizeof(double));
+  cudaStream_t rs = s;
+  cudaError_t e = enter_hi(P, s, &rs);
+  if (e == cudaSuccess)
+    e = run_graphed(P->fact_graphs[which], *P->fact[which], b, P->X, (int)P->d, P->kp, rs, P->level_ev.data(),
+                    buffers[HKS_BUF_STATS], P->L.nn * 3 * sizeof(double));
+  if (e == cudaSuccess) e = leave_hi(P, s, rs);
   if (e == cudaSuccess && which == 1 && !P->cond_levels.empty()) e = launch_cond(P, b);
   if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_factorize: %s", cudaGetErrorString(e));
   if (bad_node) *bad_node = -1;
@@ -1503,7 +1548,11 @@ static cudaError_t run_vec_part(hks_plan* P, VecProgram* v, int part, Bases& bb,
   bb.p[B_XOUT] = (char*)xout;
   StepList& sl = part == 2 ? v->down : v->steps;
   GraphCache& gc = part == 2 ? v->down_graphs : v->graphs;
-  return run_graphed(gc, sl, bb, P->X, (int)P->d, P->kp, s, nullptr, nullptr, 0);
+  cudaStream_t rs = s;
+  cudaError_t e = enter_hi(P, s, &rs);
+  if (e == cudaSuccess) e = run_graphed(gc, sl, bb, P->X, (int)P->d, P->kp, rs, nullptr, nullptr, 0);
+  if (e == cudaSuccess) e = leave_hi(P, s, rs);
+  return e;
 }
 
 static int check_part(hks_plan* P, int part, const void* xchg, const char* who) {

@@ -195,6 +195,11 @@ struct hks_plan {
   bool cond_pending = false;
   hks::DevBuf fws;                          // factorize level workspace
   hks::DevBuf cond_ws;                      // dgecon state of the split estimate
+  // factorize / solve / hmatvec programs run on a plan-owned high-priority
+  // stream (joined to and from the caller's), so the low-priority dgecon
+  // estimates only take SMs the level programs leave idle
+  cudaStream_t hi = nullptr;
+  cudaEvent_t hi_in = nullptr, hi_out = nullptr;
   std::vector<cudaEvent_t> level_ev;        // per-level factorize timing (leaf level first)
   std::map<int64_t, std::unique_ptr<hks::VecProgram>> solve_prog, mv_prog, up_prog;
 
@@ -210,6 +215,9 @@ struct hks_plan {
     for (auto e : level_ev) cudaEventDestroy(e);
     if (cond_done) cudaEventDestroy(cond_done);
     if (own_cond_stream) cudaStreamDestroy(own_cond_stream);
+    if (hi) cudaStreamDestroy(hi);
+    if (hi_in) cudaEventDestroy(hi_in);
+    if (hi_out) cudaEventDestroy(hi_out);
     if (cond_bases) cudaFree(cond_bases);
   }
 };
