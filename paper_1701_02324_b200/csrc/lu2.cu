@@ -241,9 +241,11 @@ cudaError_t launch_panel_loop(const Bases* b, const PanelDesc* d, int count, cud
   return cudaGetLastError();
 }
 
-// A[i, c] := A[perm[i], c], rows [r0, r1), a block of cb columns per CTA
-// staged through shared memory (all reads before any write); rows the
-// permutation leaves in place are neither read nor written.
+// A[i, c] := A[perm[i], c], rows [r0, r1), for a block of cb columns per
+// CTA.  The rows the permutation moves are compacted first (a matrix that
+// pivots little costs one scan of perm), then staged GS columns at a time
+// through shared memory (all reads of a column chunk before any write).
+constexpr int GS = 8;  // columns per staged chunk
 __global__ void __launch_bounds__(256) gather_rows_kernel(const Bases* __restrict__ bases_ptr,
                                                           const GatherDesc* __restrict__ descs, int cb) {
   const Bases& bases = *bases_ptr;
@@ -254,18 +256,42 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(const Bases* __restric
   double* A = at<double>(bases, D.A) + D.r0 + (size_t)c0 * D.lda;
   const int* perm = at<const int>(bases, D.perm) + D.r0;
   extern __shared__ double gsm[];
-  int* sp = reinterpret_cast<int*>(gsm + (size_t)nr * cb);
-  for (int i = threadIdx.x; i < nr; i += blockDim.x) sp[i] = perm[i] - D.r0;
+  int* dst = reinterpret_cast<int*>(gsm + (size_t)nr * GS);  // moved rows: destination, source
+  int* src = dst + nr;
+  __shared__ int moved;
+  if (threadIdx.x == 0) moved = 0;
   __syncthreads();
-  for (int c = 0; c < nc; ++c)
-    for (int i = threadIdx.x; i < nr; i += blockDim.x) {
-      const int src = sp[i];
-      if (src != i) gsm[c * nr + i] = A[src + (size_t)c * D.lda];
+  const int lane = threadIdx.x & 31;
+  for (int i0 = 0; i0 < nr; i0 += blockDim.x) {  // warp-aggregated compaction
+    const int i = i0 + threadIdx.x;
+    const int sidx = i < nr ? perm[i] - D.r0 : i;
+    const bool mv = i < nr && sidx != i;
+    const unsigned bal = __ballot_sync(0xffffffffu, mv);
+    int base = 0;
+    if (lane == 0 && bal) base = atomicAdd(&moved, __popc(bal));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (mv) {
+      const int k = base + __popc(bal & ((1u << lane) - 1u));
+      dst[k] = i;
+      src[k] = sidx;
     }
+  }
   __syncthreads();
-  for (int c = 0; c < nc; ++c)
-    for (int i = threadIdx.x; i < nr; i += blockDim.x)
-      if (sp[i] != i) A[i + (size_t)c * D.lda] = gsm[c * nr + i];
+  const int M = moved;
+  if (M == 0) return;
+  for (int cc = 0; cc < nc; cc += GS) {
+    const int ncc = min(GS, nc - cc);
+    for (int e = threadIdx.x; e < M * ncc; e += blockDim.x) {
+      const int k = e % M, c = e / M;
+      gsm[c * M + k] = A[src[k] + (size_t)(cc + c) * D.lda];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < M * ncc; e += blockDim.x) {
+      const int k = e % M, c = e / M;
+      A[dst[k] + (size_t)(cc + c) * D.lda] = gsm[c * M + k];
+    }
+    __syncthreads();
+  }
 }
 
 // Row interchanges piv[r0..r1) applied in order to columns [c0, c1).
@@ -539,9 +565,8 @@ cudaError_t launch_panel_batched(const Bases* b, const PanelDesc* d, int count, 
 cudaError_t launch_gather_batched(const Bases* b, const GatherDesc* d, int count, int max_rows, int max_cols,
                                   cudaStream_t s) {
   if (count <= 0 || max_rows <= 0 || max_cols <= 0) return cudaSuccess;
-  int cb = 8192 / max_rows;  // <= 64 KB of staged rows per CTA
-  cb = cb < 1 ? 1 : cb > 32 ? 32 : cb;
-  const size_t sm = (size_t)max_rows * cb * sizeof(double) + (size_t)max_rows * sizeof(int);
+  const int cb = 64;  // columns per CTA: one perm scan per 64 columns
+  const size_t sm = (size_t)max_rows * GS * sizeof(double) + 2 * (size_t)max_rows * sizeof(int);
   raise_smem_limit(gather_rows_kernel, sm);
   for (int first = 0; first < count; first += 65535) {
     const int cnt = count - first < 65535 ? count - first : 65535;

@@ -578,6 +578,12 @@ void add_lu_program(StepList& sl, const std::vector<LuJob>& jobs, bool with_norm
     return e ? atoi(e) : -1;
   }();
   const bool use_perm = track && (gather_env >= 0 ? gather_env != 0 : jobs.size() <= 64);
+  // The group-end interchanges (trailing columns and right-hand sides, the
+  // wide ones) always gather by the group permutation when it is recorded:
+  // one coalesced pass whatever the number of interchanges.  Sequential
+  // sweeps are latency-serialised per interchange and ill-conditioned
+  // blocks pivot almost every row (C3: 25 ms of sweeps per factorization).
+  const bool gather_end = track && gather_env != 0;
   auto ws_perm = [](const LuJob& j, int which) { return j.ws + (uint64_t)which * j.cap * 4; };  // 0 total, 1 panel, 2 group
   struct Ix {
     Swaps sw;
@@ -587,8 +593,9 @@ void add_lu_program(StepList& sl, const std::vector<LuJob>& jobs, bool with_norm
       ga.flush(sl);
     }
   };
-  auto interchange = [&](Ix& ix, const LuJob& j, Ref A, int lda, int kind, int r0, int r1, int c0, int c1) {
-    if (use_perm)
+  auto interchange = [&](Ix& ix, const LuJob& j, Ref A, int lda, int kind, int r0, int r1, int c0, int c1,
+                         bool group_end = false) {
+    if (use_perm || (group_end && gather_end && kind == 1))
       ix.ga.add(A, lda, ws_perm(j, kind == 0 ? 1 : 2), r0, j.n, c0, c1);
     else
       ix.sw.add(A, j.piv, lda, r0, r1, c0, c1);
@@ -620,6 +627,7 @@ void add_lu_program(StepList& sl, const std::vector<LuJob>& jobs, bool with_norm
         }
         PanelDesc d{j.A, j.piv, j.info, j.lda, j.n, p0, pb, kNull, kNull, kNull, g0, 0};
         if (track) d.tperm = ws_perm(j, 0);
+        if (gather_end) d.gperm = ws_perm(j, 2);
         if (use_perm) {
           d.tperm = ws_perm(j, 0);
           d.sig = ws_perm(j, 1);
@@ -652,9 +660,9 @@ void add_lu_program(StepList& sl, const std::vector<LuJob>& jobs, bool with_norm
       const int gb = std::min(kGroup, j.n - g0), ge = g0 + gb;
       const int last = g0 + ((gb - 1) / PB) * PB;  // first column of the group's last panel
       interchange(ix, j, j.A, j.lda, 0, last, ge, g0, last);
-      interchange(ix, j, j.A, j.lda, 1, g0, ge, 0, g0);
-      interchange(ix, j, j.A, j.lda, 1, g0, ge, ge, j.n);
-      if (j.r > 0) interchange(ix, j, j.B, j.ldb, 1, g0, ge, 0, j.r);
+      interchange(ix, j, j.A, j.lda, 1, g0, ge, 0, g0, true);
+      interchange(ix, j, j.A, j.lda, 1, g0, ge, ge, j.n, true);
+      if (j.r > 0) interchange(ix, j, j.B, j.ldb, 1, g0, ge, 0, j.r, true);
       const int split = ahead ? std::min(j.n, ge + kGroup) : j.n;  // columns [ge, split) now, the rest later
       Trsms& tr2 = ahead ? tr_side : tr;
       Gemms& gm2 = ahead ? gm_side : gm;
