@@ -16,6 +16,7 @@ bounded sample of the same workload.  See DESIGN.md for the definitions.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -119,7 +120,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except FileNotFoundError:
@@ -128,6 +129,12 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+
+    def wait_first(self, timeout=10.0):
+        t0 = time.perf_counter()
+        while self.proc is not None and not self.lines and time.perf_counter() - t0 < timeout:
+            time.sleep(0.01)
+        self.skip = len(self.lines)
 
     def stop(self):
         if self.proc is None:
@@ -139,7 +146,8 @@ class ClockSampler:
             self.proc.kill()
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        region = self.lines[getattr(self, "skip", 0):] or self.lines[-1:]  # samples inside the timed region
+        for ln in region:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -299,28 +307,42 @@ def gpu_arm(args, w, rank, world):
         e2.record(stream)
         return f, X, (e0, e1, e2)
 
-    for _ in range(max(args.warmup, 0)):
-        step()
+    clocks = ClockSampler(torch.cuda.current_device())
+    if not args.no_clocks:
+        clocks.start()  # NVML start-up (it stalls the context) overlaps the warm-up, not the timed steps
+    keep = None
+    for _ in range(max(args.warmup, 0)):  # same object lifetimes as the timed loop: the allocator
+        keep = step()                     # holds two factorizations' storage before timing starts
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    clocks = ClockSampler(torch.cuda.current_device())
     if not args.no_clocks:
-        clocks.start()
+        clocks.wait_first()
+        keep = step()  # the warm-up's last step right before the region (no idle gap)
+        torch.cuda.synchronize()
+        clocks.skip = len(clocks.lines)
+    # host hygiene as in timeit: no cyclic-GC pause (tens of ms with a large
+    # heap) lands between the timed launches
+    gc.collect()
+    gc.disable()
     launches0 = N.launch_count()
     r0 = torch.cuda.Event(enable_timing=True)
     r1 = torch.cuda.Event(enable_timing=True)
+    f = keep[0] if keep else None
     torch.cuda.profiler.start()  # ncu --profile-from-start off: only the timed region
     r0.record(stream)
-    evs = []
+    evs, host_t = [], []
     for _ in range(args.steps):
+        h0 = time.perf_counter()
         f, X, ev = step()
+        host_t.append((time.perf_counter() - h0) * 1e3)
         evs.append(ev)
     f.join_cond()  # the last step's dgecon estimates (condition stream) finish inside the region
     r1.record(stream)
     torch.cuda.synchronize()
     torch.cuda.profiler.stop()
+    gc.enable()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -344,6 +366,8 @@ def gpu_arm(args, w, rank, world):
 
     # e2e through the public API: pinned host B -> host x, H2D + D2H inside
     e2e_ms = []
+    gc.collect()
+    gc.disable()
     for i in range(max(2, min(args.steps, 5))):
         torch.cuda.synchronize()
         if world > 1:
@@ -352,6 +376,7 @@ def gpu_arm(args, w, rank, world):
         run.e2e()
         torch.cuda.synchronize()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    gc.enable()
     e2e_step = max_over_ranks(statistics.median(e2e_ms), world, dev)
     w_name = w.name
     setup = run.setup
@@ -412,6 +437,8 @@ def gpu_arm(args, w, rank, world):
         "solve_rhs_per_s": round(w.nrhs / (statistics.mean(t_solve) * 1e-3), 1),
         "factorize_ms": round(statistics.mean(t_fact), 4),
         "step_ms_each": [round(a + b2, 3) for a, b2 in zip(t_fact, t_solve)],
+        "host_ms_each": [round(v, 3) for v in host_t],
+        "factorize_ms_each": [round(v, 3) for v in t_fact],
         "solve_ms": round(statistics.mean(t_solve), 4),
         "step_tflops": round(total_flops / (ms_step * 1e-3) / 1e12, 3),
         "setup_s": setup,

@@ -2,6 +2,7 @@
 // (solver.py:111-270, treecode.py:41-128) and the plan-bound C-ABI entry
 // points.  See plan.h.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -262,7 +263,13 @@ cudaError_t GraphCache::write(const Bases& b, cudaStream_t s) {
 cudaError_t run_graphed(GraphCache& gc, const StepList& sl, const Bases& b, const double* X, int d,
                         const KernelParams& kp, cudaStream_t s, cudaEvent_t* ev, void* memset_ptr,
                         size_t memset_bytes, bool allow_graph) {
+  static const bool htrace = getenv("HKS_HOST_TRACE") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
   cudaError_t e = gc.write(b, s);
+  if (htrace)
+    fprintf(stderr, "HKS_HOST graph write %lld us\n",
+            (long long)std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - t0)
+                .count());
   if (e != cudaSuccess) return e;
   if (!allow_graph || !graphs_enabled() || profiling()) {
     e = memset_ptr ? cudaMemsetAsync(memset_ptr, 0, memset_bytes, s) : cudaSuccess;
@@ -1376,18 +1383,31 @@ static cudaError_t launch_cond(hks_plan* P, const Bases& b) {
     P->cond_stream = P->own_cond_stream;
   }
   if (!P->cond_done) e = cudaEventCreateWithFlags(&P->cond_done, cudaEventDisableTiming);
-  if (e == cudaSuccess && !P->cond_bases) e = cudaMalloc(&P->cond_bases, sizeof(Bases));
   if (e != cudaSuccess) return e;
   cudaStream_t cs = P->cond_stream;
   // pageable source: staged before the call returns; stream order keeps the
   // previous factorization's estimates reading their own table until done
   Bases hb = b;
   hb.p[B_VWS] = static_cast<char*>(P->cond_ws.p);  // per-matrix dlacn2 state (kGeconScratchBase)
-  e = cudaMemcpyAsync(P->cond_bases, &hb, sizeof(Bases), cudaMemcpyHostToDevice, cs);
+  // through the pinned ring of a GraphCache: a pageable copy would block the
+  // host until the condition stream reached it (measured: ~14 ms per call)
+  static const bool htrace = getenv("HKS_HOST_TRACE") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  e = P->cond_gc.write(hb, cs);
+  auto t1 = std::chrono::steady_clock::now();
+  long long wt = 0, rt = 0;
   for (size_t i = 0; i < P->cond_levels.size() && e == cudaSuccess; ++i) {
+    auto a = std::chrono::steady_clock::now();
     e = cudaStreamWaitEvent(cs, P->level_ev[P->cond_wait[i]], 0);
-    if (e == cudaSuccess) e = P->cond_levels[i]->run(P->cond_bases, P->X, (int)P->d, P->kp, cs);
+    auto b2 = std::chrono::steady_clock::now();
+    if (e == cudaSuccess) e = P->cond_levels[i]->run(P->cond_gc.dev, P->X, (int)P->d, P->kp, cs);
+    auto c = std::chrono::steady_clock::now();
+    wt += std::chrono::duration_cast<std::chrono::microseconds>(b2 - a).count();
+    rt += std::chrono::duration_cast<std::chrono::microseconds>(c - b2).count();
   }
+  if (htrace)
+    fprintf(stderr, "HKS_HOST cond write %lld us, waits %lld us, launches %lld us\n",
+            (long long)std::chrono::duration_cast<std::chrono::microseconds>(t1 - t0).count(), wt, rt);
   if (e == cudaSuccess) e = cudaEventRecord(P->cond_done, cs);
   if (e == cudaSuccess) P->cond_pending = true;
   return e;
@@ -1481,16 +1501,30 @@ extern "C" int hks_factorize(hks_plan* P, void* const* buffers, double lam, int3
     cudaEventCreate(&ev);
     P->level_ev.push_back(ev);
   }
+  static const bool htrace = getenv("HKS_HOST_TRACE") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  const auto t0 = now();
   cudaStream_t rs = s;
   cudaError_t e = enter_hi(P, s, &rs);
   if (e == cudaSuccess)
     e = run_graphed(P->fact_graphs[which], *P->fact[which], b, P->X, (int)P->d, P->kp, rs, P->level_ev.data(),
                     buffers[HKS_BUF_STATS], P->L.nn * 3 * sizeof(double));
+  const auto t1 = now();
   if (e == cudaSuccess) e = leave_hi(P, s, rs);
   if (e == cudaSuccess && which == 1 && !P->cond_levels.empty()) e = launch_cond(P, b);
+  const auto t2 = now();
   if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_factorize: %s", cudaGetErrorString(e));
   if (bad_node) *bad_node = -1;
-  return check_info(P, buffers, bad_node, s);
+  const int rc = check_info(P, buffers, bad_node, s);
+  if (htrace) {
+    const auto t3 = now();
+    auto us = [](std::chrono::steady_clock::duration d) {
+      return (long long)std::chrono::duration_cast<std::chrono::microseconds>(d).count();
+    };
+    fprintf(stderr, "HKS_HOST factorize launch %lld us, cond %lld us, sync %lld us\n", us(t1 - t0), us(t2 - t1),
+            us(t3 - t2));
+  }
+  return rc;
 }
 
 extern "C" int hks_factor_stats(hks_plan* P, void* const* buffers, double* z_cond, int32_t* info, void* stream) {

@@ -191,7 +191,7 @@ struct hks_plan {
   cudaStream_t cond_stream = nullptr;       // caller's stream (hks_set_cond_stream) or own_cond_stream
   cudaStream_t own_cond_stream = nullptr;
   cudaEvent_t cond_done = nullptr;
-  hks::Bases* cond_bases = nullptr;         // device base table of the last cond launch
+  hks::GraphCache cond_gc;                  // device base table (+ pinned ring) of the cond launches
   bool cond_pending = false;
   hks::DevBuf fws;                          // factorize level workspace
   hks::DevBuf cond_ws;                      // dgecon state of the split estimate
@@ -218,6 +218,5 @@ struct hks_plan {
     if (hi) cudaStreamDestroy(hi);
     if (hi_in) cudaEventDestroy(hi_in);
     if (hi_out) cudaEventDestroy(hi_out);
-    if (cond_bases) cudaFree(cond_bases);
   }
 };
