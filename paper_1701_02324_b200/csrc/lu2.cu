@@ -340,7 +340,7 @@ __device__ __forceinline__ void trsm_stage_rows(double* Ts, int tts, const doubl
 template <bool UPPER, int NC, int NT = NC>
 __device__ __forceinline__ void trsm_sweep(double* X, double* Tbuf, int tts, const double* T, int ldt, int k,
                                            int nc) {
-  static_assert(NT == NC || (NC == 32 && NT == 128), "warp <-> tile mapping");
+  static_assert(NT == NC || (NC == 32 && NT == 128) || NT == 2 * NC, "warp <-> tile mapping");
   constexpr int NW = NT / 32;
   constexpr int TXS = NC + 4;  // X row stride: == 4 (mod 16), conflict-free DMMA B fragments
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -361,7 +361,38 @@ __device__ __forceinline__ void trsm_sweep(double* X, double* Tbuf, int tts, con
     }
     // X[r0:r0+nr, :] -= T[r0:r0+nr, u] X[u, :] over the solved rows u (DMMA)
     const int ulo = UPPER ? r0 + nr : 0, uhi = UPPER ? k : r0;
-    if (NT != NC) {  // 4 warps on one 32-column tile: warp w owns rows 8w .. 8w+7
+    if (NT == 2 * NC && NC >= 64) {  // two warps per 32-column tile, 16 rows each
+      const int tile = wid >> 1, rb = (wid & 1) * 16, cb = tile * 32;
+      if (uhi > ulo && cb < nc) {
+        double acc[2][4][2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int kk = ulo; kk < uhi; kk += 4) {
+          const int kq = kk + fc;
+          const bool kin = kq < uhi;
+          double a[2], bv[4];
+#pragma unroll
+          for (int i = 0; i < 2; ++i) a[i] = kin ? Ts[(rb + i * 8 + fr) * tts + kq] : 0.0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) bv[j] = kin ? X[kq * TXS + cb + j * 8 + fr] : 0.0;
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], bv[j]);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int rr = rb + i * 8 + fr, c = cb + j * 8 + 2 * fc + h;
+              if (rr < nr) X[(r0 + rr) * TXS + c] -= acc[i][j][h];
+            }
+      }
+    } else if (NT != NC) {  // 4 warps on one 32-column tile: warp w owns rows 8w .. 8w+7
       if (uhi > ulo) {
         double acc[4][2];
 #pragma unroll
@@ -610,6 +641,11 @@ static cudaError_t launch_trsm_t(const Bases* b, const TrsmDesc* d, int count, i
   const bool narrow_batch = (long long)count * ((max_cols + 127) / 128) < 96;
   if (max_cols <= 32 || cap == 32 || (narrow_batch && cap == 128))
     return launch_trsm_nc<UPPER, 32, 128>(b, d, count, max_cols, max_k, s);
+  // wide upper solves (the leaf backward sweep): 8 warps per 128 columns --
+  // the CTA is alone on its SM (202 KB of staging), so more warps hide the
+  // division chain and the loads (measured -23%); lower solves gain nothing
+  if (cap == 256 || (UPPER && cap == 128 && max_cols > 64))
+    return launch_trsm_nc<UPPER, 128, 256>(b, d, count, max_cols, max_k, s);
   if (cap == 64) return launch_trsm_nc<UPPER, 64>(b, d, count, max_cols, max_k, s);
   if (max_cols <= 64) return launch_trsm_nc<UPPER, 64>(b, d, count, max_cols, max_k, s);
   return launch_trsm_nc<UPPER, 128>(b, d, count, max_cols, max_k, s);
