@@ -24,6 +24,9 @@ from . import _native as N
 from .linalg import DenseFactor, SingularMatrixError
 
 
+_HOST_TRACE = bool(__import__("os").environ.get("HKS_HOST_TRACE"))
+
+
 class FactorizationError(RuntimeError):
     """Reduced system singular; remedy is a larger lambda or tighter tau."""
 
@@ -141,6 +144,51 @@ class Factorization:
                           child_push=self._mat(N.BUF_PUSH, i, R, r), z_cond=float(self._z_cond[i]))
 
 
+class FactorStorage:
+    """Reusable factor storage of one operator.  Each Factorization leases
+    a set of the flat factor buffers; dropping it returns the set with an
+    event on the condition stream (its dgecon estimates may still read
+    Z_LU / STATS).  A set is handed out again only once that event has
+    completed (queried, never waited for); otherwise a new set is
+    allocated.  The pool therefore settles at the number of sets the
+    caller's pattern keeps in flight, and steady-state factorizations
+    allocate nothing: a GB-sized cudaMalloc inside a factorize costs tens
+    to hundreds of milliseconds (measured)."""
+
+    def __init__(self, layout, cond_stream):
+        self.layout = layout
+        self.cond_stream = cond_stream
+        self.free = []  # [bufs, event]
+
+    def lease(self):
+        for idx, (bufs, ev) in enumerate(self.free):
+            if ev.query():
+                del self.free[idx]
+                return _Lease(self, bufs)
+        return _Lease(self, {b: self.layout.alloc(b) for b in _FACTOR_BUFS})
+
+    def __del__(self):  # the storage outlives its last estimates
+        for _bufs, ev in getattr(self, "free", []):
+            try:
+                ev.synchronize()
+            except Exception:  # interpreter shutdown
+                pass
+
+
+class _Lease:
+    def __init__(self, pool, bufs):
+        self.pool = pool
+        self.bufs = bufs
+
+    def __del__(self):
+        try:
+            ev = N.torch().cuda.Event()
+            ev.record(self.pool.cond_stream)
+            self.pool.free.append((self.bufs, ev))
+        except Exception:  # interpreter shutdown: let the tensors go
+            pass
+
+
 _FACTOR_BUFS = (N.BUF_THETA, N.BUF_LEAF_LU, N.BUF_LEAF_PIV, N.BUF_PHI, N.BUF_Z_LU, N.BUF_Z_PIV,
                 N.BUF_PUSH, N.BUF_STATS)
 
@@ -151,26 +199,32 @@ def factorize(op, lam, threads=1, with_cond=True):
     if lam < 0:
         raise ValueError("lambda must be nonnegative")
     lay = op.layout
-    bufs = {b: lay.alloc(b) for b in _FACTOR_BUFS}
+    ta = time.perf_counter()
+    if getattr(op, "_factor_pool", None) is None:
+        op._factor_pool = FactorStorage(lay, op.plan.cond_stream)
+    lease = op._factor_pool.lease()
+    bufs = lease.bufs
     bad = ctypes.c_int64(-1)
     t0 = time.perf_counter()
     rc = N.fn("hks_factorize")(op.plan.handle, op.buffers(bufs), float(lam), int(bool(with_cond)),
                                ctypes.byref(bad), N.stream_ptr())
     elapsed = time.perf_counter() - t0
+    if _HOST_TRACE:
+        import sys
+        print(f"HKS_HOST py alloc {(t0 - ta) * 1e6:.0f} us, hks_factorize {elapsed * 1e6:.0f} us", file=sys.stderr)
     if rc == N.HKS_ERR_SINGULAR:
         raise SingularMatrixError(N.last_error())
     if rc == N.HKS_ERR_REDUCED_SINGULAR:
         raise FactorizationError(N.last_error())
     if rc != N.HKS_OK:
         raise N.HksError(rc, N.last_error())
-    if with_cond:  # the estimates still read Z_LU / STATS on the condition stream
-        for bi in (N.BUF_Z_LU, N.BUF_STATS):
-            bufs[bi].record_stream(op.plan.cond_stream)
     depth = op.tree.depth
     ms = np.zeros(depth + 1)
     N.call("hks_factor_level_ms", op.plan.handle, ms.ctypes.data_as(N._DP))
     level_seconds = {lev: float(ms[lev]) * 1e-3 for lev in range(depth + 1)}  # device time per level
-    return Factorization(op, float(lam), bufs, level_seconds)
+    fac = Factorization(op, float(lam), bufs, level_seconds)
+    fac._lease = lease  # the storage returns to the operator's pool with the Factorization
+    return fac
 
 
 def solve_device(f, B):
