@@ -39,51 +39,51 @@ struct GemmOp {
 // Stage the A (64 x 16) and B (16 x 64) tiles of k-block k0 into shared
 // memory as As[m][k], Bs[n][k]; global reads are coalesced along whichever
 // index is contiguous, out-of-range elements are zero-filled.
-template <int TBM>
+template <int TBM, int TBK>
 __device__ __forceinline__ void load_stage(const GemmOp& g, int m0, int n0, int k0, double* As, double* Bs) {
-  constexpr int T = 2 * TBM;  // threads
+  constexpr int T = 2 * TBM, KST = TBK + 4;  // threads, smem row stride
   const int t = threadIdx.x;
   if (!g.transA) {
 #pragma unroll
-    for (int j = 0; j < BK / (T / TBM); ++j) {
+    for (int j = 0; j < TBK / (T / TBM); ++j) {
       const int mi = t % TBM, ki = t / TBM + (T / TBM) * j;
       const int m = m0 + mi, k = k0 + ki;
       const bool ok = m < g.m && k < g.k;
-      cp_async8(As + mi * KS + ki, ok ? g.A + m + (size_t)k * g.lda : g.A, ok);
+      cp_async8(As + mi * KST + ki, ok ? g.A + m + (size_t)k * g.lda : g.A, ok);
     }
   } else {
 #pragma unroll
-    for (int j = 0; j < TBM / (T / 16); ++j) {
-      const int ki = t & 15, mi = (t >> 4) + (T / 16) * j;
+    for (int j = 0; j < TBM / (T / TBK); ++j) {
+      const int ki = t % TBK, mi = t / TBK + (T / TBK) * j;
       const int k = k0 + ki, m = m0 + mi;
       const bool ok = m < g.m && k < g.k;
-      cp_async8(As + mi * KS + ki, ok ? g.A + k + (size_t)m * g.lda : g.A, ok);
+      cp_async8(As + mi * KST + ki, ok ? g.A + k + (size_t)m * g.lda : g.A, ok);
     }
   }
   if (!g.transB) {
 #pragma unroll
-    for (int j = 0; j < BN / (T / 16); ++j) {
-      const int ki = t & 15, ni = (t >> 4) + (T / 16) * j;
+    for (int j = 0; j < BN / (T / TBK); ++j) {
+      const int ki = t % TBK, ni = t / TBK + (T / TBK) * j;
       const int k = k0 + ki, n = n0 + ni;
       const bool ok = n < g.n && k < g.k;
-      cp_async8(Bs + ni * KS + ki, ok ? g.B + k + (size_t)n * g.ldb : g.B, ok);
+      cp_async8(Bs + ni * KST + ki, ok ? g.B + k + (size_t)n * g.ldb : g.B, ok);
     }
   } else {
 #pragma unroll
-    for (int j = 0; j < BK / (T / BN); ++j) {
-      const int ni = t & (BN - 1), ki = (t / BN) + (T / BN) * j;
+    for (int j = 0; j < TBK / (T / BN); ++j) {
+      const int ni = t % BN, ki = t / BN + (T / BN) * j;
       const int n = n0 + ni, k = k0 + ki;
       const bool ok = n < g.n && k < g.k;
-      cp_async8(Bs + ni * KS + ki, ok ? g.B + n + (size_t)k * g.ldb : g.B, ok);
+      cp_async8(Bs + ni * KST + ki, ok ? g.B + n + (size_t)k * g.ldb : g.B, ok);
     }
   }
 }
 
-template <int TBM>
+template <int TBM, int TBK = BK>
 __global__ void __launch_bounds__(2 * TBM) gemm_batched_kernel(const Bases* __restrict__ bases_ptr,
                                                                 const GemmDesc* __restrict__ descs,
                                                                 int tiles_n) {
-  constexpr int BM = TBM;
+  constexpr int BM = TBM, BK = TBK, KS = TBK + 4;
   const Bases& bases = *bases_ptr;
   const GemmDesc gd = descs[blockIdx.y];
   const GemmOp g{at<const double>(bases, gd.A), at<const double>(bases, gd.B), at<double>(bases, gd.C),
@@ -118,14 +118,15 @@ __global__ void __launch_bounds__(2 * TBM) gemm_batched_kernel(const Bases* __re
   const int nk = (g.k + BK - 1) / BK;
 #pragma unroll
   for (int st = 0; st < STAGES - 1; ++st) {
-    if (st < nk) load_stage<TBM>(g, m0, n0, st * BK, As + st * BM * KS, Bs + st * BN * KS);
+    if (st < nk) load_stage<TBM, TBK>(g, m0, n0, st * BK, As + st * BM * KS, Bs + st * BN * KS);
     cp_async_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     const int pf = kt + STAGES - 1;
-    if (pf < nk) load_stage<TBM>(g, m0, n0, pf * BK, As + (pf % STAGES) * BM * KS, Bs + (pf % STAGES) * BN * KS);
+    if (pf < nk)
+      load_stage<TBM, TBK>(g, m0, n0, pf * BK, As + (pf % STAGES) * BM * KS, Bs + (pf % STAGES) * BN * KS);
     cp_async_commit();
     const double* as = As + (kt % STAGES) * BM * KS;
     const double* bs = Bs + (kt % STAGES) * BN * KS;
