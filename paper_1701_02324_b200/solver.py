@@ -165,7 +165,14 @@ class FactorStorage:
             if ev.query():
                 del self.free[idx]
                 return _Lease(self, bufs)
-        return _Lease(self, {b: self.layout.alloc(b) for b in _FACTOR_BUFS})
+        try:
+            return _Lease(self, {b: self.layout.alloc(b) for b in _FACTOR_BUFS})
+        except N.torch().cuda.OutOfMemoryError:
+            if not self.free:
+                raise
+            bufs, ev = self.free.pop(0)  # device memory is the limit: wait for the oldest set instead
+            N.torch().cuda.current_stream().wait_event(ev)
+            return _Lease(self, bufs)
 
     def __del__(self):  # the storage outlives its last estimates
         for _bufs, ev in getattr(self, "free", []):
