@@ -319,7 +319,7 @@ def gpu_arm(args, w, rank, world):
     # configs whose factor storage is a large share of HBM (C4: 67 GB) keep
     # one factorization alive at a time; the others keep the previous one
     # alive across the next step, like an application that compares them
-    lean = run.factor_bytes() * 3 > torch.cuda.mem_get_info()[1]
+    lean = run.factor_bytes() * 3 > 0.9 * torch.cuda.mem_get_info()[0]  # 3 sets: new, previous, pending
 
     clocks = ClockSampler(torch.cuda.current_device())
     if not args.no_clocks:
