@@ -47,6 +47,8 @@ def parse():
     p.add_argument("--cpu-steps", type=int, default=2)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-clocks", action="store_true", help="skip the nvidia-smi clock sampler (diagnostics)")
+    p.add_argument("--knn-trees", type=int, default=0,
+                   help="setup only: approximate kNN from this many random-projection trees (0 = exact)")
     return p.parse_args()
 
 
@@ -169,7 +171,7 @@ class SingleRunner:
     """One GPU: the whole workload through the public API (N=1 line, and
     the replicas fallback)."""
 
-    def __init__(self, w, seed):
+    def __init__(self, w, seed, knn_trees=0):
         import torch
         import paper_1701_02324_b200 as hk
         from paper_1701_02324_b200 import _native as N
@@ -184,7 +186,10 @@ class SingleRunner:
         ps = hk.PointSet(x)
         _, setup["h2d_points"] = timed(ps.device)
         tree, setup["build_tree"] = timed(lambda: hk.build_tree(ps, w.leaf_size, seed=seed))
-        knn, setup["knn"] = timed(lambda: hk.knn_bruteforce(tree.points, w.kappa))
+        if knn_trees:
+            knn, setup["knn"] = timed(lambda: hk.knn_approx(tree.points, w.kappa, trees=knn_trees))
+        else:
+            knn, setup["knn"] = timed(lambda: hk.knn_bruteforce(tree.points, w.kappa))
         skels, setup["skeletonize"] = timed(lambda: hk.build_skeletons(tree, kern, cfg, knn=knn))
         self.op, setup["assemble"] = timed(lambda: hk.build_operator(tree, skels, kern))
         self.setup = {k: round(v, 4) for k, v in setup.items()}
@@ -304,7 +309,7 @@ def gpu_arm(args, w, rank, world):
     from paper_1701_02324_b200 import _native as N
 
     dev = torch.device("cuda", torch.cuda.current_device())
-    run = ShardedRunner(w, world, rank) if world > 1 else SingleRunner(w, 0)
+    run = ShardedRunner(w, world, rank) if world > 1 else SingleRunner(w, 0, args.knn_trees)
     stream = torch.cuda.current_stream()
 
     def step():
@@ -447,6 +452,7 @@ def gpu_arm(args, w, rank, world):
                  f"synthetic: one seeded instance of {world} x {w.n} points (BASELINE.md 4.4), subtree-sharded"),
         "config": {"workload": w.name, "n": w.n, "d": w.d, "leaf": w.leaf_size, "max_rank": w.max_rank,
                    "tau": w.tau, "kappa": w.kappa, "samples": w.samples, "sample_mode": "knn_augmented",
+                   "knn": f"approx ({args.knn_trees} random-projection trees)" if args.knn_trees else "exact",
                    "h": w.h, "lambda": w.lam, "nrhs": w.nrhs,
                    "parallelism": f"subtree-sharded x{world} (NCCL shard-root exchange)" if world > 1 else "single",
                    "n_global": n_total,

@@ -248,6 +248,17 @@ int hks_knn(const double* X, int64_t n, int64_t d, int64_t k, int64_t* out, void
 int hks_knn_rows(const double* X, int64_t n, int64_t d, int64_t k, int64_t q0, int64_t nq, int64_t* out,
                  void* stream);
 
+/* Approximate kNN building blocks (no reference
+ * counterpart): every point of segment [seg_off_host[i], seg_off_host[i+1])
+ * of X against the points of its own segment (a random-projection-tree
+ * leaf), rows by position, ids = perm[position], d^2 beside them
+ * (out_idx / out_d2 n x k); and the per-row union of two (d^2, id)-sorted
+ * lists with duplicates dropped. */
+int hks_knn_segments(const double* X, int64_t n, int64_t d, int64_t k, const int64_t* seg_off_host, int64_t nseg,
+                     const int64_t* perm, int64_t* out_idx, double* out_d2, void* stream);
+int hks_knn_merge(const int64_t* a_idx, const double* a_d2, const int64_t* b_idx, const double* b_d2, int64_t n,
+                  int64_t k, int64_t* out_idx, double* out_d2, void* stream);
+
 /* sample_rows(knn_augmented), skeleton.py:111-121, for every node of one
  * level: mark = per-node bitmap of neighbours outside the node (counts to
  * the host); fill = map the host's top-up draws (ranks into the sorted rest

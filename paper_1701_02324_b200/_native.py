@@ -83,6 +83,8 @@ SIGNATURES = {
     "hks_knn_rows": [_P, _I64, _I64, _I64, _I64, _I64, _P, _P],
     "hks_knn_rows_mark_ex": [_P, _I64, _I64, _I64, _I64, _I64, _I64, _I64, _P, _I64P, _P],
     "hks_bitmap_count": [_P, _I64, _I64, _I64P, _P],
+    "hks_knn_segments": [_P, _I64, _I64, _I64, _I64P, _I64, _P, _P, _P, _P],
+    "hks_knn_merge": [_P, _P, _P, _P, _I64, _I64, _P, _P, _P],
     "hks_cross_sum": [_P, _I64, _P, _I64, _I64, _KP, _P, _P, _I64, _I64, _P, _I64, _D, _P],
     "hks_knn_rows_fill_ex": [_I64, _I64, _I64, _I64, _P, _P, _I64P, _P, _I64P, _P],
 }

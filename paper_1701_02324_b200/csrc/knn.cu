@@ -6,7 +6,9 @@
 // products of a tile are 8x8x4 DMMA fragments staged through shared memory,
 // and each warp keeps the running top-k of 16 queries in registers (lane j =
 // j-th best), inserting with a ballot when a candidate beats the k-th.
+#include <algorithm>
 #include <cfloat>
+#include <vector>
 
 #include "hks_internal.h"
 
@@ -29,14 +31,31 @@ __device__ __forceinline__ bool lex_less(double a, int ia, double b, int ib) {
   return a < b || (a == b && ia < ib);
 }
 
+// One CTA's 64 queries [q0, qend) against the candidates [clo, chi).
+// SEG: per-CTA ranges from `segs` (segmented / approximate kNN: queries of a
+// leaf of a random-projection tree against that leaf), ids mapped through
+// `perm` and d^2 written beside them; else queries [qlo + 64 b, qhi) against
+// all n points (exact kNN).
+struct KnnSeg {
+  int q0, qhi, clo, chi;
+};
+
+template <bool SEG>
 __global__ void __launch_bounds__(KT) knn_kernel(const double* __restrict__ X, const double* __restrict__ sq,
                                                  int n, int d, int kk, int qlo, int qhi,
-                                                 int64_t* __restrict__ out) {
+                                                 int64_t* __restrict__ out, const KnnSeg* __restrict__ segs,
+                                                 const int64_t* __restrict__ perm, double* __restrict__ out_d2) {
   extern __shared__ double smem[];
   double* Qs = smem;                 // QB x DS
   double* Cs = smem + QB * DS;       // CB x DS
   double* Dt = smem + 2 * QB * DS;   // QB x (CB + 1)
-  const int q0 = qlo + blockIdx.x * QB;  // queries [qlo, qhi) against all n points
+  int q0, qend, clo, chi;
+  if (SEG) {
+    const KnnSeg g = segs[blockIdx.x];
+    q0 = g.q0, qend = g.qhi, clo = g.clo, chi = g.chi;
+  } else {
+    q0 = qlo + blockIdx.x * QB, qend = qhi, clo = 0, chi = n;
+  }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int fr = lane >> 2, fc = lane & 3;
   const int wm = (wid >> 1) * 32, wn = (wid & 1) * 32;
@@ -49,16 +68,16 @@ __global__ void __launch_bounds__(KT) knn_kernel(const double* __restrict__ X, c
     lv[i] = DBL_MAX;
     li[i] = 0x7fffffff;
   }
-  auto stage = [&](double* S, int base, int k0, int dc) {
+  auto stage = [&](double* S, int base, int lim, int k0, int dc) {
     for (int e = threadIdx.x; e < 64 * DS; e += KT) {
       const int r = e / DS, k = e % DS;
       const int p = base + r;
-      S[e] = (p < n && k < dc) ? X[(size_t)p * d + k0 + k] : 0.0;
+      S[e] = (p < lim && k < dc) ? X[(size_t)p * d + k0 + k] : 0.0;
     }
   };
-  if (q_resident) stage(Qs, q0, 0, d);
+  if (q_resident) stage(Qs, q0, n, 0, d);
 
-  for (int c0 = 0; c0 < n; c0 += CB) {
+  for (int c0 = clo; c0 < chi; c0 += CB) {
     double acc[4][4][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -67,8 +86,8 @@ __global__ void __launch_bounds__(KT) knn_kernel(const double* __restrict__ X, c
     for (int k0 = 0; k0 < d; k0 += DCH) {
       const int dc = min(DCH, d - k0);
       __syncthreads();
-      if (!q_resident) stage(Qs, q0, k0, dc);
-      stage(Cs, c0, k0, dc);
+      if (!q_resident) stage(Qs, q0, n, k0, dc);
+      stage(Cs, c0, chi, k0, dc);
       __syncthreads();
       for (int kk4 = 0; kk4 < dc; kk4 += 4) {
         double a[4], b[4];
@@ -92,7 +111,7 @@ __global__ void __launch_bounds__(KT) knn_kernel(const double* __restrict__ X, c
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int c = wn + j * 8 + 2 * fc + h;
-          const double sqc = (c0 + c < n) ? sq[c0 + c] : 0.0;
+          const double sqc = (c0 + c < chi) ? sq[c0 + c] : 0.0;
           Dt[r * (CB + 1) + c] = (sqq + sqc) - 2.0 * acc[i][j][h];
         }
     }
@@ -101,7 +120,7 @@ __global__ void __launch_bounds__(KT) knn_kernel(const double* __restrict__ X, c
 #pragma unroll
     for (int qi = 0; qi < 16; ++qi) {
       const int ql = wid * 16 + qi, q = q0 + ql;
-      if (q >= qhi) continue;
+      if (q >= qend) continue;
       double tv = __shfl_sync(0xffffffffu, lv[qi], kk - 1);
       int ti = __shfl_sync(0xffffffffu, li[qi], kk - 1);
       double cv[2];
@@ -112,7 +131,7 @@ __global__ void __launch_bounds__(KT) knn_kernel(const double* __restrict__ X, c
         const int c = lane + 32 * h;
         ci[h] = c0 + c;
         cv[h] = Dt[ql * (CB + 1) + c];
-        const bool ok = ci[h] < n && ci[h] != q && lex_less(cv[h], ci[h], tv, ti);
+        const bool ok = ci[h] < chi && ci[h] != q && lex_less(cv[h], ci[h], tv, ti);
         m[h] = __ballot_sync(0xffffffffu, ok);
       }
 #pragma unroll
@@ -144,7 +163,14 @@ __global__ void __launch_bounds__(KT) knn_kernel(const double* __restrict__ X, c
 #pragma unroll
   for (int qi = 0; qi < 16; ++qi) {
     const int q = q0 + wid * 16 + qi;
-    if (q < qhi && lane < kk) out[(size_t)(q - qlo) * kk + lane] = li[qi];
+    if (q < qend && lane < kk) {
+      if (SEG) {  // rows by position, ids through perm, distances beside them
+        out[(size_t)q * kk + lane] = perm[li[qi]];
+        out_d2[(size_t)q * kk + lane] = lv[qi];
+      } else {
+        out[(size_t)(q - qlo) * kk + lane] = li[qi];
+      }
+    }
   }
 }
 
@@ -167,9 +193,9 @@ extern "C" int hks_knn_rows(const double* X, int64_t n, int64_t d, int64_t k, in
   if (e == cudaSuccess) {
     sqnorm_kernel<<<592, 256, 0, s>>>(X, n, (int)d, sq);
     const size_t sm = (size_t)(2 * QB * DS + QB * (CB + 1)) * sizeof(double);
-    raise_smem_limit(knn_kernel, sm);
-    knn_kernel<<<(unsigned)((nq + QB - 1) / QB), KT, sm, s>>>(X, sq, (int)n, (int)d, (int)k, (int)q0, (int)(q0 + nq),
-                                                             out);
+    raise_smem_limit(knn_kernel<false>, sm);
+    knn_kernel<false><<<(unsigned)((nq + QB - 1) / QB), KT, sm, s>>>(X, sq, (int)n, (int)d, (int)k, (int)q0,
+                                                                    (int)(q0 + nq), out, nullptr, nullptr, nullptr);
     e = cudaGetLastError();
     cudaFreeAsync(sq, s);
   }
@@ -179,4 +205,91 @@ extern "C" int hks_knn_rows(const double* X, int64_t n, int64_t d, int64_t k, in
 
 extern "C" int hks_knn(const double* X, int64_t n, int64_t d, int64_t k, int64_t* out, void* stream) {
   return hks_knn_rows(X, n, d, k, 0, n, out, stream);
+}
+
+// Segmented kNN: every point of segment [seg_off[i], seg_off[i+1]) against
+// the points of its own segment (a leaf of a random-projection tree).
+// Rows of out_idx / out_d2 follow positions in X; ids are perm[position].
+extern "C" int hks_knn_segments(const double* X, int64_t n, int64_t d, int64_t k, const int64_t* seg_off_host,
+                                int64_t nseg, const int64_t* perm, int64_t* out_idx, double* out_d2, void* stream) {
+  if (!X || !seg_off_host || !perm || !out_idx || !out_d2 || n < 2 || d < 1 || k < 1 || nseg < 1 ||
+      seg_off_host[0] != 0 || seg_off_host[nseg] != n)
+    return set_error(HKS_ERR_INVALID, "hks_knn_segments: bad arguments");
+  if (k > 32) return set_error(HKS_ERR_NOT_SUPPORTED, "hks_knn_segments: k <= 32 supported (got %lld)", (long long)k);
+  std::vector<KnnSeg> segs;
+  for (int64_t i = 0; i < nseg; ++i) {
+    const int64_t b = seg_off_host[i], e = seg_off_host[i + 1];
+    if (e - b < k + 1) return set_error(HKS_ERR_INVALID, "hks_knn_segments: segment %lld smaller than k + 1", (long long)i);
+    for (int64_t q = b; q < e; q += QB) segs.push_back(KnnSeg{(int)q, (int)e, (int)b, (int)e});
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* sq = nullptr;
+  KnnSeg* dsegs = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&sq), n * sizeof(double), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&dsegs), segs.size() * sizeof(KnnSeg), s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dsegs, segs.data(), segs.size() * sizeof(KnnSeg), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) {
+    sqnorm_kernel<<<592, 256, 0, s>>>(X, n, (int)d, sq);
+    const size_t sm = (size_t)(2 * QB * DS + QB * (CB + 1)) * sizeof(double);
+    raise_smem_limit(knn_kernel<true>, sm);
+    knn_kernel<true><<<(unsigned)segs.size(), KT, sm, s>>>(X, sq, (int)n, (int)d, (int)k, 0, 0, out_idx, dsegs, perm,
+                                                           out_d2);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // the host descriptors die with this call
+  if (dsegs) cudaFreeAsync(dsegs, s);
+  if (sq) cudaFreeAsync(sq, s);
+  if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_knn_segments: %s", cudaGetErrorString(e));
+  return HKS_OK;
+}
+
+namespace hks {
+namespace {
+// Per query: the union of two (d^2, id)-sorted candidate lists, duplicates
+// dropped, first k kept.
+__global__ void knn_merge_kernel(const int64_t* __restrict__ ai, const double* __restrict__ ad,
+                                 const int64_t* __restrict__ bi, const double* __restrict__ bd, int64_t n, int k,
+                                 int64_t* __restrict__ oi, double* __restrict__ od) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t* a = ai + q * k;
+    const int64_t* b = bi + q * k;
+    const double* da = ad + q * k;
+    const double* db = bd + q * k;
+    int x = 0, y = 0, o = 0;
+    int64_t last = -1;
+    double lastd = -1.0;
+    while (o < k && (x < k || y < k)) {
+      bool take_a;
+      if (x >= k) take_a = false;
+      else if (y >= k) take_a = true;
+      else take_a = da[x] < db[y] || (da[x] == db[y] && a[x] <= b[y]);
+      const int64_t id = take_a ? a[x] : b[y];
+      const double dv = take_a ? da[x] : db[y];
+      if (take_a) ++x; else ++y;
+      if (id == last && dv == lastd) continue;  // the same neighbour found by both lists
+      oi[q * k + o] = id;
+      od[q * k + o] = dv;
+      last = id;
+      lastd = dv;
+      ++o;
+    }
+    for (; o < k; ++o) {  // cannot happen with two full lists of distinct ids; defensive
+      oi[q * k + o] = last;
+      od[q * k + o] = lastd;
+    }
+  }
+}
+}  // namespace
+}  // namespace hks
+
+extern "C" int hks_knn_merge(const int64_t* a_idx, const double* a_d2, const int64_t* b_idx, const double* b_d2,
+                             int64_t n, int64_t k, int64_t* out_idx, double* out_d2, void* stream) {
+  if (!a_idx || !a_d2 || !b_idx || !b_d2 || !out_idx || !out_d2 || n < 1 || k < 1)
+    return set_error(HKS_ERR_INVALID, "hks_knn_merge: bad arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  knn_merge_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, s>>>(a_idx, a_d2, b_idx, b_d2, n,
+                                                                                      (int)k, out_idx, out_d2);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_knn_merge: %s", cudaGetErrorString(e));
+  return HKS_OK;
 }

@@ -250,3 +250,58 @@ def knn_bruteforce(ps, k):
     out = t.empty((n, k), dtype=t.int64, device=x.device)
     N.call("hks_knn", N.ptr(x), n, ps.d, k, N.ptr(out), N.stream_ptr())
     return DeviceArray(out)
+
+
+def knn_approx(ps, k, trees=8, leaf_size=1024, seed=0):
+    """Approximate k nearest neighbours (the
+    reference has only the brute force of tree.py:163-188): the union, over
+    `trees` random-projection trees (the partition of build_tree with random
+    directions and no power steps), of the exact neighbours inside each
+    leaf, merged per point by (GEMM-form d^2, index) with duplicates
+    dropped.  Distances are computed exactly as knn_bruteforce computes
+    them, so every neighbour it returns is ranked as the exact search ranks
+    it.  Work is trees x n x leaf_size pairs instead of n^2.  With one leaf
+    (leaf_size >= n) it is the exact search."""
+    if not isinstance(ps, PointSet):
+        ps = PointSet(ps)
+    n, d = ps.n, ps.d
+    if not 1 <= k <= n - 1:
+        raise ValueError("need 1 <= k <= n - 1")
+    if trees < 1:
+        raise ValueError("trees must be >= 1")
+    t = N.torch()
+    x = ps.device()
+    depth = tree_depth(n, max(int(leaf_size), 2))
+    while depth > 0 and n >> depth < k + 1:  # every leaf must hold k + 1 points
+        depth -= 1
+    begin, end = node_ranges(n, depth)
+    leaves = begin[(1 << depth) - 1:]
+    seg = np.concatenate([leaves, [n]]).astype(np.int64)
+    nint = (1 << depth) - 1
+    best_i = best_d = None
+    for tr in range(trees):
+        rng = np.random.default_rng([int(seed), 101, tr])
+        starts = rng.standard_normal((max(nint, 1), d))
+        starts /= np.linalg.norm(starts, axis=1, keepdims=True)
+        xt = t.empty_like(x)
+        perm = t.empty(n, dtype=t.int64, device=x.device)
+        dirs = t.zeros((max(nint, 1), d), dtype=t.float64, device=x.device)
+        vals = t.zeros(max(nint, 1), dtype=t.float64, device=x.device)
+        N.call("hks_build_tree", N.ptr(x), n, d, depth, 0, N.ptr(N.to_device(starts)), N.ptr(xt), N.ptr(perm),
+               N.ptr(dirs), N.ptr(vals), N.stream_ptr())
+        ip = t.empty((n, k), dtype=t.int64, device=x.device)
+        dp = t.empty((n, k), dtype=t.float64, device=x.device)
+        N.call("hks_knn_segments", N.ptr(xt), n, d, k, seg.ctypes.data_as(N._I64P), len(seg) - 1, N.ptr(perm),
+               N.ptr(ip), N.ptr(dp), N.stream_ptr())
+        ti = t.empty_like(ip)
+        td = t.empty_like(dp)
+        ti[perm] = ip  # rows back to the point set's order
+        td[perm] = dp
+        if best_i is None:
+            best_i, best_d = ti, td
+            continue
+        oi, od = t.empty_like(ti), t.empty_like(td)
+        N.call("hks_knn_merge", N.ptr(best_i), N.ptr(best_d), N.ptr(ti), N.ptr(td), n, k, N.ptr(oi), N.ptr(od),
+               N.stream_ptr())
+        best_i, best_d = oi, od
+    return DeviceArray(best_i)
