@@ -153,9 +153,24 @@ __global__ void __launch_bounds__(QT) qr_wpart(const QrNode* __restrict__ nodes,
   const QrNode q = nodes[c.node];
   double* out = wpart + q.poff + (size_t)(blockIdx.x - q.chunk0) * q.n;
   const int r0 = max(c.r0, k);
+  // v of this chunk staged once; loads batched 8 rows at a time (the sum
+  // itself stays in row order: the same bits as the plain loop)
+  __shared__ double vs[QCH];
+  for (int r = r0 + threadIdx.x; r < c.r1; r += QT) vs[r - c.r0] = q.v[r];
+  __syncthreads();
+  const double* __restrict__ A = q.A;
+  const size_t lda = q.lda;
   for (int j = k + 1 + threadIdx.x; j < q.n; j += QT) {
     double sum = 0.0;
-    for (int r = r0; r < c.r1; ++r) sum = fma(q.v[r], q.A[(size_t)r * q.lda + j], sum);
+    int r = r0;
+    for (; r + 8 <= c.r1; r += 8) {
+      double a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] = A[(size_t)(r + u) * lda + j];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) sum = fma(vs[r + u - c.r0], a[u], sum);
+    }
+    for (; r < c.r1; ++r) sum = fma(vs[r - c.r0], A[(size_t)r * lda + j], sum);
     out[j] = sum;
   }
 }
@@ -169,17 +184,40 @@ __global__ void __launch_bounds__(QT) qr_update(const QrNode* __restrict__ nodes
   const QrNode q = nodes[c.node];
   double* nout = npart + q.poff + (size_t)(blockIdx.x - q.chunk0) * q.n;
   const int r0 = max(c.r0, k);
+  // v staged in shared memory and 8-row batches of loads ahead of their
+  // stores: the compiler can no longer serialise every load behind the
+  // previous store (A and v may alias as far as it knows).  Arithmetic and
+  // its order are unchanged.
+  __shared__ double vs[QCH];
+  if (s.vnz)
+    for (int r = r0 + threadIdx.x; r < c.r1; r += QT) vs[r - c.r0] = q.v[r];
+  __syncthreads();
+  double* __restrict__ A = q.A;
+  const size_t lda = q.lda;
   for (int j = k + 1 + threadIdx.x; j < q.n; j += QT) {
     double w = 0.0;
     if (s.vnz)
       for (int cc = 0; cc < q.nchunk; ++cc) w += wpart[q.poff + (size_t)cc * q.n + j];
     double ns = 0.0;
-    for (int r = r0; r < c.r1; ++r) {
-      double* a = q.A + (size_t)r * q.lda + j;
-      double val = *a;
+    int r = r0;
+    for (; r + 8 <= c.r1; r += 8) {
+      double val[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) val[u] = A[(size_t)(r + u) * lda + j];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (s.vnz) {
+          val[u] -= 2.0 * (vs[r + u - c.r0] * w);  // r[k:, k:] -= 2 outer(v, v @ r[k:, k:])  (linalg.py:100)
+          A[(size_t)(r + u) * lda + j] = val[u];
+        }
+        if (r + u > k) ns = fma(val[u], val[u], ns);
+      }
+    }
+    for (; r < c.r1; ++r) {
+      double val = A[(size_t)r * lda + j];
       if (s.vnz) {
-        val -= 2.0 * (q.v[r] * w);  // r[k:, k:] -= 2 outer(v, v @ r[k:, k:])  (linalg.py:100)
-        *a = val;
+        val -= 2.0 * (vs[r - c.r0] * w);
+        A[(size_t)r * lda + j] = val;
       }
       if (r > k) ns = fma(val, val, ns);
     }
