@@ -42,24 +42,30 @@ __device__ __forceinline__ int64_t row_id(const int64_t* ids, int64_t base, int 
   return ids ? ids[i] : base + i;
 }
 
-// Accumulates the 16 pair terms of one thread: its row `lr` (against 16
-// columns cbase..cbase+15) or its column (against 16 rows), depending on
-// the caller's mapping; stage = shared X tiles for one d-chunk.
+// 4 x 4 register block of pair terms: rows rb + 16u, columns cb + 16v of the
+// staged tiles (u, v < 4), accumulated over k in order with (x_row - x_col)
+// -- the diff-form distance of kernels.py:56-61 per pair, 8 shared-memory
+// loads per 16 pairs.
 template <bool POLY>
-__device__ __forceinline__ void accumulate16(const double* xa, const double* xb16, int xb_stride,
-                                             int dc, double (&acc)[16]) {
+__device__ __forceinline__ void accumulate4x4(const double* Xr, const double* Xc, int xs, int dc, int rb, int cb,
+                                              double (&acc)[4][4]) {
   for (int k = 0; k < dc; ++k) {
-    const double a = xa[k];
+    double a[4], b[4];
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const double b = xb16[q * xb_stride + k];
-      if (POLY) {
-        acc[q] = fma(a, b, acc[q]);
-      } else {
-        const double df = a - b;
-        acc[q] = fma(df, df, acc[q]);
+    for (int u = 0; u < 4; ++u) a[u] = Xr[(rb + 16 * u) * xs + k];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) b[v] = Xc[(cb + 16 * v) * xs + k];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        if (POLY) {
+          acc[u][v] = fma(a[u], b[v], acc[u][v]);
+        } else {
+          const double df = a[u] - b[v];
+          acc[u][v] = fma(df, df, acc[u][v]);
+        }
       }
-    }
   }
 }
 
@@ -103,54 +109,46 @@ __global__ void __launch_bounds__(256) eval_kernel(const double* __restrict__ X,
   double* Xr = stage_area;
   double* Xc = stage_area + TM * XS;
   const int t = threadIdx.x;
-  // ROW_MAJOR: thread owns one column and 16 rows (coalesced row-major store);
-  // else one row and 16 columns (coalesced column-major store)
-  const int own = t & 63, grp = (t >> 6) * 16;
-  double acc[16];
+  // 4 x 4 pairs per thread: rows rb + 16u, columns cb + 16v.  The lanes of a
+  // warp run along the stored index (rows for column-major output, columns
+  // for row-major), so every store of a (u, v) is one coalesced segment.
+  const int rb = ROW_MAJOR ? (t >> 4) : (t & 15), cb = ROW_MAJOR ? (t & 15) : (t >> 4);
+  double acc[4][4];
 #pragma unroll
-  for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
   const bool poly = kp.family == HKS_POLYNOMIAL;
   for (int k0 = 0; k0 < d; k0 += DC) {
     const int dc = min(DC, d - k0);
     stage(X, X, d, erows, e.row0, e.m, r0, ecols, e.col0, e.n, c0, k0, dc, Xr, Xc);
     __syncthreads();
-    const double* mine = ROW_MAJOR ? Xc + own * XS : Xr + own * XS;
-    const double* other = ROW_MAJOR ? Xr + grp * XS : Xc + grp * XS;
-    // keep the subtraction order (x_row - x_col) fixed in both mappings
-    if (poly) {
-      accumulate16<true>(mine, other, XS, dc, acc);
-    } else if (ROW_MAJOR) {
-      for (int k = 0; k < dc; ++k) {
-        const double b = mine[k];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const double df = other[q * XS + k] - b;
-          acc[q] = fma(df, df, acc[q]);
-        }
-      }
-    } else {
-      accumulate16<false>(mine, other, XS, dc, acc);
-    }
+    if (poly)
+      accumulate4x4<true>(Xr, Xc, XS, dc, rb, cb, acc);
+    else
+      accumulate4x4<false>(Xr, Xc, XS, dc, rb, cb, acc);
     __syncthreads();
   }
   const bool mirror = sym && r0 != c0;
   double* Kt = stage_area;  // 64 x 65 tile for the mirrored store (the staging area is free now)
   static_assert(TM * (TN + 1) <= (TM + TN) * XS, "tile must fit the staging area");
 #pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    const int i = ROW_MAJOR ? r0 + grp + q : r0 + own;
-    const int j = ROW_MAJOR ? c0 + own : c0 + grp + q;
-    double v = 0.0;
-    if (i < e.m && j < e.n) {
-      v = kernel_value(kp, acc[q]);
-      if (i == j) v += ediag;
-      if (ROW_MAJOR)
-        eout[(size_t)i * e.ldo + j] = v;
-      else
-        eout[i + (size_t)j * e.ldo] = v;
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int ii = rb + 16 * u, jj = cb + 16 * v;
+      const int i = r0 + ii, j = c0 + jj;
+      double val = 0.0;
+      if (i < e.m && j < e.n) {
+        val = kernel_value(kp, acc[u][v]);
+        if (i == j) val += ediag;
+        if (ROW_MAJOR)
+          eout[(size_t)i * e.ldo + j] = val;
+        else
+          eout[i + (size_t)j * e.ldo] = val;
+      }
+      if (mirror) Kt[jj * (TM + 1) + ii] = val;  // Kt[jj][ii]
     }
-    if (mirror) Kt[(grp + q) * (TM + 1) + own] = v;  // Kt[jj][ii]
-  }
   if (mirror) {  // K[c0 + jj, r0 + ii] = K[r0 + ii, c0 + jj], stored coalesced along jj
     __syncthreads();
     for (int ii = t >> 6; ii < TM; ii += 4) {
@@ -163,7 +161,7 @@ __global__ void __launch_bounds__(256) eval_kernel(const double* __restrict__ X,
 constexpr int KC = 16;  // right-hand sides per pass
 
 // XC: the column points (X itself except in cross sums, hks_cross_sum).
-__global__ void __launch_bounds__(256) ksum_kernel(const double* __restrict__ X, const double* __restrict__ XC,
+__global__ void __launch_bounds__(256, 3) ksum_kernel(const double* __restrict__ X, const double* __restrict__ XC,
                                                    int d, KernelParams kp,
                                                    const Bases* __restrict__ bases_ptr,
                                                    const SumDesc* __restrict__ descs) {
@@ -184,31 +182,36 @@ __global__ void __launch_bounds__(256) ksum_kernel(const double* __restrict__ X,
   double* Kt = stage_area;
   static_assert(TM * (TN + 1) <= (TM + TN) * XS, "kernel tile must fit the staging area");
   const int t = threadIdx.x;
-  const int own = t & 63, grp = (t >> 6) * 16;
+  const int own = t & 63;  // row of the K W product
   const int kq = (t >> 6) * 4;  // 4 right-hand sides per thread in the product
   const bool poly = kp.family == HKS_POLYNOMIAL;
   for (int kb = 0; kb < s.k; kb += KC) {
     const int kc = min(KC, s.k - kb);
     double out[4] = {0.0, 0.0, 0.0, 0.0};
     for (int c0 = 0; c0 < s.n; c0 += TN) {
-      double acc[16];
+      double acc[4][4];
 #pragma unroll
-      for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+      const int rb = t & 15, cb = t >> 4;
       for (int k0 = 0; k0 < d; k0 += DC) {
         const int dc = min(DC, d - k0);
         stage(X, XC, d, srows, s.row0, s.m, r0, scols, s.col0, s.n, c0, k0, dc, Xr, Xc);
         __syncthreads();
         if (poly)
-          accumulate16<true>(Xr + own * XS, Xc + grp * XS, XS, dc, acc);
+          accumulate4x4<true>(Xr, Xc, XS, dc, rb, cb, acc);
         else
-          accumulate16<false>(Xr + own * XS, Xc + grp * XS, XS, dc, acc);
+          accumulate4x4<false>(Xr, Xc, XS, dc, rb, cb, acc);
         __syncthreads();
       }
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const int j = c0 + grp + q;
-        Kt[own * (TN + 1) + grp + q] = (r0 + own < s.m && j < s.n) ? kernel_value(kp, acc[q]) : 0.0;
-      }
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int ii = rb + 16 * u, jj = cb + 16 * v;
+          Kt[ii * (TN + 1) + jj] = (r0 + ii < s.m && c0 + jj < s.n) ? kernel_value(kp, acc[u][v]) : 0.0;
+        }
       for (int e2 = t; e2 < TN * KC; e2 += blockDim.x) {
         const int j = e2 / KC, c = e2 % KC;
         Ws[e2] = (c0 + j < s.n && c < kc) ? sW[(c0 + j) + (size_t)(kb + c) * s.ldw] : 0.0;
