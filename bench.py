@@ -208,14 +208,11 @@ class SingleRunner:
             return solve_device(f, self.B)
         # C5: GMRES on the treecode matvec, preconditioned by the factorization,
         # one right-hand side at a time (krylov.py:155-188)
-        import torch
-        X = torch.empty_like(self.B)
-        self.krylov = []
-        for j in range(self.B.shape[0]):
-            X[j], rep = self.hk.hybrid_solve(self.op, f, self.B[j], tol=self.w.gmres_tol, max_iter=500,
-                                             restart=self.w.gmres_restart)
-            self.krylov.append(rep.iterations)
-        return X
+        from paper_1701_02324_b200.krylov import hybrid_solve_multi
+        X, reps = hybrid_solve_multi(self.op, f, self.B.t(), tol=self.w.gmres_tol, max_iter=500,
+                                     restart=self.w.gmres_restart)  # k GMRES solves, batched operators
+        self.krylov = [r.iterations for r in reps]
+        return X.t()
 
     def relres(self, X):
         import torch
@@ -228,11 +225,11 @@ class SingleRunner:
         if self.w.method == "hybrid":  # hybrid_solve takes tree-ordered host vectors (krylov.py:155-188)
             perm = np.asarray(self.tree.perm)
             bt = self.b[perm]
+            from paper_1701_02324_b200.krylov import hybrid_solve_multi
+            xt, _ = hybrid_solve_multi(self.op, f, bt, tol=self.w.gmres_tol, max_iter=500,
+                                       restart=self.w.gmres_restart)
             x = np.empty_like(self.b)
-            for j in range(self.b.shape[1]):
-                xt, _ = self.hk.hybrid_solve(self.op, f, bt[:, j], tol=self.w.gmres_tol, max_iter=500,
-                                             restart=self.w.gmres_restart)
-                x[perm, j] = xt
+            x[perm] = xt
             return x
         xh = self.hk.solve_multi(f, self.Bh, in_tree_order=False)
         return xh.cpu().numpy() if hasattr(xh, "cpu") else xh

@@ -253,3 +253,156 @@ def hybrid_solve_sharded(op, f, b, tol=1e-8, max_iter=500, restart=50):
 
     x, rep = gmres(apply_a, apply_minv, bd, tol=tol, max_iter=max_iter, restart=restart, comm=op.comm)
     return (x.cpu().numpy() if host else x), rep
+
+
+def gmres_multi(apply_a, apply_minv, B, tol=1e-8, max_iter=500, restart=50):
+    """k independent restarted GMRES solves (krylov.py:40-143, one per
+    column of the (k, n) device block B) run in lockstep, so every operator
+    application is ONE batched call over the columns still iterating:
+    apply_a / apply_minv map an (m, n) block to an (m, n) block.  Each
+    column's recurrence, stopping tests and reports are its own; the
+    batched hmatvec / solve give every column the bits a single-column call
+    gives it (ksum and the DMMA products are column-independent), so each
+    column equals gmres() on that column alone.  Returns (X, [reports])."""
+    if tol <= 0:
+        raise ValueError("tol must be positive")
+    if restart < 1:
+        raise ValueError("restart must be >= 1")
+    t = N.torch()
+    B = B.to(t.float64).contiguous()
+    k, n = B.shape
+    vec = _Vec(n, restart + 2)
+    t0 = time.perf_counter()
+    reps = [KrylovReport() for _ in range(k)]
+    X = t.zeros((k, n), dtype=t.float64, device=B.device)
+    bnorm = [vec.norm(B[c]) for c in range(k)]
+    live = []
+    for c in range(k):
+        if bnorm[c] == 0.0:
+            reps[c].converged = True
+        else:
+            live.append(c)
+
+    def A(cols, V):
+        return apply_a(V.contiguous()) if cols else V
+
+    def M(cols, V):
+        return apply_minv(V.contiguous()) if cols else V
+
+    stop = set()  # columns done (converged, broken down or out of iterations)
+    while True:
+        cols = [c for c in live if c not in stop and reps[c].iterations < max_iter]
+        for c in live:
+            if c not in cols:
+                stop.add(c)
+        if not cols:
+            break
+        R = B[cols] - A(cols, X[cols])
+        st = {}
+        for a, c in enumerate(cols):
+            rnorm = vec.norm(R[a])
+            if rnorm / bnorm[c] <= tol:
+                reps[c].converged = True
+                stop.add(c)
+                continue
+            steps = min(restart, max_iter - reps[c].iterations)
+            V = t.empty((steps + 1, n), dtype=t.float64, device=B.device)
+            V[0] = R[a] / rnorm
+            g = np.zeros(steps + 1)
+            g[0] = rnorm
+            st[c] = dict(V=V, H=np.zeros((steps + 1, steps)), cs=np.empty(steps), sn=np.empty(steps), g=g,
+                         steps=steps, k=0, breakdown=False, done=False,
+                         hcol=t.zeros(steps + 1, dtype=t.float64, device=B.device))
+        while True:  # the Arnoldi steps of this cycle, batched over the columns still in it
+            act = [c for c in st if not st[c]["done"]]
+            if not act:
+                break
+            Vk = t.stack([st[c]["V"][st[c]["k"]] for c in act])
+            W = A(act, M(act, Vk)).clone()  # fresh buffer: no aliasing of the bases
+            for a, c in enumerate(act):
+                s = st[c]
+                kk, V, H, hcol, w = s["k"], s["V"], s["H"], s["hcol"], W[a]
+                win = vec.norm(w)
+                hcol.zero_()
+                for i in range(kk + 1):  # modified Gram-Schmidt (krylov.py:84-86)
+                    vec.dots(V[i:i + 1], 1, w, out=hcol[i:i + 1])
+                    vec.axpys(V[i:i + 1], 1, hcol[i:i + 1], -1.0, w)
+                ov = vec.dots(V, kk + 1, w, out=t.empty(kk + 1, dtype=t.float64, device=B.device))
+                ovh = ov.cpu().numpy()
+                H[: kk + 1, kk] = hcol[: kk + 1].cpu().numpy()
+                if win > 0 and np.max(np.abs(ovh)) > _REORTH_THRESHOLD * win:  # krylov.py:89-92
+                    H[: kk + 1, kk] += ovh
+                    vec.axpys(V, kk + 1, ov, -1.0, w)
+                sub = vec.norm(w)
+                H[kk + 1, kk] = sub
+                cs, sn, g = s["cs"], s["sn"], s["g"]
+                for i in range(kk):  # accumulated Givens rotations (krylov.py:98-101)
+                    hi, hj = H[i, kk], H[i + 1, kk]
+                    H[i, kk] = cs[i] * hi + sn[i] * hj
+                    H[i + 1, kk] = -sn[i] * hi + cs[i] * hj
+                den = np.hypot(H[kk, kk], sub)
+                if den == 0.0:
+                    cs[kk], sn[kk] = 1.0, 0.0
+                else:
+                    cs[kk], sn[kk] = H[kk, kk] / den, sub / den
+                H[kk, kk], H[kk + 1, kk] = den, 0.0
+                g[kk + 1] = -sn[kk] * g[kk]
+                g[kk] = cs[kk] * g[kk]
+                est = abs(g[kk + 1]) / bnorm[c]
+                reps[c].residuals.append(est)
+                reps[c].iterations += 1
+                s["breakdown"] = sub == 0.0
+                if not s["breakdown"]:
+                    V[kk + 1] = w / sub
+                s["k"] = kk + 1
+                if s["breakdown"] or est <= tol or s["k"] >= s["steps"]:
+                    s["done"] = True
+        upd_cols = [c for c in st if st[c]["k"] > 0]
+        if upd_cols:
+            U = t.zeros((len(upd_cols), n), dtype=t.float64, device=B.device)
+            for a, c in enumerate(upd_cols):
+                s = st[c]
+                y = scipy.linalg.solve_triangular(s["H"][: s["k"], : s["k"]], s["g"][: s["k"]])
+                vec.axpys(s["V"], s["k"], N.to_device(y), 1.0, U[a])
+            X[upd_cols] = X[upd_cols] + M(upd_cols, U)
+            Rt = B[upd_cols] - A(upd_cols, X[upd_cols])
+            for a, c in enumerate(upd_cols):
+                true_rel = vec.norm(Rt[a]) / bnorm[c]
+                reps[c].residuals[-1] = true_rel
+                if true_rel <= tol:
+                    reps[c].converged = True
+                    stop.add(c)
+                elif st[c]["breakdown"]:
+                    stop.add(c)
+        for c in st:
+            if c not in stop and reps[c].iterations < max_iter:
+                reps[c].restarts += 1
+    if live:
+        Rf = B[live] - A(live, X[live])
+        for a, c in enumerate(live):
+            reps[c].final_residual = vec.norm(Rf[a]) / bnorm[c]
+    wall = time.perf_counter() - t0
+    for r in reps:
+        r.wall_time = wall
+    return X, reps
+
+
+def hybrid_solve_multi(op, f, B, tol=1e-8, max_iter=500, restart=50):
+    """hybrid_solve (krylov.py:155-188) for an (n, k) block of right-hand
+    sides (tree order, host or device): k GMRES solves in lockstep with
+    batched matvecs / preconditioner solves (gmres_multi).  Returns X of the
+    same kind and shape and one KrylovReport per column; column j equals
+    hybrid_solve(op, f, B[:, j])."""
+    lam = f.lam
+    if op.kernel.regularization != lam:
+        raise ValueError(f"factorization lambda {lam} does not match operator lambda {op.kernel.regularization}")
+    t = N.torch()
+    from .solver import solve_device
+    dev = isinstance(B, t.Tensor) and B.is_cuda
+    Bt = (B.to(t.float64) if dev else N.to_device(np.asarray(B, dtype=np.float64)))
+    if Bt.dim() != 2 or Bt.shape[0] != op.n:
+        raise ValueError(f"expected an ({op.n}, k) right-hand side block")
+    X, reps = gmres_multi(lambda V: treecode.hmatvec_device(op, V, lam), lambda V: solve_device(f, V),
+                          Bt.t().contiguous(), tol=tol, max_iter=max_iter, restart=restart)
+    X = X.t()
+    return (X if dev else X.cpu().numpy()), reps
