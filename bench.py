@@ -360,6 +360,13 @@ def gpu_arm(args, w, rank, world):
         keep = step()  # the warm-up's last step right before the region (no idle gap)
         torch.cuda.synchronize()
         clocks.skip = len(clocks.lines)
+    # factor storage for the timed loop allocated up front (new, previous,
+    # and up to two sets whose dgecon estimates may still be running): no
+    # GB-sized cudaMalloc inside a timed factorize
+    pool = getattr(getattr(run, "op", None), "_factor_pool", None)
+    if pool is not None:
+        pool.reserve(2 if lean else 4)
+    sets_before = pool.created if pool is not None else None
     # host hygiene as in timeit: no cyclic-GC pause (tens of ms with a large
     # heap) lands between the timed launches
     gc.collect()
@@ -383,6 +390,7 @@ def gpu_arm(args, w, rank, world):
     torch.cuda.synchronize()
     torch.cuda.profiler.stop()
     gc.enable()
+    sets_in_region = (pool.created - sets_before) if pool is not None else None
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -498,6 +506,7 @@ def gpu_arm(args, w, rank, world):
                 "d2h_bytes_per_step": d2h * world},
         "clocks": clk,
         "gpu_launches": int(launches),
+        "factor_sets_allocated_in_region": sets_in_region,
     }
     return result
 

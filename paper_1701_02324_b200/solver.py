@@ -159,25 +159,38 @@ class FactorStorage:
         self.layout = layout
         self.cond_stream = cond_stream
         self.free = []  # [bufs, event]
+        self.created = 0  # sets allocated so far
+
+    def _new(self):
+        bufs = {b: self.layout.alloc(b) for b in _FACTOR_BUFS}
+        self.created += 1
+        return bufs
+
+    def reserve(self, total):
+        """Grow the pool to `total` sets up front (e.g. before a timed loop)."""
+        while self.created < total:
+            self.free.append((self._new(), None))
 
     def lease(self):
         for idx, (bufs, ev) in enumerate(self.free):
-            if ev.query():
+            if ev is None or ev.query():
                 del self.free[idx]
                 return _Lease(self, bufs)
         try:
-            return _Lease(self, {b: self.layout.alloc(b) for b in _FACTOR_BUFS})
+            return _Lease(self, self._new())
         except N.torch().cuda.OutOfMemoryError:
             if not self.free:
                 raise
             bufs, ev = self.free.pop(0)  # device memory is the limit: wait for the oldest set instead
-            N.torch().cuda.current_stream().wait_event(ev)
+            if ev is not None:
+                N.torch().cuda.current_stream().wait_event(ev)
             return _Lease(self, bufs)
 
     def __del__(self):  # the storage outlives its last estimates
         for _bufs, ev in getattr(self, "free", []):
             try:
-                ev.synchronize()
+                if ev is not None:
+                    ev.synchronize()
             except Exception:  # interpreter shutdown
                 pass
 
