@@ -182,23 +182,45 @@ __global__ void __launch_bounds__(2 * TBM) gemm_batched_kernel(const Bases* __re
 }
 
 // dst = alpha * op(src) / alpha * I / 0 / dst + alpha * op(src), one descriptor per block.
-__global__ void copy_batched_kernel(const Bases* __restrict__ bases_ptr, const CopyDesc* __restrict__ descs) {
+// 32 x 32 output tiles, 256 threads (8 rows of 32 lanes); a transposed
+// copy goes through a shared tile so both its reads and its writes are
+// coalesced (the leaf level's phi = P^T and the pushes' P^T).
+__global__ void __launch_bounds__(256) copy_batched_kernel(const Bases* __restrict__ bases_ptr,
+                                                           const CopyDesc* __restrict__ descs) {
   const Bases& bases = *bases_ptr;
   const CopyDesc c = descs[blockIdx.y];
   const double* src = (c.mode == 0 || c.mode == 3) ? at<const double>(bases, c.src) : nullptr;
   double* dst = at<double>(bases, c.dst);
-  const int total = c.m * c.n;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-    const int i = e % c.m, j = e / c.m;
-    double v;
-    if (c.mode == 0 || c.mode == 3) {
-      v = c.trans ? src[j + (size_t)i * c.lds] : src[i + (size_t)j * c.lds];
-      v *= c.alpha;
-      if (c.mode == 3) v += dst[i + (size_t)j * c.ldd];
-    } else {
-      v = (c.mode == 1 && i == j) ? c.alpha : 0.0;
+  __shared__ double tile[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int tm = (c.m + 31) / 32, tn = (c.n + 31) / 32;
+  for (int tix = blockIdx.x; tix < tm * tn; tix += gridDim.x) {
+    const int i0 = (tix % tm) * 32, j0 = (tix / tm) * 32;
+    if (c.mode == 0 && c.trans) {  // dst(i, j) = alpha src(j, i): read along j, write along i
+      __syncthreads();
+      for (int ii = ty; ii < 32; ii += 8) {
+        const int i = i0 + ii, j = j0 + tx;
+        tile[ii][tx] = (i < c.m && j < c.n) ? src[j + (size_t)i * c.lds] : 0.0;
+      }
+      __syncthreads();
+      for (int jj = ty; jj < 32; jj += 8) {
+        const int i = i0 + tx, j = j0 + jj;
+        if (i < c.m && j < c.n) dst[i + (size_t)j * c.ldd] = tile[tx][jj] * c.alpha;
+      }
+      continue;
     }
-    dst[i + (size_t)j * c.ldd] = v;
+    for (int jj = ty; jj < 32; jj += 8) {
+      const int i = i0 + tx, j = j0 + jj;
+      if (i >= c.m || j >= c.n) continue;
+      double v;
+      if (c.mode == 0 || c.mode == 3) {
+        v = (c.trans ? src[j + (size_t)i * c.lds] : src[i + (size_t)j * c.lds]) * c.alpha;
+        if (c.mode == 3) v += dst[i + (size_t)j * c.ldd];
+      } else {
+        v = (c.mode == 1 && i == j) ? c.alpha : 0.0;
+      }
+      dst[i + (size_t)j * c.ldd] = v;
+    }
   }
 }
 
@@ -234,7 +256,7 @@ cudaError_t launch_gemm_batched(const Bases* bases, const GemmDesc* d_descs, int
 cudaError_t launch_copy_batched(const Bases* bases, const CopyDesc* d_descs, int count, int max_elems,
                                 cudaStream_t stream) {
   if (count <= 0 || max_elems <= 0) return cudaSuccess;
-  int bx = (max_elems + 255) / 256;
+  int bx = (max_elems + 1023) / 1024;  // ~ one 32 x 32 tile per CTA
   if (bx > 64) bx = 64;
   for (int first = 0; first < count; first += 65535) {
     const int cnt = count - first < 65535 ? count - first : 65535;
