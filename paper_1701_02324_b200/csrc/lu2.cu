@@ -337,13 +337,15 @@ __device__ __forceinline__ void trsm_stage_rows(double* Ts, int tts, const doubl
 // One triangular sweep X := T^-1 X over a k x NC block of right-hand sides
 // already in shared memory (X row-major, ld NC + 4); T is read through the
 // double-buffered 32-row staging area Tbuf (ld tts).  Ends with a barrier.
-// Bx (optional, ld ldb): X comes from / goes back to global memory block by
-// block -- each 32-row block of X is loaded with the T rows of its step
-// (one cp.async group, prefetched while the previous block computes) and
-// stored as soon as it is final, instead of whole-X load / store phases.
+// Bin / Bout (optional, ld ldb): X comes from / goes back to global memory
+// block by block -- each 32-row block of X is loaded (rows through `perm`
+// when given) with the T rows of its step (one cp.async group, prefetched
+// while the previous block computes) and stored as soon as it is final,
+// instead of whole-X load / store phases.
 template <bool UPPER, int NC, int NT = NC>
 __device__ __forceinline__ void trsm_sweep(double* X, double* Tbuf, int tts, const double* T, int ldt, int k,
-                                           int nc, double* Bx = nullptr, int ldb = 0) {
+                                           int nc, const double* Bin = nullptr, double* Bout = nullptr,
+                                           int ldb = 0, const int* perm = nullptr) {
   static_assert(NT == NC || (NC == 32 && NT == 128) || NT == 2 * NC, "warp <-> tile mapping");
   constexpr int NW = NT / 32;
   constexpr int TXS = NC + 4;  // X row stride: == 4 (mod 16), conflict-free DMMA B fragments
@@ -351,15 +353,17 @@ __device__ __forceinline__ void trsm_sweep(double* X, double* Tbuf, int tts, con
   const int nblk = (k + 31) / 32;
   auto stage_x = [&](int blk) {  // rows of X block blk, lanes along a column's rows
     const int xr0 = blk * 32, xnr = min(32, k - xr0);
-    for (int c = wid; c < nc; c += NW)
-      if (lane < xnr) cp_async8(X + (xr0 + lane) * TXS + c, Bx + xr0 + lane + (size_t)c * ldb, true);
+    if (lane < xnr) {
+      const int src = perm ? perm[xr0 + lane] : xr0 + lane;
+      for (int c = wid; c < nc; c += NW) cp_async8(X + (xr0 + lane) * TXS + c, Bin + src + (size_t)c * ldb, true);
+    }
   };
   auto store_x = [&](int blk) {
     const int xr0 = blk * 32, xnr = min(32, k - xr0);
     for (int c = wid; c < nc; c += NW)
-      if (lane < xnr) Bx[xr0 + lane + (size_t)c * ldb] = X[(xr0 + lane) * TXS + c];
+      if (lane < xnr) Bout[xr0 + lane + (size_t)c * ldb] = X[(xr0 + lane) * TXS + c];
   };
-  if (Bx) stage_x(UPPER ? nblk - 1 : 0);
+  if (Bin) stage_x(UPPER ? nblk - 1 : 0);
   trsm_stage_rows<UPPER, NW>(Tbuf, tts, T, ldt, k, UPPER ? nblk - 1 : 0, wid, lane);
   cp_async_commit();
   const int fr = lane >> 2, fc = lane & 3;
@@ -369,9 +373,9 @@ __device__ __forceinline__ void trsm_sweep(double* X, double* Tbuf, int tts, con
     double* Ts = Tbuf + (bb & 1) * 32 * tts;
     cp_async_wait<0>();
     __syncthreads();  // X / this block's rows of T landed; the previous block's solve is complete
-    if (Bx && bb > 0) store_x(UPPER ? b + 1 : b - 1);  // the previous block is final
+    if (Bout && bb > 0) store_x(UPPER ? b + 1 : b - 1);  // the previous block is final
     if (bb + 1 < nblk) {
-      if (Bx) stage_x(UPPER ? b - 1 : b + 1);
+      if (Bin) stage_x(UPPER ? b - 1 : b + 1);
       trsm_stage_rows<UPPER, NW>(Tbuf + ((bb + 1) & 1) * 32 * tts, tts, T, ldt, k, UPPER ? b - 1 : b + 1, wid,
                                  lane);
       cp_async_commit();
@@ -489,7 +493,7 @@ __device__ __forceinline__ void trsm_sweep(double* X, double* Tbuf, int tts, con
     }
   }
   __syncthreads();
-  if (Bx) store_x(UPPER ? 0 : nblk - 1);
+  if (Bout) store_x(UPPER ? 0 : nblk - 1);
 }
 
 template <bool UPPER, int NC, int NT>
@@ -511,7 +515,7 @@ __global__ void __launch_bounds__(NT) trsm_kernel(const Bases* __restrict__ base
   (void)wid;
   // X streams in and out block by block inside the sweep (256-byte coalesced
   // LDGSTS along each column's rows)
-  trsm_sweep<UPPER, NC, NT>(X, Tbuf, tts, T, D.ldt, k, nc, B, D.ldb);
+  trsm_sweep<UPPER, NC, NT>(X, Tbuf, tts, T, D.ldt, k, nc, B, B, D.ldb);
 }
 
 // Whole getrs of a small matrix (n <= kGetrsFusedMax) in one CTA per block of
@@ -535,14 +539,14 @@ __global__ void __launch_bounds__(NT) getrs_fused_kernel(const Bases* __restrict
   double* X = tsm;
   double* Tbuf = tsm + kcap * TXS;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // the whole gathered B in flight at once (measured: better than streaming
+  // it block by block into the latency-bound sweeps)
   for (int i = lane; i < n; i += 32) {
     const int src = perm[i];
     for (int c = wid; c < nc; c += NT / 32) cp_async8(X + i * TXS + c, B + src + (size_t)c * D.ldb, true);
   }
   if (D.lower) trsm_sweep<false, NC, NT>(X, Tbuf, tts, LU, D.lda, n, nc);
-  trsm_sweep<true, NC, NT>(X, Tbuf, tts, LU, D.lda, n, nc);
-  for (int c = wid; c < nc; c += NT / 32)
-    for (int i = lane; i < n; i += 32) B[i + (size_t)c * D.ldb] = X[i * TXS + c];
+  trsm_sweep<true, NC, NT>(X, Tbuf, tts, LU, D.lda, n, nc, nullptr, B, D.ldb);  // stores streamed out
 }
 
 // ||A||_1 (max column abs sum) of each n x n matrix, before factoring.
