@@ -363,10 +363,11 @@ def gpu_arm(args, w, rank, world):
     # factor storage for the timed loop allocated up front (new, previous,
     # and up to two sets whose dgecon estimates may still be running): no
     # GB-sized cudaMalloc inside a timed factorize
-    pool = getattr(getattr(run, "op", None), "_factor_pool", None)
-    if pool is not None:
-        pool.reserve(2 if lean else 4)
-    sets_before = pool.created if pool is not None else None
+    pools = [p for p in ([getattr(run.op, "_factor_pool", None)] + list(getattr(run.op, "_factor_pools", ())))
+             if p is not None]
+    for p in pools:
+        p.reserve(2 if lean else 4)
+    sets_before = sum(p.created for p in pools)
     # host hygiene as in timeit: no cyclic-GC pause (tens of ms with a large
     # heap) lands between the timed launches
     gc.collect()
@@ -390,7 +391,7 @@ def gpu_arm(args, w, rank, world):
     torch.cuda.synchronize()
     torch.cuda.profiler.stop()
     gc.enable()
-    sets_in_region = (pool.created - sets_before) if pool is not None else None
+    sets_in_region = sum(p.created for p in pools) - sets_before
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()

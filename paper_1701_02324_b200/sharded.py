@@ -499,8 +499,12 @@ def factorize_sharded(op, lam, with_cond=True):
     sk, spec, comm, s = op.skeletons, op.spec, op.comm, op.s
     P = comm.world
     ll, tl = sk.local_layout, sk.top_layout
-    lb = {b: ll.alloc(b, min_elems=s * s if b == N.BUF_THETA else 1) for b in _FACTOR_BUFS}
-    tb = {b: tl.alloc(b) for b in _FACTOR_BUFS}
+    if getattr(op, "_factor_pools", None) is None:  # reusable storage (solver.FactorStorage)
+        from .solver import FactorStorage
+        op._factor_pools = (FactorStorage(ll, op.local.cond_stream, {N.BUF_THETA: s * s}),
+                            FactorStorage(tl, op.top.cond_stream))
+    lease_l, lease_t = op._factor_pools[0].lease(), op._factor_pools[1].lease()
+    lb, tb = lease_l.bufs, lease_t.bufs
     bad = ctypes.c_int64(-1)
     rc = N.fn("hks_factorize")(op.local.handle, op.local_buffers(lb), float(lam), int(bool(with_cond)),
                                ctypes.byref(bad), N.stream_ptr())
@@ -529,10 +533,6 @@ def factorize_sharded(op, lam, with_cond=True):
                                ctypes.byref(bad), N.stream_ptr())
     if rc != N.HKS_OK:
         _raise_factor(rc, lambda m: m)
-    if with_cond:
-        for bi in (N.BUF_Z_LU, N.BUF_STATS):
-            lb[bi].record_stream(op.local.cond_stream)
-            tb[bi].record_stream(op.top.cond_stream)
     ms_l = np.zeros(spec.local_depth + 1)
     ms_t = np.zeros(spec.p + 1)
     N.call("hks_factor_level_ms", op.local.handle, ms_l.ctypes.data_as(N._DP))
@@ -540,7 +540,9 @@ def factorize_sharded(op, lam, with_cond=True):
     level_seconds = {lev: float(ms_t[lev]) * 1e-3 for lev in range(spec.p)}
     for ell in range(spec.local_depth + 1):
         level_seconds[spec.p + ell] = float(ms_l[ell]) * 1e-3
-    return ShardedFactorization(op, lam, lb, tb, level_seconds)
+    fac = ShardedFactorization(op, lam, lb, tb, level_seconds)
+    fac._leases = (lease_l, lease_t)  # the storage returns to the operator's pools with the factorization
+    return fac
 
 
 def _exchange_blocks(op, k):

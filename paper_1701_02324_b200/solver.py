@@ -155,14 +155,15 @@ class FactorStorage:
     allocate nothing: a GB-sized cudaMalloc inside a factorize costs tens
     to hundreds of milliseconds (measured)."""
 
-    def __init__(self, layout, cond_stream):
+    def __init__(self, layout, cond_stream, min_elems=None):
         self.layout = layout
         self.cond_stream = cond_stream
+        self.min_elems = min_elems or {}
         self.free = []  # [bufs, event]
         self.created = 0  # sets allocated so far
 
     def _new(self):
-        bufs = {b: self.layout.alloc(b) for b in _FACTOR_BUFS}
+        bufs = {b: self.layout.alloc(b, min_elems=self.min_elems.get(b, 1)) for b in _FACTOR_BUFS}
         self.created += 1
         return bufs
 
