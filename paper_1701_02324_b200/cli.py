@@ -1,7 +1,7 @@
 """``hikersolve``-compatible command line on the GPU path (cli.py of the
 reference).
 
-Subcommands gen / build / matvec / factor / solve / krr / verify take the
+Subcommands gen / build / matvec / factor / solve / krr / bench / verify take the
 reference's flags and config file (``key = value`` lines, ``#`` comments,
 ``lambda`` alias; precedence flags > file > defaults, config.py:17-120) and
 print one JSON report of schema ``hikersolve-report-1`` ({version,
@@ -162,6 +162,13 @@ def build_parser():
             p.add_argument("--out-pred", dest="out_pred")
         p.add_argument("--method", choices=("direct", "hybrid"), default="direct")
         p.add_argument("--operator", choices=("compressed", "dense"), default="compressed")
+    p = sub.add_parser("bench", help="scaling benchmark")
+    p.add_argument("--sizes", default="")
+    p.add_argument("--dense-sizes", dest="dense_sizes", default="")
+    p.add_argument("--shape", default="cube", choices=sorted(set(SHAPE_ALIASES) | set(SHAPES)))
+    p.add_argument("--d", type=int, default=3)
+    p.add_argument("--repeats", type=int, default=5)
+    _flags(p, "build")
     p = sub.add_parser("verify", help="sampled-row error metrics on a standard instance")
     p.add_argument("--n", type=int, required=True)
     p.add_argument("--d", type=int, default=3)
@@ -353,6 +360,61 @@ def cmd_krr(args):
                    sk.max_rank_per_level(tr), errors, kr)
 
 
+def standard_pipeline(cfg):
+    """The GPU stages packaged for metrics.scaling_benchmark (cli.py:465-490
+    of the reference): tree, kNN (knn_augmented only) + skeletons,
+    operator, factorize, solve in tree order."""
+    from . import build_operator, build_skeletons, build_tree, factorize, knn_bruteforce, solve
+    from .metrics import BenchmarkPipeline
+    kernel = cfg.kernel_spec()
+
+    def skeletonize(tr):
+        knn = None
+        if cfg.sample_mode == "knn_augmented":
+            knn = knn_bruteforce(tr.points, min(cfg.knn, tr.n - 1))
+        return build_skeletons(tr, kernel, cfg.skeleton_config(), knn=knn)
+
+    return BenchmarkPipeline(
+        build=lambda ps: build_tree(ps, cfg.leaf, seed=cfg.seed),
+        skeletonize=skeletonize,
+        assemble=lambda tr, sk: build_operator(tr, sk, kernel),
+        factorize=lambda op: factorize(op, cfg.lam),
+        solve=lambda f, b: solve(f, b, in_tree_order=True),
+    )
+
+
+def _sizes(text):
+    return [int(v) for v in text.split(",") if v.strip()]
+
+
+class _BenchConfig:
+    def __init__(self, shape, d, kernel):
+        self.shape, self.d, self.kernel = shape, d, kernel
+
+
+def cmd_bench(args):
+    """Scaling benchmark (cli.py:429-454): phase times per size as
+    `<phase>_n<n>` timings and the fitted exponents as `exponent_<phase>`."""
+    from .metrics import scaling_benchmark
+    cfg = _config(args)
+    sizes, dense_sizes = _sizes(args.sizes), _sizes(args.dense_sizes)
+    if not sizes and not dense_sizes:
+        raise ValueError("bench needs --sizes and/or --dense-sizes")
+    shape = SHAPE_ALIASES.get(args.shape, args.shape)
+    res = scaling_benchmark(sizes, _BenchConfig(shape, args.d, cfg.kernel_spec()), cfg.seed,
+                            pipeline=standard_pipeline(cfg) if sizes else None,
+                            dense_sizes=dense_sizes or None, solve_repeats=args.repeats)
+    timings = {}
+    for phase, values in res["timings"].items():
+        ns = res["dense_sizes"] if phase.startswith("dense") else res["sizes"]
+        timings.update({f"{phase}_n{n}": v for n, v in zip(ns, values)})
+    errors = {f"exponent_{phase}": p for phase, p in res["exponents"].items()}
+    extra = {"sizes": res["sizes"], "shape": shape, "d": args.d}
+    if dense_sizes:
+        extra["dense_sizes"] = dense_sizes
+    return _report(cfg, "bench", extra, timings, errors=errors)
+
+
 VERIFY_DEFAULTS = dict(kernel="gaussian", h=0.3, lam=1e-2, tau=1e-7, sample_mode="exact", max_rank=384)
 
 
@@ -371,7 +433,7 @@ def cmd_verify(args):
 
 
 COMMANDS = {"gen": cmd_gen, "build": cmd_build, "matvec": cmd_matvec, "factor": cmd_factor, "solve": cmd_solve,
-            "krr": cmd_krr, "verify": cmd_verify}
+            "krr": cmd_krr, "bench": cmd_bench, "verify": cmd_verify}
 
 
 def run(argv=None):

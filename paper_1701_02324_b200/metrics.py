@@ -10,6 +10,10 @@ partial sums added in a fixed order.
 
 from __future__ import annotations
 
+import time
+from dataclasses import dataclass
+from typing import Callable
+
 import numpy as np
 
 from . import _native as N
@@ -96,3 +100,107 @@ def sampled_error_report(op, f, b=None, rows=256, seed=0):
         "true_residual": float(nrm(res_true) / nrm(bd[0][Rd])),
         "residual_vs_Ktilde": float(nrm(res_tilde) / nrm(bd[0])),
     }
+
+
+# --------------------------------------------------------------------------
+# Scaling benchmark (oracle.py:147-232 of the reference)
+# --------------------------------------------------------------------------
+
+DENSE_MAX_POINTS = 8192
+
+
+@dataclass(frozen=True)
+class BenchmarkPipeline:
+    """The fast-path stages a scaling benchmark times (oracle.py:147-155):
+    build(PointSet) -> tree, skeletonize(tree) -> skeletons,
+    assemble(tree, skeletons) -> operator, factorize(operator) ->
+    factorization, solve(factorization, b) -> x."""
+
+    build: Callable
+    skeletonize: Callable
+    assemble: Callable
+    factorize: Callable
+    solve: Callable
+
+
+def _median_time(fn, repeats, warmup=False):
+    """Median wall time of `fn` over `repeats` calls (oracle.py:158-167),
+    with the device drained on both sides of every call so asynchronous
+    GPU work is inside the interval it belongs to."""
+    sync = N.torch().cuda.synchronize
+    times, result = [], None
+    if warmup:
+        fn()
+    for _ in range(repeats):
+        sync()
+        t0 = time.perf_counter()
+        result = fn()
+        sync()
+        times.append(time.perf_counter() - t0)
+    return float(np.median(times)), result
+
+
+def fit_exponent(sizes, seconds):
+    """Least-squares slope of log(time) against log(n) (oracle.py:170-174)."""
+    xs = np.log(np.asarray(sizes, dtype=np.float64))
+    ys = np.log(np.asarray(seconds, dtype=np.float64))
+    return float(np.polyfit(xs, ys, 1)[0])
+
+
+def dense_kernel_matrix(kernel, ps, lam):
+    """K(X, X) + lam I as a host array, evaluated on the GPU (oracle.py:27-33;
+    same n <= 8192 limit and message)."""
+    if ps.n > DENSE_MAX_POINTS:
+        raise ValueError(f"dense oracle is limited to n <= {DENSE_MAX_POINTS}")
+    from .kernels import eval_block
+    out = eval_block(kernel, ps.coords, ps.coords)
+    out[np.diag_indices(ps.n)] += lam
+    return out
+
+
+def scaling_benchmark(sizes, cfg, seed, pipeline=None, dense_sizes=None, solve_repeats=5):
+    """Per-phase times of the fast path over `sizes` with log-log exponent
+    fits, plus the dense factor + solve contrast over `dense_sizes`
+    (oracle.py:177-232: same phases, repeat counts, RNG streams and report
+    keys).  `cfg` needs `shape`, `d` and `kernel` (lambda = its
+    regularization); `pipeline` (e.g. cli.standard_pipeline) is required
+    when `sizes` is nonempty."""
+    from . import data
+    from .linalg import factor_dense, solve_dense
+    report = {"sizes": list(map(int, sizes or [])), "timings": {}, "exponents": {}}
+    if sizes:
+        if pipeline is None:
+            raise ValueError("fast-path sizes need an injected pipeline")
+        phases = {"build": [], "skeletonize": [], "assemble": [], "factorize": [], "solve": []}
+        for n in sizes:
+            ps = data.generate(cfg.shape, n, seed, d=cfg.d)
+            t, tree = _median_time(lambda: pipeline.build(ps), 1)
+            phases["build"].append(t)
+            t, skels = _median_time(lambda: pipeline.skeletonize(tree), 1)
+            phases["skeletonize"].append(t)
+            t, op = _median_time(lambda: pipeline.assemble(tree, skels), 1)
+            phases["assemble"].append(t)
+            t, f = _median_time(lambda: pipeline.factorize(op), 3)
+            phases["factorize"].append(t)
+            b = np.random.default_rng([int(seed), 23, int(n)]).standard_normal(n)
+            t, _ = _median_time(lambda: pipeline.solve(f, b), solve_repeats, warmup=True)
+            phases["solve"].append(t)
+        report["timings"] = {k: list(map(float, v)) for k, v in phases.items()}
+        report["exponents"] = {k: fit_exponent(sizes, v) for k, v in phases.items()}
+    if dense_sizes:
+        dense = {"dense_assemble": [], "dense_factor": [], "dense_solve": []}
+        lam = cfg.kernel.regularization
+        for n in dense_sizes:
+            ps = data.generate(cfg.shape, n, seed, d=cfg.d)
+            b = np.random.default_rng([int(seed), 29, int(n)]).standard_normal(n)
+            t, a = _median_time(lambda: dense_kernel_matrix(cfg.kernel, ps, lam), solve_repeats)
+            dense["dense_assemble"].append(t)
+            t, fd = _median_time(lambda: factor_dense(a), solve_repeats)
+            dense["dense_factor"].append(t)
+            t, _ = _median_time(lambda: solve_dense(fd, b), solve_repeats)
+            dense["dense_solve"].append(t)
+        report["dense_sizes"] = list(map(int, dense_sizes))
+        for key, values in dense.items():
+            report["timings"][key] = list(map(float, values))
+            report["exponents"][key] = fit_exponent(dense_sizes, values)
+    return report

@@ -86,3 +86,18 @@ def test_gen_report_and_error_convention(tmp_path, capsys):
     with pytest.raises(SystemExit) as e:
         cli.run(["solve", "--points", "x"])  # --rhs missing: parser error, same convention
     assert e.value.code == 1
+
+
+def test_bench_host_checks(capsys):
+    """bench's argument errors (cli.py:429-434) and the scaling benchmark's
+    host logic (oracle.py:170-187), no GPU work."""
+    from paper_1701_02324_b200 import metrics
+    assert cli.run(["bench"]) == 1
+    assert "bench needs --sizes and/or --dense-sizes" in capsys.readouterr().err
+    with pytest.raises(ValueError, match="injected pipeline"):
+        metrics.scaling_benchmark([128], None, 0, pipeline=None)
+    assert metrics.scaling_benchmark([], None, 0) == {"sizes": [], "timings": {}, "exponents": {}}
+    n = np.array([128, 256, 512, 1024])
+    assert metrics.fit_exponent(n, 3e-6 * n ** 1.5) == pytest.approx(1.5)
+    with pytest.raises(ValueError, match="limited to n <= 8192"):
+        metrics.dense_kernel_matrix(None, PointSet(np.zeros((8193, 1))), 1.0)

@@ -73,3 +73,27 @@ def test_cli_verify(capsys):
     assert e["sampled_residual_vs_Ktilde"] < 1e-6  # oracle/hks_oracle.py on this instance: 1.36e-7
     assert e["sampled_matvec_relerr_vs_K"] < 1e-3  # exact sampling, tau 1e-7: Ktilde is close to K
     assert rep["config_echo"]["sample_mode"] == "exact"
+
+
+def test_cli_bench(capsys):
+    """The scaling benchmark through the GPU pipeline (test_cli.py:168-178 of
+    the reference): per-size phase timings and fitted exponents, dense
+    contrast included."""
+    rep = _run(capsys, "bench", "--sizes", "128,256", "--dense-sizes", "64,128", "--leaf", "32", "--max-rank", "16",
+               "--samples", "32", "--repeats", "2", "--threads", "1")
+    assert "exponent_factorize" in rep["errors"] and "exponent_dense_factor" in rep["errors"]
+    assert "factorize_n256" in rep["timings"] and "dense_solve_n128" in rep["timings"]
+    assert rep["config_echo"]["sizes"] == [128, 256] and rep["config_echo"]["dense_sizes"] == [64, 128]
+    assert all(v > 0 for v in rep["timings"].values())
+
+
+def test_scaling_benchmark_dense_matches_oracle():
+    """dense_kernel_matrix on the GPU equals the oracle's dense K + lam I."""
+    from paper_1701_02324_b200 import metrics
+    from paper_1701_02324_b200.data import generate
+    from paper_1701_02324_b200.kernels import KernelSpec
+    ps = generate("uniform_cube", 300, 5, d=3)
+    k = KernelSpec("gaussian", h=0.4, regularization=0.1)
+    A = metrics.dense_kernel_matrix(k, ps, 0.1)
+    ref = O.kernel_block("gaussian", ps.coords, ps.coords, h=0.4) + 0.1 * np.eye(300)
+    np.testing.assert_allclose(A, ref, rtol=1e-13, atol=1e-15)
