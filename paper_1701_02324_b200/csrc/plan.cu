@@ -787,16 +787,12 @@ void add_theta_hat(Copies& cp, const Ctx& c, int64_t i, Ref Y) {
   cp.fill(adv(Y, rl), R, rr, rl, false);
 }
 
-// dgecon scratch of the split estimate: the largest level's matrices x
-// gecon_stride(R) doubles (the levels run in order on the condition stream)
+// dgecon scratch of the split estimate: every internal node x
+// gecon_stride(max R) doubles (levels are batched into groups, below)
 size_t cond_scratch_elems(const hks_plan& P) {
-  size_t need = 0;
-  for (int64_t lev = 0; lev < P.L.depth; ++lev) {
-    int maxR = 0;
-    for (int64_t i = P.L.first(lev); i < P.L.first(lev) + P.L.count(lev); ++i) maxR = std::max<int>(maxR, (int)P.R(i));
-    need = std::max(need, (size_t)P.L.count(lev) * gecon_stride(maxR));
-  }
-  return need;
+  int maxR = 0;
+  for (int64_t i = 0; i < P.L.first(P.L.depth); ++i) maxR = std::max<int>(maxR, (int)P.R(i));
+  return (size_t)std::max<int64_t>(P.L.first(P.L.depth), 1) * gecon_stride(maxR);
 }
 
 size_t factorize_workspace(const hks_plan& P) {
@@ -819,7 +815,21 @@ size_t factorize_workspace(const hks_plan& P) {
 int64_t cond_start_level() {
   static const int64_t v = [] {
     const char* e = getenv("HKS_COND_START_LEVEL");
-    return e ? (int64_t)atoi(e) : (int64_t)4;
+    return e ? (int64_t)atoi(e) : (int64_t)3;
+  }();
+  return v;
+}
+
+// Levels batched per estimate group: the estimate is a chain of
+// kGeconSteps + 1 short launches whose length does not depend on the
+// number of matrices, so one chain for all levels deeper than the start
+// level and one for the levels above it (after the root) replaces one
+// chain per level on the serial condition stream (HKS_COND_GROUPS=0: one
+// group per level).
+bool cond_grouped() {
+  static const bool v = [] {
+    const char* e = getenv("HKS_COND_GROUPS");
+    return !(e && atoi(e) == 0);
   }();
   return v;
 }
@@ -855,6 +865,9 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl,
     gm.flush(sl);
   }
   bool push_pending = false;
+  std::vector<LuDesc> cond_group;  // estimates not yet emitted (see cond_grouped)
+  int cond_maxR = 0;
+  double cond_lb = 0;
   for (int64_t lev = L.depth - 1; lev >= 0; --lev) {  // internal levels (solver.py:139-161)
     sl.mark();
     if (push_pending) {
@@ -919,19 +932,25 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl,
     if (with_cond) sl.join();
     add_lu_program(sl, jobs, false);
     if (with_cond && cond_levels) {
-      double lb = 0;
-      for (auto& d : lu) lb += 16.0 * d.n * d.n;
-      cond_levels->emplace_back(new StepList());
-      // split estimate: short-lived CTAs turn the SMs over to the
-      // factorization's kernels between LU applications (lu.cu)
-      for (int ph = 0; ph <= kGeconSteps; ++ph)
-        cond_levels->back()->add(ST_GECON, lu, maxR, 1 + ph, ph ? 2.0 * lb / 16.0 : 0.0, ph ? lb / 2.0 : 0.0);
-      // level_ev recorded when this level is done -- or, for the wide deep
-      // levels, when the factorization reaches the narrow top levels
-      // (cond_start_level): the estimates then fill SMs the latency-bound
-      // top levels leave idle instead of competing with wide levels
-      const int64_t start = std::min<int64_t>(lev, cond_start_level());
-      cond_wait->push_back((int)(L.depth - start + 1));
+      for (auto& d : lu) cond_lb += 16.0 * d.n * d.n;
+      cond_group.insert(cond_group.end(), lu.begin(), lu.end());
+      cond_maxR = std::max(cond_maxR, maxR);
+      // the estimates of levels deeper than cond_start_level wait until the
+      // factorization reaches it: they then fill SMs the latency-bound top
+      // levels leave idle instead of competing with the wide levels
+      const int64_t start = cond_start_level();
+      if (!cond_grouped() || lev == 0 || lev == start) {
+        cond_levels->emplace_back(new StepList());
+        // split estimate: short-lived CTAs turn the SMs over to the
+        // factorization's kernels between LU applications (lu.cu)
+        for (int ph = 0; ph <= kGeconSteps; ++ph)
+          cond_levels->back()->add(ST_GECON, cond_group, cond_maxR, 1 + ph, ph ? 2.0 * cond_lb / 16.0 : 0.0,
+                                   ph ? cond_lb / 2.0 : 0.0);
+        cond_wait->push_back((int)(L.depth - std::min<int64_t>(lev, start) + 1));
+        cond_group.clear();
+        cond_maxR = 0;
+        cond_lb = 0;
+      }
     }
     if (lev == 0 && !L.has_up(0)) continue;
     g_f.flush(sl);
