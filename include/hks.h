@@ -291,6 +291,11 @@ int hks_skeletonize_level(const double* X, int64_t d, const hks_kernel* kern, in
                           double* interp_buf, const int64_t* interp_off, int64_t* ranks_host,
                           void* stream);
 
+/* hks_skeletonize_level keeps its stream-ordered workspace in the device's
+ * default memory pool from level to level; this returns it (after the last
+ * level; skeleton.py's build_skeletons calls it once). */
+int hks_skeleton_workspace_release(void* stream);
+
 /* ----- instrumentation ----------------------------------------------------------
  * hks_profile(1, ...) resets and starts per-kind CUDA-event timing of every
  * plan step; hks_profile(0, out) stops; out[kind * 4 + {launches, ms, flops,

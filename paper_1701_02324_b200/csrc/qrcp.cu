@@ -324,6 +324,22 @@ cudaError_t run_qrcp(std::vector<QrNode>& nodes, double tau, const std::vector<d
 
 using namespace hks;
 
+// Return the skeletonization workspace kept in the default pool (above).
+extern "C" int hks_skeleton_workspace_release(void* stream) {
+  int dev = 0;
+  cudaMemPool_t pool;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+  if (e == cudaSuccess) e = cudaDeviceGetDefaultMemPool(&pool, dev);
+  if (e == cudaSuccess) {
+    uint64_t keep = 0;
+    e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    if (e == cudaSuccess) e = cudaMemPoolTrimTo(pool, 0);
+  }
+  if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_skeleton_workspace_release: %s", cudaGetErrorString(e));
+  return HKS_OK;
+}
+
 // interpolative_decomposition / pivoted_qr (linalg.py:43-136) on one matrix.
 extern "C" int hks_interp_decomp(double* A, int64_t m, int64_t n, int64_t lda, double tol, int64_t max_rank,
                                  int64_t* pivots, double* interp, int64_t* rank_host, void* stream) {
@@ -356,6 +372,18 @@ extern "C" int hks_skeletonize_level(const double* X, int64_t d, const hks_kerne
     return set_error(HKS_ERR_INVALID, "hks_skeletonize_level: bad arguments");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const KernelParams kp = make_kernel_params(kern);
+  // The stream-ordered workspace stays in the device's default pool between
+  // levels (its release threshold would otherwise unmap GBs at every
+  // synchronisation and map them again at the next level);
+  // hks_skeleton_workspace_release() returns it once the skeletons are built.
+  {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   // batches of nodes whose sampled blocks fit a workspace budget
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);

@@ -367,6 +367,7 @@ def build_skeletons_sharded(tree, kernel, config, knn_local, spec, comm):
         cands, coff = _candidates(top_skel, top, top_ranks, ids, x.device)
         top_ranks[ids] = _skeletonize(x, tree.d, kern, level, int(ids[0]), rows, roff, cands, coff, config,
                                       top_skel, top_interp, top, ids)
+    N.call("hks_skeleton_workspace_release", N.stream_ptr())
     local_skel = skel - spec.begin  # the subtree plan evaluates on the shard's own points
     return ShardedSkeletons(spec, config, lay, interp, local_skel, skel, ranks, top, top_interp, top_skel,
                             top_ranks)

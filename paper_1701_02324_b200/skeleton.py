@@ -271,6 +271,7 @@ def build_skeletons(tree, kernel, config=None, knn=None, threads=1):
             raise RuntimeError(f"skeletonization failed at node {node} (level {level})") from \
                 N.HksError(rc, msg)
         ranks[first:first + count] = out_ranks
+    N.call("hks_skeleton_workspace_release", N.stream_ptr())
     return SkeletonSet(tree, config, lay, interp, skel, ranks, rows_count)
 
 
@@ -279,4 +280,5 @@ N.SIGNATURES.update({
     "hks_knn_rows_fill": [N._I64, N._I64, N._I64, N._P, N._P, N._I64P, N._P, N._I64P, N._P],
     "hks_skeletonize_level": [N._P, N._I64, N._KP, N._I64, N._I64, N._P, N._I64P, N._P, N._I64P,
                               N._D, N._I64, N._P, N._I64P, N._P, N._I64P, N._I64P, N._P],
+    "hks_skeleton_workspace_release": [N._P],
 })
