@@ -346,7 +346,7 @@ template <bool UPPER, int NC, int NT = NC>
 __device__ __forceinline__ void trsm_sweep(double* X, double* Tbuf, int tts, const double* T, int ldt, int k,
                                            int nc, const double* Bin = nullptr, double* Bout = nullptr,
                                            int ldb = 0, const int* perm = nullptr) {
-  static_assert(NT == NC || (NC == 32 && NT == 128) || NT == 2 * NC, "warp <-> tile mapping");
+  static_assert(NT == NC || (NC == 32 && (NT == 128 || NT == 256)) || NT == 2 * NC, "warp <-> tile mapping");
   constexpr int NW = NT / 32;
   constexpr int TXS = NC + 4;  // X row stride: == 4 (mod 16), conflict-free DMMA B fragments
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -414,26 +414,35 @@ __device__ __forceinline__ void trsm_sweep(double* X, double* Tbuf, int tts, con
             }
       }
     } else if (NT != NC) {  // 4 warps on one 32-column tile: warp w owns rows 8w .. 8w+7
-      if (uhi > ulo) {
-        double acc[4][2];
+      // (8 warps: warps 4..7 take the second half of the solved rows u and
+      // subtract their partial sums after warps 0..3, a fixed order)
+      constexpr int KSPLIT = NW / 4;
+      const int part = wid / 4, rw = wid % 4;
+      const int kh = KSPLIT == 1 ? uhi : ulo + ((uhi - ulo) / 8) * 4;
+      const int klo2 = part == 0 ? ulo : kh, khi2 = part == 0 ? kh : uhi;
+      double acc[4][2];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
-        for (int kk = ulo; kk < uhi; kk += 4) {
-          const int kq = kk + fc;
-          const bool kin = kq < uhi;
-          const double a = kin ? Ts[(wid * 8 + fr) * tts + kq] : 0.0;
-          double bv[4];
+      for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
+      for (int kk = klo2; kk < khi2; kk += 4) {
+        const int kq = kk + fc;
+        const bool kin = kq < khi2;
+        const double a = kin ? Ts[(rw * 8 + fr) * tts + kq] : 0.0;
+        double bv[4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) bv[j] = kin ? X[kq * TXS + j * 8 + fr] : 0.0;
+        for (int j = 0; j < 4; ++j) bv[j] = kin ? X[kq * TXS + j * 8 + fr] : 0.0;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) dmma884(acc[j][0], acc[j][1], a, bv[j]);
-        }
-        const int rr = wid * 8 + fr;
+        for (int j = 0; j < 4; ++j) dmma884(acc[j][0], acc[j][1], a, bv[j]);
+      }
+      const int rr = rw * 8 + fr;
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+      for (int p = 0; p < KSPLIT; ++p) {
+        if (p > 0) __syncthreads();  // uniform: KSPLIT is a compile-time constant
+        if (part == p && khi2 > klo2)
 #pragma unroll
-          for (int h = 0; h < 2; ++h)
-            if (rr < nr) X[(r0 + rr) * TXS + j * 8 + 2 * fc + h] -= acc[j][h];
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              if (rr < nr) X[(r0 + rr) * TXS + j * 8 + 2 * fc + h] -= acc[j][h];
       }
     } else if (uhi > ulo && wid * 32 < nc) {
       const int cb = wid * 32;  // this warp's 32 columns
@@ -687,10 +696,17 @@ cudaError_t launch_getrs_fused(const Bases* b, const GetrsDesc* d, int count, in
   constexpr int NC = 32;
   const int kcap = (max_n + 31) / 32 * 32, tts = kcap + 4;
   const size_t sm = (size_t)(kcap * (NC + 4) + 2 * 32 * tts) * sizeof(double);
-  raise_smem_limit(getrs_fused_kernel<NC, 128>, sm);
+  // few matrices (the solve's top levels): 8 warps, the sweeps' updates
+  // split over the solved rows
+  const bool wide = (long long)count * ((max_cols + NC - 1) / NC) < 96 && getenv("HKS_GETRS_NT128") == nullptr;
+  if (wide) raise_smem_limit(getrs_fused_kernel<NC, 256>, sm);
+  else raise_smem_limit(getrs_fused_kernel<NC, 128>, sm);
   for (int first = 0; first < count; first += 65535) {
     const int cnt = count - first < 65535 ? count - first : 65535;
-    getrs_fused_kernel<NC, 128><<<dim3((max_cols + NC - 1) / NC, cnt), 128, sm, s>>>(b, d + first, kcap, tts);
+    if (wide)
+      getrs_fused_kernel<NC, 256><<<dim3((max_cols + NC - 1) / NC, cnt), 256, sm, s>>>(b, d + first, kcap, tts);
+    else
+      getrs_fused_kernel<NC, 128><<<dim3((max_cols + NC - 1) / NC, cnt), 128, sm, s>>>(b, d + first, kcap, tts);
   }
   return cudaGetLastError();
 }
