@@ -186,6 +186,7 @@ constexpr int kGetrsFusedMax = 256;
 struct GetrsDesc {
   Ref LU, perm, B;
   int n, lda, ldb, ncols, lower, pad;
+  Ref Bin;  // right-hand sides read from here (ld ldb) when not kNull, else from B
 };
 
 // Row gather A[i, c] := A[perm[i], c] for rows [r0, r1) and columns [c0, c1)

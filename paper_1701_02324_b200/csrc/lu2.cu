@@ -544,6 +544,7 @@ __global__ void __launch_bounds__(NT) getrs_fused_kernel(const Bases* __restrict
   const double* LU = at<const double>(bases, D.LU);
   const int* perm = at<const int>(bases, D.perm);
   double* B = at<double>(bases, D.B) + (size_t)c0 * D.ldb;
+  const double* Bin = D.Bin != kNull ? at<const double>(bases, D.Bin) + (size_t)c0 * D.ldb : B;
   extern __shared__ double tsm[];
   double* X = tsm;
   double* Tbuf = tsm + kcap * TXS;
@@ -552,7 +553,7 @@ __global__ void __launch_bounds__(NT) getrs_fused_kernel(const Bases* __restrict
   // it block by block into the latency-bound sweeps)
   for (int i = lane; i < n; i += 32) {
     const int src = perm[i];
-    for (int c = wid; c < nc; c += NT / 32) cp_async8(X + i * TXS + c, B + src + (size_t)c * D.ldb, true);
+    for (int c = wid; c < nc; c += NT / 32) cp_async8(X + i * TXS + c, Bin + src + (size_t)c * D.ldb, true);
   }
   if (D.lower) trsm_sweep<false, NC, NT>(X, Tbuf, tts, LU, D.lda, n, nc);
   trsm_sweep<true, NC, NT>(X, Tbuf, tts, LU, D.lda, n, nc, nullptr, B, D.ldb);  // stores streamed out

@@ -427,6 +427,7 @@ struct LuJob {
   int r, ldb;
   Ref ws = kNull;  // int32 [total perm | panel perm | group perm], `cap` ints each (kNull: swap sweeps)
   int cap = 0;
+  Ref Bsrc = kNull;  // add_lu_solve_program: right-hand sides read from here (ld ldb), B := A^-1 Bsrc
 };
 
 // Row permutations replace interchange sweeps for matrices up to this size
@@ -732,7 +733,7 @@ void add_lu_solve_program(StepList& sl, const std::vector<LuJob>& jobs) {
     double f = 0, bytes = 0;
     for (auto& j : jobs) {
       if (j.r <= 0 || j.n <= 0) continue;
-      v.push_back(GetrsDesc{j.A, j.ws, j.B, j.n, j.lda, j.ldb, j.r, 1, 0});
+      v.push_back(GetrsDesc{j.A, j.ws, j.B, j.n, j.lda, j.ldb, j.r, 1, 0, j.Bsrc});
       mc = std::max(mc, j.r);
       f += 2.0 * j.n * j.n * (double)j.r;
       bytes += 8.0 * ((double)j.n * j.n + 2.0 * j.n * j.r);
@@ -740,6 +741,10 @@ void add_lu_solve_program(StepList& sl, const std::vector<LuJob>& jobs) {
     sl.add(ST_GETRS_FUSED, v, nmax, mc, f, bytes);
     return;
   }
+  Copies cs;  // separate sources: B := Bsrc first
+  for (auto& j : jobs)
+    if (j.r > 0 && j.Bsrc != kNull) cs.copy(j.Bsrc, j.ldb, 0, j.B, j.ldb, j.n, j.r);
+  cs.flush(sl);
   Swaps sw;
   Gathers ga;
   for (auto& j : jobs) {
@@ -1032,8 +1037,10 @@ void build_solve(const hks_plan& P, int64_t kk, int part, StepList& sl) {
         const int rl = c.r(a), rr = c.r(bb), R = rl + rr, r = c.r(i);
         const Ref Si = c.block(B_VWS, S, i, k), Gi = c.block(B_VWS, G, i, k), Gbi = c.block(B_VWS, Gb, i, k);
         const Ref C = c.coup(i);
-        cp.copy(Si, R, 0, Gi, R, R, k);
-        jobs.push_back(LuJob{c.z_lu(i), R, R, c.z_piv(i), kNull, kNull, Gi, k, R, c.z_ws(i), (int)L.ccap[i]});
+        // G = Z^-1 S (solver.py:222-226), S kept for the update below
+        LuJob zj{c.z_lu(i), R, R, c.z_piv(i), kNull, kNull, Gi, k, R, c.z_ws(i), (int)L.ccap[i]};
+        zj.Bsrc = Si;
+        jobs.push_back(zj);
         g1.add(C, rl, 0, adv(Gi, rl), R, 0, Gbi, R, rl, k, rr, 1.0, 0.0);
         g1.add(C, rl, 1, Gi, R, 0, adv(Gbi, rl), R, rr, k, rl, 1.0, 0.0);
         if (!L.has_up(i)) continue;
