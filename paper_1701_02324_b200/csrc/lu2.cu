@@ -564,8 +564,8 @@ __global__ void __launch_bounds__(NT) getrs_fused_kernel(const Bases* __restrict
 __global__ void norm1_kernel(const Bases* __restrict__ bases_ptr, const LuDesc* __restrict__ descs) {
   const Bases& bases = *bases_ptr;
   const LuDesc L = descs[blockIdx.x];
-  __shared__ double rv[8];
-  __shared__ int ri[8];
+  __shared__ double rv[32];
+  __shared__ int ri[32];
   const double* A = at<const double>(bases, L.A);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double best = 0.0;
@@ -714,7 +714,9 @@ cudaError_t launch_getrs_fused(const Bases* b, const GetrsDesc* d, int count, in
 
 cudaError_t launch_norm1_batched(const Bases* b, const LuDesc* d, int count, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
-  norm1_kernel<<<count, 256, 0, s>>>(b, d);
+  // few matrices (the top levels, where the norm gates the level's LU):
+  // 32 warps per matrix; the column sums and their max do not depend on it
+  norm1_kernel<<<count, count < 148 ? 1024 : 256, 0, s>>>(b, d);
   return cudaGetLastError();
 }
 
