@@ -627,7 +627,9 @@ cudaError_t launch_panel_batched(const Bases* b, const PanelDesc* d, int count, 
 cudaError_t launch_gather_batched(const Bases* b, const GatherDesc* d, int count, int max_rows, int max_cols,
                                   cudaStream_t s) {
   if (count <= 0 || max_rows <= 0 || max_cols <= 0) return cudaSuccess;
-  const int cb = 64;  // columns per CTA: one perm scan per 64 columns
+  // columns per CTA: one perm scan per 64 columns; narrow batches (the top
+  // levels) take one staged chunk per CTA instead of a chain of 8
+  const int cb = (long long)count * ((max_cols + 63) / 64) < 148 ? GS : 64;
   const size_t sm = (size_t)max_rows * GS * sizeof(double) + 2 * (size_t)max_rows * sizeof(int);
   raise_smem_limit(gather_rows_kernel, sm);
   for (int first = 0; first < count; first += 65535) {
