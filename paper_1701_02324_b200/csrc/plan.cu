@@ -843,6 +843,29 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl,
                      std::vector<std::unique_ptr<StepList>>* cond_levels, std::vector<int>* cond_wait) {
   const Ctx c(P);
   const Layout& L = P.L;
+  // What the narrow top levels need that depends on no factor -- Z := I and
+  // push := P^T (solver.py:145, 158) -- in one side branch beside the leaf
+  // level (joined before the first internal level): two fewer launches in
+  // each latency-bound level.  Wide levels keep them in-level (their bytes
+  // would compete with the leaf level's).
+  bool early_pending = false;
+  const int64_t early_levels = std::min<int64_t>(L.depth, 6);  // levels 0..5: <= 32 nodes
+  auto early_node = [&](int64_t i) { return i < L.first(early_levels); };
+  {
+    Copies early;
+    for (int64_t i = 0; i < L.first(early_levels); ++i) {
+      const int R = c.r(2 * i + 1) + c.r(2 * i + 2), r = c.r(i);
+      early.fill(c.z_lu(i), R, R, R, true);
+      if (L.has_up(i)) early.copy(c.interp(i), r, 1, c.push(i), R, R, r);
+    }
+    if (!early.v.empty()) {
+      sl.fork();
+      sl.side(true);
+      early.flush(sl);
+      sl.side(false);
+      early_pending = true;
+    }
+  }
   sl.mark();
   if (L.mode != PM_TOP) {  // leaf level (solver.py:128-137): A = K + lam I, LU with P^T carried -> phi, theta = P phi
     std::vector<EvalDesc> ev;
@@ -875,9 +898,9 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl,
   double cond_lb = 0;
   for (int64_t lev = L.depth - 1; lev >= 0; --lev) {  // internal levels (solver.py:139-161)
     sl.mark();
-    if (push_pending) {
+    if (push_pending || early_pending) {
       sl.join();
-      push_pending = false;
+      push_pending = early_pending = false;
     }
     // Algebraically identical to solver.py:145-158 with the interpolation
     // folded in before the reduced solve: V = thhat P^T (R x r), Y = Z^-1 V,
@@ -894,7 +917,7 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl,
       const int rl = c.r(a), rr = c.r(b), R = rl + rr, r = c.r(i);
       maxR = std::max(maxR, R);
       const Ref Z = c.z_lu(i), C = c.coup(i);
-      c_id.fill(Z, R, R, R, true);
+      if (!early_node(i)) c_id.fill(Z, R, R, R, true);  // else Z = I from the early branch
       g_z.add(c.theta(a), rl, 0, C, rl, 0, adv(Z, (int64_t)rl * R), R, rl, rr, rl, 1.0, 1.0);
       g_z.add(c.theta(b), rr, 0, C, rl, 1, adv(Z, rl), R, rr, rl, rr, 1.0, 1.0);
       lu.push_back(LuDesc{Z, c.z_piv(i), c.info(i), c.anorm(i), with_cond ? c.rcond(i) : kNull, R, R});
@@ -918,7 +941,7 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl,
       // F = B Y (solver.py:86-89, 156); push = P^T - F (solver.py:158)
       g_f.add(C, rl, 0, adv(Y, rl), R, 0, F, R, rl, r, rr, 1.0, 0.0);
       g_f.add(C, rl, 1, Y, R, 0, adv(F, rl), R, rr, r, rl, 1.0, 0.0);
-      c_t.copy(Pi, r, 1, pu, R, R, r);
+      if (!early_node(i)) c_t.copy(Pi, r, 1, pu, R, R, r);  // else push = P^T from the early branch
       c_p.accumulate(F, R, pu, R, R, r, -1.0);
       // W = V - thhat F ; theta = P W (solver.py:157)
       g_tf.add(c.theta(a), rl, 0, F, R, 0, W, R, rl, r, rl, -1.0, 1.0);
