@@ -479,14 +479,10 @@ __global__ void __launch_bounds__(GECON_THREADS) gecon_kernel(const Bases* __res
 // and its order are those of gecon_kernel, so the results are identical.
 enum GeconState { GS_A = 0, GS_B, GS_C, GS_D, GS_E, GS_DONE };
 
-__global__ void __launch_bounds__(GECON_THREADS) gecon_step_kernel(const Bases* __restrict__ bases_ptr,
-                                                          const LuDesc* __restrict__ descs, int stride,
-                                                          int phase) {
-  const Bases& bases = *bases_ptr;
-  const LuDesc L = descs[blockIdx.x];
+__device__ __forceinline__ void gecon_step_one(const Bases& bases, const LuDesc& L, int m, int stride, int phase) {
   if (L.rcond == kNull) return;
   const int n = L.n;
-  double* st = at<double>(bases, make_ref(kGeconScratchBase, 0)) + (size_t)blockIdx.x * stride;
+  double* st = at<double>(bases, make_ref(kGeconScratchBase, 0)) + (size_t)m * stride;
   double* gx = st;                     // n
   double* gsgn = st + n;               // n (+-1)
   double* sc = st + 2 * (size_t)n;     // state, kase, iter, j, est
@@ -624,6 +620,19 @@ __global__ void __launch_bounds__(GECON_THREADS) gecon_step_kernel(const Bases* 
   }
 }
 
+// One phase of the estimates of `count` matrices; a CTA walks matrices
+// blockIdx.x, + gridDim.x, ...  A grid smaller than the batch leaves SMs
+// with no estimate CTA at all, where the factorization's register-heavy
+// kernels (the panels) can start at once.
+__global__ void __launch_bounds__(GECON_THREADS) gecon_step_kernel(const Bases* __restrict__ bases_ptr,
+                                                          const LuDesc* __restrict__ descs, int count,
+                                                          int stride, int phase) {
+  for (int m = blockIdx.x; m < count; m += gridDim.x) {
+    gecon_step_one(*bases_ptr, descs[m], m, stride, phase);
+    __syncthreads();  // the next matrix reuses the shared vector
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_getrf_batched(const Bases* b, const LuDesc* d, int count, int max_n, cudaStream_t s) {
@@ -672,7 +681,17 @@ cudaError_t launch_gecon_batched(const Bases* b, const LuDesc* d, int count, int
   if (phase >= 0) {  // split estimate: phase 0 initialises, 1..kGeconSteps apply + advance
     const size_t sm = (size_t)(max_n > 0 ? max_n : 1) * sizeof(double);
     raise_smem_limit(gecon_step_kernel, sm);
-    gecon_step_kernel<<<count, GECON_THREADS, sm, s>>>(b, d, gecon_stride(max_n), phase);
+    // CTAs per estimate launch: batches up to 4 waves of SMs are walked by
+    // at most 112 CTAs, leaving SMs free for the factorization's panels
+    // (plan.cu cond_start_level); larger batches get one CTA per matrix so
+    // the chain does not outlast the factorization.  HKS_GECON_GRID: the cap
+    // (0 = one CTA per matrix).
+    static const int cap = [] {
+      const char* e = getenv("HKS_GECON_GRID");
+      return e ? atoi(e) : 112;
+    }();
+    const int grid = cap > 0 && count > cap && count <= 4 * 148 ? cap : count;
+    gecon_step_kernel<<<grid, GECON_THREADS, sm, s>>>(b, d, count, gecon_stride(max_n), phase);
     return cudaGetLastError();
   }
   const size_t sm = (size_t)(max_n > 0 ? max_n : 1) * (2 * sizeof(double) + sizeof(int));

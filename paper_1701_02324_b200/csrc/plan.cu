@@ -817,12 +817,18 @@ size_t factorize_workspace(const hks_plan& P) {
 
 // The dgecon estimates of levels deeper than this start once the
 // factorization has finished this level (HKS_COND_START_LEVEL overrides).
-int64_t cond_start_level() {
-  static const int64_t v = [] {
+// Measured (C2, depth 9): starting the deep levels' chain at level 6 with at
+// most 112 estimate CTAs (lu.cu) beats starting it at level 3 with one CTA
+// per matrix (16.7 vs 16.9 ms); for deeper trees (C3, depth 11: ~2000
+// matrices in the chain) the capped chain outlasts the factorization and
+// level 3 with one CTA per matrix is best (152 vs 157 ms).
+int64_t cond_start_level(int64_t depth) {
+  static const int64_t forced = [] {
     const char* e = getenv("HKS_COND_START_LEVEL");
-    return e ? (int64_t)atoi(e) : (int64_t)3;
+    return e ? (int64_t)atoi(e) : (int64_t)-1;
   }();
-  return v;
+  if (forced >= 0) return forced;
+  return depth <= 9 ? 6 : 3;
 }
 
 // Levels batched per estimate group: the estimate is a chain of
@@ -966,7 +972,7 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl,
       // the estimates of levels deeper than cond_start_level wait until the
       // factorization reaches it: they then fill SMs the latency-bound top
       // levels leave idle instead of competing with the wide levels
-      const int64_t start = cond_start_level();
+      const int64_t start = cond_start_level(L.depth);
       if (!cond_grouped() || lev == 0 || lev == start) {
         cond_levels->emplace_back(new StepList());
         // split estimate: short-lived CTAs turn the SMs over to the
