@@ -334,6 +334,20 @@ __device__ __forceinline__ void trsm_stage_rows(double* Ts, int tts, const doubl
     cp_async8(Ts + lane * tts + cc, ok ? T + (r0 + lane) + (size_t)cc * ldt : T, ok);
 }
 
+// a / b, correctly rounded (bit-identical to the IEEE division), from the
+// correctly rounded reciprocal y = 1 / b computed off the caller's
+// dependency chain: q = a y, one FMA residual, one FMA correction
+// (Markstein).  Three dependent operations instead of the division
+// sequence; operands near the exponent limits branch to the division.
+__device__ __noinline__ double div_slow(double a, double b) { return a / b; }
+__device__ __forceinline__ double div_rn(double a, double b, double y) {
+  const double aa = fabs(a), ab = fabs(b);
+  const bool safe = (aa == 0.0 || (aa > 0x1p-900 && aa < 0x1p900)) && ab > 0x1p-900 && ab < 0x1p900;
+  if (__builtin_expect(!safe, 0)) return div_slow(a, b);
+  const double q = a * y;
+  return fma(fma(-q, b, a), y, q);
+}
+
 // One triangular sweep X := T^-1 X over a k x NC block of right-hand sides
 // already in shared memory (X row-major, ld NC + 4); T is read through the
 // double-buffered 32-row staging area Tbuf (ld tts).  Ends with a barrier.
@@ -351,6 +365,7 @@ __device__ __forceinline__ void trsm_sweep(double* X, double* Tbuf, int tts, con
   constexpr int TXS = NC + 4;  // X row stride: == 4 (mod 16), conflict-free DMMA B fragments
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int nblk = (k + 31) / 32;
+  __shared__ double rdiag[32];
   auto stage_x = [&](int blk) {  // rows of X block blk, lanes along a column's rows
     const int xr0 = blk * 32, xnr = min(32, k - xr0);
     if (lane < xnr) {
@@ -380,6 +395,8 @@ __device__ __forceinline__ void trsm_sweep(double* X, double* Tbuf, int tts, con
                                  lane);
       cp_async_commit();
     }
+    // reciprocals of this block's diagonal, off the solve's dependency chain
+    if (UPPER && tid < nr) rdiag[tid] = 1.0 / Ts[tid * tts + r0 + tid];
     // X[r0:r0+nr, :] -= T[r0:r0+nr, u] X[u, :] over the solved rows u (DMMA)
     const int ulo = UPPER ? r0 + nr : 0, uhi = UPPER ? k : r0;
     if (NT == 2 * NC && NC >= 64) {  // two warps per 32-column tile, 16 rows each
@@ -490,7 +507,7 @@ __device__ __forceinline__ void trsm_sweep(double* X, double* Tbuf, int tts, con
 #pragma unroll
         for (int j = 31; j >= 0; --j) {
           if (j < nr) {
-            x[j] /= Ts[j * tts + r0 + j];  // a true division, as dtrsm (c5 is sensitive to it)
+            x[j] = div_rn(x[j], Ts[j * tts + r0 + j], rdiag[j]);  // == x[j] / T(j, j), as dtrsm (c5 is sensitive to it)
 #pragma unroll
             for (int i = 0; i < j; ++i) x[i] -= Ts[i * tts + r0 + j] * x[j];
           }
