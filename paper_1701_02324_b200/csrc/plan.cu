@@ -129,7 +129,12 @@ cudaError_t StepList::run(const Bases* b, const double* X, int d, const KernelPa
     while (ev && next_mark < marks_.size() && marks_[next_mark] == si) record(ev[next_mark++], main);
     if (st.kind == ST_FORK || st.kind == ST_JOIN) {
       if (!side_) {
-        cudaError_t e = cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking);
+        // side branches (work nothing on the main chain waits for soon):
+        // a priority between the main chain's and the dgecon stream's
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        cudaError_t e = cudaStreamCreateWithPriority(&side_, cudaStreamNonBlocking,
+                                                     node_priorities() ? (lo + hi) / 2 : 0);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&fork_ev_, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&join_ev_, cudaEventDisableTiming);
         if (e != cudaSuccess) return e;
@@ -260,6 +265,17 @@ cudaError_t GraphCache::write(const Bases& b, cudaStream_t s) {
   return e;
 }
 
+// Graph nodes keep the priority of the stream they were captured on (main
+// chain highest, side branches lower) when instantiated with
+// cudaGraphInstantiateFlagUseNodePriority (HKS_NODE_PRIO=0: off).
+bool node_priorities() {
+  static const bool v = [] {
+    const char* e = getenv("HKS_NODE_PRIO");
+    return !(e && atoi(e) == 0);
+  }();
+  return v;
+}
+
 cudaError_t run_graphed(GraphCache& gc, const StepList& sl, const Bases& b, const double* X, int d,
                         const KernelParams& kp, cudaStream_t s, cudaEvent_t* ev, void* memset_ptr,
                         size_t memset_bytes, bool allow_graph) {
@@ -276,8 +292,10 @@ cudaError_t run_graphed(GraphCache& gc, const StepList& sl, const Bases& b, cons
     return e == cudaSuccess ? sl.run(gc.dev, X, d, kp, s, ev) : e;
   }
   if (!gc.exec) {  // capture once: the graph reads its bases from gc.dev
-    if (!gc.cs) {
-      e = cudaStreamCreateWithFlags(&gc.cs, cudaStreamNonBlocking);
+    if (!gc.cs) {  // captured at the highest priority (the nodes keep it: per-node priorities below)
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      e = cudaStreamCreateWithPriority(&gc.cs, cudaStreamNonBlocking, node_priorities() ? hi : 0);
       if (e != cudaSuccess) return e;
     }
     e = cudaStreamBeginCapture(gc.cs, cudaStreamCaptureModeThreadLocal);
@@ -286,7 +304,8 @@ cudaError_t run_graphed(GraphCache& gc, const StepList& sl, const Bases& b, cons
     cudaGraph_t g = nullptr;
     e = cudaStreamEndCapture(gc.cs, &g);
     if (er != cudaSuccess) e = er;
-    if (e == cudaSuccess) e = cudaGraphInstantiate(&gc.exec, g, 0);
+    if (e == cudaSuccess)
+      e = cudaGraphInstantiate(&gc.exec, g, node_priorities() ? cudaGraphInstantiateFlagUseNodePriority : 0);
     if (g) cudaGraphDestroy(g);
     if (e != cudaSuccess) return e;
   } else {

@@ -152,6 +152,7 @@ struct GraphCache {
 };
 
 bool graphs_enabled();
+bool node_priorities();  // graph nodes keep their capture stream's priority (plan.cu)
 
 // Runs `sl` with bases `b` on stream s (graph replay unless profiling or
 // HKS_GRAPHS=0); `memset_ptr` (if any) is zeroed first, inside the graph.
