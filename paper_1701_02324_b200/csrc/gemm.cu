@@ -181,6 +181,109 @@ __global__ void __launch_bounds__(2 * TBM) gemm_batched_kernel(const Bases* __re
   }
 }
 
+// Skinny products (n <= 16: the solves' k right-hand sides): 128 x 16
+// output tiles, each warp 32 rows x 16 columns, so a CTA streams 128 rows
+// of A per k-slab instead of computing a 64 x 64 tile three quarters
+// empty.  Same k-slab order and DMMA fragment order per output element as
+// gemm_batched_kernel: the results are bit-identical to it.
+constexpr int SBM = 128, SBN = 16;
+__global__ void __launch_bounds__(128) gemm_skinny_kernel(const Bases* __restrict__ bases_ptr,
+                                                          const GemmDesc* __restrict__ descs) {
+  const Bases& bases = *bases_ptr;
+  const GemmDesc gd = descs[blockIdx.y];
+  const GemmOp g{at<const double>(bases, gd.A), at<const double>(bases, gd.B), at<double>(bases, gd.C),
+                 gd.m, gd.n, gd.k, gd.lda, gd.ldb, gd.ldc, gd.transA, gd.transB, gd.alpha, gd.beta};
+  const int m0 = blockIdx.x * SBM;
+  if (m0 >= g.m) return;
+  extern __shared__ double gsm[];
+  double* As = gsm;                        // STAGES x SBM x KS
+  double* Bs = gsm + STAGES * SBM * KS;    // STAGES x SBN x KS
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int wm = wid * 32, fr = lane >> 2, fc = lane & 3;
+  auto load = [&](int k0, double* as, double* bs) {
+    if (!g.transA) {
+#pragma unroll
+      for (int ki = 0; ki < BK; ++ki) {
+        const int m = m0 + t, k = k0 + ki;
+        const bool ok = m < g.m && k < g.k;
+        cp_async8(as + t * KS + ki, ok ? g.A + m + (size_t)k * g.lda : g.A, ok);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < SBM / 8; ++j) {
+        const int ki = t % BK, mi = t / BK + 8 * j;
+        const int m = m0 + mi, k = k0 + ki;
+        const bool ok = m < g.m && k < g.k;
+        cp_async8(as + mi * KS + ki, ok ? g.A + k + (size_t)m * g.lda : g.A, ok);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int a = t % 16, b = t / 16 + 8 * j;  // !transB: a = k, b = n; transB: a = n, b = k
+      const int ki = g.transB ? b : a, ni = g.transB ? a : b;
+      const int k = k0 + ki;
+      const bool ok = ni < g.n && k < g.k;
+      cp_async8(bs + ni * KS + ki, ok ? (g.transB ? g.B + ni + (size_t)k * g.ldb : g.B + k + (size_t)ni * g.ldb) : g.B,
+                ok);
+    }
+  };
+  if (g.beta != 0.0)
+    for (int e = t; e < SBN * (SBM / 8); e += 128) {
+      const int c = e / (SBM / 8), r = m0 + (e % (SBM / 8)) * 8;
+      if (c < g.n && r < g.m) asm volatile("prefetch.global.L2 [%0];" ::"l"(g.C + r + (size_t)c * g.ldc));
+    }
+  double acc[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int nk = (g.k + BK - 1) / BK;
+#pragma unroll
+  for (int st = 0; st < STAGES - 1; ++st) {
+    if (st < nk) load(st * BK, As + st * SBM * KS, Bs + st * SBN * KS);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    const int pf = kt + STAGES - 1;
+    if (pf < nk) load(pf * BK, As + (pf % STAGES) * SBM * KS, Bs + (pf % STAGES) * SBN * KS);
+    cp_async_commit();
+    const double* as = As + (kt % STAGES) * SBM * KS;
+    const double* bs = Bs + (kt % STAGES) * SBN * KS;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double a[4], b[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = as[(wm + i * 8 + fr) * KS + kk + fc];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) b[j] = bs[(j * 8 + fr) * KS + kk + fc];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+  }
+  cp_async_wait<0>();
+  const double alpha = g.alpha, beta = g.beta;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = m0 + wm + i * 8 + fr;
+    if (r >= g.m) continue;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = j * 8 + 2 * fc + h;
+        if (c >= g.n) continue;
+        double v = acc[i][j][h];
+        if (beta != 0.0) v = alpha * v + beta * g.C[r + (size_t)c * g.ldc];
+        else if (alpha != 1.0) v *= alpha;
+        g.C[r + (size_t)c * g.ldc] = v;
+      }
+  }
+}
+
 // dst = alpha * op(src) / alpha * I / 0 / dst + alpha * op(src), one descriptor per block.
 // 32 x 32 output tiles, 256 threads (8 rows of 32 lanes); a transposed
 // copy goes through a shared tile so both its reads and its writes are
@@ -235,6 +338,16 @@ cudaError_t launch_gemm_batched(const Bases* bases, const GemmDesc* d_descs, int
   }();
   // 128-row tiles (8 warps) once the products are tall and the grid is
   // large: more warps per SM and half the B-operand staging per flop
+  static const bool skinny_ok = getenv("HKS_GEMM_SKINNY") == nullptr || atoi(getenv("HKS_GEMM_SKINNY")) != 0;
+  if (skinny_ok && max_n <= SBN) {  // the solves' right-hand-side blocks
+    const size_t sm = (size_t)STAGES * (SBM + SBN) * KS * sizeof(double);
+    raise_smem_limit(gemm_skinny_kernel, sm);
+    for (int first = 0; first < count; first += 65535) {
+      const int cnt = count - first < 65535 ? count - first : 65535;
+      gemm_skinny_kernel<<<dim3((max_m + SBM - 1) / SBM, cnt), 128, sm, stream>>>(bases, d_descs + first);
+    }
+    return cudaGetLastError();
+  }
   const bool tall = forced == 128;  // measured: no gain over 64-row tiles on the plans' products
   const int BM = tall ? 128 : 64;
   const int tm = (max_m + BM - 1) / BM, tn = (max_n + BN - 1) / BN;
