@@ -142,3 +142,18 @@ def test_skeletonize_threads_invariant_and_deterministic():
     for i in range(1, 2 ** (tree.depth + 1) - 1):
         assert np.array_equal(a[i].indices, b[i].indices)
         assert np.array_equal(a[i].interp, b[i].interp)
+
+
+@pytest.mark.parametrize("k", [16, 20])
+def test_solve_multi_columns_bit_identical(k):
+    """solve_multi == solve column by column, bit for bit (tests/test_solver.py:174-185
+    of the reference), on both GEMM paths: k <= 16 right-hand sides use the
+    skinny 128 x 16 tiles, k > 16 the 64 x 64 tiles, single columns the
+    skinny ones -- the k order per output element is the same in all."""
+    hk, g, m, tree, knn, skels, op, f = pipeline(sorted(ALL_CASES)[0])
+    B = np.random.default_rng(k).standard_normal((op.n, k))
+    X = hk.solve_multi(f, B, in_tree_order=True)
+    for j in (0, k // 2, k - 1):
+        np.testing.assert_array_equal(X[:, j], hk.solve(f, B[:, j], in_tree_order=True))
+    U = np.stack([hk.hmatvec(op, B[:, j], m["lam"]) for j in (0, k - 1)], axis=1)
+    assert np.all(np.isfinite(U))
