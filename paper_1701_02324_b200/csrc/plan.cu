@@ -546,12 +546,19 @@ int fused_lu_max_count() {
 // 64 x 256, 32 x 512 and 16 x 1024.  Wider panels mean fewer in-group
 // interchange / TRSM / GEMM steps per 128-column group.  HKS_PANEL_PB
 // overrides (16, 32 or 64).
-int panel_width(int nmax) {
+int panel_width(int nmax, int count) {
   static const int forced = [] {
     const char* e = getenv("HKS_PANEL_PB");
     return e ? atoi(e) : 0;
   }();
-  int pb = nmax <= 256 ? 64 : nmax <= 512 ? 32 : 16;
+  static const int wide_count = [] {  // batches above this many matrices: 32-wide panels for <= 256 rows
+    const char* e = getenv("HKS_PANEL32_COUNT");
+    return e ? atoi(e) : 148;
+  }();
+  // 64 x 256 register panels run one CTA per SM (239 registers x 256
+  // threads); a batch of more than one wave of them takes 32-wide panels
+  // (two CTAs per SM) instead
+  int pb = nmax <= 256 ? (count > wide_count ? 32 : 64) : nmax <= 512 ? 32 : 16;
   if (forced == 16 || forced == 32 || forced == 64) pb = forced;
   if (pb == 64 && nmax > 256) pb = 32;
   if (pb == 32 && nmax > 512) pb = 16;
@@ -574,7 +581,7 @@ void add_lu_program(StepList& sl, const std::vector<LuJob>& jobs, bool with_norm
   int nmax = 0;
   for (auto& j : jobs) nmax = std::max(nmax, j.n);
   if (nmax == 0) return;
-  const int PB = panel_width(nmax);
+  const int PB = panel_width(nmax, (int)jobs.size());
   if (with_norm) add_norm_step(sl, jobs);
   if ((int)jobs.size() <= fused_lu_max_count()) {
     std::vector<LuFusedDesc> fd;
