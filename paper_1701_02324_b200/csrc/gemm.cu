@@ -187,8 +187,18 @@ __global__ void __launch_bounds__(2 * TBM) gemm_batched_kernel(const Bases* __re
 // empty.  Same k-slab order and DMMA fragment order per output element as
 // gemm_batched_kernel: the results are bit-identical to it.
 constexpr int SBM = 128, SBN = 16;
+#ifndef HKS_SKINNY_BK
+#define HKS_SKINNY_BK 16
+#endif
+#ifndef HKS_SKINNY_STAGES
+#define HKS_SKINNY_STAGES 3
+#endif
+// 16-deep k-slabs, 3 stages (measured: 8-deep slabs with 4 stages, four
+// CTAs per SM instead of three, are slower on the solve)
+constexpr int SBK = HKS_SKINNY_BK, SST = HKS_SKINNY_STAGES, SKS = SBK + 4;  // SKS == 4 (mod 8): conflict-free fragments
 __global__ void __launch_bounds__(128) gemm_skinny_kernel(const Bases* __restrict__ bases_ptr,
                                                           const GemmDesc* __restrict__ descs) {
+  constexpr int BK = SBK, STAGES = SST, KS = SKS;
   const Bases& bases = *bases_ptr;
   const GemmDesc gd = descs[blockIdx.y];
   const GemmOp g{at<const double>(bases, gd.A), at<const double>(bases, gd.B), at<double>(bases, gd.C),
@@ -210,17 +220,17 @@ __global__ void __launch_bounds__(128) gemm_skinny_kernel(const Bases* __restric
       }
     } else {
 #pragma unroll
-      for (int j = 0; j < SBM / 8; ++j) {
-        const int ki = t % BK, mi = t / BK + 8 * j;
+      for (int j = 0; j < SBM * BK / 128; ++j) {
+        const int ki = t % BK, mi = t / BK + (128 / BK) * j;
         const int m = m0 + mi, k = k0 + ki;
         const bool ok = m < g.m && k < g.k;
         cp_async8(as + mi * KS + ki, ok ? g.A + k + (size_t)m * g.lda : g.A, ok);
       }
     }
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int a = t % 16, b = t / 16 + 8 * j;  // !transB: a = k, b = n; transB: a = n, b = k
-      const int ki = g.transB ? b : a, ni = g.transB ? a : b;
+    for (int j = 0; j < SBN * BK / 128; ++j) {
+      const int e = t + 128 * j;  // !transB: along k then n; transB: along n then k
+      const int ki = g.transB ? e / SBN : e % BK, ni = g.transB ? e % SBN : e / BK;
       const int k = k0 + ki;
       const bool ok = ni < g.n && k < g.k;
       cp_async8(bs + ni * KS + ki, ok ? (g.transB ? g.B + ni + (size_t)k * g.ldb : g.B + k + (size_t)ni * g.ldb) : g.B,
@@ -340,7 +350,7 @@ cudaError_t launch_gemm_batched(const Bases* bases, const GemmDesc* d_descs, int
   // large: more warps per SM and half the B-operand staging per flop
   static const bool skinny_ok = getenv("HKS_GEMM_SKINNY") == nullptr || atoi(getenv("HKS_GEMM_SKINNY")) != 0;
   if (skinny_ok && max_n <= SBN) {  // the solves' right-hand-side blocks
-    const size_t sm = (size_t)STAGES * (SBM + SBN) * KS * sizeof(double);
+    const size_t sm = (size_t)SST * (SBM + SBN) * SKS * sizeof(double);
     raise_smem_limit(gemm_skinny_kernel, sm);
     for (int first = 0; first < count; first += 65535) {
       const int cnt = count - first < 65535 ? count - first : 65535;
