@@ -614,6 +614,35 @@ def gather_rows(comm, spec, X):
     return t.cat([blocks[q, :, : int(spec.shard_sizes[q])] for q in range(comm.world)], dim=1)
 
 
+def cross_predict_sharded(kernel, test, op, w_local):
+    """KRR prediction K(test, train) w (cli.py:415-422) over training
+    points sharded by subtree: each rank sums its own shard's sources
+    (``metrics.cross_sum`` on the shard's tree-ordered points, never storing
+    K), then the P partial sums are all-gathered and added in rank order, so
+    every rank returns the same (nq,) device vector, independent of the
+    collective's reduction order.  ``w_local`` is this rank's slice of the
+    tree-ordered weights (e.g. a row of ``solve_sharded``'s result)."""
+    from .metrics import cross_sum
+    from .tree import PointSet
+    t = N.torch()
+    spec, comm = op.spec, op.comm
+    w = w_local.to(t.float64).reshape(1, -1).contiguous()
+    if w.shape[1] != spec.size:
+        raise ValueError(f"weights must have length {spec.size} on rank {spec.rank}")
+    test = test if isinstance(test, PointSet) else PointSet(np.asarray(test, dtype=np.float64))
+    xs = op._x_local.contiguous()
+    part = cross_sum(kernel, test.device(), xs, w)[0].contiguous()
+    if comm.world == 1:
+        return part
+    out = t.empty(comm.world * part.numel(), dtype=t.float64, device=part.device)
+    comm.all_gather(out, part)
+    blocks = out.view(comm.world, -1)
+    acc = blocks[0].clone()
+    for q in range(1, comm.world):
+        acc += blocks[q]
+    return acc
+
+
 def timed_setup(fn):
     t0 = time.perf_counter()
     out = fn()

@@ -71,6 +71,8 @@ def main():
     xh, rep = hybrid_solve_sharded(op, f, B[0], tol=1e-9, max_iter=40, restart=5)
     res.update(xh=xh.cpu().numpy(), h_iters=rep.iterations, h_res=np.array(rep.residuals),
                h_final=rep.final_residual)
+    xq = np.random.default_rng([a.seed, 99]).random((300, a.d))  # KRR test points
+    res["pred"] = S.cross_predict_sharded(kern, xq, op, X[0]).cpu().numpy()
     res.update(x=X.cpu().numpy(), x2=X2.cpu().numpy(), u=U.cpu().numpy(), xfull=full.cpu().numpy())
     for i in range(1, (1 << (tree.depth + 1)) - 1):
         if i in sk:

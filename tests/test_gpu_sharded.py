@@ -68,7 +68,9 @@ def _reference(n, d, leaf, s, kappa, tau, h, lam, seed):
     xs = hk.solve_multi(f, bt, in_tree_order=True)
     u = np.stack([hk.hmatvec(op, bt[:, j], lam) for j in range(bt.shape[1])], axis=1)
     xh, rep = hk.hybrid_solve(op, f, bt[:, 0], tol=1e-9, max_iter=40, restart=5)
-    return dict(tree=tree, knn=np.asarray(knn), sk=sk, x=xs, u=u, zc=f.z_cond_per_level(), xh=xh, rep=rep)
+    xq = np.random.default_rng([seed, 99]).random((300, d))  # the worker's KRR test points
+    return dict(tree=tree, knn=np.asarray(knn), sk=sk, x=xs, u=u, zc=f.z_cond_per_level(), xh=xh, rep=rep,
+                predict=lambda w: hk.cross_predict(kern, xq, tree.points, w))
 
 
 CASES = {
@@ -118,4 +120,10 @@ def test_sharded_matches_unsharded(tmp_path, case):
             assert z <= ref["zc"][int(lev)] * (1 + 1e-8) + 1e-12
             if lev < p:
                 assert z == pytest.approx(ref["zc"][int(lev)], rel=1e-8)
+        # KRR predict over the training shards (partials summed in rank order): identical on every
+        # rank, equal to the unsharded prediction up to the summation order
+        # (same weights: the gathered sharded solution; |K| <= 1, so the bound scales with sum |w|)
+        w = ranks[0]["xfull"][0]
+        np.testing.assert_array_equal(res["pred"], ranks[0]["pred"])
+        np.testing.assert_allclose(res["pred"], ref["predict"](w), rtol=0, atol=1e-14 * np.abs(w).sum())
     assert seen == set(range(1, nn)), "some skeletons were produced by no rank"
