@@ -631,12 +631,19 @@ def cross_predict_sharded(kernel, test, op, w_local):
         raise ValueError(f"weights must have length {spec.size} on rank {spec.rank}")
     test = test if isinstance(test, PointSet) else PointSet(np.asarray(test, dtype=np.float64))
     xs = op._x_local.contiguous()
-    part = cross_sum(kernel, test.device(), xs, w)[0].contiguous()
+    return sum_in_rank_order(comm, cross_sum(kernel, test.device(), xs, w)[0])
+
+
+def sum_in_rank_order(comm, part):
+    """Every rank's `part` added in rank order ((p0 + p1) + p2 ...), the
+    same bits on every rank whatever the backend's reduction order."""
+    t = N.torch()
+    part = part.contiguous()
     if comm.world == 1:
         return part
-    out = t.empty(comm.world * part.numel(), dtype=t.float64, device=part.device)
+    out = t.empty(comm.world * part.numel(), dtype=part.dtype, device=part.device)
     comm.all_gather(out, part)
-    blocks = out.view(comm.world, -1)
+    blocks = out.view(comm.world, *part.shape)
     acc = blocks[0].clone()
     for q in range(1, comm.world):
         acc += blocks[q]

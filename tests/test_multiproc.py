@@ -106,7 +106,7 @@ def _shard_comm_worker(rank, world, port, q):
     import torch
     import torch.distributed as dist
     sys.path.insert(0, str(ROOT))
-    from paper_1701_02324_b200.sharded import ShardComm, or_reduce_bitmaps
+    from paper_1701_02324_b200.sharded import ShardComm, or_reduce_bitmaps, sum_in_rank_order
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -120,7 +120,9 @@ def _shard_comm_worker(rank, world, port, q):
         orb = or_reduce_bitmaps(allbm, world)
         s = torch.tensor([1.0 + rank])
         comm.all_reduce_sum_(s)
-        q.put((rank, out.tolist(), orb.tolist(), comm.all_reduce_max(rank * 7), float(s.item())))
+        part = torch.tensor([0.1, 1e16, -1e16] if rank == 0 else [0.2, 1.0, 3.0], dtype=torch.float64)
+        ro = sum_in_rank_order(comm, part)  # the sharded KRR predict's reduction
+        q.put((rank, out.tolist(), orb.tolist(), comm.all_reduce_max(rank * 7), float(s.item()), ro.tolist()))
     finally:
         dist.destroy_process_group()
 
@@ -140,7 +142,8 @@ def test_shard_comm_gloo():
         p.join(timeout=60)
         assert p.exitcode == 0
     for r in range(2):
-        out, orb, mx, sm = got[r]
+        out, orb, mx, sm, ro = got[r]
+        assert ro == [0.1 + 0.2, 1e16 + 1.0, -1e16 + 3.0]  # (p0 + p1) bits on every rank
         assert out == [0.0, 1.0, 2.0, 10.0, 11.0, 12.0]
         assert orb == [3, 0, (1 << 4) | (1 << 5)]
         assert mx == 7 and sm == 3.0
