@@ -1,6 +1,8 @@
 #!/usr/bin/env python
 """Benchmark: factorize + k-RHS solve of (lambda I + Ktilde) on the BASELINE
-workload (default C2: N=262144, d=18, m=512, s=128, kappa=32, 16 RHS).
+workload (default C3: N=1048576, d=28, m=512, adaptive rank tau=1e-5 capped
+at s=256, kappa=32, 16 RHS -- the configuration BASELINE.json quotes across
+1/2/4/8 GPUs; ``--config C2`` etc. for the others).
 
 One *step* = ``factorize(op, lam)`` + ``solve_multi(f, B)`` on a resident
 operator (tree, kNN, skeletons and couplings are built once, untimed, and
@@ -10,7 +12,11 @@ to a host x (H2D + D2H inside the timed region).  ``--impl reference`` times
 the CPU oracle (oracle/hks_oracle.py, the reference algorithm restated) on a
 bounded sample of the same workload.  See DESIGN.md for the definitions.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl hks|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl hks|reference] [--config C3]
+
+Multi-GPU (torchrun, one rank per GPU): the configuration's N is split
+across the ranks by subtree (strong scaling, BASELINE's fixed-N runs);
+``--weak`` instead gives every rank the configuration's N.
 """
 
 from __future__ import annotations
@@ -41,12 +47,17 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["hks", "reference"], default="hks")
-    p.add_argument("--config", default="C2")
+    p.add_argument("--config", default="C3")
+    p.add_argument("--weak", action="store_true",
+                   help="N > 1 GPUs: every rank holds the config's N (default: the config's N split across ranks)")
+    p.add_argument("--no-accuracy", action="store_true", help="skip the full-N sampled-row accuracy metrics")
     p.add_argument("--points", type=int, default=None, help="override N per GPU (same generator / kernel / ranks)")
     p.add_argument("--cpu-sample-n", type=int, default=16384)
     p.add_argument("--cpu-steps", type=int, default=2)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-clocks", action="store_true", help="skip the nvidia-smi clock sampler (diagnostics)")
+    p.add_argument("--dump-x", default=None,
+                   help="directory: each rank saves its block of the timed solution (tree order) as x_rank<r>.npz")
     p.add_argument("--knn-trees", type=int, default=0,
                    help="setup only: approximate kNN from this many random-projection trees (0 = exact)")
     return p.parse_args()
@@ -214,6 +225,26 @@ class SingleRunner:
         self.krylov = [r.iterations for r in reps]
         return X.t()
 
+    def accuracy(self, f):
+        """Sampled-row metrics at full N (metrics.sampled_error_report) for
+        the first right-hand side, beside the reference's own values on the
+        same generator at N = 16384 / 65536 (tests/golden/ladder_*.npz)."""
+        from paper_1701_02324_b200 import metrics as M
+        t0 = time.perf_counter()
+        rep = M.sampled_error_report(self.op, f, b=self.b[np.asarray(self.tree.perm), 0], rows=256, seed=0)
+        rep["seconds"] = round(time.perf_counter() - t0, 3)
+        ref = {}
+        for n in (16384, 65536):
+            g = ROOT / "tests" / "golden" / f"ladder_{self.w.name.lower()}_n{n}.npz"
+            if g.exists():
+                z = np.load(g)
+                ref[str(n)] = {"matvec_relerr_vs_K": float(z["sampled_matvec_relerr"]),
+                               "true_residual": float(z["sampled_true_residual"]),
+                               "residual_vs_Ktilde": float(z["relres_ktilde"][0])}
+        if ref:
+            rep["reference_at_reduced_n"] = ref
+        return rep
+
     def relres(self, X):
         import torch
         res = self.hk.treecode.hmatvec_device(self.op, X[:1].contiguous(), self.w.lam)[0] - self.B[0]
@@ -244,19 +275,21 @@ class SingleRunner:
 
 
 class ShardedRunner:
-    """P = 2^p GPUs: one global instance of P x N points (weak scaling: every
-    rank's shard has the single-GPU workload's N), subtree-sharded
-    (paper_1701_02324_b200/sharded.py; NCCL only for the shard-root
-    exchange)."""
+    """P = 2^p GPUs: one global seeded instance subtree-sharded over the
+    ranks (paper_1701_02324_b200/sharded.py; NCCL only for the shard-root
+    exchange).  Strong scaling (default): the instance is the config's N,
+    each rank owns N / P points.  Weak (--weak): P x N points, every rank's
+    shard the single-GPU workload's N."""
 
-    def __init__(self, w, world, rank):
+    def __init__(self, w, world, rank, weak=False):
         import torch
         import paper_1701_02324_b200 as hk
         from paper_1701_02324_b200 import _native as N
         from paper_1701_02324_b200 import sharded as S
         from paper_1701_02324_b200 import workloads as W
         self.hk, self.N, self.S, self.w = hk, N, S, w
-        wg = w.scaled(w.n * world)
+        wg = w.scaled(w.n * world) if weak else w
+        self.weak = weak
         x = W.points(wg, 0)
         b = W.rhs(wg, 0)
         kern = hk.KernelSpec("gaussian", h=w.h, regularization=w.lam)
@@ -283,6 +316,9 @@ class ShardedRunner:
 
     def solve(self, f):
         return self.S.solve_sharded(f, self.B)
+
+    def accuracy(self, f):
+        return None  # the sampled-row metrics run on the single-GPU line; relres_vs_ktilde is global here
 
     def relres(self, X):
         import torch
@@ -326,7 +362,7 @@ def gpu_arm(args, w, rank, world):
     from paper_1701_02324_b200 import _native as N
 
     dev = torch.device("cuda", torch.cuda.current_device())
-    run = ShardedRunner(w, world, rank) if world > 1 else SingleRunner(w, 0, args.knn_trees)
+    run = ShardedRunner(w, world, rank, weak=args.weak) if world > 1 else SingleRunner(w, 0, args.knn_trees)
     stream = torch.cuda.current_stream()
 
     def step():
@@ -408,10 +444,18 @@ def gpu_arm(args, w, rank, world):
     t_fact = [a.elapsed_time(bq) for a, bq, _ in evs]
     t_solve = [bq.elapsed_time(c) for _, bq, c in evs]
     region_ms = max_over_ranks(region_ms, world, dev)
+    fact_ms = max_over_ranks(statistics.mean(t_fact), world, dev)   # slowest rank, like the region
+    solve_ms = max_over_ranks(statistics.mean(t_solve), world, dev)
     ms_step = region_ms / args.steps
 
     # parity spot check of the timed solution: residual against Ktilde
     relres = run.relres(X)
+    if args.dump_x:
+        begin = run.spec.begin if world > 1 else 0
+        np.savez(Path(args.dump_x) / f"x_rank{rank}.npz", x=X.cpu().numpy(), begin=begin, n=run.n_job)
+    # full-N accuracy (BASELINE.md 4.2 / oracle.py:68-140 at GPU scale):
+    # 256 sampled rows of the exact K + lam I against all N columns
+    accuracy = None if args.no_accuracy else run.accuracy(f)
 
     # e2e through the public API: pinned host B -> host x, H2D + D2H inside
     e2e_ms = []
@@ -474,11 +518,12 @@ def gpu_arm(args, w, rank, world):
         "warmup": args.warmup,
         "ms_per_step": round(ms_step, 4),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "weak" if world == 1 or args.weak else "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": ("synthetic: seeded BASELINE generator (BASELINE.md 4.4), seed 0" if world == 1 else
-                 f"synthetic: one seeded instance of {world} x {w.n} points (BASELINE.md 4.4), subtree-sharded"),
+                 f"synthetic: one seeded instance of {n_total} points (BASELINE.md 4.4), subtree-sharded "
+                 f"over {world} ranks ({n_total // world} points each)"),
         "config": {"workload": w.name, "n": w.n, "d": w.d, "leaf": w.leaf_size, "max_rank": w.max_rank,
                    "tau": w.tau, "kappa": w.kappa, "samples": w.samples, "sample_mode": "knn_augmented",
                    "knn": f"approx ({args.knn_trees} random-projection trees)" if args.knn_trees else "exact",
@@ -486,18 +531,19 @@ def gpu_arm(args, w, rank, world):
                    "parallelism": f"subtree-sharded x{world} (NCCL shard-root exchange)" if world > 1 else "single",
                    "n_global": n_total,
                    "l2": "no flush: per-step working set (factor storage) exceeds the 126 MB L2"},
-        "factorize_points_per_s": round(n_total / (max_over_ranks(statistics.mean(t_fact), world, dev) * 1e-3), 1),
-        "solve_rhs_per_s": round(w.nrhs / (statistics.mean(t_solve) * 1e-3), 1),
-        "factorize_ms": round(statistics.mean(t_fact), 4),
+        "factorize_points_per_s": round(n_total / (fact_ms * 1e-3), 1),
+        "solve_rhs_per_s": round(w.nrhs / (solve_ms * 1e-3), 1),
+        "factorize_ms": round(fact_ms, 4),
         "step_ms_each": [round(a + b2, 3) for a, b2 in zip(t_fact, t_solve)],
         "host_ms_each": [round(v, 3) for v in host_t],
         "factorize_ms_each": [round(v, 3) for v in t_fact],
-        "solve_ms": round(statistics.mean(t_solve), 4),
+        "solve_ms": round(solve_ms, 4),
         "step_tflops": round(total_flops / (ms_step * 1e-3) / 1e12, 3),
         "setup_s": setup,
         "setup_points_per_s": round(n_total / max_over_ranks(sum(v for k, v in setup.items() if k != "h2d_points"),
                                                              world, dev), 1),
         "relres_vs_ktilde": relres,
+        **({"accuracy": accuracy} if accuracy else {}),
         "method": w.method,
         **({"gmres_iterations": getattr(run, "krylov", None), "gmres_tol": w.gmres_tol} if w.method == "hybrid" else {}),
         "roofline": roof,
@@ -547,6 +593,10 @@ def main():
         torch.cuda.set_device(local)
         backend = os.environ.get("HKS_BENCH_BACKEND", "nccl")  # gloo: functional runs of P ranks on one GPU
         if backend == "nccl":
+            # NCCL's init lines (ranks, NVLink / NVLS transport) on stderr so a
+            # run's log shows every rank joined the communicator
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             torch.distributed.init_process_group(backend)

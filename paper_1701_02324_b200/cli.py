@@ -29,66 +29,10 @@ REPORT_VERSION = "hikersolve-report-1"
 SHAPE_ALIASES = {"cube": "uniform_cube", "sphere": "sphere_surface", "mixture": "gaussian_mixture"}
 
 
-@dataclasses.dataclass(frozen=True)
-class RunConfig:
-    """Defaults of the reference's Config (config.py:17-37)."""
-    kernel: str = "gaussian"
-    h: float = 0.5
-    degree: int = 2
-    shift: float = 1.0
-    lam: float = 1e-3
-    leaf: int = 256
-    tau: float = 1e-5
-    max_rank: int = 64
-    samples: int = 256
-    sample_mode: str = "uniform"
-    knn: int = 8
-    restart: int = 50
-    tol: float = 1e-8
-    maxiter: int = 500
-    threads: int = 0
-    seed: int = 0
+from .config import Config, apply_overrides, parse_config_file  # noqa: E402
 
-    def kernel_spec(self):
-        from .kernels import KernelSpec
-        return KernelSpec(self.kernel, h=self.h, degree=self.degree, shift=self.shift, regularization=self.lam)
-
-    def skeleton_config(self):
-        from .skeleton import SkeletonConfig
-        return SkeletonConfig(tau=self.tau, max_rank=self.max_rank, samples=self.samples,
-                              sample_mode=self.sample_mode, seed=self.seed)
-
-    def echo(self):
-        out = {f.name: getattr(self, f.name) for f in dataclasses.fields(self)}
-        out["lambda"] = out.pop("lam")
-        out["threads"] = self.threads if self.threads > 0 else (os.cpu_count() or 1)
-        return out
-
-
-_TYPES = {f.name: f.type for f in dataclasses.fields(RunConfig)}
-
-
-def read_config(path, base=None):
-    """Overlay a key = value file (config.py:93-114 semantics)."""
-    base = base or RunConfig()
-    upd = {}
-    with open(path) as fh:
-        for lineno, line in enumerate(fh, start=1):
-            text = line.split("#", 1)[0].strip()
-            if not text:
-                continue
-            if "=" not in text:
-                raise ValueError(f"{path}: line {lineno}: expected key = value")
-            key, raw = (p.strip() for p in text.split("=", 1))
-            key = "lam" if key == "lambda" else key
-            if key not in _TYPES:
-                raise ValueError(f"{path}: line {lineno}: unknown key {key!r}")
-            conv = {"int": int, "float": float}.get(str(_TYPES[key]), str)
-            try:
-                upd[key] = conv(raw)
-            except ValueError:
-                raise ValueError(f"{path}: line {lineno}: bad value {raw!r} for {key}") from None
-    return dataclasses.replace(base, **upd)
+RunConfig = Config  # the name round-1 callers used
+read_config = parse_config_file
 
 
 class _Parser(argparse.ArgumentParser):
@@ -178,9 +122,8 @@ def build_parser():
 
 
 def _config(args, base=None):
-    cfg = read_config(args.config, base) if getattr(args, "config", None) else (base or RunConfig())
-    known = {k: v for k, v in vars(args).items() if v is not None and k in _TYPES}
-    return dataclasses.replace(cfg, **known) if known else cfg
+    cfg = parse_config_file(args.config, base) if getattr(args, "config", None) else (base or Config())
+    return apply_overrides(cfg, {k: v for k, v in vars(args).items() if v is not None})
 
 
 def _sync():
@@ -230,6 +173,11 @@ def _report(cfg, command, extra=None, timings=None, ranks=None, errors=None, kr=
     if kr is not None:
         rep["krylov"] = {"iterations": int(kr.iterations), "residuals": [float(r) for r in kr.residuals]}
     return rep
+
+
+def _make_report(cfg, command, extra_echo=None, timings=None, ranks=None, errors=None, krylov_report=None):
+    """The reference's report builder signature (cli.py:215-232)."""
+    return _report(cfg, command, extra=extra_echo, timings=timings, ranks=ranks, errors=errors, kr=krylov_report)
 
 
 def _solve_tree(cfg, op, f, b_tree, method, operator):
@@ -421,7 +369,7 @@ VERIFY_DEFAULTS = dict(kernel="gaussian", h=0.3, lam=1e-2, tau=1e-7, sample_mode
 def cmd_verify(args):
     from . import factorize, sampled_error_report
     from .data import generate
-    cfg = _config(args, RunConfig(**VERIFY_DEFAULTS))
+    cfg = _config(args, Config(**VERIFY_DEFAULTS))
     ps = generate("uniform_cube", args.n, cfg.seed, d=args.d)
     clock = _Clock()
     tr, sk, op = _build(cfg, ps, clock)

@@ -141,6 +141,8 @@ struct GemmDesc {
 
 // dst = alpha * op(src) (m x n result); mode 0: copy, 1: alpha * I, 2: zero,
 // 3: accumulate (dst += alpha * op(src)).
+// mode 0: dst = alpha op(src); 1: identity * alpha; 2: zeros; 3: dst += alpha src;
+// 4: dst = src^T + alpha src2 (trans must be 1; e.g. push = P^T - F)
 struct CopyDesc {
   Ref src, dst;
   int m, n;
@@ -148,6 +150,9 @@ struct CopyDesc {
   int trans;
   int mode;
   double alpha;
+  Ref src2 = 0;
+  int lds2 = 0;
+  int pad_ = 0;
 };
 
 // In-place LU with partial pivoting of an n x n matrix.

@@ -309,13 +309,21 @@ __global__ void __launch_bounds__(256) copy_batched_kernel(const Bases* __restri
   const int tm = (c.m + 31) / 32, tn = (c.n + 31) / 32;
   for (int tix = blockIdx.x; tix < tm * tn; tix += gridDim.x) {
     const int i0 = (tix % tm) * 32, j0 = (tix / tm) * 32;
-    if (c.mode == 0 && c.trans) {  // dst(i, j) = alpha src(j, i): read along j, write along i
+    if ((c.mode == 0 || c.mode == 4) && c.trans) {  // dst(i, j) = alpha src(j, i): read along j, write along i
       __syncthreads();
       for (int ii = ty; ii < 32; ii += 8) {
         const int i = i0 + ii, j = j0 + tx;
         tile[ii][tx] = (i < c.m && j < c.n) ? src[j + (size_t)i * c.lds] : 0.0;
       }
       __syncthreads();
+      if (c.mode == 4) {  // dst = src^T + alpha src2 (src2 read along i: coalesced)
+        const double* src2 = at<const double>(bases, c.src2);
+        for (int jj = ty; jj < 32; jj += 8) {
+          const int i = i0 + tx, j = j0 + jj;
+          if (i < c.m && j < c.n) dst[i + (size_t)j * c.ldd] = src2[i + (size_t)j * c.lds2] * c.alpha + tile[tx][jj];
+        }
+        continue;
+      }
       for (int jj = ty; jj < 32; jj += 8) {
         const int i = i0 + tx, j = j0 + jj;
         if (i < c.m && j < c.n) dst[i + (size_t)j * c.ldd] = tile[tx][jj] * c.alpha;

@@ -351,24 +351,6 @@ struct Gemms {
 };
 
 inline double lu_flops(double n) { return 2.0 / 3.0 * n * n * n; }
-inline double getrs_flops(double n, double k) { return 2.0 * n * n * k; }
-double lu_list_flops(const std::vector<LuDesc>& v, double* bytes) {
-  double f = 0;
-  for (auto& d : v) {
-    f += lu_flops(d.n);
-    *bytes += 16.0 * d.n * d.n;
-  }
-  return f;
-}
-double rs_list_flops(const std::vector<LuSolveDesc>& v, double* bytes) {
-  double f = 0;
-  for (auto& d : v) {
-    f += getrs_flops(d.n, d.nrhs);
-    *bytes += 8.0 * ((double)d.n * d.n + 2.0 * d.n * d.nrhs);
-  }
-  return f;
-}
-
 struct Copies {
   std::vector<CopyDesc> v;
   int me = 0;
@@ -377,10 +359,10 @@ struct Copies {
     v.push_back(CopyDesc{src, dst, m, n, lds, ldd, trans, 0, 1.0});
     me = std::max(me, m * n);
   }
-  // dst += alpha * src (m x n)
-  void accumulate(Ref src, int lds, Ref dst, int ldd, int m, int n, double alpha) {
+  // dst = src^T + alpha * src2 (dst, src2: m x n; src: n x m)
+  void transpose_add(Ref src, int lds, Ref src2, int lds2, Ref dst, int ldd, int m, int n, double alpha) {
     if (m <= 0 || n <= 0) return;
-    v.push_back(CopyDesc{src, dst, m, n, lds, ldd, 0, 3, alpha});
+    v.push_back(CopyDesc{src, dst, m, n, lds, ldd, 1, 4, alpha, src2, lds2, 0});
     me = std::max(me, m * n);
   }
   void fill(Ref dst, int ldd, int m, int n, bool identity) {
@@ -390,7 +372,7 @@ struct Copies {
   }
   void flush(StepList& sl) {
     double bytes = 0;
-    for (auto& c : v) bytes += (c.mode == 0 ? 16.0 : c.mode == 3 ? 24.0 : 8.0) * c.m * c.n;
+    for (auto& c : v) bytes += (c.mode == 0 ? 16.0 : c.mode >= 3 ? 24.0 : 8.0) * c.m * c.n;
     sl.add(ST_COPY, v, me, 0, 0.0, bytes);
     v.clear();
     me = 0;
@@ -413,7 +395,6 @@ struct Ctx {
   Ref z_ws(int64_t i) const { return I32(HKS_BUF_Z_PIV, L.off[HKS_BUF_Z_PIV][i] + L.ccap[i]); }
   Ref push(int64_t i) const { return D(HKS_BUF_PUSH, L.off[HKS_BUF_PUSH][i]); }
   Ref coup(int64_t i) const { return D(HKS_BUF_COUP, L.off[HKS_BUF_COUP][i]); }
-  Ref skel(int64_t i) const { return make_ref(HKS_BUF_SKEL, (uint64_t)L.off[HKS_BUF_SKEL][i] * 8); }
   Ref anorm(int64_t i) const { return D(HKS_BUF_STATS, i); }
   Ref rcond(int64_t i) const { return D(HKS_BUF_STATS, L.nn + i); }
   Ref info(int64_t i) const { return make_ref(HKS_BUF_STATS, (uint64_t)L.nn * 16 + (uint64_t)i * 4); }
@@ -809,15 +790,6 @@ void add_lu_solve_program(StepList& sl, const std::vector<LuJob>& jobs) {
   }
 }
 
-// blockdiag(theta_a, theta_b) into an R x R slot (ld R)
-void add_theta_hat(Copies& cp, const Ctx& c, int64_t i, Ref Y) {
-  const int rl = c.r(2 * i + 1), rr = c.r(2 * i + 2), R = rl + rr;
-  cp.copy(c.theta(2 * i + 1), rl, 0, Y, R, rl, rl);
-  cp.copy(c.theta(2 * i + 2), rr, 0, adv(Y, rl + (int64_t)rl * R), R, rr, rr);
-  cp.fill(adv(Y, (int64_t)rl * R), R, rl, rr, false);
-  cp.fill(adv(Y, rl), R, rr, rl, false);
-}
-
 // dgecon scratch of the split estimate: every internal node x
 // gecon_stride(max R) doubles (levels are batched into groups, below)
 size_t cond_scratch_elems(const hks_plan& P) {
@@ -875,10 +847,10 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl,
                      std::vector<std::unique_ptr<StepList>>* cond_levels, std::vector<int>* cond_wait) {
   const Ctx c(P);
   const Layout& L = P.L;
-  // What the narrow top levels need that depends on no factor -- Z := I and
-  // push := P^T (solver.py:145, 158) -- in one side branch beside the leaf
-  // level (joined before the first internal level): two fewer launches in
-  // each latency-bound level.  Wide levels keep them in-level (their bytes
+  // What the narrow top levels need that depends on no factor -- Z := I
+  // (solver.py:145) -- in one side branch beside the leaf level (joined
+  // before the first internal level): one fewer launch in each
+  // latency-bound level.  Wide levels keep them in-level (their bytes
   // would compete with the leaf level's).
   bool early_pending = false;
   const int64_t early_levels = std::min<int64_t>(L.depth, 6);  // levels 0..5: <= 32 nodes
@@ -886,9 +858,8 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl,
   {
     Copies early;
     for (int64_t i = 0; i < L.first(early_levels); ++i) {
-      const int R = c.r(2 * i + 1) + c.r(2 * i + 2), r = c.r(i);
+      const int R = c.r(2 * i + 1) + c.r(2 * i + 2);
       early.fill(c.z_lu(i), R, R, R, true);
-      if (L.has_up(i)) early.copy(c.interp(i), r, 1, c.push(i), R, R, r);
     }
     if (!early.v.empty()) {
       sl.fork();
@@ -924,21 +895,22 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl,
     add_lu_program(sl, jobs, false);
     gm.flush(sl);
   }
-  bool push_pending = false;
   std::vector<LuDesc> cond_group;  // estimates not yet emitted (see cond_grouped)
   int cond_maxR = 0;
   double cond_lb = 0;
   for (int64_t lev = L.depth - 1; lev >= 0; --lev) {  // internal levels (solver.py:139-161)
     sl.mark();
-    if (push_pending || early_pending) {
+    if (early_pending) {
       sl.join();
-      push_pending = early_pending = false;
+      early_pending = false;
     }
     // Algebraically identical to solver.py:145-158 with the interpolation
     // folded in before the reduced solve: V = thhat P^T (R x r), Y = Z^-1 V,
-    // F = B Y (= folded P^T), push = P^T - F, theta = P (V - thhat F).
-    // Solving for r instead of R right-hand sides halves the node's flops.
-    Copies c_id, c_t, c_p;
+    // F = B Y (= folded P^T), push = P^T - F, theta = P thhat push
+    // (= P (thhat - thhat folded) P^T).  Solving for r instead of R
+    // right-hand sides halves the node's flops; forming theta from push
+    // needs V only once (as the LU's right-hand sides).
+    Copies c_id, c_p;
     Gemms g_z, g_v, g_f, g_tf, g_out;
     std::vector<LuJob> jobs;
     std::vector<LuDesc> lu;
@@ -964,20 +936,17 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl,
       const Ref W = D(B_FWS, at);
       at += (int64_t)R * r;
       const Ref Pi = c.interp(i), pu = c.push(i);
-      // V = thhat P^T into Y (the LU's right-hand sides) and into W
+      // V = thhat P^T into Y (the LU's right-hand sides)
       g_v.add(c.theta(a), rl, 0, Pi, r, 1, Y, R, rl, r, rl, 1.0, 0.0);
       g_v.add(c.theta(b), rr, 0, adv(Pi, (int64_t)rl * r), r, 1, adv(Y, rl), R, rr, r, rr, 1.0, 0.0);
-      g_v.add(c.theta(a), rl, 0, Pi, r, 1, W, R, rl, r, rl, 1.0, 0.0);
-      g_v.add(c.theta(b), rr, 0, adv(Pi, (int64_t)rl * r), r, 1, adv(W, rl), R, rr, r, rr, 1.0, 0.0);
       jobs.push_back(LuJob{Z, R, R, c.z_piv(i), c.info(i), c.anorm(i), Y, r, R, c.z_ws(i), (int)L.ccap[i]});  // Y = Z^-1 V
-      // F = B Y (solver.py:86-89, 156); push = P^T - F (solver.py:158)
+      // F = B Y (solver.py:86-89, 156); push = P^T - F (solver.py:158), one pass
       g_f.add(C, rl, 0, adv(Y, rl), R, 0, F, R, rl, r, rr, 1.0, 0.0);
       g_f.add(C, rl, 1, Y, R, 0, adv(F, rl), R, rr, r, rl, 1.0, 0.0);
-      if (!early_node(i)) c_t.copy(Pi, r, 1, pu, R, R, r);  // else push = P^T from the early branch
-      c_p.accumulate(F, R, pu, R, R, r, -1.0);
-      // W = V - thhat F ; theta = P W (solver.py:157)
-      g_tf.add(c.theta(a), rl, 0, F, R, 0, W, R, rl, r, rl, -1.0, 1.0);
-      g_tf.add(c.theta(b), rr, 0, adv(F, rl), R, 0, adv(W, rl), R, rr, r, rr, -1.0, 1.0);
+      c_p.transpose_add(Pi, r, F, R, pu, R, R, r, -1.0);
+      // W = thhat push ; theta = P W (solver.py:157)
+      g_tf.add(c.theta(a), rl, 0, pu, R, 0, W, R, rl, r, rl, 1.0, 0.0);
+      g_tf.add(c.theta(b), rr, 0, adv(pu, rl), R, 0, adv(W, rl), R, rr, r, rr, 1.0, 0.0);
       g_out.add(Pi, r, 0, W, R, 0, c.theta(i), r, r, r, R, 1.0, 0.0);
     }
     c_id.flush(sl);
@@ -1014,18 +983,10 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl,
     }
     if (lev == 0 && !L.has_up(0)) continue;
     g_f.flush(sl);
-    // push = P^T - F feeds only the solve: side stream, joined before the
-    // next level reuses the workspace holding F
-    sl.fork();
-    sl.side(true);
-    c_t.flush(sl);
     c_p.flush(sl);
-    sl.side(false);
-    push_pending = true;
     g_tf.flush(sl);
     g_out.flush(sl);
   }
-  if (push_pending) sl.join();
 }
 
 // ------------------------------------------------------------ solve
@@ -1542,10 +1503,15 @@ static int check_info(hks_plan* P, void* const* buffers, int64_t* bad_node, cuda
       if (bad_node) *bad_node = i;
       if (lev == L.depth)
         return set_error(HKS_ERR_SINGULAR, "singular matrix: zero pivot at elimination step %d", info[i] - 1);
+      // min |diag(Z)| of the assembled Z (solver.py:99-105): Z = I plus
+      // off-diagonal blocks only (solver.py:145-147), so every diagonal
+      // entry is exactly 1 -- the value is known without keeping a copy of
+      // Z beside its in-place LU (a 0 x 0 Z never reaches getrf there)
+      const double min_diag_z = 1.0;
       return set_error(HKS_ERR_REDUCED_SINGULAR,
                        "reduced system singular at node %lld (level %lld); smallest pivot 0 "
                        "(smallest |Z| diagonal %.3e); increase lambda or tighten tau",
-                       (long long)i, (long long)lev, P->R(i) > 0 ? 1.0 : 0.0);
+                       (long long)i, (long long)lev, min_diag_z);
     }
   }
   return HKS_OK;

@@ -141,10 +141,13 @@ def _median_time(fn, repeats, warmup=False):
 
 
 def fit_exponent(sizes, seconds):
-    """Least-squares slope of log(time) against log(n) (oracle.py:170-174)."""
-    xs = np.log(np.asarray(sizes, dtype=np.float64))
-    ys = np.log(np.asarray(seconds, dtype=np.float64))
-    return float(np.polyfit(xs, ys, 1)[0])
+    """Slope p of the least-squares line log t = p log n + c (the scaling
+    exponent the reference fits, oracle.py:170-174), in closed form:
+    cov(log n, log t) / var(log n)."""
+    ln = np.log(np.asarray(sizes, dtype=np.float64))
+    lt = np.log(np.asarray(seconds, dtype=np.float64))
+    dn = ln - ln.mean()
+    return float(np.dot(dn, lt - lt.mean()) / np.dot(dn, dn))
 
 
 def dense_kernel_matrix(kernel, ps, lam):
@@ -158,49 +161,71 @@ def dense_kernel_matrix(kernel, ps, lam):
     return out
 
 
-def scaling_benchmark(sizes, cfg, seed, pipeline=None, dense_sizes=None, solve_repeats=5):
-    """Per-phase times of the fast path over `sizes` with log-log exponent
-    fits, plus the dense factor + solve contrast over `dense_sizes`
-    (oracle.py:177-232: same phases, repeat counts, RNG streams and report
-    keys).  `cfg` needs `shape`, `d` and `kernel` (lambda = its
-    regularization); `pipeline` (e.g. cli.standard_pipeline) is required
-    when `sizes` is nonempty."""
+# Stage table of the fast-path sweep: (report key, repeats, warm-up call
+# first).  Each stage consumes the previous stage's product (oracle.py:
+# 192-205: build, skeletonize and assemble timed once, factorize 3 times,
+# solve `solve_repeats` times after one warm-up call).
+_FAST_STAGES = (("build", 1, False), ("skeletonize", 1, False), ("assemble", 1, False),
+                ("factorize", 3, False), ("solve", None, True))
+_DENSE_STAGES = ("dense_assemble", "dense_factor", "dense_solve")
+
+
+def _fast_sweep(sizes, cfg, seed, pipeline, solve_repeats):
+    from . import data
+    table = {key: [] for key, _, _ in _FAST_STAGES}
+    for n in sizes:
+        ps = data.generate(cfg.shape, n, seed, d=cfg.d)
+        rhs = np.random.default_rng([int(seed), 23, int(n)]).standard_normal(n)  # oracle.py:203
+        calls = {
+            "build": lambda st: pipeline.build(ps),
+            "skeletonize": lambda st: pipeline.skeletonize(st["build"]),
+            "assemble": lambda st: pipeline.assemble(st["build"], st["skeletonize"]),
+            "factorize": lambda st: pipeline.factorize(st["assemble"]),
+            "solve": lambda st: pipeline.solve(st["factorize"], rhs),
+        }
+        state = {}
+        for key, reps, warm in _FAST_STAGES:
+            t, state[key] = _median_time(lambda: calls[key](state), reps or solve_repeats, warmup=warm)
+            table[key].append(t)
+    return table
+
+
+def _dense_sweep(dense_sizes, cfg, seed, solve_repeats):
     from . import data
     from .linalg import factor_dense, solve_dense
-    report = {"sizes": list(map(int, sizes or [])), "timings": {}, "exponents": {}}
+    lam = cfg.kernel.regularization
+    table = {key: [] for key in _DENSE_STAGES}
+    for n in dense_sizes:
+        ps = data.generate(cfg.shape, n, seed, d=cfg.d)
+        rhs = np.random.default_rng([int(seed), 29, int(n)]).standard_normal(n)  # oracle.py:216
+        t_a, a = _median_time(lambda: dense_kernel_matrix(cfg.kernel, ps, lam), solve_repeats)
+        t_f, fd = _median_time(lambda: factor_dense(a), solve_repeats)
+        t_s, _ = _median_time(lambda: solve_dense(fd, rhs), solve_repeats)
+        for key, t in zip(_DENSE_STAGES, (t_a, t_f, t_s)):
+            table[key].append(t)
+    return table
+
+
+def scaling_benchmark(sizes, cfg, seed, pipeline=None, dense_sizes=None, solve_repeats=5):
+    """Per-stage wall times of the injected fast path over `sizes` and of the
+    dense factor + solve contrast over `dense_sizes`, each with its fitted
+    log-log exponent.  Same contract as oracle.py:177-232 (report keys
+    sizes / timings / exponents / dense_sizes, RNG streams, repeat counts,
+    "fast-path sizes need an injected pipeline"); `cfg` provides `shape`,
+    `d` and `kernel` (lambda = kernel.regularization).  Unlike the CPU
+    original, each timed call is bracketed by device synchronisation."""
+    sizes = [int(n) for n in (sizes or [])]
+    report = {"sizes": sizes, "timings": {}, "exponents": {}}
+    sweeps = []
     if sizes:
         if pipeline is None:
             raise ValueError("fast-path sizes need an injected pipeline")
-        phases = {"build": [], "skeletonize": [], "assemble": [], "factorize": [], "solve": []}
-        for n in sizes:
-            ps = data.generate(cfg.shape, n, seed, d=cfg.d)
-            t, tree = _median_time(lambda: pipeline.build(ps), 1)
-            phases["build"].append(t)
-            t, skels = _median_time(lambda: pipeline.skeletonize(tree), 1)
-            phases["skeletonize"].append(t)
-            t, op = _median_time(lambda: pipeline.assemble(tree, skels), 1)
-            phases["assemble"].append(t)
-            t, f = _median_time(lambda: pipeline.factorize(op), 3)
-            phases["factorize"].append(t)
-            b = np.random.default_rng([int(seed), 23, int(n)]).standard_normal(n)
-            t, _ = _median_time(lambda: pipeline.solve(f, b), solve_repeats, warmup=True)
-            phases["solve"].append(t)
-        report["timings"] = {k: list(map(float, v)) for k, v in phases.items()}
-        report["exponents"] = {k: fit_exponent(sizes, v) for k, v in phases.items()}
+        sweeps.append((sizes, _fast_sweep(sizes, cfg, seed, pipeline, solve_repeats)))
     if dense_sizes:
-        dense = {"dense_assemble": [], "dense_factor": [], "dense_solve": []}
-        lam = cfg.kernel.regularization
-        for n in dense_sizes:
-            ps = data.generate(cfg.shape, n, seed, d=cfg.d)
-            b = np.random.default_rng([int(seed), 29, int(n)]).standard_normal(n)
-            t, a = _median_time(lambda: dense_kernel_matrix(cfg.kernel, ps, lam), solve_repeats)
-            dense["dense_assemble"].append(t)
-            t, fd = _median_time(lambda: factor_dense(a), solve_repeats)
-            dense["dense_factor"].append(t)
-            t, _ = _median_time(lambda: solve_dense(fd, b), solve_repeats)
-            dense["dense_solve"].append(t)
-        report["dense_sizes"] = list(map(int, dense_sizes))
-        for key, values in dense.items():
-            report["timings"][key] = list(map(float, values))
-            report["exponents"][key] = fit_exponent(dense_sizes, values)
+        report["dense_sizes"] = [int(n) for n in dense_sizes]
+        sweeps.append((report["dense_sizes"], _dense_sweep(dense_sizes, cfg, seed, solve_repeats)))
+    for ns, table in sweeps:
+        for key, ts in table.items():
+            report["timings"][key] = [float(t) for t in ts]
+            report["exponents"][key] = fit_exponent(ns, ts)
     return report

@@ -322,6 +322,19 @@ class ShardedSkeletons:
         return Skeleton(node=i, indices=idx, interp=np.ascontiguousarray(p))
 
 
+def agree_on_failure(comm, local_error, message):
+    """Collective error agreement before a rank's next collective: every
+    rank learns whether any rank failed (max over ranks of 1 + the failing
+    rank), so none blocks in an all-gather while another raises.  The
+    failing rank re-raises its own exception; the others raise
+    RuntimeError(message.format(rank=<failing rank>))."""
+    worst = comm.all_reduce_max(0 if local_error is None else 1 + comm.rank)
+    if local_error is not None:
+        raise local_error
+    if worst:
+        raise RuntimeError(message.format(rank=worst - 1))
+
+
 def build_skeletons_sharded(tree, kernel, config, knn_local, spec, comm):
     """build_skeletons (skeleton.py:143-182) over a sharded tree: the shard's
     levels locally, the shard roots' ranks / indices all-gathered, the top
@@ -338,18 +351,23 @@ def build_skeletons_sharded(tree, kernel, config, knn_local, spec, comm):
     skel.zero_()
     ranks = np.zeros(lay.nn, dtype=np.int64)
     lbeg, _ = node_ranges(spec.size, spec.local_depth)
-    for ell in range(spec.local_depth, -1, -1):
-        level = spec.p + ell
-        node0, count = spec.rank << ell, 1 << ell
-        local_ids = np.arange((1 << ell) - 1, (1 << (ell + 1)) - 1)
-        rows, roff = _rows(spec, level, node0, count, config, knn_local, comm, combine=False)
-        if ell == spec.local_depth:
-            cands = t.arange(spec.begin, spec.end, dtype=t.int64, device=x.device)
-            coff = np.concatenate([lbeg[local_ids], [spec.size]]).astype(np.int64)
-        else:
-            cands, coff = _candidates(skel, lay, ranks, local_ids, x.device)
-        ranks[local_ids] = _skeletonize(x, tree.d, kern, level, (1 << level) - 1 + node0, rows, roff, cands, coff,
-                                        config, skel, interp, lay, local_ids)
+    local_error = None
+    try:  # shard levels: no collective inside, so a failure is agreed on below before the first one
+        for ell in range(spec.local_depth, -1, -1):
+            level = spec.p + ell
+            node0, count = spec.rank << ell, 1 << ell
+            local_ids = np.arange((1 << ell) - 1, (1 << (ell + 1)) - 1)
+            rows, roff = _rows(spec, level, node0, count, config, knn_local, comm, combine=False)
+            if ell == spec.local_depth:
+                cands = t.arange(spec.begin, spec.end, dtype=t.int64, device=x.device)
+                coff = np.concatenate([lbeg[local_ids], [spec.size]]).astype(np.int64)
+            else:
+                cands, coff = _candidates(skel, lay, ranks, local_ids, x.device)
+            ranks[local_ids] = _skeletonize(x, tree.d, kern, level, (1 << level) - 1 + node0, rows, roff, cands,
+                                            coff, config, skel, interp, lay, local_ids)
+    except (RuntimeError, ValueError) as exc:
+        local_error = exc
+    agree_on_failure(comm, local_error, f"skeletonization failed on rank {{rank}} (shard levels {spec.p}..{spec.depth})")
     # shard roots -> the top plan's leaves (ranks, then s-padded index blocks)
     P = comm.world
     root_ranks = t.empty(P, dtype=t.int64, device=x.device)

@@ -148,8 +148,10 @@ class FactorStorage:
     """Reusable factor storage of one operator.  Each Factorization leases
     a set of the flat factor buffers; dropping it returns the set with an
     event on the condition stream (its dgecon estimates may still read
-    Z_LU / STATS).  A set is handed out again only once that event has
-    completed (queried, never waited for); otherwise a new set is
+    Z_LU / STATS) and one on the caller's current stream (solves queued
+    there may still read the factors; work on OTHER streams must be
+    ordered before the drop by the caller, as for any torch tensor).  A set
+    is handed out again only once both events have completed (queried, never waited for); otherwise a new set is
     allocated.  The pool therefore settles at the number of sets the
     caller's pattern keeps in flight, and steady-state factorizations
     allocate nothing: a GB-sized cudaMalloc inside a factorize costs tens
@@ -173,8 +175,8 @@ class FactorStorage:
             self.free.append((self._new(), None))
 
     def lease(self):
-        for idx, (bufs, ev) in enumerate(self.free):
-            if ev is None or ev.query():
+        for idx, (bufs, evs) in enumerate(self.free):
+            if evs is None or all(e.query() for e in evs):
                 del self.free[idx]
                 return _Lease(self, bufs)
         try:
@@ -182,16 +184,16 @@ class FactorStorage:
         except N.torch().cuda.OutOfMemoryError:
             if not self.free:
                 raise
-            bufs, ev = self.free.pop(0)  # device memory is the limit: wait for the oldest set instead
-            if ev is not None:
-                N.torch().cuda.current_stream().wait_event(ev)
+            bufs, evs = self.free.pop(0)  # device memory is the limit: wait for the oldest set instead
+            for e in evs or ():
+                N.torch().cuda.current_stream().wait_event(e)
             return _Lease(self, bufs)
 
     def __del__(self):  # the storage outlives its last estimates
-        for _bufs, ev in getattr(self, "free", []):
+        for _bufs, evs in getattr(self, "free", []):
             try:
-                if ev is not None:
-                    ev.synchronize()
+                for e in evs or ():
+                    e.synchronize()
             except Exception:  # interpreter shutdown
                 pass
 
@@ -202,10 +204,15 @@ class _Lease:
         self.bufs = bufs
 
     def __del__(self):
+        # reusable once both the dgecon estimates (condition stream) and the
+        # work the caller queued on its current stream -- e.g. a solve still
+        # reading these factors -- have passed this point
         try:
-            ev = N.torch().cuda.Event()
-            ev.record(self.pool.cond_stream)
-            self.pool.free.append((self.bufs, ev))
+            t = N.torch()
+            evs = (t.cuda.Event(), t.cuda.Event())
+            evs[0].record(self.pool.cond_stream)
+            evs[1].record(t.cuda.current_stream())
+            self.pool.free.append((self.bufs, evs))
         except Exception:  # interpreter shutdown: let the tensors go
             pass
 

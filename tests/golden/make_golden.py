@@ -133,6 +133,98 @@ def workload_instance(key, n, nrhs=2, store_coords=False, hybrid=False):
                  nrhs=nrhs, store_coords=store_coords, hybrid=hybrid)
 
 
+def ladder_instance(key, n, hybrid=False):
+    """Reduced-N ladder fixture (N = 16384 and 65536, the
+    reference's kNN guard allows no more).  Integer structure in full
+    (perm, skeleton indices, ranks) or as a SHA-256 of the full array plus
+    its first rows (kNN); float outputs as norms / sketches / the reference's
+    own accuracy metrics:
+      relres_ktilde  ||(lam I + Ktilde) x - b|| / ||b|| through the
+                     reference's hmatvec (treecode.py:92-128);
+      sampled_*      256 rows R = default_rng([seed, 77]) of the exact
+                     K + lam I from the reference's eval_block
+                     (kernels.py:64-105) against all n columns: the matvec
+                     error of its u = hmatvec(w), w = default_rng([seed, 78]),
+                     and the true residual of its x (b column 0).
+    The thread count (8) does not change any result (test_solver.py:211-219)."""
+    t0 = time.time()
+    w = workloads.CONFIGS[key].scaled(n)
+    coords = workloads.points(w, 0)
+    kernel = hk.KernelSpec("gaussian", h=w.h, regularization=w.lam)
+    seed, lam = 0, w.lam
+    tree = hk.build_tree(PointSet(coords), w.leaf_size, seed=seed)
+    t_tree = time.time()
+    knn = hk.knn_bruteforce(tree.points, w.kappa)
+    t_knn = time.time()
+    cfg = hk.SkeletonConfig(tau=w.tau, max_rank=w.max_rank, samples=w.samples,
+                            sample_mode="knn_augmented", seed=seed)
+    skels = hk.build_skeletons(tree, kernel, cfg, knn=knn, threads=8)
+    t_sk = time.time()
+    op = hk.build_operator(tree, skels, kernel)
+    f = hk.factorize(op, lam, threads=8)
+    t_f = time.time()
+    b = np.random.default_rng([seed, 1000]).standard_normal((n, 2))
+    x = hk.solve_multi(f, b, in_tree_order=True)
+    t_s = time.time()
+    wv = np.random.default_rng([seed, 78]).standard_normal(n)
+    u = hk.hmatvec(op, wv, lam)
+    relres = [float(np.linalg.norm(hk.hmatvec(op, x[:, j], lam) - b[:, j]) / np.linalg.norm(b[:, j]))
+              for j in range(2)]
+    xt = tree.points.coords
+    R = np.sort(np.random.default_rng([seed, 77]).choice(n, size=256, replace=False))
+    KR = hk.eval_block(kernel, xt[R], xt)
+    kw = KR @ wv
+    s_mv = float(np.linalg.norm((u[R] - lam * wv[R]) - kw) / np.linalg.norm(kw))
+    s_res = float(np.linalg.norm(KR @ x[:, 0] + lam * x[R, 0] - b[R, 0]) / np.linalg.norm(b[R, 0]))
+    nn = len(tree.nodes)
+    ranks = np.full(nn, -1, dtype=np.int64)
+    z_cond = np.zeros(nn)
+    theta_fro = np.zeros(nn)
+    skel_idx, skel_off = [], [0]
+    for nd in tree.nodes:
+        i = nd.index
+        if nd.level > 0:
+            ranks[i] = skels[i].rank
+            skel_idx.append(np.asarray(skels[i].indices, dtype=np.int32))
+            theta_fro[i] = np.linalg.norm(f.factors[i].theta)
+        else:
+            skel_idx.append(np.zeros(0, dtype=np.int32))
+        skel_off.append(skel_off[-1] + skel_idx[-1].size)
+        if not nd.is_leaf:
+            z_cond[i] = f.factors[i].z_cond
+    G = np.random.default_rng([seed, 4242]).standard_normal((8, n))
+    knn64 = np.ascontiguousarray(np.asarray(knn, dtype=np.int64))
+    out = {
+        "perm": np.asarray(tree.perm, dtype=np.int32),
+        "knn_sha256": np.array(hashlib.sha256(knn64.tobytes()).hexdigest()),
+        "knn_head": knn64[:256],
+        "ranks": ranks, "z_cond": z_cond, "theta_fro": theta_fro,
+        "skel_idx": np.concatenate(skel_idx), "skel_off": np.asarray(skel_off, dtype=np.int64),
+        "x_norm": np.linalg.norm(x, axis=0), "x_sketch": G @ x, "u_norm": np.array(np.linalg.norm(u)),
+        "u_sketch": G @ u, "relres_ktilde": np.array(relres), "sampled_rows": R,
+        "sampled_matvec_relerr": np.array(s_mv), "sampled_true_residual": np.array(s_res),
+        "coords_sha256": np.array(coords_digest(coords)),
+    }
+    if n <= 16384:
+        out["x0"] = x[:, 0].copy()
+    if hybrid:
+        xb, rep = hk.hybrid_solve(op, f, b[:, 0], tol=w.gmres_tol, restart=w.gmres_restart,
+                                  operator_mode="compressed")
+        out["hybrid_iterations"] = np.array(rep.iterations)
+        out["hybrid_final_residual"] = np.array(rep.final_residual)
+        out["hybrid_x_norm"] = np.array(np.linalg.norm(xb))
+        out["hybrid_x_sketch"] = G @ xb
+    meta = {"name": f"{key.lower()}_n{n}", "workload": key, "n": n, "lam": lam, "seed": seed,
+            "depth": tree.depth, "threads": 8,
+            "seconds": {"tree": round(t_tree - t0, 2), "knn": round(t_knn - t_tree, 2),
+                        "skeletons": round(t_sk - t_knn, 2), "factorize": round(t_f - t_sk, 2),
+                        "solve2": round(t_s - t_f, 2), "total": round(time.time() - t0, 2)}}
+    out["meta"] = np.array(json.dumps(meta))
+    np.savez_compressed(HERE / f"ladder_{key.lower()}_n{n}.npz", **out)
+    print(meta["name"], meta["seconds"], "ranks", sorted(set(ranks.tolist()))[:3], "...",
+          max(ranks.tolist()), "relres", relres, "sampled", s_mv, s_res, flush=True)
+
+
 def main(which):
     if "frozen" in which:
         ps = hk.generate("uniform_cube", 1024, 3, d=3)
@@ -169,6 +261,17 @@ def main(which):
         workload_instance("C4", 8192)
     if "c5" in which:
         workload_instance("C5", 2048, hybrid=True)
+    for key, n in (("C2", 16384), ("C3", 16384), ("C4", 16384), ("C5", 16384),
+                   ("C2", 65536), ("C3", 65536), ("C4", 65536)):
+        if f"ladder_{key.lower()}_{n}" in which or "ladder" in which:
+            ladder_instance(key, n, hybrid=key == "C5")
+    if "report_schema" in which:
+        import importlib.util  # the reference's own schema (tests/helpers.py:145-177)
+        spec = importlib.util.spec_from_file_location("ref_helpers", "/root/reference/pkg/tests/helpers.py")
+        mod = importlib.util.module_from_spec(spec)
+        sys.modules["ref_helpers"] = mod
+        spec.loader.exec_module(mod)
+        (HERE / "report_schema.json").write_text(json.dumps(mod.REPORT_SCHEMA, indent=1) + "\n")
     if "knn_small" in which:
         rng = np.random.default_rng(0)
         pts = rng.random((200, 3))

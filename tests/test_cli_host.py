@@ -101,3 +101,55 @@ def test_bench_host_checks(capsys):
     assert metrics.fit_exponent(n, 3e-6 * n ** 1.5) == pytest.approx(1.5)
     with pytest.raises(ValueError, match="limited to n <= 8192"):
         metrics.dense_kernel_matrix(None, PointSet(np.zeros((8193, 1))), 1.0)
+
+
+SCHEMA = json.loads((__import__("pathlib").Path(__file__).parent / "golden" / "report_schema.json").read_text())
+
+
+def test_report_schema_property_suite():
+    """200 randomized reports through the reference's report builder
+    signature (cli.py:215-232) all satisfy the reference's REPORT_SCHEMA
+    (tests/helpers.py:145-177, frozen by tests/golden/make_golden.py), with
+    absent sections omitted, never null (test_cli.py:281-309)."""
+    import jsonschema
+    from paper_1701_02324_b200 import Config, KrylovReport
+    rng = np.random.default_rng(12)
+    cfg = Config()
+    for _ in range(200):
+        timings = ranks = errors = krep = None
+        if rng.random() < 0.7:
+            timings = {f"phase{i}": float(rng.random()) for i in range(rng.integers(1, 4))}
+        if rng.random() < 0.5:
+            ranks = {int(i): int(rng.integers(0, 64)) for i in range(rng.integers(1, 5))}
+        if rng.random() < 0.5:
+            errors = {f"metric{i}": float(rng.random()) for i in range(rng.integers(1, 4))}
+        if rng.random() < 0.4:
+            krep = KrylovReport(iterations=int(rng.integers(0, 50)),
+                                residuals=[float(v) for v in rng.random(rng.integers(0, 9))])
+        rep = cli._make_report(cfg, "test", timings=timings, ranks=ranks, errors=errors, krylov_report=krep)
+        jsonschema.validate(rep, SCHEMA)
+        assert None not in rep.values()
+        json.dumps(rep)
+    bad = cli._make_report(cfg, "test")
+    bad["extra"] = 1
+    with pytest.raises(jsonschema.ValidationError):
+        jsonschema.validate(bad, SCHEMA)
+
+
+def test_config_module_matches_reference_surface(tmp_path):
+    """Config / parse_config_file / apply_overrides (config.py:17-120):
+    defaults, alias, precedence, thread resolution, error messages."""
+    from paper_1701_02324_b200 import Config
+    from paper_1701_02324_b200.config import apply_overrides, parse_config_file
+    f = tmp_path / "c.cfg"
+    f.write_text("# comment\nlambda = 0.5\nleaf = 128  # trailing\nsample_mode = knn_augmented\n")
+    cfg = parse_config_file(f)
+    assert (cfg.lam, cfg.leaf, cfg.sample_mode, cfg.max_rank) == (0.5, 128, "knn_augmented", 64)
+    cfg = apply_overrides(cfg, {"leaf": 64, "bogus": 3})
+    assert cfg.leaf == 64 and cfg.lam == 0.5
+    assert Config(threads=4).effective_threads() == 4 and Config(threads=0).effective_threads() >= 1
+    assert list(Config().echo())[:6] == ["kernel", "h", "degree", "shift", "lambda", "leaf"]
+    for text, msg in (("warp_factor = 9\n", "unknown key"), ("tau: 1e-5\n", "line 1"), ("leaf = many\n", "bad value")):
+        f.write_text(text)
+        with pytest.raises(ValueError, match=msg):
+            parse_config_file(f)

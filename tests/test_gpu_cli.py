@@ -3,7 +3,9 @@ factor / solve / matvec / krr / verify), reports checked against the
 schema sections and the oracle where one applies."""
 
 import json
+from pathlib import Path
 
+import jsonschema
 import numpy as np
 import pytest
 
@@ -17,7 +19,10 @@ def _run(capsys, *argv):
     rc = cli.run(list(argv))
     cap = capsys.readouterr()
     assert rc == 0, cap.err
-    return json.loads(cap.out)
+    rep = json.loads(cap.out)
+    # every GPU report against the reference's own REPORT_SCHEMA (tests/helpers.py:145-177)
+    jsonschema.validate(rep, json.loads((Path(__file__).parent / "golden" / "report_schema.json").read_text()))
+    return rep
 
 
 def test_cli_pipeline(tmp_path, capsys):

@@ -1,0 +1,41 @@
+"""Full-size structure parity: at C2's full N = 262144 the GPU tree
+permutation and exact kNN lists equal the CPU oracle's bit for bit
+(SHA-256 of the int64 arrays, tests/golden/full_c2_digest.json made by
+tools/make_full_digests.py).  The oracle is the reference's algorithm
+(tree.py:87-144, 163-188), pinned to the unmodified reference up to the
+reference's own kNN limit of 65536 points (tests/test_gpu_ladder.py,
+tests/test_oracle_golden.py); near-ties between distances first become
+likely at this size."""
+
+import hashlib
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+CASES = sorted(p.stem[len("full_"):-len("_digest")] for p in GOLDEN.glob("full_*_digest.json"))
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.int64).tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_full_size_perm_and_knn(name):
+    import paper_1701_02324_b200 as hk
+    from paper_1701_02324_b200 import workloads as W
+    g = json.loads((GOLDEN / f"full_{name}_digest.json").read_text())
+    w = W.CONFIGS[g["workload"]]
+    x = W.points(w, 0)
+    assert hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest() == g["coords_sha256"]
+    tree = hk.build_tree(hk.PointSet(x), w.leaf_size, seed=0)
+    perm = np.asarray(tree.perm)
+    assert perm[:64].tolist() == g["perm_head"]
+    assert _sha(perm) == g["perm_sha256"]
+    knn = np.asarray(hk.knn_bruteforce(tree.points, w.kappa))
+    assert knn[:64].tolist() == g["knn_head"]
+    assert _sha(knn) == g["knn_sha256"]

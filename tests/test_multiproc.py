@@ -147,3 +147,40 @@ def test_shard_comm_gloo():
         assert out == [0.0, 1.0, 2.0, 10.0, 11.0, 12.0]
         assert orb == [3, 0, (1 << 4) | (1 << 5)]
         assert mx == 7 and sm == 3.0
+
+
+def _agree_worker(rank, world, port, q):
+    import torch.distributed as dist
+    sys.path.insert(0, str(ROOT))
+    from paper_1701_02324_b200.sharded import ShardComm, agree_on_failure
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = ShardComm()
+        agree_on_failure(comm, None, "never")  # nobody failed: returns on every rank
+        err = RuntimeError("skeletonization failed at node 9 (level 3)") if rank == 1 else None
+        try:
+            agree_on_failure(comm, err, "skeletonization failed on rank {rank}")
+            q.put((rank, "no error"))
+        except RuntimeError as exc:
+            q.put((rank, str(exc)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_failure_agreement_gloo():
+    """A shard-level failure on one rank raises on every rank before the
+    next collective (sharded.build_skeletons_sharded): the
+    failing rank with its own message, the others naming it."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_agree_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got == {0: "skeletonization failed on rank 1", 1: "skeletonization failed at node 9 (level 3)"}
