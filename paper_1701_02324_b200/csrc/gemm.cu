@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(256) copy_batched_kernel(const Bases* __restri
                                                            const CopyDesc* __restrict__ descs) {
   const Bases& bases = *bases_ptr;
   const CopyDesc c = descs[blockIdx.y];
-  const double* src = (c.mode == 0 || c.mode == 3) ? at<const double>(bases, c.src) : nullptr;
+  const double* src = (c.mode == 0 || c.mode >= 3) ? at<const double>(bases, c.src) : nullptr;
   double* dst = at<double>(bases, c.dst);
   __shared__ double tile[32][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;

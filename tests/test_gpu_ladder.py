@@ -10,9 +10,9 @@ fixtures made by the UNMODIFIED reference (tests/golden/make_golden.py,
   GPU's within a factor 10 either way, no absolute floor;
 * the sampled-row metrics (256 rows of the exact K + lam I, BASELINE.md
   4.2): within a factor 1.5 of the reference's;
-* x against the reference's x: relative difference within the forward
-  error bound of two backward-stable solves, 100 x cond-free estimate
-  relres_ref * ||b|| / (lam ||x||) ... stated per case below (RTOL_X);
+* x against the reference's x (sketches on 8 Gaussian vectors, the whole x
+  at N = 16384): within 1e-6 relative -- both solve the same Ktilde system,
+  whose reduced matrices reach z_cond ~ 1e6 at C3;
 * C5: the hybrid GMRES iteration count equals the reference's.
 """
 
@@ -75,9 +75,53 @@ def test_ladder_structure_bit_exact(name):
     ranks = skels.ranks
     assert np.array_equal(ranks[1:], g["ranks"][1:])
     off, idx = g["skel_off"], g["skel_idx"]
-    diff = [i for i in range(1, len(ranks))
-            if not np.array_equal(np.asarray(skels[i].indices), idx[off[i]: off[i + 1]].astype(np.int64))]
-    assert not diff, f"skeleton index sets differ at nodes {diff[:10]}"
+    ref = {i: idx[off[i]: off[i + 1]].astype(np.int64) for i in range(1, len(ranks))}
+    diff = [i for i in range(1, len(ranks)) if not np.array_equal(np.asarray(skels[i].indices), ref[i])]
+    # "skeleton index sets must match except where pivots tie" (north star):
+    # every node whose candidates are the reference's and whose pivot
+    # sequence still differs must diverge at a near-tie of two column norms
+    # (audited with the oracle's QRCP, linalg.py:43-104); its ancestors may
+    # then differ too (their candidates do).
+    tainted = set()
+    for i in sorted(diff, reverse=True):
+        kids = (2 * i + 1, 2 * i + 2)
+        if tree.nodes[i].is_leaf or not (set(kids) & tainted):
+            gap = _tie_gap(w, tree, knn, i, np.asarray(skels[i].indices), ref[i], ref)
+            assert gap <= 1e-10, f"node {i}: pivot sequences diverge at a column-norm gap of {gap:.2e}"
+        tainted.add(i)
+
+
+def _tie_gap(w, tree, knn, i, got, want, ref):
+    """Relative column-norm gap at the first step where the GPU's pivot
+    sequence `got` leaves the reference's `want` for node i: the oracle's
+    QRCP (from-scratch norms, oracle/hks_oracle.py) is advanced along the
+    reference's pivots and the residual norms of the two competing columns
+    compared.  Returns |n_ref - n_gpu| / n_max."""
+    from oracle import hks_oracle as O
+    nd = tree.nodes[i]
+    x = np.asarray(tree.points.coords)
+    rows = O.sample_rows(w.n, nd.begin, nd.end, i, w.samples, "knn_augmented", 0, np.asarray(knn))
+    cands = np.arange(nd.begin, nd.end) if nd.is_leaf else np.concatenate([ref[2 * i + 1], ref[2 * i + 2]])
+    a = O.kernel_block("gaussian", x[rows], x[cands], h=w.h)
+    pos = {int(c): j for j, c in enumerate(cands)}
+    k = int(np.flatnonzero(got[: len(want)] != want[: len(got)])[0])
+    r = a.copy()
+    cols = list(range(r.shape[1]))
+    for step in range(k):  # Householder steps along the reference's pivots
+        j = cols.index(pos[int(want[step])])
+        cols[step], cols[j] = cols[j], cols[step]
+        r[:, [step, j]] = r[:, [j, step]]
+        v = r[step:, step].copy()
+        alpha = -np.copysign(np.linalg.norm(v), v[0]) if v[0] != 0 else -np.linalg.norm(v)
+        v[0] -= alpha
+        vn = np.linalg.norm(v)
+        if vn > 0:
+            v /= vn
+            r[step:, step:] -= 2.0 * np.outer(v, v @ r[step:, step:])
+    norms = np.sqrt(np.sum(r[k:, k:] ** 2, axis=0))
+    n_ref = norms[cols.index(pos[int(want[k])]) - k]
+    n_gpu = norms[cols.index(pos[int(got[k])]) - k]
+    return abs(n_ref - n_gpu) / norms.max()
 
 
 @pytest.mark.parametrize("name", CASES)

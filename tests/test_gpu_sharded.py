@@ -113,7 +113,11 @@ def test_sharded_matches_unsharded(tmp_path, case):
         np.testing.assert_allclose(res["xfull"], ref["x"].T, rtol=0, atol=1e-11 * np.abs(ref["x"]).max())
         # hybrid GMRES over the shards: same iterations, same solution
         assert int(res["h_iters"]) == ref["rep"].iterations
-        np.testing.assert_allclose(res["h_res"], ref["rep"].residuals, rtol=0.5, atol=1e-13)
+        # Givens estimates agree; the last entry is the recomputed true
+        # residual (krylov.py:131-139), a roundoff-level number below the
+        # 1e-9 tolerance in both runs
+        np.testing.assert_allclose(res["h_res"][:-1], ref["rep"].residuals[:-1], rtol=0.5, atol=1e-13)
+        assert res["h_res"][-1] <= 1e-9 and ref["rep"].residuals[-1] <= 1e-9
         np.testing.assert_allclose(res["xh"], ref["xh"][b:e], rtol=0, atol=1e-10 * np.abs(ref["xh"]).max())
         # per-level z_cond: top levels identical on every rank, shard levels bounded by the global max
         for lev, z in zip(res["zc_levels"], res["zc"]):
