@@ -10,6 +10,8 @@
 // ksum: U = K(X_rows, X_cols) W (+ lam W) without ever writing K to memory
 // -- each 64x64 kernel tile is built in shared memory and consumed at once
 // (hmatvec's leaf level, treecode.py:99-101; sampled residual checks).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "hks_internal.h"
 
@@ -240,6 +242,246 @@ __global__ void __launch_bounds__(256, 3) ksum_kernel(const double* __restrict__
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// GEMM-form distances on the FP64 tensor path (d >= kMmaMinDim): the 64 x 64
+// dot-product tile X_r X_c^T is a DMMA.884 GEMM over d (4 warps of 32 x 32
+// fragments, 16-deep k-slabs staged by cp.async in a 3-stage pipeline, as
+// gemm.cu), the squared norms come from the same staged slabs (sequential
+// FMA over k), and d^2 = (|x|^2 + |y|^2) - 2 x.y.  The epilogue applies the
+// kernel through a shared tile.  Properties kept from the diff form: K(X, Y)
+// == K(Y, X)^T bit for bit (the DMMA's per-element k order and the norm
+// sums do not depend on which operand is which), K(x, x) == 1 exactly (a
+// point against itself gets d^2 = 0), d^2 >= 0.  The values differ from
+// the diff form by roundoff of size eps (|x|^2 + |y|^2) in d^2.
+constexpr int kMmaMinDim = 64;
+constexpr int MBK = 16, MKS = MBK + 4, MST = 3;  // slab depth, smem row stride, pipeline stages
+constexpr int MT = 64;                            // tile rows = tile columns
+constexpr size_t kMmaStageBytes = (size_t)MST * 2 * MT * MKS * sizeof(double);
+
+struct PointRows {
+  const double* X;
+  const int64_t* ids;  // nullptr: base + i
+  int64_t base;
+  int count;           // valid rows
+  __device__ __forceinline__ const double* row(int i, int d) const {
+    return X + (ids ? ids[i] : base + i) * (int64_t)d;
+  }
+};
+
+// Stage k-slab [k0, k0 + 16) of 64 rows (from r0) and 64 columns (from c0):
+// 16 consecutive threads per point row (128-byte coalesced segments).
+__device__ __forceinline__ void mma_stage(const PointRows& R, int r0, const PointRows& C, int c0, int d, int k0,
+                                          double* As, double* Bs) {
+  const int t = threadIdx.x, kk = t & 15, i0 = t >> 4;
+  const int k = k0 + kk;
+#pragma unroll
+  for (int j = 0; j < MT / 8; ++j) {
+    const int i = i0 + 8 * j;
+    const bool okr = r0 + i < R.count && k < d;
+    cp_async8(As + i * MKS + kk, okr ? R.row(r0 + i, d) + k : R.X, okr);
+    const bool okc = c0 + i < C.count && k < d;
+    cp_async8(Bs + i * MKS + kk, okc ? C.row(c0 + i, d) + k : C.X, okc);
+  }
+}
+
+// acc (this warp's 32 x 32 block of the 64 x 64 tile) = X_r X_c^T over all
+// d; nr / nc (shared, 64 each) receive the squared norms of the tile's rows
+// (when want_rows) and columns.  Ends with every thread past a barrier.
+__device__ __forceinline__ void mma_dot_tile(const PointRows& R, int r0, const PointRows& C, int c0, int d,
+                                             double* stage_smem, bool want_rows, double* nr, double* nc,
+                                             double (&acc)[4][4][2]) {
+  double* As = stage_smem;
+  double* Bs = stage_smem + MST * MT * MKS;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int wm = (wid >> 1) * 32, wn = (wid & 1) * 32, fr = lane >> 2, fc = lane & 3;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  double nrm = 0.0;  // threads 0..63: row t; 64..127: column t - 64
+  const bool norm_thread = t >= MT || want_rows;
+  const int nk = (d + MBK - 1) / MBK;
+#pragma unroll
+  for (int st = 0; st < MST - 1; ++st) {
+    if (st < nk) mma_stage(R, r0, C, c0, d, st * MBK, As + st * MT * MKS, Bs + st * MT * MKS);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<MST - 2>();
+    __syncthreads();
+    const int pf = kt + MST - 1;
+    if (pf < nk) mma_stage(R, r0, C, c0, d, pf * MBK, As + (pf % MST) * MT * MKS, Bs + (pf % MST) * MT * MKS);
+    cp_async_commit();
+    const double* as = As + (kt % MST) * MT * MKS;
+    const double* bs = Bs + (kt % MST) * MT * MKS;
+#pragma unroll
+    for (int kk = 0; kk < MBK; kk += 4) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = as[(wm + i * 8 + fr) * MKS + kk + fc];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = bs[(wn + j * 8 + fr) * MKS + kk + fc];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+    if (norm_thread) {  // squared norm in k order (zero-filled tail adds nothing)
+      const double* v = t < MT ? as + t * MKS : bs + (t - MT) * MKS;
+#pragma unroll
+      for (int kk = 0; kk < MBK; ++kk) nrm = fma(v[kk], v[kk], nrm);
+    }
+  }
+  cp_async_wait<0>();
+  if (t < MT) {
+    if (want_rows) nr[t] = nrm;
+  } else {
+    nc[t - MT] = nrm;
+  }
+  __syncthreads();  // norms visible; the staging area is free
+}
+
+__device__ __forceinline__ double mma_kernel_value(const KernelParams& kp, double dot, double sq) {
+  if (kp.family == HKS_POLYNOMIAL) {
+    const double t = dot + kp.shift;
+    if (kp.degree == 1) return t;
+    if (kp.degree == 2) return t * t;
+    return pow(t, (double)kp.degree);
+  }
+  return kernel_value(kp, sq);
+}
+
+// Writes this warp's fragment of kernel values into Kt (64 x 65, Kt[ii][jj]).
+// same_points: rows and columns index the same point array, so equal ids
+// are the same point (d^2 = 0).
+__device__ __forceinline__ void mma_values_to_smem(const KernelParams& kp, const double (&acc)[4][4][2],
+                                                   const double* nr, const double* nc, const PointRows& R, int r0,
+                                                   const PointRows& C, int c0, bool same_points, double* Kt) {
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int wm = (wid >> 1) * 32, wn = (wid & 1) * 32, fr = lane >> 2, fc = lane & 3;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int ii = wm + i * 8 + fr, jj = wn + j * 8 + 2 * fc + h;
+        double v = 0.0;
+        if (r0 + ii < R.count && c0 + jj < C.count) {
+          const double dot = acc[i][j][h];
+          double sq = fmax((nr[ii] + nc[jj]) - 2.0 * dot, 0.0);
+          if (same_points) {
+            const int64_t gi = R.ids ? R.ids[r0 + ii] : R.base + r0 + ii;
+            const int64_t gj = C.ids ? C.ids[c0 + jj] : C.base + c0 + jj;
+            if (gi == gj) sq = 0.0;
+          }
+          v = mma_kernel_value(kp, dot, sq);
+        }
+        Kt[ii * (MT + 1) + jj] = v;
+      }
+}
+
+template <bool ROW_MAJOR>
+__global__ void __launch_bounds__(128) eval_mma_kernel(const double* __restrict__ X, int d, KernelParams kp,
+                                                       const Bases* __restrict__ bases_ptr,
+                                                       const EvalDesc* __restrict__ descs, int tiles_n) {
+  const Bases& bases = *bases_ptr;
+  const EvalDesc e = descs[blockIdx.y];
+  const int r0 = (blockIdx.x / tiles_n) * MT, c0 = (blockIdx.x % tiles_n) * MT;
+  if (r0 >= e.m || c0 >= e.n) return;
+  const bool sym = !ROW_MAJOR && e.rows == kNull && e.cols == kNull && e.row0 == e.col0 && e.m == e.n;
+  if (sym && r0 > c0) return;
+  extern __shared__ double msm[];
+  __shared__ double nr[MT], nc[MT];
+  const PointRows R{X, e.rows == kNull ? nullptr : at<const int64_t>(bases, e.rows), e.row0, e.m};
+  const PointRows C{X, e.cols == kNull ? nullptr : at<const int64_t>(bases, e.cols), e.col0, e.n};
+  double acc[4][4][2];
+  mma_dot_tile(R, r0, C, c0, d, msm, true, nr, nc, acc);
+  double* Kt = msm;  // 64 x 65 value tile in the (free) staging area
+  mma_values_to_smem(kp, acc, nr, nc, R, r0, C, c0, true, Kt);
+  __syncthreads();
+  double* eout = at<double>(bases, e.out);
+  const double ediag = e.diag ? bases.lam : 0.0;
+  const int t = threadIdx.x;
+  // coalesced stores: lanes along the stored index
+  for (int q = t; q < MT * MT; q += 128) {
+    const int a = q & 63, b2 = q >> 6;  // a: fast index
+    const int ii = ROW_MAJOR ? b2 : a, jj = ROW_MAJOR ? a : b2;
+    const int i = r0 + ii, j = c0 + jj;
+    if (i >= e.m || j >= e.n) continue;
+    double v = Kt[ii * (MT + 1) + jj];
+    if (i == j) v += ediag;
+    if (ROW_MAJOR)
+      eout[(size_t)i * e.ldo + j] = v;
+    else
+      eout[i + (size_t)j * e.ldo] = v;
+  }
+  if (sym && r0 != c0) {  // mirrored tile K[c0 + jj, r0 + ii], coalesced along jj
+    for (int q = t; q < MT * MT; q += 128) {
+      const int jj = q & 63, ii = q >> 6;
+      const int i = r0 + ii, j = c0 + jj;
+      if (i < e.m && j < e.n) eout[j + (size_t)i * e.ldo] = Kt[ii * (MT + 1) + jj];
+    }
+  }
+}
+
+constexpr int MKC = 16;  // right-hand sides per pass
+
+__global__ void __launch_bounds__(128, 3) ksum_mma_kernel(const double* __restrict__ X, const double* __restrict__ XC,
+                                                       int d, KernelParams kp, const Bases* __restrict__ bases_ptr,
+                                                       const SumDesc* __restrict__ descs) {
+  const Bases& bases = *bases_ptr;
+  const SumDesc s = descs[blockIdx.y];
+  const int r0 = blockIdx.x * MT;
+  if (r0 >= s.m) return;
+  extern __shared__ double msm[];
+  __shared__ double nr[MT], nc[MT];
+  __shared__ double Ws[MT * MKC];
+  const PointRows R{X, s.rows == kNull ? nullptr : at<const int64_t>(bases, s.rows), s.row0, s.m};
+  const PointRows C{XC, s.cols == kNull ? nullptr : at<const int64_t>(bases, s.cols), s.col0, s.n};
+  const bool same = X == XC;
+  const double* sW = at<const double>(bases, s.W);
+  double* sU = at<double>(bases, s.U);
+  double* Kt = msm;
+  const int t = threadIdx.x, own = t & 63, kq = (t >> 6) * (MKC / 2);
+  for (int kb = 0; kb < s.k; kb += MKC) {
+    const int kc = min(MKC, s.k - kb);
+    double out[MKC / 2];
+#pragma unroll
+    for (int q = 0; q < MKC / 2; ++q) out[q] = 0.0;
+    for (int c0 = 0; c0 < s.n; c0 += MT) {
+      double acc[4][4][2];
+      mma_dot_tile(R, r0, C, c0, d, msm, c0 == 0, nr, nc, acc);
+      mma_values_to_smem(kp, acc, nr, nc, R, r0, C, c0, same, Kt);
+      for (int e2 = t; e2 < MT * MKC; e2 += 128) {
+        const int j = e2 / MKC, c = e2 % MKC;
+        Ws[e2] = (c0 + j < s.n && c < kc) ? sW[(c0 + j) + (size_t)(kb + c) * s.ldw] : 0.0;
+      }
+      __syncthreads();
+      for (int j = 0; j < MT; ++j) {  // columns in order: the same sum order as the diff-form kernel
+        const double kv = Kt[own * (MT + 1) + j];
+#pragma unroll
+        for (int q = 0; q < MKC / 2; ++q) out[q] = fma(kv, Ws[j * MKC + kq + q], out[q]);
+      }
+      __syncthreads();  // Kt / Ws reused by the next tile
+    }
+    const int i = r0 + own;
+    if (i < s.m) {
+#pragma unroll
+      for (int q = 0; q < MKC / 2; ++q) {
+        const int c = kq + q;
+        if (c >= kc) continue;
+        double* u = sU + i + (size_t)(kb + c) * s.ldu;
+        double v = out[q];
+        if (s.diag) v += bases.lam * sW[i + (size_t)(kb + c) * s.ldw];
+        if (s.beta != 0.0) v += s.beta * *u;
+        *u = v;
+      }
+    }
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_eval_batched(const double* X, int d, KernelParams kp, const Bases* bases,
@@ -247,6 +489,20 @@ cudaError_t launch_eval_batched(const double* X, int d, KernelParams kp, const B
                                       cudaStream_t stream) {
   if (count <= 0 || max_m <= 0 || max_n <= 0) return cudaSuccess;
   const int tm = (max_m + TM - 1) / TM, tn = (max_n + TN - 1) / TN;
+  if (d >= kMmaMinDim && getenv("HKS_DIFF_FORM") == nullptr) {  // tensor-path distances
+    static_assert(MT == TM && MT == TN, "tile shapes");
+    if (row_major) raise_smem_limit(eval_mma_kernel<true>, kMmaStageBytes);
+    else raise_smem_limit(eval_mma_kernel<false>, kMmaStageBytes);
+    for (int first = 0; first < count; first += 65535) {
+      const int cnt = count - first < 65535 ? count - first : 65535;
+      dim3 grid(tm * tn, cnt);
+      if (row_major)
+        eval_mma_kernel<true><<<grid, 128, kMmaStageBytes, stream>>>(X, d, kp, bases, d_descs + first, tn);
+      else
+        eval_mma_kernel<false><<<grid, 128, kMmaStageBytes, stream>>>(X, d, kp, bases, d_descs + first, tn);
+    }
+    return cudaGetLastError();
+  }
   for (int first = 0; first < count; first += 65535) {
     const int cnt = count - first < 65535 ? count - first : 65535;
     dim3 grid(tm * tn, cnt);
@@ -261,6 +517,15 @@ cudaError_t launch_eval_batched(const double* X, int d, KernelParams kp, const B
 cudaError_t launch_ksum_batched(const double* X, int d, KernelParams kp, const Bases* bases,
                                 const SumDesc* d_descs, int count, int max_m, cudaStream_t stream, const double* XC) {
   if (count <= 0 || max_m <= 0) return cudaSuccess;
+  if (d >= kMmaMinDim && getenv("HKS_DIFF_FORM") == nullptr) {  // tensor-path distances
+    raise_smem_limit(ksum_mma_kernel, kMmaStageBytes);
+    for (int first = 0; first < count; first += 65535) {
+      const int cnt = count - first < 65535 ? count - first : 65535;
+      ksum_mma_kernel<<<dim3((max_m + MT - 1) / MT, cnt), 128, kMmaStageBytes, stream>>>(X, XC ? XC : X, d, kp,
+                                                                                      bases, d_descs + first);
+    }
+    return cudaGetLastError();
+  }
   for (int first = 0; first < count; first += 65535) {
     const int cnt = count - first < 65535 ? count - first : 65535;
     dim3 grid((max_m + TM - 1) / TM, cnt);

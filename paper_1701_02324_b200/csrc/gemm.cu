@@ -27,6 +27,20 @@ namespace {
 constexpr int BN = 64, BK = HKS_GEMM_BK, KS = BK + 4;  // KS: smem row stride (bank spread)
 constexpr int STAGES = HKS_GEMM_STAGES;  // cp.async pipeline depth
 
+// Shared-memory layout of a staged operand follows its global contiguity,
+// so every cp.async warp writes consecutive addresses (no bank conflicts on
+// the LDGSTS stores -- the transposing [m][k] store of a column-major A was
+// 4-way conflicted, 38% of the shared-memory wavefronts):
+//   k-contiguous in global (A^T, B):  [row][k], row stride KS = BK + 4
+//   row-contiguous in global (A, B^T): [k][row], row stride R + 4
+// Both strides are 4 (mod 16) doubles, so the DMMA fragment loads (8 rows x
+// 4 k per warp) hit distinct banks in either layout.
+template <int R>
+struct OperandLayout {
+  static constexpr int RS = R + 4;                                     // [k][row] stride
+  static constexpr int kElems = (R * KS > BK * RS) ? R * KS : BK * RS;  // per stage
+};
+
 struct GemmOp {
   const double* A;
   const double* B;
@@ -36,22 +50,22 @@ struct GemmOp {
 };
 
 
-// Stage the A (64 x 16) and B (16 x 64) tiles of k-block k0 into shared
-// memory as As[m][k], Bs[n][k]; global reads are coalesced along whichever
-// index is contiguous, out-of-range elements are zero-filled.
+// Stage the A (TBM x TBK) and B (TBK x 64) tiles of k-block k0 into shared
+// memory (layouts above); out-of-range elements are zero-filled.
 template <int TBM, int TBK>
 __device__ __forceinline__ void load_stage(const GemmOp& g, int m0, int n0, int k0, double* As, double* Bs) {
-  constexpr int T = 2 * TBM, KST = TBK + 4;  // threads, smem row stride
+  constexpr int T = 2 * TBM, KST = TBK + 4;  // threads, [row][k] stride
+  constexpr int AMS = TBM + 4, BNS = BN + 4;  // [k][row] strides
   const int t = threadIdx.x;
-  if (!g.transA) {
+  if (!g.transA) {  // A column-major: m contiguous -> As[k][m]
 #pragma unroll
     for (int j = 0; j < TBK / (T / TBM); ++j) {
       const int mi = t % TBM, ki = t / TBM + (T / TBM) * j;
       const int m = m0 + mi, k = k0 + ki;
       const bool ok = m < g.m && k < g.k;
-      cp_async8(As + mi * KST + ki, ok ? g.A + m + (size_t)k * g.lda : g.A, ok);
+      cp_async8(As + ki * AMS + mi, ok ? g.A + m + (size_t)k * g.lda : g.A, ok);
     }
-  } else {
+  } else {  // A^T stored: k contiguous -> As[m][k]
 #pragma unroll
     for (int j = 0; j < TBM / (T / TBK); ++j) {
       const int ki = t % TBK, mi = t / TBK + (T / TBK) * j;
@@ -60,7 +74,7 @@ __device__ __forceinline__ void load_stage(const GemmOp& g, int m0, int n0, int 
       cp_async8(As + mi * KST + ki, ok ? g.A + k + (size_t)m * g.lda : g.A, ok);
     }
   }
-  if (!g.transB) {
+  if (!g.transB) {  // B column-major: k contiguous -> Bs[n][k]
 #pragma unroll
     for (int j = 0; j < BN / (T / TBK); ++j) {
       const int ki = t % TBK, ni = t / TBK + (T / TBK) * j;
@@ -68,13 +82,13 @@ __device__ __forceinline__ void load_stage(const GemmOp& g, int m0, int n0, int 
       const bool ok = n < g.n && k < g.k;
       cp_async8(Bs + ni * KST + ki, ok ? g.B + k + (size_t)n * g.ldb : g.B, ok);
     }
-  } else {
+  } else {  // B^T stored: n contiguous -> Bs[k][n]
 #pragma unroll
     for (int j = 0; j < TBK / (T / BN); ++j) {
       const int ni = t % BN, ki = t / BN + (T / BN) * j;
       const int n = n0 + ni, k = k0 + ki;
       const bool ok = n < g.n && k < g.k;
-      cp_async8(Bs + ni * KST + ki, ok ? g.B + n + (size_t)k * g.ldb : g.B, ok);
+      cp_async8(Bs + ki * BNS + ni, ok ? g.B + n + (size_t)k * g.ldb : g.B, ok);
     }
   }
 }
@@ -91,13 +105,22 @@ __global__ void __launch_bounds__(2 * TBM) gemm_batched_kernel(const Bases* __re
   const int m0 = (blockIdx.x / tiles_n) * BM, n0 = (blockIdx.x % tiles_n) * BN;
   if (m0 >= g.m || n0 >= g.n) return;
 
+  constexpr int AE = OperandLayout<TBM>::kElems, BE = OperandLayout<BN>::kElems;
   extern __shared__ double gsm[];
-  double* As = gsm;                       // STAGES x BM x KS
-  double* Bs = gsm + STAGES * BM * KS;    // STAGES x BN x KS
+  double* As = gsm;                       // STAGES x AE
+  double* Bs = gsm + STAGES * AE;         // STAGES x BE
 
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int wm = (wid >> 1) * 32, wn = (wid & 1) * 32;
   const int fr = lane >> 2, fc = lane & 3;
+  // fragment offsets in either layout: element (row, k) at row * rs + k * ks
+  const int ars = g.transA ? KS : 1, aks = g.transA ? 1 : BM + 4;
+  const int brs = g.transB ? 1 : KS, bks = g.transB ? BN + 4 : 1;
+  int aoff[4], boff[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) aoff[i] = (wm + i * 8 + fr) * ars + fc * aks;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) boff[j] = (wn + j * 8 + fr) * brs + fc * bks;
 
   // The DMMA sum starts at 0 (k order fixed by the tiles); the epilogue
   // forms alpha*sum + beta*C.  The C tile is prefetched into L2 at the
@@ -118,25 +141,24 @@ __global__ void __launch_bounds__(2 * TBM) gemm_batched_kernel(const Bases* __re
   const int nk = (g.k + BK - 1) / BK;
 #pragma unroll
   for (int st = 0; st < STAGES - 1; ++st) {
-    if (st < nk) load_stage<TBM, TBK>(g, m0, n0, st * BK, As + st * BM * KS, Bs + st * BN * KS);
+    if (st < nk) load_stage<TBM, TBK>(g, m0, n0, st * BK, As + st * AE, Bs + st * BE);
     cp_async_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     const int pf = kt + STAGES - 1;
-    if (pf < nk)
-      load_stage<TBM, TBK>(g, m0, n0, pf * BK, As + (pf % STAGES) * BM * KS, Bs + (pf % STAGES) * BN * KS);
+    if (pf < nk) load_stage<TBM, TBK>(g, m0, n0, pf * BK, As + (pf % STAGES) * AE, Bs + (pf % STAGES) * BE);
     cp_async_commit();
-    const double* as = As + (kt % STAGES) * BM * KS;
-    const double* bs = Bs + (kt % STAGES) * BN * KS;
+    const double* as = As + (kt % STAGES) * AE;
+    const double* bs = Bs + (kt % STAGES) * BE;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       double a[4], b[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = as[(wm + i * 8 + fr) * KS + kk + fc];
+      for (int i = 0; i < 4; ++i) a[i] = as[aoff[i] + kk * aks];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = bs[(wn + j * 8 + fr) * KS + kk + fc];
+      for (int j = 0; j < 4; ++j) b[j] = bs[boff[j] + kk * bks];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -205,18 +227,25 @@ __global__ void __launch_bounds__(128) gemm_skinny_kernel(const Bases* __restric
                  gd.m, gd.n, gd.k, gd.lda, gd.ldb, gd.ldc, gd.transA, gd.transB, gd.alpha, gd.beta};
   const int m0 = blockIdx.x * SBM;
   if (m0 >= g.m) return;
+  // operand layouts as in gemm_batched_kernel (OperandLayout): [k][row] for
+  // row-contiguous global operands, [row][k] for k-contiguous ones
+  constexpr int AMS = SBM + 4, BNS = SBN + 4;
+  constexpr int AE = (SBM * KS > BK * AMS) ? SBM * KS : BK * AMS;
+  constexpr int BE = (SBN * KS > BK * BNS) ? SBN * KS : BK * BNS;
   extern __shared__ double gsm[];
-  double* As = gsm;                        // STAGES x SBM x KS
-  double* Bs = gsm + STAGES * SBM * KS;    // STAGES x SBN x KS
+  double* As = gsm;                        // STAGES x AE
+  double* Bs = gsm + STAGES * AE;          // STAGES x BE
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int wm = wid * 32, fr = lane >> 2, fc = lane & 3;
+  const int ars = g.transA ? KS : 1, aks = g.transA ? 1 : AMS;
+  const int brs = g.transB ? 1 : KS, bks = g.transB ? BNS : 1;
   auto load = [&](int k0, double* as, double* bs) {
-    if (!g.transA) {
+    if (!g.transA) {  // m contiguous -> as[k][m]
 #pragma unroll
       for (int ki = 0; ki < BK; ++ki) {
         const int m = m0 + t, k = k0 + ki;
         const bool ok = m < g.m && k < g.k;
-        cp_async8(as + t * KS + ki, ok ? g.A + m + (size_t)k * g.lda : g.A, ok);
+        cp_async8(as + ki * AMS + t, ok ? g.A + m + (size_t)k * g.lda : g.A, ok);
       }
     } else {
 #pragma unroll
@@ -229,12 +258,12 @@ __global__ void __launch_bounds__(128) gemm_skinny_kernel(const Bases* __restric
     }
 #pragma unroll
     for (int j = 0; j < SBN * BK / 128; ++j) {
-      const int e = t + 128 * j;  // !transB: along k then n; transB: along n then k
+      const int e = t + 128 * j;  // !transB: along k then n -> bs[n][k]; transB: along n then k -> bs[k][n]
       const int ki = g.transB ? e / SBN : e % BK, ni = g.transB ? e % SBN : e / BK;
       const int k = k0 + ki;
       const bool ok = ni < g.n && k < g.k;
-      cp_async8(bs + ni * KS + ki, ok ? (g.transB ? g.B + ni + (size_t)k * g.ldb : g.B + k + (size_t)ni * g.ldb) : g.B,
-                ok);
+      cp_async8(bs + ni * brs + ki * bks,
+                ok ? (g.transB ? g.B + ni + (size_t)k * g.ldb : g.B + k + (size_t)ni * g.ldb) : g.B, ok);
     }
   };
   if (g.beta != 0.0)
@@ -250,24 +279,24 @@ __global__ void __launch_bounds__(128) gemm_skinny_kernel(const Bases* __restric
   const int nk = (g.k + BK - 1) / BK;
 #pragma unroll
   for (int st = 0; st < STAGES - 1; ++st) {
-    if (st < nk) load(st * BK, As + st * SBM * KS, Bs + st * SBN * KS);
+    if (st < nk) load(st * BK, As + st * AE, Bs + st * BE);
     cp_async_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     const int pf = kt + STAGES - 1;
-    if (pf < nk) load(pf * BK, As + (pf % STAGES) * SBM * KS, Bs + (pf % STAGES) * SBN * KS);
+    if (pf < nk) load(pf * BK, As + (pf % STAGES) * AE, Bs + (pf % STAGES) * BE);
     cp_async_commit();
-    const double* as = As + (kt % STAGES) * SBM * KS;
-    const double* bs = Bs + (kt % STAGES) * SBN * KS;
+    const double* as = As + (kt % STAGES) * AE;
+    const double* bs = Bs + (kt % STAGES) * BE;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       double a[4], b[2];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = as[(wm + i * 8 + fr) * KS + kk + fc];
+      for (int i = 0; i < 4; ++i) a[i] = as[(wm + i * 8 + fr) * ars + (kk + fc) * aks];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) b[j] = bs[(j * 8 + fr) * KS + kk + fc];
+      for (int j = 0; j < 2; ++j) b[j] = bs[(j * 8 + fr) * brs + (kk + fc) * bks];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -358,7 +387,9 @@ cudaError_t launch_gemm_batched(const Bases* bases, const GemmDesc* d_descs, int
   // large: more warps per SM and half the B-operand staging per flop
   static const bool skinny_ok = getenv("HKS_GEMM_SKINNY") == nullptr || atoi(getenv("HKS_GEMM_SKINNY")) != 0;
   if (skinny_ok && max_n <= SBN) {  // the solves' right-hand-side blocks
-    const size_t sm = (size_t)SST * (SBM + SBN) * SKS * sizeof(double);
+    constexpr int sae = (SBM * SKS > SBK * (SBM + 4)) ? SBM * SKS : SBK * (SBM + 4);
+    constexpr int sbe = (SBN * SKS > SBK * (SBN + 4)) ? SBN * SKS : SBK * (SBN + 4);
+    const size_t sm = (size_t)SST * (sae + sbe) * sizeof(double);
     raise_smem_limit(gemm_skinny_kernel, sm);
     for (int first = 0; first < count; first += 65535) {
       const int cnt = count - first < 65535 ? count - first : 65535;
@@ -372,7 +403,9 @@ cudaError_t launch_gemm_batched(const Bases* bases, const GemmDesc* d_descs, int
   for (int first = 0; first < count; first += 65535) {
     const int cnt = count - first < 65535 ? count - first : 65535;
     dim3 grid(tm * tn, cnt);
-    const size_t sm = (size_t)STAGES * (BM + BN) * KS * sizeof(double);
+    const size_t sm = (size_t)STAGES *
+                      ((tall ? OperandLayout<128>::kElems : OperandLayout<64>::kElems) + OperandLayout<BN>::kElems) *
+                      sizeof(double);
     if (tall) {
       raise_smem_limit(gemm_batched_kernel<128>, sm);
       gemm_batched_kernel<128><<<grid, 256, sm, stream>>>(bases, d_descs + first, tn);

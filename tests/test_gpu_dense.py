@@ -49,6 +49,9 @@ def test_eval_block_vs_oracle_and_symmetry(hk, family, d):
     # exponent in the value (d = 784 leaves exponents of ~80)
     sq = ((x[:, None, :] - y[None, :, :]) ** 2).sum(-1)
     cond = sq / (2 * 0.9 ** 2) if family == "gaussian" else np.ones_like(sq)
+    if d >= 64:  # GEMM-form distances on the tensor path: the roundoff scales with |x|^2 + |y|^2, not d^2
+        nn = (x * x).sum(1)[:, None] + (y * y).sum(1)[None, :]
+        cond = nn / (2 * 0.9 ** 2)
     tol = 8 * np.spacing(np.abs(ref)) + np.abs(ref) * 4 * np.sqrt(d) * 2.3e-16 * cond + 1e-300
     assert np.all(np.abs(got - ref) <= tol)
     if family != "polynomial":

@@ -79,24 +79,30 @@ def test_ladder_structure_bit_exact(name):
     diff = [i for i in range(1, len(ranks)) if not np.array_equal(np.asarray(skels[i].indices), ref[i])]
     # "skeleton index sets must match except where pivots tie" (north star):
     # every node whose candidates are the reference's and whose pivot
-    # sequence still differs must diverge at a near-tie of two column norms
-    # (audited with the oracle's QRCP, linalg.py:43-104); its ancestors may
-    # then differ too (their candidates do).
+    # sequence still differs must diverge either at a near-tie of two column
+    # norms or past the block's numerical rank -- fixed-rank configurations
+    # (tau = 1e-300) keep pivoting on residual columns of norm ~1e-16 of the
+    # first pivot's, where the choice is decided by rounding (the reference
+    # itself picks differently there with 1 and 8 BLAS threads: C4 N=16384
+    # node 8 at step 220, |R_kk| / |R_00| = 9e-17).  Audited with the
+    # oracle's QRCP (linalg.py:43-104); ancestors may then differ too.
     tainted = set()
     for i in sorted(diff, reverse=True):
         kids = (2 * i + 1, 2 * i + 2)
         if tree.nodes[i].is_leaf or not (set(kids) & tainted):
-            gap = _tie_gap(w, tree, knn, i, np.asarray(skels[i].indices), ref[i], ref)
-            assert gap <= 1e-10, f"node {i}: pivot sequences diverge at a column-norm gap of {gap:.2e}"
+            gap, floor = _tie_gap(w, tree, knn, i, np.asarray(skels[i].indices), ref[i], ref)
+            assert gap <= 1e-10 or floor <= 1e-13, (
+                f"node {i}: pivot sequences diverge at a column-norm gap of {gap:.2e} "
+                f"(remaining norms {floor:.2e} of the first pivot's)")
         tainted.add(i)
 
 
 def _tie_gap(w, tree, knn, i, got, want, ref):
-    """Relative column-norm gap at the first step where the GPU's pivot
-    sequence `got` leaves the reference's `want` for node i: the oracle's
-    QRCP (from-scratch norms, oracle/hks_oracle.py) is advanced along the
-    reference's pivots and the residual norms of the two competing columns
-    compared.  Returns |n_ref - n_gpu| / n_max."""
+    """At the first step where the GPU's pivot sequence `got` leaves the
+    reference's `want` for node i, with the oracle's QRCP (from-scratch
+    norms, oracle/hks_oracle.py) advanced along the reference's pivots:
+    (|n_ref - n_gpu| / n_max of the two competing columns' residual norms,
+    n_max / the first pivot's norm)."""
     from oracle import hks_oracle as O
     nd = tree.nodes[i]
     x = np.asarray(tree.points.coords)
@@ -106,6 +112,7 @@ def _tie_gap(w, tree, knn, i, got, want, ref):
     pos = {int(c): j for j, c in enumerate(cands)}
     k = int(np.flatnonzero(got[: len(want)] != want[: len(got)])[0])
     r = a.copy()
+    first = np.sqrt(np.sum(r ** 2, axis=0)).max()
     cols = list(range(r.shape[1]))
     for step in range(k):  # Householder steps along the reference's pivots
         j = cols.index(pos[int(want[step])])
@@ -121,7 +128,7 @@ def _tie_gap(w, tree, knn, i, got, want, ref):
     norms = np.sqrt(np.sum(r[k:, k:] ** 2, axis=0))
     n_ref = norms[cols.index(pos[int(want[k])]) - k]
     n_gpu = norms[cols.index(pos[int(got[k])]) - k]
-    return abs(n_ref - n_gpu) / norms.max()
+    return abs(n_ref - n_gpu) / norms.max(), norms.max() / first
 
 
 @pytest.mark.parametrize("name", CASES)
