@@ -334,17 +334,36 @@ __device__ __noinline__ void trsv_fast(const double* LU, int lda, int n, double*
     }
     __syncthreads();
     const int lo = forward ? r0 + nr : 0, hi = forward ? n : r0;
-    for (int i = lo + tid; i < hi; i += nt) {
-      double s = x[i];
-      if (!trans) {
+    if (!trans) {  // thread per row i, lanes along the rows of each column (coalesced)
+      for (int i = lo + tid; i < hi; i += nt) {
+        double s = x[i];
 #pragma unroll 8
         for (int j = 0; j < nr; ++j) s -= LU[i + (size_t)(r0 + j) * lda] * x[r0 + j];
-      } else {
-        const double* col = LU + r0 + (size_t)i * lda;  // op(T)(i, r0 + j) = T(r0 + j, i)
-#pragma unroll 8
-        for (int j = 0; j < nr; ++j) s -= col[j] * x[r0 + j];
+        x[i] = s;
       }
-      x[i] = s;
+    } else {
+      // op(T)(i, r0 + j) = T(r0 + j, i): row i of op(T) is a contiguous piece
+      // of column i of T, so one warp takes row i with its lanes along that
+      // piece (one coalesced 256-byte load instead of 32 strided ones per
+      // thread, which made the transposed sweeps L1-transaction bound), four
+      // rows per warp in flight, warp-sum reductions
+      const int nw = nt >> 5, wid = tid >> 5;
+      const double xl = lane < nr ? x[r0 + lane] : 0.0;
+      for (int i0 = lo + 4 * wid; i0 < hi; i0 += 4 * nw) {
+        double p[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          p[q] = (i0 + q < hi && lane < nr) ? LU[r0 + lane + (size_t)(i0 + q) * lda] * xl : 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) p[q] = warp_sum(p[q]);
+        if (lane < 4 && i0 + lane < hi) {
+          double sq = p[0];
+#pragma unroll
+          for (int q = 1; q < 4; ++q)
+            if (lane == q) sq = p[q];
+          x[i0 + lane] -= sq;
+        }
+      }
     }
     __syncthreads();
   }
@@ -368,7 +387,7 @@ __device__ int block_iamax(const double* x, int n, double* rv, int* ri) {
 #ifndef GECON_THREADS
 #define GECON_THREADS 256
 #endif
-__global__ void __launch_bounds__(GECON_THREADS) gecon_kernel(const Bases* __restrict__ bases_ptr,
+__global__ void __launch_bounds__(GECON_THREADS, 2) gecon_kernel(const Bases* __restrict__ bases_ptr,
                                                      const LuDesc* __restrict__ descs) {
   const Bases& bases = *bases_ptr;
   const LuDesc L = descs[blockIdx.x];
@@ -476,7 +495,10 @@ __global__ void __launch_bounds__(GECON_THREADS) gecon_kernel(const Bases* __res
 // (two triangular sweeps) and the SMs turn over quickly.  The dlacn2 state
 // of each matrix (x, sign vector, est, j, iter, next step) lives in global
 // scratch (base kGeconScratchBase, `stride` doubles per matrix).  Arithmetic
-// and its order are those of gecon_kernel, so the results are identical.
+// and its order are those of gecon_kernel, so the results are identical
+// (both share trsv_fast; its transposed sweeps sum each row as a warp
+// reduction, an order LAPACK does not fix either -- z_cond is an estimate,
+// checked to 1e-3 against dgecon).
 enum GeconState { GS_A = 0, GS_B, GS_C, GS_D, GS_E, GS_DONE };
 
 __device__ __forceinline__ void gecon_step_one(const Bases& bases, const LuDesc& L, int m, int stride, int phase) {
@@ -624,7 +646,7 @@ __device__ __forceinline__ void gecon_step_one(const Bases& bases, const LuDesc&
 // blockIdx.x, + gridDim.x, ...  A grid smaller than the batch leaves SMs
 // with no estimate CTA at all, where the factorization's register-heavy
 // kernels (the panels) can start at once.
-__global__ void __launch_bounds__(GECON_THREADS) gecon_step_kernel(const Bases* __restrict__ bases_ptr,
+__global__ void __launch_bounds__(GECON_THREADS, 2) gecon_step_kernel(const Bases* __restrict__ bases_ptr,
                                                           const LuDesc* __restrict__ descs, int count,
                                                           int stride, int phase) {
   for (int m = blockIdx.x; m < count; m += gridDim.x) {

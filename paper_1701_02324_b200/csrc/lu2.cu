@@ -324,15 +324,6 @@ __global__ void swap_kernel(const Bases* __restrict__ bases_ptr, const SwapDesc*
 // second buffer while the current block computes.  Shared memory is sized
 // by the step's largest k, so narrow / shallow solves pack several CTAs per
 // SM.
-// XOR swizzle of the TRSM staging tiles (X: [row][col], T rows: [row][k]):
-// the physical column is col ^ ((row >> 2) & 3) (T: except the 32 columns
-// of the block's own diagonal block, which only the register solve reads).  Row strides are 4 (mod 16)
-// doubles, so the DMMA fragment reads (4 rows x 8 columns) stay
-// conflict-free, and the swizzle spreads the column-wise LDGSTS stores
-// (32 consecutive rows of one column, the coalesced global direction) over
-// all 16 bank pairs instead of 4.
-__device__ __forceinline__ int swz(int row, int col) { return col ^ ((row >> 2) & 3); }
-
 template <bool UPPER, int NW>
 __device__ __forceinline__ void trsm_stage_rows(double* Ts, int tts, const double* T, int ldt, int k, int b,
                                                 int wid, int lane) {
@@ -340,7 +331,7 @@ __device__ __forceinline__ void trsm_stage_rows(double* Ts, int tts, const doubl
   const int klo = UPPER ? r0 : 0, khi = UPPER ? k : r0 + nr;
   const bool ok = lane < nr;
   for (int cc = klo + wid; cc < khi; cc += NW)
-    cp_async8(Ts + lane * tts + (cc - r0 < 32u ? cc : swz(lane, cc)), ok ? T + (r0 + lane) + (size_t)cc * ldt : T, ok);
+    cp_async8(Ts + lane * tts + cc, ok ? T + (r0 + lane) + (size_t)cc * ldt : T, ok);
 }
 
 // a / b, correctly rounded (bit-identical to the IEEE division), from the
@@ -379,14 +370,13 @@ __device__ __forceinline__ void trsm_sweep(double* X, double* Tbuf, int tts, con
     const int xr0 = blk * 32, xnr = min(32, k - xr0);
     if (lane < xnr) {
       const int src = perm ? perm[xr0 + lane] : xr0 + lane;
-      for (int c = wid; c < nc; c += NW)
-        cp_async8(X + (xr0 + lane) * TXS + swz(xr0 + lane, c), Bin + src + (size_t)c * ldb, true);
+      for (int c = wid; c < nc; c += NW) cp_async8(X + (xr0 + lane) * TXS + c, Bin + src + (size_t)c * ldb, true);
     }
   };
   auto store_x = [&](int blk) {
     const int xr0 = blk * 32, xnr = min(32, k - xr0);
     for (int c = wid; c < nc; c += NW)
-      if (lane < xnr) Bout[xr0 + lane + (size_t)c * ldb] = X[(xr0 + lane) * TXS + swz(xr0 + lane, c)];
+      if (lane < xnr) Bout[xr0 + lane + (size_t)c * ldb] = X[(xr0 + lane) * TXS + c];
   };
   if (Bin) stage_x(UPPER ? nblk - 1 : 0);
   trsm_stage_rows<UPPER, NW>(Tbuf, tts, T, ldt, k, UPPER ? nblk - 1 : 0, wid, lane);
@@ -422,9 +412,9 @@ __device__ __forceinline__ void trsm_sweep(double* X, double* Tbuf, int tts, con
           const bool kin = kq < uhi;
           double a[2], bv[4];
 #pragma unroll
-          for (int i = 0; i < 2; ++i) a[i] = kin ? Ts[(rb + i * 8 + fr) * tts + swz(rb + i * 8 + fr, kq)] : 0.0;
+          for (int i = 0; i < 2; ++i) a[i] = kin ? Ts[(rb + i * 8 + fr) * tts + kq] : 0.0;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) bv[j] = kin ? X[kq * TXS + swz(kq, cb + j * 8 + fr)] : 0.0;
+          for (int j = 0; j < 4; ++j) bv[j] = kin ? X[kq * TXS + cb + j * 8 + fr] : 0.0;
 #pragma unroll
           for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -437,7 +427,7 @@ __device__ __forceinline__ void trsm_sweep(double* X, double* Tbuf, int tts, con
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int rr = rb + i * 8 + fr, c = cb + j * 8 + 2 * fc + h;
-              if (rr < nr) X[(r0 + rr) * TXS + swz(r0 + rr, c)] -= acc[i][j][h];
+              if (rr < nr) X[(r0 + rr) * TXS + c] -= acc[i][j][h];
             }
       }
     } else if (NT != NC) {  // 4 warps on one 32-column tile: warp w owns rows 8w .. 8w+7
@@ -453,10 +443,10 @@ __device__ __forceinline__ void trsm_sweep(double* X, double* Tbuf, int tts, con
       for (int kk = klo2; kk < khi2; kk += 4) {
         const int kq = kk + fc;
         const bool kin = kq < khi2;
-        const double a = kin ? Ts[(rw * 8 + fr) * tts + swz(rw * 8 + fr, kq)] : 0.0;
+        const double a = kin ? Ts[(rw * 8 + fr) * tts + kq] : 0.0;
         double bv[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) bv[j] = kin ? X[kq * TXS + swz(kq, j * 8 + fr)] : 0.0;
+        for (int j = 0; j < 4; ++j) bv[j] = kin ? X[kq * TXS + j * 8 + fr] : 0.0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma884(acc[j][0], acc[j][1], a, bv[j]);
       }
@@ -469,7 +459,7 @@ __device__ __forceinline__ void trsm_sweep(double* X, double* Tbuf, int tts, con
           for (int j = 0; j < 4; ++j)
 #pragma unroll
             for (int h = 0; h < 2; ++h)
-              if (rr < nr) X[(r0 + rr) * TXS + swz(r0 + rr, j * 8 + 2 * fc + h)] -= acc[j][h];
+              if (rr < nr) X[(r0 + rr) * TXS + j * 8 + 2 * fc + h] -= acc[j][h];
       }
     } else if (uhi > ulo && wid * 32 < nc) {
       const int cb = wid * 32;  // this warp's 32 columns
@@ -483,9 +473,9 @@ __device__ __forceinline__ void trsm_sweep(double* X, double* Tbuf, int tts, con
         const bool kin = kq < uhi;
         double a[4], bv[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = kin ? Ts[(i * 8 + fr) * tts + swz(i * 8 + fr, kq)] : 0.0;
+        for (int i = 0; i < 4; ++i) a[i] = kin ? Ts[(i * 8 + fr) * tts + kq] : 0.0;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) bv[j] = kin ? X[kq * TXS + swz(kq, cb + j * 8 + fr)] : 0.0;
+        for (int j = 0; j < 4; ++j) bv[j] = kin ? X[kq * TXS + cb + j * 8 + fr] : 0.0;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -498,7 +488,7 @@ __device__ __forceinline__ void trsm_sweep(double* X, double* Tbuf, int tts, con
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int rr = i * 8 + fr, c = cb + j * 8 + 2 * fc + h;
-            if (rr < nr) X[(r0 + rr) * TXS + swz(r0 + rr, c)] -= acc[i][j][h];
+            if (rr < nr) X[(r0 + rr) * TXS + c] -= acc[i][j][h];
           }
     }
     __syncthreads();
@@ -506,7 +496,7 @@ __device__ __forceinline__ void trsm_sweep(double* X, double* Tbuf, int tts, con
     if (tid < nc) {
       double x[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) x[i] = i < nr ? X[(r0 + i) * TXS + (tid ^ ((i >> 2) & 3))] : 0.0;  // r0 % 32 == 0
+      for (int i = 0; i < 32; ++i) x[i] = i < nr ? X[(r0 + i) * TXS + tid] : 0.0;
       if (!UPPER) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -525,7 +515,7 @@ __device__ __forceinline__ void trsm_sweep(double* X, double* Tbuf, int tts, con
       }
 #pragma unroll
       for (int i = 0; i < 32; ++i)
-        if (i < nr) X[(r0 + i) * TXS + (tid ^ ((i >> 2) & 3))] = x[i];
+        if (i < nr) X[(r0 + i) * TXS + tid] = x[i];
     }
   }
   __syncthreads();
@@ -580,7 +570,7 @@ __global__ void __launch_bounds__(NT) getrs_fused_kernel(const Bases* __restrict
   // it block by block into the latency-bound sweeps)
   for (int i = lane; i < n; i += 32) {
     const int src = perm[i];
-    for (int c = wid; c < nc; c += NT / 32) cp_async8(X + i * TXS + swz(i, c), Bin + src + (size_t)c * D.ldb, true);
+    for (int c = wid; c < nc; c += NT / 32) cp_async8(X + i * TXS + c, Bin + src + (size_t)c * D.ldb, true);
   }
   if (D.lower) trsm_sweep<false, NC, NT>(X, Tbuf, tts, LU, D.lda, n, nc);
   trsm_sweep<true, NC, NT>(X, Tbuf, tts, LU, D.lda, n, nc, nullptr, B, D.ldb);  // stores streamed out
