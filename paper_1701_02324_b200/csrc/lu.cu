@@ -642,6 +642,234 @@ __device__ __forceinline__ void gecon_step_one(const Bases& bases, const LuDesc&
   }
 }
 
+// ------------------------------------------------------------------
+// Warp-per-matrix form of the split estimate (what the factorization
+// launches).  The estimate is a chain of latency-bound triangular sweeps;
+// one warp per matrix (instead of one 256-thread CTA) keeps ~16 matrices
+// in flight per SM with no CTA barriers, so a phase over a level's ~2000
+// matrices runs in about one wave instead of seven, and the SMs turn over
+// to the factorization's kernels after a few tens of microseconds.  Same
+// dlacn2 state machine and scratch layout as gecon_step_one.
+constexpr int GW_WARPS = 4;                    // warps (matrices) per CTA
+constexpr int GW_TILE = 32 * 33;               // transposed-sweep staging tile per warp
+
+// x := op(T)^-1 x for the LU in LU (unit lower / non-unit upper part, op =
+// transpose when trans), x in this warp's shared slice.
+__device__ void trsv_warp(const double* LU, int lda, int n, double* x, double* tile, bool upper, bool trans) {
+  const int lane = threadIdx.x & 31;
+  const bool forward = (!upper && !trans) || (upper && trans);
+  const int nblk = (n + 31) / 32;
+  for (int bb = 0; bb < nblk; ++bb) {
+    const int b = forward ? bb : nblk - 1 - bb;
+    const int r0 = b * 32, nr = min(32, n - r0);
+    double t[32], rd;
+    trsv_load_diag(LU, lda, n, b, upper, trans, t, rd);
+    double v = lane < nr ? x[r0 + lane] : 0.0;
+    if (forward) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (lane == j) v *= rd;
+        const double xj = __shfl_sync(0xffffffffu, v, j);
+        if (lane > j) v -= t[j] * xj;
+      }
+    } else {
+#pragma unroll
+      for (int j = 31; j >= 0; --j) {
+        if (lane == j) v *= rd;
+        const double xj = __shfl_sync(0xffffffffu, v, j);
+        if (lane < j) v -= t[j] * xj;
+      }
+    }
+    if (lane < nr) x[r0 + lane] = v;
+    __syncwarp();
+    const int lo = forward ? r0 + nr : 0, hi = forward ? n : r0;
+    if (!trans) {  // lane per row, each column's rows contiguous (coalesced)
+      for (int i = lo + lane; i < hi; i += 32) {
+        double s = x[i];
+#pragma unroll 8
+        for (int j = 0; j < nr; ++j) s -= LU[i + (size_t)(r0 + j) * lda] * x[r0 + j];
+        x[i] = s;
+      }
+    } else {
+      // op(T)(i, r0 + j) = T(r0 + j, i): 32 columns of T at a time through a
+      // padded shared tile (one coalesced 256-byte load per column), then
+      // lane q sums row c0 + q from the tile (stride 33: conflict-free)
+      for (int c0 = lo; c0 < hi; c0 += 32) {
+        const int nq = min(32, hi - c0);
+        for (int q = 0; q < nq; ++q) tile[q * 33 + lane] = lane < nr ? LU[r0 + lane + (size_t)(c0 + q) * lda] : 0.0;
+        __syncwarp();
+        if (lane < nq) {
+          double s = x[c0 + lane];
+#pragma unroll 8
+          for (int j = 0; j < nr; ++j) s -= tile[lane * 33 + j] * x[r0 + j];
+          x[c0 + lane] = s;
+        }
+        __syncwarp();
+      }
+    }
+    __syncwarp();
+  }
+}
+
+__device__ __forceinline__ double warp_asum(const double* x, int n) {
+  double s = 0.0;
+  for (int i = threadIdx.x & 31; i < n; i += 32) s += fabs(x[i]);
+  return warp_sum(s);
+}
+
+__device__ __forceinline__ int warp_iamax(const double* x, int n) {
+  ArgMax a{-1.0, 0x7fffffff};
+  for (int i = threadIdx.x & 31; i < n; i += 32) a = argmax_pick(a, ArgMax{fabs(x[i]), i});
+  return warp_argmax(a).i;
+}
+
+__device__ void gecon_warp_one(const Bases& bases, const LuDesc& L, int m, int stride, int phase, double* x,
+                               double* tile) {
+  if (L.rcond == kNull) return;
+  const int n = L.n, lane = threadIdx.x & 31;
+  double* st = at<double>(bases, make_ref(kGeconScratchBase, 0)) + (size_t)m * stride;
+  double* gx = st;
+  double* gsgn = st + n;
+  double* sc = st + 2 * (size_t)n;
+  double* rcond = at<double>(bases, L.rcond);
+  if (phase == 0) {
+    int state = GS_A;
+    if (n == 0) {
+      if (lane == 0) *rcond = 1.0;
+      state = GS_DONE;
+    } else {
+      const double anorm = *at<const double>(bases, L.anorm);
+      if (anorm == 0.0 || (L.info != kNull && *at<const int>(bases, L.info) != 0)) {
+        if (lane == 0) *rcond = 0.0;
+        state = GS_DONE;
+      }
+    }
+    if (state != GS_DONE)
+      for (int i = lane; i < n; i += 32) gx[i] = 1.0 / n;
+    if (lane == 0) {
+      sc[0] = state;
+      sc[1] = 1;
+      sc[2] = 0;
+      sc[3] = 0;
+      sc[4] = 0.0;
+    }
+    return;
+  }
+  int state = (int)sc[0];
+  if (state == GS_DONE) return;
+  const double* LUa = at<const double>(bases, L.A);
+  const int kase = (int)sc[1];
+  int iter = (int)sc[2], j = (int)sc[3];
+  double est = sc[4];
+  for (int i = lane; i < n; i += 32) x[i] = gx[i];
+  __syncwarp();
+  if (kase == 1) {
+    trsv_warp(LUa, L.lda, n, x, tile, false, false);
+    trsv_warp(LUa, L.lda, n, x, tile, true, false);
+  } else {
+    trsv_warp(LUa, L.lda, n, x, tile, true, true);
+    trsv_warp(LUa, L.lda, n, x, tile, false, true);
+  }
+  int next_kase = 1;
+  auto set_alt = [&]() {
+    for (int i = lane; i < n; i += 32) {
+      const double sg = (i % 2 == 0) ? 1.0 : -1.0;
+      x[i] = sg * (1.0 + (double)i / (double)(n - 1));
+    }
+    next_kase = 1;
+    state = GS_E;
+  };
+  auto set_unit = [&](int jj) {
+    for (int i = lane; i < n; i += 32) x[i] = (i == jj) ? 1.0 : 0.0;
+    next_kase = 1;
+    state = GS_C;
+  };
+  if (state == GS_A) {
+    if (n == 1) {
+      est = fabs(x[0]);
+      state = GS_DONE;
+    } else {
+      est = warp_asum(x, n);
+      for (int i = lane; i < n; i += 32) {
+        x[i] = x[i] >= 0.0 ? 1.0 : -1.0;
+        gsgn[i] = x[i];
+      }
+      next_kase = 2;
+      state = GS_B;
+    }
+  } else if (state == GS_B) {
+    j = warp_iamax(x, n);
+    iter = 2;
+    __syncwarp();
+    set_unit(j);
+  } else if (state == GS_C) {
+    const double estold = est;
+    est = warp_asum(x, n);
+    int diff = 0;
+    for (int i = lane; i < n; i += 32) {
+      const double xs = x[i] >= 0.0 ? 1.0 : -1.0;
+      if (xs != gsgn[i]) diff = 1;
+    }
+    diff = __any_sync(0xffffffffu, diff);
+    if (!diff || est <= estold) {
+      set_alt();
+    } else {
+      for (int i = lane; i < n; i += 32) {
+        x[i] = x[i] >= 0.0 ? 1.0 : -1.0;
+        gsgn[i] = x[i];
+      }
+      next_kase = 2;
+      state = GS_D;
+    }
+  } else if (state == GS_D) {
+    const int jlast = j;
+    j = warp_iamax(x, n);
+    __syncwarp();
+    if (x[jlast] != fabs(x[j]) && iter < 5) {
+      ++iter;
+      __syncwarp();
+      set_unit(j);
+    } else {
+      __syncwarp();
+      set_alt();
+    }
+  } else {
+    const double temp = 2.0 * (warp_asum(x, n) / (double)(3 * n));
+    if (temp > est) est = temp;
+    state = GS_DONE;
+  }
+  __syncwarp();
+  if (state == GS_DONE) {
+    if (lane == 0) {
+      const double anorm = *at<const double>(bases, L.anorm);
+      *rcond = est != 0.0 ? (1.0 / est) / anorm : 0.0;
+    }
+  } else {
+    for (int i = lane; i < n; i += 32) gx[i] = x[i];
+  }
+  if (lane == 0) {
+    sc[0] = state;
+    sc[1] = next_kase;
+    sc[2] = iter;
+    sc[3] = j;
+    sc[4] = est;
+  }
+}
+
+// xs: doubles of each warp's x slice (>= the batch's largest n)
+__global__ void __launch_bounds__(32 * GW_WARPS) gecon_warp_kernel(const Bases* __restrict__ bases_ptr,
+                                                                   const LuDesc* __restrict__ descs, int count,
+                                                                   int stride, int phase, int xs) {
+  extern __shared__ double gw[];
+  const int w = threadIdx.x >> 5;
+  double* x = gw + (size_t)w * (xs + GW_TILE);
+  double* tile = x + xs;
+  for (int m = blockIdx.x * GW_WARPS + w; m < count; m += gridDim.x * GW_WARPS) {
+    gecon_warp_one(*bases_ptr, descs[m], m, stride, phase, x, tile);
+    __syncwarp();
+  }
+}
+
 // One phase of the estimates of `count` matrices; a CTA walks matrices
 // blockIdx.x, + gridDim.x, ...  A grid smaller than the batch leaves SMs
 // with no estimate CTA at all, where the factorization's register-heavy
@@ -700,6 +928,15 @@ cudaError_t launch_getrs_batched(const Bases* b, const LuSolveDesc* d, int count
 
 cudaError_t launch_gecon_batched(const Bases* b, const LuDesc* d, int count, int max_n, cudaStream_t s, int phase) {
   if (count <= 0) return cudaSuccess;
+  static const bool warp_form = getenv("HKS_GECON_CTA") == nullptr;
+  if (phase >= 0 && warp_form) {  // one warp per matrix, all matrices in one wave where they fit
+    const int xs = ((max_n > 0 ? max_n : 1) + 1) / 2 * 2;
+    const size_t sm = (size_t)GW_WARPS * (xs + GW_TILE) * sizeof(double);
+    raise_smem_limit(gecon_warp_kernel, sm);
+    const int grid = (count + GW_WARPS - 1) / GW_WARPS;
+    gecon_warp_kernel<<<grid, 32 * GW_WARPS, sm, s>>>(b, d, count, gecon_stride(max_n), phase, xs);
+    return cudaGetLastError();
+  }
   if (phase >= 0) {  // split estimate: phase 0 initialises, 1..kGeconSteps apply + advance
     const size_t sm = (size_t)(max_n > 0 ? max_n : 1) * sizeof(double);
     raise_smem_limit(gecon_step_kernel, sm);
