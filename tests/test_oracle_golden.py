@@ -146,3 +146,20 @@ def test_hybrid_golden(name):
                      lambda v: O.solve(t, sk, cp, fac, v), b, tol=1e-10, restart=50)
     assert rep["iterations"] == int(g["hybrid_iterations"])
     assert np.linalg.norm(x - g["hybrid_x"]) <= 1e-7 * np.linalg.norm(g["hybrid_x"])
+
+
+@pytest.mark.parametrize("name", ["c2_n16384", "c3_n16384", "c4_n16384"])
+def test_oracle_tree_knn_vs_ladder_fixture(name):
+    """The oracle's tree permutation and exact kNN lists equal the
+    unmodified reference's on the N = 16384 ladder instances
+    (tests/golden/ladder_*.npz; tree.py:87-144, 163-188)."""
+    import hashlib
+    import json
+    from paper_1701_02324_b200 import workloads as W
+    z = np.load(GOLDEN / f"ladder_{name}.npz")
+    meta = json.loads(str(z["meta"]))
+    w = W.CONFIGS[meta["workload"]].scaled(meta["n"])
+    tree = O.build_tree(W.points(w, 0), w.leaf_size, 0)
+    assert np.array_equal(tree.perm, z["perm"].astype(np.int64))
+    nl = O.knn(tree.coords, w.kappa)
+    assert hashlib.sha256(np.ascontiguousarray(nl, dtype=np.int64).tobytes()).hexdigest() == str(z["knn_sha256"])
