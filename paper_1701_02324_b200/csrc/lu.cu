@@ -683,20 +683,44 @@ __device__ void trsv_warp(const double* LU, int lda, int n, double* x, double* t
     if (lane < nr) x[r0 + lane] = v;
     __syncwarp();
     const int lo = forward ? r0 + nr : 0, hi = forward ? n : r0;
-    if (!trans) {  // lane per row, each column's rows contiguous (coalesced)
-      for (int i = lo + lane; i < hi; i += 32) {
-        double s = x[i];
-#pragma unroll 8
-        for (int j = 0; j < nr; ++j) s -= LU[i + (size_t)(r0 + j) * lda] * x[r0 + j];
-        x[i] = s;
+    if (!trans) {
+      // lane per row, each column's rows contiguous (coalesced); a lane keeps
+      // up to 16 rows in flight per column so the loads overlap (the sweep
+      // is a chain of 32-row steps -- with one row at a time every step
+      // waited out ~30 dependent load latencies)
+      constexpr int RQ = 16;
+      for (int base = lo; base < hi; base += 32 * RQ) {
+        double acc[RQ];
+#pragma unroll
+        for (int q = 0; q < RQ; ++q) {
+          const int i = base + lane + 32 * q;
+          acc[q] = i < hi ? x[i] : 0.0;
+        }
+        for (int j = 0; j < nr; ++j) {
+          const double xj = x[r0 + j];
+          const double* col = LU + (size_t)(r0 + j) * lda;
+#pragma unroll
+          for (int q = 0; q < RQ; ++q) {
+            const int i = base + lane + 32 * q;
+            if (i < hi) acc[q] -= col[i] * xj;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < RQ; ++q) {
+          const int i = base + lane + 32 * q;
+          if (i < hi) x[i] = acc[q];
+        }
       }
     } else {
       // op(T)(i, r0 + j) = T(r0 + j, i): 32 columns of T at a time through a
-      // padded shared tile (one coalesced 256-byte load per column), then
-      // lane q sums row c0 + q from the tile (stride 33: conflict-free)
+      // padded shared tile (one coalesced 256-byte load per column, all 32
+      // in flight), then lane q sums row c0 + q from the tile (stride 33:
+      // conflict-free)
       for (int c0 = lo; c0 < hi; c0 += 32) {
         const int nq = min(32, hi - c0);
-        for (int q = 0; q < nq; ++q) tile[q * 33 + lane] = lane < nr ? LU[r0 + lane + (size_t)(c0 + q) * lda] : 0.0;
+#pragma unroll
+        for (int q = 0; q < 32; ++q)
+          tile[q * 33 + lane] = (q < nq && lane < nr) ? LU[r0 + lane + (size_t)(c0 + q) * lda] : 0.0;
         __syncwarp();
         if (lane < nq) {
           double s = x[c0 + lane];
