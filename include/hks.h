@@ -171,10 +171,17 @@ int hks_hmatvec_part(hks_plan* plan, void* const* buffers, const double* w, doub
                      int32_t part, double* xchg, void* stream);
 
 /* build_operator, treecode.py:41-62: the sibling couplings K(q_l, q_r) from
- * HKS_BUF_SKEL into HKS_BUF_COUP.  Leaf blocks are never stored (they are
- * re-evaluated inside factorize and the fused hmatvec; hks_leaf_block gives
- * the HierarchicalOperator.leaf_blocks diagnostic view). */
+ * HKS_BUF_SKEL into HKS_BUF_COUP.  Leaf blocks: by default re-evaluated
+ * inside factorize and the fused hmatvec; hks_plan_cache_leaves evaluates
+ * them once into plan-owned device memory (N x m doubles, as the
+ * reference's build_operator caches HierarchicalOperator.leaf_blocks,
+ * treecode.py:48-51), after which factorize copies K_aa + lam I and the
+ * hmatvec leaf level is a batched GEMM -- call it before the plan's first
+ * factorize / solve / hmatvec (HKS_ERR_INVALID otherwise; a no-op for top
+ * plans).  hks_leaf_block gives the leaf_blocks diagnostic view (the cached
+ * values when cached). */
 int hks_build_operator(hks_plan* plan, void* const* buffers, void* stream);
+int hks_plan_cache_leaves(hks_plan* plan, void* stream);
 int hks_leaf_block(hks_plan* plan, int64_t leaf, double* out, void* stream);
 
 /* factorize, solver.py:111-186.  Reads INTERP, COUP; writes THETA, LEAF_LU,

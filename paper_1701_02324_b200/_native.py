@@ -61,6 +61,7 @@ SIGNATURES = {
     "hks_plan_destroy": [_P],
     "hks_build_operator": [_P, _BUFS, _P],
     "hks_leaf_block": [_P, _I64, _P, _P],
+    "hks_plan_cache_leaves": [_P, _P],
     "hks_factorize": [_P, _BUFS, _D, _I32, _I64P, _P],
     "hks_factor_stats": [_P, _BUFS, _DP, _I32P, _P],
     "hks_solve": [_P, _BUFS, _P, _P, _I64, _P],

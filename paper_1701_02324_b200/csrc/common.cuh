@@ -142,7 +142,8 @@ struct GemmDesc {
 // dst = alpha * op(src) (m x n result); mode 0: copy, 1: alpha * I, 2: zero,
 // 3: accumulate (dst += alpha * op(src)).
 // mode 0: dst = alpha op(src); 1: identity * alpha; 2: zeros; 3: dst += alpha src;
-// 4: dst = src^T + alpha src2 (trans must be 1; e.g. push = P^T - F)
+// 4: dst = src^T + alpha src2 (trans must be 1; e.g. push = P^T - F);
+// 5: dst = Bases::lam * src; 6: dst = src + Bases::lam I (trans 0 for 5, 6)
 struct CopyDesc {
   Ref src, dst;
   int m, n;

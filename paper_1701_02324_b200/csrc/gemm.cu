@@ -366,6 +366,11 @@ __global__ void __launch_bounds__(256) copy_batched_kernel(const Bases* __restri
       if (c.mode == 0 || c.mode == 3) {
         v = (c.trans ? src[j + (size_t)i * c.lds] : src[i + (size_t)j * c.lds]) * c.alpha;
         if (c.mode == 3) v += dst[i + (size_t)j * c.ldd];
+      } else if (c.mode == 5) {
+        v = bases.lam * src[i + (size_t)j * c.lds];
+      } else if (c.mode == 6) {
+        v = src[i + (size_t)j * c.lds];
+        if (i == j) v += bases.lam;
       } else {
         v = (c.mode == 1 && i == j) ? c.alpha : 0.0;
       }

@@ -359,6 +359,18 @@ struct Copies {
     v.push_back(CopyDesc{src, dst, m, n, lds, ldd, trans, 0, 1.0});
     me = std::max(me, m * n);
   }
+  // dst = lam * src (lam: the call's Bases::lam)
+  void lam_scale(Ref src, int lds, Ref dst, int ldd, int m, int n) {
+    if (m <= 0 || n <= 0) return;
+    v.push_back(CopyDesc{src, dst, m, n, lds, ldd, 0, 5, 1.0});
+    me = std::max(me, m * n);
+  }
+  // dst = src + lam I (lam: the call's Bases::lam)
+  void add_lam_diag(Ref src, int lds, Ref dst, int ldd, int m, int n) {
+    if (m <= 0 || n <= 0) return;
+    v.push_back(CopyDesc{src, dst, m, n, lds, ldd, 0, 6, 1.0});
+    me = std::max(me, m * n);
+  }
   // dst = src^T + alpha * src2 (dst, src2: m x n; src: n x m)
   void transpose_add(Ref src, int lds, Ref src2, int lds2, Ref dst, int ldd, int m, int n, double alpha) {
     if (m <= 0 || n <= 0) return;
@@ -372,7 +384,7 @@ struct Copies {
   }
   void flush(StepList& sl) {
     double bytes = 0;
-    for (auto& c : v) bytes += (c.mode == 0 ? 16.0 : c.mode >= 3 ? 24.0 : 8.0) * c.m * c.n;
+    for (auto& c : v) bytes += (c.mode == 0 || c.mode >= 5 ? 16.0 : c.mode >= 3 ? 24.0 : 8.0) * c.m * c.n;
     sl.add(ST_COPY, v, me, 0, 0.0, bytes);
     v.clear();
     me = 0;
@@ -878,7 +890,10 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl,
     int mx = 0;
     for (int64_t i = L.first(L.depth); i < L.nn; ++i) {
       const int m = (int)L.size[i], r = L.has_up(i) ? c.r(i) : 0;
-      ev.push_back(EvalDesc{kNull, kNull, L.begin[i], L.begin[i], m, m, c.leaf_lu(i), m, 1});
+      if (P.leaf_cached)  // K_aa + lam I from the cached leaf block
+        cp.add_lam_diag(abs_ref(static_cast<const double*>(P.leaf_cache.p) + P.leaf_off[i]), m, c.leaf_lu(i), m, m, m);
+      else
+        ev.push_back(EvalDesc{kNull, kNull, L.begin[i], L.begin[i], m, m, c.leaf_lu(i), m, 1});
       mx = std::max(mx, m);
       if (r > 0) cp.copy(c.interp(i), r, 1, c.phi(i), m, m, r);  // phi = P^T, then A^-1 P^T
       jobs.push_back(LuJob{c.leaf_lu(i), m, m, c.leaf_piv(i), c.info(i), kNull, r > 0 ? c.phi(i) : kNull, r, m,
@@ -1166,7 +1181,18 @@ void build_matvec(const hks_plan& P, int64_t kk, int part, StepList& sl) {
   const int64_t S = 0, A = stk;
   const bool sub = L.mode == PM_SUBTREE;
   if (part != 2) {
-    if (L.mode != PM_TOP) {  // leaves: u = K w + lam w, K never stored (treecode.py:99-101)
+    if (L.mode != PM_TOP && P.leaf_cached) {  // leaves from the cached blocks: u = lam w, u += K_aa w
+      Copies lw;
+      Gemms g;
+      for (int64_t i = L.first(L.depth); i < L.nn; ++i) {
+        const int m = (int)L.size[i];
+        lw.lam_scale(D(B_VIN, L.begin[i]), n, D(B_VOUT, L.begin[i]), n, m, k);
+        g.add(abs_ref(static_cast<const double*>(P.leaf_cache.p) + P.leaf_off[i]), m, 0, D(B_VIN, L.begin[i]), n, 0,
+              D(B_VOUT, L.begin[i]), n, m, k, m, 1.0, 1.0);
+      }
+      lw.flush(sl);
+      g.flush(sl);
+    } else if (L.mode != PM_TOP) {  // leaves: u = K w + lam w, K never stored (treecode.py:99-101)
       std::vector<SumDesc> ks;
       int mx = 0;
       for (int64_t i = L.first(L.depth); i < L.nn; ++i) {
@@ -1401,10 +1427,58 @@ extern "C" int hks_build_operator(hks_plan* P, void* const* buffers, void* strea
   return HKS_OK;
 }
 
+// Evaluate and keep every leaf block K_aa (no lam) of the plan in device
+// memory (treecode.py:48-51 caches them).  Must precede the first
+// factorize / hmatvec of the plan (their level programs are built on first
+// use and then bake the choice in).
+extern "C" int hks_plan_cache_leaves(hks_plan* P, void* stream) {
+  if (!P) return set_error(HKS_ERR_INVALID, "hks_plan_cache_leaves: null plan");
+  if (P->leaf_cached || P->L.mode == PM_TOP) return HKS_OK;
+  if (P->fact[0] || P->fact[1] || !P->mv_prog.empty() || !P->solve_prog.empty())
+    return set_error(HKS_ERR_INVALID, "hks_plan_cache_leaves: the plan's programs are already built");
+  const Layout& L = P->L;
+  cudaStream_t s = as_stream(stream);
+  P->leaf_off.assign(L.nn, -1);
+  int64_t total = 0;
+  int mx = 0;
+  for (int64_t i = L.first(L.depth); i < L.nn; ++i) {
+    P->leaf_off[i] = total;
+    total += L.size[i] * L.size[i];
+    mx = std::max<int>(mx, (int)L.size[i]);
+  }
+  cudaError_t e = P->leaf_cache.ensure((size_t)std::max<int64_t>(total, 1) * sizeof(double));
+  if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_plan_cache_leaves: %s", cudaGetErrorString(e));
+  StepList sl;
+  std::vector<EvalDesc> ev;
+  for (int64_t i = L.first(L.depth); i < L.nn; ++i) {
+    const int m = (int)L.size[i];
+    ev.push_back(EvalDesc{kNull, kNull, L.begin[i], L.begin[i], m, m,
+                          abs_ref(static_cast<double*>(P->leaf_cache.p) + P->leaf_off[i]), m, 0});
+  }
+  sl.add(ST_EVAL_CM, ev, mx, mx);
+  e = sl.upload(s);
+  Bases b{};
+  Bases* db = nullptr;
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&db), sizeof(Bases), s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(db, &b, sizeof(Bases), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = sl.run(db, P->X, (int)P->d, P->kp, s);
+  if (db) cudaFreeAsync(db, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // the uploaded descriptors die with `sl`
+  if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_plan_cache_leaves: %s", cudaGetErrorString(e));
+  P->leaf_cached = true;
+  return HKS_OK;
+}
+
 extern "C" int hks_leaf_block(hks_plan* P, int64_t leaf, double* out, void* stream) {
   if (!P || leaf < P->L.first(P->L.depth) || leaf >= P->L.nn)
     return set_error(HKS_ERR_INVALID, "hks_leaf_block: bad leaf %lld", (long long)leaf);
   const int64_t m = P->L.size[leaf];
+  if (P->leaf_cached) {  // the exact values factorize / hmatvec use
+    cudaError_t e = cudaMemcpyAsync(out, static_cast<const double*>(P->leaf_cache.p) + P->leaf_off[leaf],
+                                    (size_t)m * m * sizeof(double), cudaMemcpyDeviceToDevice, as_stream(stream));
+    if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_leaf_block: %s", cudaGetErrorString(e));
+    return HKS_OK;
+  }
   return hks_eval_block(P->X, P->d, &P->kern, nullptr, P->L.begin[leaf], m, nullptr, P->L.begin[leaf], m, out, m, 0,
                         0.0, stream);
 }

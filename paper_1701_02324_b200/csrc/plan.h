@@ -180,6 +180,13 @@ struct hks_plan {
   hks::KernelParams kp{};
   hks_kernel kern{};
 
+  // cached leaf blocks K_aa (no lam), column-major m x m each (treecode.py:
+  // 48-51 caches them too): hks_plan_cache_leaves.  Factorize then copies
+  // K_aa + lam I into the LU storage and hmatvec's leaf level is a GEMM,
+  // instead of evaluating the kernel every call.
+  hks::DevBuf leaf_cache;
+  std::vector<int64_t> leaf_off;            // element offset of each leaf's block (by heap index)
+  bool leaf_cached = false;
   hks::StepList coup_steps;                 // build_operator
   hks::GraphCache coup_exec;
   std::unique_ptr<hks::StepList> fact[2];   // factorize without / with the anorm steps for dgecon

@@ -440,6 +440,8 @@ class ShardedOperator:
         self.local_coup = sk.local_layout.alloc(N.BUF_COUP)
         self.top_coup = sk.top_layout.alloc(N.BUF_COUP)
         N.call("hks_build_operator", self.local.handle, self.local_buffers(), N.stream_ptr())
+        from .treecode import cache_leaf_blocks
+        self.leaf_cache = cache_leaf_blocks(self.local.handle, spec.size, int(tree._end[-1] - tree._begin[-1]))
         N.call("hks_build_operator", self.top.handle, self.top_buffers(), N.stream_ptr())
 
     @property

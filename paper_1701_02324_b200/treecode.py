@@ -76,6 +76,8 @@ class HierarchicalOperator:
         self.plan = Plan(tree, skeletons, kernel)
         self.coup_buf = lay.alloc(N.BUF_COUP)
         N.call("hks_build_operator", self.plan.handle, self.buffers(), N.stream_ptr())
+        self.leaf_cache = cache_leaf_blocks(self.plan.handle, tree.n, int(tree._end[-1] - tree._begin[-1])
+                                            if tree.depth else tree.n)
         nint = (1 << tree.depth) - 1
         self.leaf_blocks = _LazyBlocks(range(nint, lay.nn), self._leaf_block)
         self.couplings = _LazyBlocks(range(nint), self._coupling)
@@ -111,6 +113,24 @@ class HierarchicalOperator:
 
     def _coupling(self, i):
         return self.coupling_device(i).cpu().numpy().copy()
+
+
+def cache_leaf_blocks(plan_handle, n, leaf_size):
+    """Keep the plan's leaf blocks K_aa on the device (the reference's
+    build_operator caches leaf_blocks too, treecode.py:48-51) when they take
+    at most 8% of the device's memory -- C2, C3, C5 (1-4.3 GB); not C4
+    (34 GB beside its 67 GB factor sets).  HKS_LEAF_CACHE=0/1 forces it.
+    Returns whether the blocks are cached."""
+    import os
+    env = os.environ.get("HKS_LEAF_CACHE")
+    t = N.torch()
+    if env is not None:
+        want = env != "0"
+    else:
+        want = 8.0 * n * leaf_size <= 0.08 * t.cuda.get_device_properties(N.device()).total_memory
+    if want:
+        N.call("hks_plan_cache_leaves", plan_handle, N.stream_ptr())
+    return want
 
 
 def build_operator(tree, skeletons, kernel):
