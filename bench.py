@@ -251,19 +251,34 @@ class SingleRunner:
         return float(torch.linalg.vector_norm(res) / torch.linalg.vector_norm(self.B[0]))
 
     def e2e(self):
-        """pinned host B (input order) -> host x through the public API."""
+        """pinned host B (input order) -> host x through the public API.  The
+        H2D copy of B runs on a copy stream beside the factorization (it
+        does not depend on it); the solve waits for it, and x comes back as
+        one D2H copy into pinned memory."""
+        import torch
+        if self.w.method != "hybrid":
+            cs = getattr(self, "_copy_stream", None) or torch.cuda.Stream()
+            self._copy_stream = cs
+            with torch.cuda.stream(cs):
+                Bd = self.Bh.to(self.N.device(), non_blocking=True)
+            ev = cs.record_event()
+            f = self.hk.factorize(self.op, self.w.lam)
+            torch.cuda.current_stream().wait_event(ev)
+            Bd.record_stream(torch.cuda.current_stream())
+            X = self.hk.solve_multi(f, Bd, in_tree_order=False)
+            xh = torch.empty(X.shape, dtype=torch.float64, pin_memory=True)
+            xh.copy_(X, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            return xh
+        # hybrid_solve takes tree-ordered host vectors (krylov.py:155-188)
         f = self.hk.factorize(self.op, self.w.lam)
-        if self.w.method == "hybrid":  # hybrid_solve takes tree-ordered host vectors (krylov.py:155-188)
-            perm = np.asarray(self.tree.perm)
-            bt = self.b[perm]
-            from paper_1701_02324_b200.krylov import hybrid_solve_multi
-            xt, _ = hybrid_solve_multi(self.op, f, bt, tol=self.w.gmres_tol, max_iter=500,
-                                       restart=self.w.gmres_restart)
-            x = np.empty_like(self.b)
-            x[perm] = xt
-            return x
-        xh = self.hk.solve_multi(f, self.Bh, in_tree_order=False)
-        return xh.cpu().numpy() if hasattr(xh, "cpu") else xh
+        perm = np.asarray(self.tree.perm)
+        bt = self.b[perm]
+        from paper_1701_02324_b200.krylov import hybrid_solve_multi
+        xt, _ = hybrid_solve_multi(self.op, f, bt, tol=self.w.gmres_tol, max_iter=500, restart=self.w.gmres_restart)
+        x = np.empty_like(self.b)
+        x[perm] = xt
+        return x
 
     @property
     def io_bytes(self):
@@ -328,10 +343,17 @@ class ShardedRunner:
         return float(torch.sqrt(num[0] / num[1]))
 
     def e2e(self):
-        """pinned host block of the shard's right-hand sides -> host x rows."""
+        """pinned host block of the shard's right-hand sides -> host x rows
+        (the H2D copy beside the factorization, as SingleRunner.e2e)."""
         import torch
-        B = self.Bh.to(self.N.device(), non_blocking=True)
+        cs = getattr(self, "_copy_stream", None) or torch.cuda.Stream()
+        self._copy_stream = cs
+        with torch.cuda.stream(cs):
+            B = self.Bh.to(self.N.device(), non_blocking=True)
+        ev = cs.record_event()
         f = self.S.factorize_sharded(self.op, self.w.lam)
+        torch.cuda.current_stream().wait_event(ev)
+        B.record_stream(torch.cuda.current_stream())
         X = self.S.solve_sharded(f, B)
         xh = torch.empty(X.shape, dtype=torch.float64, pin_memory=True)
         xh.copy_(X, non_blocking=True)

@@ -52,51 +52,57 @@ struct GemmOp {
 
 // Stage the A (TBM x TBK) and B (TBK x 64) tiles of k-block k0 into shared
 // memory (layouts above); out-of-range elements are zero-filled.
+// One operand tile into shared memory in 16-byte pairs along its contiguous
+// dimension: CD x OD elements (contiguous x other), smem [o][c] with row
+// stride S, global element (c, o) at base[c + o * ld].  `vec`: the base is
+// 16-byte aligned and ld is even, so every in-range pair is one cp.async of
+// 16 bytes (half the LDGSTS of 8-byte copies); pairs crossing the edge and
+// unaligned operands fall back to two zero-filling 8-byte copies.
+template <int CD, int OD, int S, int T>
+__device__ __forceinline__ void stage_pairs(double* sm, const double* base, int ld, int c0, int climit, int o0,
+                                            int olimit, bool vec) {
+  constexpr int PC = CD / 2;
+  static_assert((PC * OD) % T == 0, "tile / thread mapping");
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int j = 0; j < (PC * OD) / T; ++j) {
+    const int e = t + j * T;
+    const int c = 2 * (e % PC), o = e / PC;
+    const int gc = c0 + c, go = o0 + o;
+    double* dst = sm + o * S + c;
+    const double* src = base + gc + (size_t)go * ld;
+    const bool oko = go < olimit;
+    if (vec && oko && gc + 1 < climit) {
+      cp_async16(dst, src);
+    } else {
+      const bool ok0 = oko && gc < climit, ok1 = oko && gc + 1 < climit;
+      cp_async8(dst, ok0 ? src : base, ok0);
+      cp_async8(dst + 1, ok1 ? src + 1 : base, ok1);
+    }
+  }
+}
+
+// Stage the A (TBM x TBK) and B (TBK x 64) tiles of k-block k0 into shared
+// memory (layouts above); out-of-range elements are zero-filled.
 template <int TBM, int TBK>
-__device__ __forceinline__ void load_stage(const GemmOp& g, int m0, int n0, int k0, double* As, double* Bs) {
+__device__ __forceinline__ void load_stage(const GemmOp& g, int m0, int n0, int k0, double* As, double* Bs, bool va,
+                                           bool vb) {
   constexpr int T = 2 * TBM, KST = TBK + 4;  // threads, [row][k] stride
   constexpr int AMS = TBM + 4, BNS = BN + 4;  // [k][row] strides
-  const int t = threadIdx.x;
-  if (!g.transA) {  // A column-major: m contiguous -> As[k][m]
-#pragma unroll
-    for (int j = 0; j < TBK / (T / TBM); ++j) {
-      const int mi = t % TBM, ki = t / TBM + (T / TBM) * j;
-      const int m = m0 + mi, k = k0 + ki;
-      const bool ok = m < g.m && k < g.k;
-      cp_async8(As + ki * AMS + mi, ok ? g.A + m + (size_t)k * g.lda : g.A, ok);
-    }
-  } else {  // A^T stored: k contiguous -> As[m][k]
-#pragma unroll
-    for (int j = 0; j < TBM / (T / TBK); ++j) {
-      const int ki = t % TBK, mi = t / TBK + (T / TBK) * j;
-      const int k = k0 + ki, m = m0 + mi;
-      const bool ok = m < g.m && k < g.k;
-      cp_async8(As + mi * KST + ki, ok ? g.A + k + (size_t)m * g.lda : g.A, ok);
-    }
-  }
-  if (!g.transB) {  // B column-major: k contiguous -> Bs[n][k]
-#pragma unroll
-    for (int j = 0; j < BN / (T / TBK); ++j) {
-      const int ki = t % TBK, ni = t / TBK + (T / TBK) * j;
-      const int k = k0 + ki, n = n0 + ni;
-      const bool ok = n < g.n && k < g.k;
-      cp_async8(Bs + ni * KST + ki, ok ? g.B + k + (size_t)n * g.ldb : g.B, ok);
-    }
-  } else {  // B^T stored: n contiguous -> Bs[k][n]
-#pragma unroll
-    for (int j = 0; j < TBK / (T / BN); ++j) {
-      const int ni = t % BN, ki = t / BN + (T / BN) * j;
-      const int n = n0 + ni, k = k0 + ki;
-      const bool ok = n < g.n && k < g.k;
-      cp_async8(Bs + ki * BNS + ni, ok ? g.B + n + (size_t)k * g.ldb : g.B, ok);
-    }
-  }
+  if (!g.transA)  // A column-major: m contiguous -> As[k][m]
+    stage_pairs<TBM, TBK, AMS, T>(As, g.A, g.lda, m0, g.m, k0, g.k, va);
+  else  // A^T stored: k contiguous -> As[m][k]
+    stage_pairs<TBK, TBM, KST, T>(As, g.A, g.lda, k0, g.k, m0, g.m, va);
+  if (!g.transB)  // B column-major: k contiguous -> Bs[n][k]
+    stage_pairs<TBK, BN, KST, T>(Bs, g.B, g.ldb, k0, g.k, n0, g.n, vb);
+  else  // B^T stored: n contiguous -> Bs[k][n]
+    stage_pairs<BN, TBK, BNS, T>(Bs, g.B, g.ldb, n0, g.n, k0, g.k, vb);
 }
 
 template <int TBM, int TBK = BK>
 __global__ void __launch_bounds__(2 * TBM) gemm_batched_kernel(const Bases* __restrict__ bases_ptr,
                                                                 const GemmDesc* __restrict__ descs,
-                                                                int tiles_n) {
+                                                                int tiles_n, bool g_vec16) {
   constexpr int BM = TBM, BK = TBK, KS = TBK + 4;
   const Bases& bases = *bases_ptr;
   const GemmDesc gd = descs[blockIdx.y];
@@ -106,7 +112,7 @@ __global__ void __launch_bounds__(2 * TBM) gemm_batched_kernel(const Bases* __re
   if (m0 >= g.m || n0 >= g.n) return;
 
   constexpr int AE = OperandLayout<TBM>::kElems, BE = OperandLayout<BN>::kElems;
-  extern __shared__ double gsm[];
+  extern __shared__ __align__(16) double gsm[];
   double* As = gsm;                       // STAGES x AE
   double* Bs = gsm + STAGES * AE;         // STAGES x BE
 
@@ -139,16 +145,18 @@ __global__ void __launch_bounds__(2 * TBM) gemm_batched_kernel(const Bases* __re
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int nk = (g.k + BK - 1) / BK;
+  const bool va = g_vec16 && ((reinterpret_cast<uintptr_t>(g.A) & 15) == 0) && (g.lda % 2 == 0);
+  const bool vb = g_vec16 && ((reinterpret_cast<uintptr_t>(g.B) & 15) == 0) && (g.ldb % 2 == 0);
 #pragma unroll
   for (int st = 0; st < STAGES - 1; ++st) {
-    if (st < nk) load_stage<TBM, TBK>(g, m0, n0, st * BK, As + st * AE, Bs + st * BE);
+    if (st < nk) load_stage<TBM, TBK>(g, m0, n0, st * BK, As + st * AE, Bs + st * BE, va, vb);
     cp_async_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     const int pf = kt + STAGES - 1;
-    if (pf < nk) load_stage<TBM, TBK>(g, m0, n0, pf * BK, As + (pf % STAGES) * AE, Bs + (pf % STAGES) * BE);
+    if (pf < nk) load_stage<TBM, TBK>(g, m0, n0, pf * BK, As + (pf % STAGES) * AE, Bs + (pf % STAGES) * BE, va, vb);
     cp_async_commit();
     const double* as = As + (kt % STAGES) * AE;
     const double* bs = Bs + (kt % STAGES) * BE;
@@ -232,7 +240,7 @@ __global__ void __launch_bounds__(128) gemm_skinny_kernel(const Bases* __restric
   constexpr int AMS = SBM + 4, BNS = SBN + 4;
   constexpr int AE = (SBM * KS > BK * AMS) ? SBM * KS : BK * AMS;
   constexpr int BE = (SBN * KS > BK * BNS) ? SBN * KS : BK * BNS;
-  extern __shared__ double gsm[];
+  extern __shared__ __align__(16) double gsm[];
   double* As = gsm;                        // STAGES x AE
   double* Bs = gsm + STAGES * AE;          // STAGES x BE
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
@@ -403,6 +411,7 @@ cudaError_t launch_gemm_batched(const Bases* bases, const GemmDesc* d_descs, int
     return cudaGetLastError();
   }
   const bool tall = forced == 128;  // measured: no gain over 64-row tiles on the plans' products
+  static const bool vec16 = getenv("HKS_GEMM_VEC16") == nullptr || atoi(getenv("HKS_GEMM_VEC16")) != 0;
   const int BM = tall ? 128 : 64;
   const int tm = (max_m + BM - 1) / BM, tn = (max_n + BN - 1) / BN;
   for (int first = 0; first < count; first += 65535) {
@@ -413,10 +422,10 @@ cudaError_t launch_gemm_batched(const Bases* bases, const GemmDesc* d_descs, int
                       sizeof(double);
     if (tall) {
       raise_smem_limit(gemm_batched_kernel<128>, sm);
-      gemm_batched_kernel<128><<<grid, 256, sm, stream>>>(bases, d_descs + first, tn);
+      gemm_batched_kernel<128><<<grid, 256, sm, stream>>>(bases, d_descs + first, tn, vec16);
     } else {
       raise_smem_limit(gemm_batched_kernel<64>, sm);
-      gemm_batched_kernel<64><<<grid, 128, sm, stream>>>(bases, d_descs + first, tn);
+      gemm_batched_kernel<64><<<grid, 128, sm, stream>>>(bases, d_descs + first, tn, vec16);
     }
   }
   return cudaGetLastError();
