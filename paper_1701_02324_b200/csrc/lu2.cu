@@ -356,7 +356,7 @@ __device__ __forceinline__ double div_rn(double a, double b, double y) {
 // when given) with the T rows of its step (one cp.async group, prefetched
 // while the previous block computes) and stored as soon as it is final,
 // instead of whole-X load / store phases.
-template <bool UPPER, int NC, int NT = NC>
+template <bool UPPER, int NC, int NT = NC, bool SINGLE_T = false>
 __device__ __forceinline__ void trsm_sweep(double* X, double* Tbuf, int tts, const double* T, int ldt, int k,
                                            int nc, const double* Bin = nullptr, double* Bout = nullptr,
                                            int ldb = 0, const int* perm = nullptr) {
@@ -385,14 +385,15 @@ __device__ __forceinline__ void trsm_sweep(double* X, double* Tbuf, int tts, con
   for (int bb = 0; bb < nblk; ++bb) {
     const int b = UPPER ? nblk - 1 - bb : bb;
     const int r0 = b * 32, nr = min(32, k - r0);
-    double* Ts = Tbuf + (bb & 1) * 32 * tts;
+    double* Ts = SINGLE_T ? Tbuf : Tbuf + (bb & 1) * 32 * tts;
     cp_async_wait<0>();
     __syncthreads();  // X / this block's rows of T landed; the previous block's solve is complete
     if (Bout && bb > 0) store_x(UPPER ? b + 1 : b - 1);  // the previous block is final
     if (bb + 1 < nblk) {
       if (Bin) stage_x(UPPER ? b - 1 : b + 1);
-      trsm_stage_rows<UPPER, NW>(Tbuf + ((bb + 1) & 1) * 32 * tts, tts, T, ldt, k, UPPER ? b - 1 : b + 1, wid,
-                                 lane);
+      if (!SINGLE_T)  // next block's rows of T into the other buffer, behind this block's work
+        trsm_stage_rows<UPPER, NW>(Tbuf + ((bb + 1) & 1) * 32 * tts, tts, T, ldt, k, UPPER ? b - 1 : b + 1, wid,
+                                   lane);
       cp_async_commit();
     }
     // reciprocals of this block's diagonal, off the solve's dependency chain
@@ -517,12 +518,17 @@ __device__ __forceinline__ void trsm_sweep(double* X, double* Tbuf, int tts, con
       for (int i = 0; i < 32; ++i)
         if (i < nr) X[(r0 + i) * TXS + tid] = x[i];
     }
+    if (SINGLE_T && bb + 1 < nblk) {  // one T buffer (half the staging smem): refill once it is read
+      __syncthreads();
+      trsm_stage_rows<UPPER, NW>(Tbuf, tts, T, ldt, k, UPPER ? b - 1 : b + 1, wid, lane);
+      cp_async_commit();
+    }
   }
   __syncthreads();
   if (Bout) store_x(UPPER ? 0 : nblk - 1);
 }
 
-template <bool UPPER, int NC, int NT>
+template <bool UPPER, int NC, int NT, bool SINGLE_T = false>
 __global__ void __launch_bounds__(NT) trsm_kernel(const Bases* __restrict__ bases_ptr,
                                                   const TrsmDesc* __restrict__ descs, int kcap, int tts) {
   constexpr int TXS = NC + 4;
@@ -541,7 +547,7 @@ __global__ void __launch_bounds__(NT) trsm_kernel(const Bases* __restrict__ base
   (void)wid;
   // X streams in and out block by block inside the sweep (256-byte coalesced
   // LDGSTS along each column's rows)
-  trsm_sweep<UPPER, NC, NT>(X, Tbuf, tts, T, D.ldt, k, nc, B, B, D.ldb);
+  trsm_sweep<UPPER, NC, NT, SINGLE_T>(X, Tbuf, tts, T, D.ldt, k, nc, B, B, D.ldb);
 }
 
 // Whole getrs of a small matrix (n <= kGetrsFusedMax) in one CTA per block of
@@ -665,16 +671,17 @@ cudaError_t launch_swap_batched(const Bases* b, const SwapDesc* d, int count, in
   return cudaGetLastError();
 }
 
-template <bool UPPER, int NC, int NT = NC>
+template <bool UPPER, int NC, int NT = NC, bool SINGLE_T = false>
 static cudaError_t launch_trsm_nc(const Bases* b, const TrsmDesc* d, int count, int max_cols, int max_k,
                                   cudaStream_t s) {
   // tts == 4 (mod 16), and > every column r0 + 31 the register diagonal solve touches
   const int kcap = (max_k + 31) / 32 * 32, tts = kcap + 4;
-  const size_t sm = (size_t)(kcap * (NC + 4) + 2 * 32 * tts) * sizeof(double);
-  raise_smem_limit(trsm_kernel<UPPER, NC, NT>, sm);
+  const size_t sm = (size_t)(kcap * (NC + 4) + (SINGLE_T ? 1 : 2) * 32 * tts) * sizeof(double);
+  raise_smem_limit(trsm_kernel<UPPER, NC, NT, SINGLE_T>, sm);
   for (int first = 0; first < count; first += 65535) {
     const int cnt = count - first < 65535 ? count - first : 65535;
-    trsm_kernel<UPPER, NC, NT><<<dim3((max_cols + NC - 1) / NC, cnt), NT, sm, s>>>(b, d + first, kcap, tts);
+    trsm_kernel<UPPER, NC, NT, SINGLE_T><<<dim3((max_cols + NC - 1) / NC, cnt), NT, sm, s>>>(b, d + first, kcap,
+                                                                                          tts);
   }
   return cudaGetLastError();
 }
@@ -686,6 +693,13 @@ static cudaError_t launch_trsm_t(const Bases* b, const TrsmDesc* d, int count, i
     const char* e = getenv("HKS_TRSM_NC");
     return e ? atoi(e) : 128;
   }();
+  // experiment knob: 64-column blocks with 4 warps and one T staging buffer
+  // (103 KB of shared memory at k = 128: two CTAs per SM instead of one)
+  static const int single_t = [] {
+    const char* e = getenv("HKS_TRSM_SINGLE_T");
+    return e ? atoi(e) : 0;
+  }();
+  if (single_t && max_cols > 32) return launch_trsm_nc<UPPER, 64, 128, true>(b, d, count, max_cols, max_k, s);
   // few matrices (the narrow top levels): 32-column blocks, 4x the CTAs for
   // the latency-bound sweeps; wide batches keep 128 (more reuse of T)
   const bool narrow_batch = (long long)count * ((max_cols + 127) / 128) < 96;
