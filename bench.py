@@ -517,7 +517,7 @@ def gpu_arm(args, w, rank, world):
         achieved = kd["bytes"] / (kd["ms"] * 1e-3) / 1e9
         roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
-    traffic_file = ROOT / "profiles" / "ncu_traffic_r01.json"
+    traffic_file = ROOT / "profiles" / "ncu_traffic_r02.json"
     roof["traffic"] = None
     if traffic_file.exists():
         tr = json.loads(traffic_file.read_text())
