@@ -14,7 +14,8 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libhks.so"
+# HKS_LIB_NAME selects a variant build in _lib/ (A/B experiments); default libhks.so
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / os.environ.get("HKS_LIB_NAME", "libhks.so")
 
 HKS_OK = 0
 HKS_ERR_INVALID = 1

@@ -894,6 +894,255 @@ __global__ void __launch_bounds__(32 * GW_WARPS) gecon_warp_kernel(const Bases* 
   }
 }
 
+// ------------------------------------------------------------------
+// CTA-per-matrix form with many loads in flight (the default since round
+// 2): 128 threads per matrix, four matrices per SM.  A triangular sweep is
+// a chain of 32-row block steps whose off-diagonal update streams the
+// block's 32 columns of the LU from HBM; with a few rows per thread and one
+// column at a time, every step waited out ~32 dependent load latencies.
+// Here a thread keeps 4 rows x 4 columns of loads in flight (non-transposed
+// sweeps) and every warp stages its own 32-column chunks of the transposed
+// panel through a padded shared tile (one coalesced 256-byte load per
+// column, 32 in flight).  Same dlacn2 state machine as gecon_step_one.
+constexpr int GC_THREADS = 128;
+constexpr int GC_WARPS = GC_THREADS / 32;
+
+__device__ __noinline__ void trsv_cta(const double* LU, int lda, int n, double* x, double* tiles, bool upper,
+                                      bool trans) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const bool forward = (!upper && !trans) || (upper && trans);
+  const int nblk = (n + 31) / 32;
+  double* tile = tiles + wid * (32 * 33);
+  double t[32], rd = 1.0;
+  if (tid < 32) trsv_load_diag(LU, lda, n, forward ? 0 : nblk - 1, upper, trans, t, rd);
+  for (int bb = 0; bb < nblk; ++bb) {
+    const int b = forward ? bb : nblk - 1 - bb;
+    const int r0 = b * 32, nr = min(32, n - r0);
+    if (tid < 32) {
+      double v = lane < nr ? x[r0 + lane] : 0.0;
+      if (forward) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (lane == j) v *= rd;
+          const double xj = __shfl_sync(0xffffffffu, v, j);
+          if (lane > j) v -= t[j] * xj;
+        }
+      } else {
+#pragma unroll
+        for (int j = 31; j >= 0; --j) {
+          if (lane == j) v *= rd;
+          const double xj = __shfl_sync(0xffffffffu, v, j);
+          if (lane < j) v -= t[j] * xj;
+        }
+      }
+      if (lane < nr) x[r0 + lane] = v;
+      if (bb + 1 < nblk) trsv_load_diag(LU, lda, n, forward ? b + 1 : b - 1, upper, trans, t, rd);
+    }
+    __syncthreads();
+    const int lo = forward ? r0 + nr : 0, hi = forward ? n : r0;
+    if (!trans) {
+      constexpr int RQ = 4, JU = 4;
+      for (int base = lo; base < hi; base += GC_THREADS * RQ) {
+        double acc[RQ];
+#pragma unroll
+        for (int q = 0; q < RQ; ++q) {
+          const int i = base + tid + GC_THREADS * q;
+          acc[q] = i < hi ? x[i] : 0.0;
+        }
+        for (int j0 = 0; j0 < nr; j0 += JU) {
+          double lv[JU][RQ];
+#pragma unroll
+          for (int jj = 0; jj < JU; ++jj)
+#pragma unroll
+            for (int q = 0; q < RQ; ++q) {
+              const int i = base + tid + GC_THREADS * q;
+              lv[jj][q] = (i < hi && j0 + jj < nr) ? LU[i + (size_t)(r0 + j0 + jj) * lda] : 0.0;
+            }
+#pragma unroll
+          for (int jj = 0; jj < JU; ++jj) {
+            const double xj = j0 + jj < nr ? x[r0 + j0 + jj] : 0.0;
+#pragma unroll
+            for (int q = 0; q < RQ; ++q) acc[q] -= lv[jj][q] * xj;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < RQ; ++q) {
+          const int i = base + tid + GC_THREADS * q;
+          if (i < hi) x[i] = acc[q];
+        }
+      }
+    } else {
+      for (int c0 = lo + 32 * wid; c0 < hi; c0 += 32 * GC_WARPS) {
+        const int nq = min(32, hi - c0);
+#pragma unroll
+        for (int q = 0; q < 32; ++q)
+          tile[q * 33 + lane] = (q < nq && lane < nr) ? LU[r0 + lane + (size_t)(c0 + q) * lda] : 0.0;
+        __syncwarp();
+        if (lane < nq) {
+          double sacc = x[c0 + lane];
+#pragma unroll 8
+          for (int j = 0; j < nr; ++j) sacc -= tile[lane * 33 + j] * x[r0 + j];
+          x[c0 + lane] = sacc;
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__device__ void gecon_cta_one(const Bases& bases, const LuDesc& L, int m, int stride, int phase, double* x,
+                              double* tiles) {
+  if (L.rcond == kNull) return;
+  const int n = L.n;
+  double* st = at<double>(bases, make_ref(kGeconScratchBase, 0)) + (size_t)m * stride;
+  double* gx = st;
+  double* gsgn = st + n;
+  double* sc = st + 2 * (size_t)n;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double* rcond = at<double>(bases, L.rcond);
+  __shared__ double red_v[8];
+  __shared__ int red_i[8];
+  __shared__ int s_diff;
+  if (phase == 0) {
+    int state = GS_A;
+    if (n == 0) {
+      if (tid == 0) *rcond = 1.0;
+      state = GS_DONE;
+    } else {
+      const double anorm = *at<const double>(bases, L.anorm);
+      if (anorm == 0.0 || (L.info != kNull && *at<const int>(bases, L.info) != 0)) {
+        if (tid == 0) *rcond = 0.0;
+        state = GS_DONE;
+      }
+    }
+    if (state != GS_DONE)
+      for (int i = tid; i < n; i += nt) gx[i] = 1.0 / n;
+    if (tid == 0) {
+      sc[0] = state;
+      sc[1] = 1;
+      sc[2] = 0;
+      sc[3] = 0;
+      sc[4] = 0.0;
+    }
+    return;
+  }
+  int state = (int)sc[0];
+  if (state == GS_DONE) return;
+  const double* LUa = at<const double>(bases, L.A);
+  const int kase = (int)sc[1];
+  int iter = (int)sc[2], j = (int)sc[3];
+  double est = sc[4];
+  for (int i = tid; i < n; i += nt) x[i] = gx[i];
+  __syncthreads();
+  if (kase == 1) {
+    trsv_cta(LUa, L.lda, n, x, tiles, false, false);
+    trsv_cta(LUa, L.lda, n, x, tiles, true, false);
+  } else {
+    trsv_cta(LUa, L.lda, n, x, tiles, true, true);
+    trsv_cta(LUa, L.lda, n, x, tiles, false, true);
+  }
+  int next_kase = 1;
+  auto set_alt = [&]() {
+    for (int i = tid; i < n; i += nt) {
+      const double sg = (i % 2 == 0) ? 1.0 : -1.0;
+      x[i] = sg * (1.0 + (double)i / (double)(n - 1));
+    }
+    next_kase = 1;
+    state = GS_E;
+  };
+  auto set_unit = [&](int jj) {
+    for (int i = tid; i < n; i += nt) x[i] = (i == jj) ? 1.0 : 0.0;
+    next_kase = 1;
+    state = GS_C;
+  };
+  if (state == GS_A) {
+    if (n == 1) {
+      est = fabs(x[0]);
+      state = GS_DONE;
+    } else {
+      est = block_asum(x, n, red_v);
+      for (int i = tid; i < n; i += nt) {
+        x[i] = x[i] >= 0.0 ? 1.0 : -1.0;
+        gsgn[i] = x[i];
+      }
+      next_kase = 2;
+      state = GS_B;
+    }
+  } else if (state == GS_B) {
+    j = block_iamax(x, n, red_v, red_i);
+    iter = 2;
+    __syncthreads();
+    set_unit(j);
+  } else if (state == GS_C) {
+    const double estold = est;
+    est = block_asum(x, n, red_v);
+    if (tid == 0) s_diff = 0;
+    __syncthreads();
+    for (int i = tid; i < n; i += nt) {
+      const double xs = x[i] >= 0.0 ? 1.0 : -1.0;
+      if (xs != gsgn[i]) s_diff = 1;
+    }
+    __syncthreads();
+    const int diff = s_diff;
+    __syncthreads();
+    if (!diff || est <= estold) {
+      set_alt();
+    } else {
+      for (int i = tid; i < n; i += nt) {
+        x[i] = x[i] >= 0.0 ? 1.0 : -1.0;
+        gsgn[i] = x[i];
+      }
+      next_kase = 2;
+      state = GS_D;
+    }
+  } else if (state == GS_D) {
+    const int jlast = j;
+    j = block_iamax(x, n, red_v, red_i);
+    __syncthreads();
+    if (x[jlast] != fabs(x[j]) && iter < 5) {
+      ++iter;
+      __syncthreads();
+      set_unit(j);
+    } else {
+      __syncthreads();
+      set_alt();
+    }
+  } else {
+    const double temp = 2.0 * (block_asum(x, n, red_v) / (double)(3 * n));
+    if (temp > est) est = temp;
+    state = GS_DONE;
+  }
+  __syncthreads();
+  if (state == GS_DONE) {
+    if (tid == 0) {
+      const double anorm = *at<const double>(bases, L.anorm);
+      *rcond = est != 0.0 ? (1.0 / est) / anorm : 0.0;
+    }
+  } else {
+    for (int i = tid; i < n; i += nt) gx[i] = x[i];
+  }
+  if (tid == 0) {
+    sc[0] = state;
+    sc[1] = next_kase;
+    sc[2] = iter;
+    sc[3] = j;
+    sc[4] = est;
+  }
+}
+
+__global__ void __launch_bounds__(GC_THREADS, 4) gecon_cta_kernel(const Bases* __restrict__ bases_ptr,
+                                                                  const LuDesc* __restrict__ descs, int count,
+                                                                  int stride, int phase, int xs) {
+  extern __shared__ double gcsm[];
+  double* x = gcsm;
+  double* tiles = gcsm + xs;
+  for (int m = blockIdx.x; m < count; m += gridDim.x) {
+    gecon_cta_one(*bases_ptr, descs[m], m, stride, phase, x, tiles);
+    __syncthreads();
+  }
+}
+
 // One phase of the estimates of `count` matrices; a CTA walks matrices
 // blockIdx.x, + gridDim.x, ...  A grid smaller than the batch leaves SMs
 // with no estimate CTA at all, where the factorization's register-heavy
@@ -952,8 +1201,18 @@ cudaError_t launch_getrs_batched(const Bases* b, const LuSolveDesc* d, int count
 
 cudaError_t launch_gecon_batched(const Bases* b, const LuDesc* d, int count, int max_n, cudaStream_t s, int phase) {
   if (count <= 0) return cudaSuccess;
-  static const bool warp_form = getenv("HKS_GECON_CTA") == nullptr;
-  if (phase >= 0 && warp_form) {  // one warp per matrix, all matrices in one wave where they fit
+  static const int form = [] {  // 0: CTA-per-matrix, 128 threads (default); 1: warp per matrix; 2: 256-thread CTA
+    const char* e = getenv("HKS_GECON_FORM");
+    return e ? atoi(e) : 0;
+  }();
+  if (phase >= 0 && form == 0) {
+    const int xs = ((max_n > 0 ? max_n : 1) + 1) / 2 * 2;
+    const size_t sm = (size_t)(xs + GC_WARPS * 32 * 33) * sizeof(double);
+    raise_smem_limit(gecon_cta_kernel, sm);
+    gecon_cta_kernel<<<count, GC_THREADS, sm, s>>>(b, d, count, gecon_stride(max_n), phase, xs);
+    return cudaGetLastError();
+  }
+  if (phase >= 0 && form == 1) {  // one warp per matrix, all matrices in one wave where they fit
     const int xs = ((max_n > 0 ? max_n : 1) + 1) / 2 * 2;
     const size_t sm = (size_t)GW_WARPS * (xs + GW_TILE) * sizeof(double);
     raise_smem_limit(gecon_warp_kernel, sm);
