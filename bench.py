@@ -204,6 +204,7 @@ class SingleRunner:
         skels, setup["skeletonize"] = timed(lambda: hk.build_skeletons(tree, kern, cfg, knn=knn))
         self.op, setup["assemble"] = timed(lambda: hk.build_operator(tree, skels, kern))
         self.setup = {k: round(v, 4) for k, v in setup.items()}
+        print(f"bench: {w.name} N={w.n} setup {self.setup}", file=sys.stderr, flush=True)
         self.tree = tree
         # right-hand sides resident in tree order, column-major (k, n)
         self.B = N.to_device(np.ascontiguousarray(self.b[np.asarray(tree.perm)].T))
@@ -399,7 +400,7 @@ def gpu_arm(args, w, rank, world):
     # configs whose factor storage is a large share of HBM (C4: 67 GB) keep
     # one factorization alive at a time; the others keep the previous one
     # alive across the next step, like an application that compares them
-    lean = run.factor_bytes() * 3 > 0.9 * torch.cuda.mem_get_info()[0]  # 3 sets: new, previous, pending
+    lean = run.factor_bytes() * 4 > 0.8 * torch.cuda.mem_get_info()[0]  # 4 sets: new, previous, 2 pending
 
     clocks = ClockSampler(torch.cuda.current_device())
     if not args.no_clocks:

@@ -170,9 +170,14 @@ class FactorStorage:
         return bufs
 
     def reserve(self, total):
-        """Grow the pool to `total` sets up front (e.g. before a timed loop)."""
+        """Grow the pool to `total` sets up front (e.g. before a timed loop),
+        or as many as device memory holds.  Returns the number of sets."""
         while self.created < total:
-            self.free.append((self._new(), None))
+            try:
+                self.free.append((self._new(), None))
+            except N.torch().cuda.OutOfMemoryError:
+                break
+        return self.created
 
     def lease(self):
         for idx, (bufs, evs) in enumerate(self.free):
