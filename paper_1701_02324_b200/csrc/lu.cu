@@ -718,9 +718,14 @@ __device__ void trsv_warp(const double* LU, int lda, int n, double* x, double* t
       // conflict-free)
       for (int c0 = lo; c0 < hi; c0 += 32) {
         const int nq = min(32, hi - c0);
-#pragma unroll
-        for (int q = 0; q < 32; ++q)
-          tile[q * 33 + lane] = (q < nq && lane < nr) ? LU[r0 + lane + (size_t)(c0 + q) * lda] : 0.0;
+        // cp.async: all 32 column loads in flight (a register load + shared
+        // store pair per column serialised one DRAM latency per column)
+        for (int q = 0; q < 32; ++q) {
+          const bool ok = q < nq && lane < nr;
+          cp_async8(tile + q * 33 + lane, ok ? LU + r0 + lane + (size_t)(c0 + q) * lda : LU, ok);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
         __syncwarp();
         if (lane < nq) {
           double s = x[c0 + lane];
@@ -974,9 +979,14 @@ __device__ __noinline__ void trsv_cta(const double* LU, int lda, int n, double* 
     } else {
       for (int c0 = lo + 32 * wid; c0 < hi; c0 += 32 * GC_WARPS) {
         const int nq = min(32, hi - c0);
-#pragma unroll
-        for (int q = 0; q < 32; ++q)
-          tile[q * 33 + lane] = (q < nq && lane < nr) ? LU[r0 + lane + (size_t)(c0 + q) * lda] : 0.0;
+        // cp.async: all 32 column loads in flight (a register load + shared
+        // store pair per column serialised one DRAM latency per column)
+        for (int q = 0; q < 32; ++q) {
+          const bool ok = q < nq && lane < nr;
+          cp_async8(tile + q * 33 + lane, ok ? LU + r0 + lane + (size_t)(c0 + q) * lda : LU, ok);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
         __syncwarp();
         if (lane < nq) {
           double sacc = x[c0 + lane];
