@@ -684,32 +684,25 @@ __device__ void trsv_warp(const double* LU, int lda, int n, double* x, double* t
     __syncwarp();
     const int lo = forward ? r0 + nr : 0, hi = forward ? n : r0;
     if (!trans) {
-      // lane per row, each column's rows contiguous (coalesced); a lane keeps
-      // up to 16 rows in flight per column so the loads overlap (the sweep
-      // is a chain of 32-row steps -- with one row at a time every step
-      // waited out ~30 dependent load latencies)
-      constexpr int RQ = 16;
-      for (int base = lo; base < hi; base += 32 * RQ) {
-        double acc[RQ];
-#pragma unroll
-        for (int q = 0; q < RQ; ++q) {
-          const int i = base + lane + 32 * q;
-          acc[q] = i < hi ? x[i] : 0.0;
+      // 32 rows x the block's 32 columns at a time through the padded tile
+      // (cp.async: the 32 column segments of 256 bytes all in flight), then
+      // lane q updates row c0 + q
+      for (int c0 = lo; c0 < hi; c0 += 32) {
+        const int nq = min(32, hi - c0);
+        for (int j = 0; j < 32; ++j) {
+          const bool ok = j < nr && lane < nq;
+          cp_async8(tile + j * 33 + lane, ok ? LU + c0 + lane + (size_t)(r0 + j) * lda : LU, ok);
         }
-        for (int j = 0; j < nr; ++j) {
-          const double xj = x[r0 + j];
-          const double* col = LU + (size_t)(r0 + j) * lda;
-#pragma unroll
-          for (int q = 0; q < RQ; ++q) {
-            const int i = base + lane + 32 * q;
-            if (i < hi) acc[q] -= col[i] * xj;
-          }
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncwarp();
+        if (lane < nq) {
+          double sacc = x[c0 + lane];
+#pragma unroll 8
+          for (int j = 0; j < nr; ++j) sacc -= tile[j * 33 + lane] * x[r0 + j];
+          x[c0 + lane] = sacc;
         }
-#pragma unroll
-        for (int q = 0; q < RQ; ++q) {
-          const int i = base + lane + 32 * q;
-          if (i < hi) x[i] = acc[q];
-        }
+        __syncwarp();
       }
     } else {
       // op(T)(i, r0 + j) = T(r0 + j, i): 32 columns of T at a time through a
@@ -1211,9 +1204,9 @@ cudaError_t launch_getrs_batched(const Bases* b, const LuSolveDesc* d, int count
 
 cudaError_t launch_gecon_batched(const Bases* b, const LuDesc* d, int count, int max_n, cudaStream_t s, int phase) {
   if (count <= 0) return cudaSuccess;
-  static const int form = [] {  // 0: CTA-per-matrix, 128 threads (default); 1: warp per matrix; 2: 256-thread CTA
+  static const int form = [] {  // 1: warp per matrix (default); 0: 128-thread CTA per matrix; 2: 256-thread CTA
     const char* e = getenv("HKS_GECON_FORM");
-    return e ? atoi(e) : 0;
+    return e ? atoi(e) : 1;
   }();
   if (phase >= 0 && form == 0) {
     const int xs = ((max_n > 0 ? max_n : 1) + 1) / 2 * 2;
