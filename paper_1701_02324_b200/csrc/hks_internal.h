@@ -47,6 +47,17 @@ cudaError_t launch_trsm_batched(const Bases* b, const TrsmDesc* d, int count, in
 cudaError_t launch_lu_fused(const Bases* b, const LuFusedDesc* d, int count, int max_n, int max_r,
                             cudaStream_t s);
 cudaError_t launch_norm1_batched(const Bases* b, const LuDesc* d, int count, cudaStream_t s);
+
+// Tall-skinny QR pre-reduction (tsqr.cu): R (c x c, row-major, upper
+// triangular, initially zero or a previous result) absorbs the nrows rows of
+// S (row-major, ld lds; destroyed).  tri != 0: S is itself upper triangular.
+struct TsqrJob {
+  double* R;
+  double* S;
+  int c, lds, nrows, tri;
+};
+int tsqr_slab_rows();
+cudaError_t launch_tsqr_absorb(const TsqrJob* d_jobs, int count, cudaStream_t s);
 // dgecon estimates; phase -1: one monolithic launch; phase 0..kGeconSteps:
 // the split estimate (init, then one LU application + dlacn2 step per
 // launch) with per-matrix state in base kGeconScratchBase.

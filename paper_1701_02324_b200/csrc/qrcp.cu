@@ -18,6 +18,8 @@
 // P[:, J] is exactly the identity (linalg.py:129-135).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <utility>
 #include <vector>
 
 #include "hks_internal.h"
@@ -255,6 +257,7 @@ __global__ void qr_id(const QrNode* __restrict__ nodes, const QrState* __restric
     for (int t = threadIdx.x; t < r; t += blockDim.x) skel[i][t] = cands[i][q.piv[t]];
 }
 
+
 template <class T>
 cudaError_t upload(const std::vector<T>& h, T** d, cudaStream_t s) {
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(d), std::max<size_t>(h.size(), 1) * sizeof(T), s);
@@ -262,11 +265,123 @@ cudaError_t upload(const std::vector<T>& h, T** d, cudaStream_t s) {
   return e;
 }
 
+// Pre-reduction policy: blocks with at least kTsqrMinRows rows and twice as
+// many rows as columns (HKS_TSQR=0 disables; the QRCP then runs on the
+// sampled block itself, as the reference does).
+constexpr int kTsqrMinRows = 1024;
+bool tsqr_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("HKS_TSQR");
+    return !(e && atoi(e) == 0);
+  }();
+  return v;
+}
+bool tsqr_eligible(int m, int n) { return tsqr_enabled() && m >= kTsqrMinRows && m >= 2 * n && n >= 1; }
+
+// Replaces every eligible node's workspace by its triangular factor: row
+// chunks of the block are absorbed into per-chunk triangles (one CTA each),
+// the triangles merged pairwise.  On return the nodes point at their R
+// (m = n, lda = n); *rscratch / *djobs are stream-ordered allocations the
+// caller frees after the QRCP.
+cudaError_t tsqr_prereduce(std::vector<QrNode>& nodes, double** rscratch, TsqrJob** djobs, cudaStream_t s) {
+  const int B = tsqr_slab_rows();
+  int64_t total_rows = 0;
+  int cmax = 0;
+  for (auto& q : nodes)
+    if (tsqr_eligible(q.m, q.n)) {
+      total_rows += q.m;
+      cmax = std::max(cmax, q.n);
+    }
+  if (total_rows == 0) return cudaSuccess;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // rows per job: at least two triangles' worth (a merge costs about half a
+  // triangle of absorbed rows), otherwise ~6 jobs per SM over the batch
+  int64_t rpj = std::max<int64_t>(2 * (int64_t)cmax, (total_rows + 6 * sms - 1) / (6 * sms));
+  rpj = (rpj + B - 1) / B * B;
+  std::vector<TsqrJob> jobs;                 // stage 0, then the merge stages back to back
+  std::vector<std::pair<int, int>> stages;   // (first job, count)
+  struct Plan {
+    int node, nch;
+    size_t roff;
+  };
+  std::vector<Plan> plans;
+  size_t rtotal = 0;
+  int max_nch = 1;
+  for (int i = 0; i < (int)nodes.size(); ++i) {
+    const QrNode& q = nodes[i];
+    if (!tsqr_eligible(q.m, q.n)) continue;
+    const int nch = (int)((q.m + rpj - 1) / rpj);
+    plans.push_back(Plan{i, nch, rtotal});
+    rtotal += (size_t)nch * q.n * q.n;
+    max_nch = std::max(max_nch, nch);
+  }
+  for (auto& p : plans) {
+    const QrNode& q = nodes[p.node];
+    for (int ch = 0; ch < p.nch; ++ch) {
+      const int64_t r0 = (int64_t)ch * rpj, r1 = std::min<int64_t>(q.m, r0 + rpj);
+      jobs.push_back(TsqrJob{nullptr, q.A + (size_t)r0 * q.lda, q.n, q.lda, (int)(r1 - r0), 0});
+      jobs.back().R = reinterpret_cast<double*>(p.roff + (size_t)ch * q.n * q.n);  // offset, rebased below
+    }
+  }
+  stages.push_back({0, (int)jobs.size()});
+  for (int st = 1; st < max_nch; st *= 2) {
+    const int first = (int)jobs.size();
+    for (auto& p : plans) {
+      const QrNode& q = nodes[p.node];
+      for (int ch = 0; ch + st < p.nch; ch += 2 * st) {
+        TsqrJob j{nullptr, nullptr, q.n, q.n, q.n, 1};
+        j.R = reinterpret_cast<double*>(p.roff + (size_t)ch * q.n * q.n);
+        j.S = reinterpret_cast<double*>(p.roff + (size_t)(ch + st) * q.n * q.n);
+        jobs.push_back(j);
+      }
+    }
+    stages.push_back({first, (int)jobs.size() - first});
+  }
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(rscratch), rtotal * sizeof(double), s);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(*rscratch, 0, rtotal * sizeof(double), s);
+  if (e != cudaSuccess) return e;
+  for (size_t k = 0; k < jobs.size(); ++k) {  // rebase the scratch offsets
+    TsqrJob& j = jobs[k];
+    j.R = *rscratch + reinterpret_cast<size_t>(j.R);
+    if (j.tri) j.S = *rscratch + reinterpret_cast<size_t>(j.S);
+  }
+  e = upload(jobs, djobs, s);
+  for (auto& st : stages)
+    if (e == cudaSuccess && st.second > 0) e = launch_tsqr_absorb(*djobs + st.first, st.second, s);
+  if (e != cudaSuccess) return e;
+  // `jobs` is pageable host memory read by the asynchronous upload
+  e = cudaStreamSynchronize(s);
+  for (auto& p : plans) {
+    QrNode& q = nodes[p.node];
+    q.A = *rscratch + p.roff;
+    q.m = q.n;
+    q.lda = q.n;
+  }
+  return e;
+}
+
 // Runs the QRCP + ID on a batch of prepared workspaces.
 cudaError_t run_qrcp(std::vector<QrNode>& nodes, double tau, const std::vector<double*>& P,
                      const std::vector<const int64_t*>& cands, const std::vector<int64_t*>& skel,
-                     std::vector<int64_t>& ranks_out, cudaStream_t s) {
+                     std::vector<int64_t>& ranks_out, cudaStream_t s, bool copy_r_back = false) {
   const int count = (int)nodes.size();
+  std::vector<QrNode> orig;
+  if (copy_r_back) orig = nodes;
+  // Tall blocks are first reduced to their c x c triangular factor (tsqr.cu):
+  // the QRCP below then streams c x c instead of l' x c per step.
+  double* rscratch = nullptr;
+  TsqrJob* djobs = nullptr;
+  {
+    cudaError_t te = tsqr_prereduce(nodes, &rscratch, &djobs, s);
+    if (te != cudaSuccess) {
+      if (rscratch) cudaFreeAsync(rscratch, s);
+      if (djobs) cudaFreeAsync(djobs, s);
+      return te;
+    }
+  }
   std::vector<QrChunk> ch;
   int64_t poff = 0;
   int kmax_all = 0;
@@ -309,11 +424,18 @@ cudaError_t run_qrcp(std::vector<QrNode>& nodes, double tau, const std::vector<d
     }
     qr_id<<<count, 256, 0, s>>>(dn, dst, dP, skel.empty() ? nullptr : dcand, skel.empty() ? nullptr : dskel, dranks);
     ranks_out.resize(count);
+    // callers that read R from the workspace (hks_interp_decomp): the first
+    // kmax rows of a pre-reduced node's triangle go back into its block
+    for (int i = 0; i < (int)orig.size() && e == cudaSuccess; ++i)
+      if (orig[i].A != nodes[i].A && nodes[i].kmax > 0)
+        e = cudaMemcpy2DAsync(orig[i].A, (size_t)orig[i].lda * sizeof(double), nodes[i].A,
+                              (size_t)nodes[i].lda * sizeof(double), (size_t)nodes[i].n * sizeof(double),
+                              nodes[i].kmax, cudaMemcpyDeviceToDevice, s);
     if (e == cudaSuccess) e = cudaMemcpyAsync(ranks_out.data(), dranks, count * sizeof(int64_t), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   }
   for (void* p : {(void*)dn, (void*)dc, (void*)dst, (void*)npart, (void*)wpart, (void*)dP, (void*)dcand,
-                  (void*)dskel, (void*)dranks})
+                  (void*)dskel, (void*)dranks, (void*)rscratch, (void*)djobs})
     if (p) cudaFreeAsync(p, s);
   if (e == cudaSuccess) e = cudaGetLastError();
   return e;
@@ -351,7 +473,7 @@ extern "C" int hks_interp_decomp(double* A, int64_t m, int64_t n, int64_t lda, d
   std::vector<QrNode> nodes(1);
   nodes[0] = QrNode{A, v, pivots, (int)m, (int)n, (int)lda, (int)std::min<int64_t>(std::min(m, n), max_rank), 0, 0, 0};
   std::vector<int64_t> ranks;
-  if (e == cudaSuccess) e = run_qrcp(nodes, tol, {interp}, {}, {}, ranks, s);
+  if (e == cudaSuccess) e = run_qrcp(nodes, tol, {interp}, {}, {}, ranks, s, true);
   if (v) cudaFreeAsync(v, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return set_error(HKS_ERR_CUDA, "hks_interp_decomp: %s", cudaGetErrorString(e));
@@ -393,8 +515,9 @@ extern "C" int hks_skeletonize_level(const double* X, int64_t d, const hks_kerne
     int64_t i1 = i0;
     size_t bytes = 0;
     while (i1 < count) {
-      const size_t b = (size_t)(row_off[i1 + 1] - row_off[i1]) * (cand_off[i1 + 1] - cand_off[i1]) * 8 +
-                       (size_t)(row_off[i1 + 1] - row_off[i1]) * 8;
+      const size_t rm = (size_t)(row_off[i1 + 1] - row_off[i1]), rc = (size_t)(cand_off[i1 + 1] - cand_off[i1]);
+      // sampled block + Householder vector (+ the triangle of the pre-reduction)
+      const size_t b = rm * rc * 8 + rm * 8 + (tsqr_eligible((int)rm, (int)rc) ? rc * rc * 8 : 0);
       if (i1 > i0 && bytes + b > budget) break;
       bytes += b;
       ++i1;
