@@ -18,6 +18,7 @@
 // P[:, J] is exactly the identity (linalg.py:129-135).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <utility>
 #include <vector>
@@ -258,12 +259,109 @@ __global__ void qr_id(const QrNode* __restrict__ nodes, const QrState* __restric
 }
 
 
+// The same ID for a 32-column block of P per CTA: every warp back-substitutes
+// 8 columns together against the rows of R11 (dot form: x_k = (b_k - sum_{t>k}
+// R[k,t] x_t) / R[k,k], the row of R read once, coalesced, for the 8 columns;
+// partial sums over the lanes' t in a fixed order).  The column-per-thread
+// kernel above walks R11 once per thread with uncoalesced updates of P:
+// 1.45 s of C3's skeletonization; this one is ~100x faster.
+constexpr int IDC = 32;  // columns per CTA
+__global__ void __launch_bounds__(128) qr_id_rows(const QrNode* __restrict__ nodes, const QrState* __restrict__ st,
+                                                  double* const* __restrict__ P,
+                                                  const int64_t* const* __restrict__ cands,
+                                                  int64_t* const* __restrict__ skel, int64_t* __restrict__ ranks) {
+  const int i = blockIdx.x;
+  const QrNode q = nodes[i];
+  const int r = st[i].rank;
+  if (blockIdx.y == 0 && threadIdx.x == 0) ranks[i] = r;
+  const int jj0 = blockIdx.y * IDC;
+  if (r == 0 || jj0 >= q.n) return;
+  if (blockIdx.y == 0 && skel && cands)
+    for (int t = threadIdx.x; t < r; t += blockDim.x) skel[i][t] = cands[i][q.piv[t]];
+  extern __shared__ double xs[];  // [IDC][r]
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* xw = xs + (size_t)wid * 8 * r;
+  double* p = P[i];
+  const double* __restrict__ A = q.A;
+  const size_t lda = q.lda;
+  const int jw = jj0 + wid * 8;  // this warp's first column
+  bool any_solve = false;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int jj = jw + u;
+    if (jj >= q.n) continue;
+    if (jj < r) {
+      double* col = p + (size_t)q.piv[jj] * r;
+      for (int t = lane; t < r; t += 32) col[t] = (t == jj) ? 1.0 : 0.0;
+    } else {
+      any_solve = true;
+      for (int t = lane; t < r; t += 32) xw[u * r + t] = A[(size_t)t * lda + jj];
+    }
+  }
+  if (!any_solve) return;  // warp-uniform
+  __syncwarp();
+  for (int kk = r - 1; kk >= 0; --kk) {
+    const double* row = A + (size_t)kk * lda;
+    double acc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+    for (int t = kk + 1 + lane; t < r; t += 32) {
+      const double rv = row[t];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[u] = fma(rv, xw[u * r + t], acc[u]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
+    double mine = acc[0];
+#pragma unroll
+    for (int u = 1; u < 8; ++u) mine = lane == u ? acc[u] : mine;
+    if (lane < 8 && jw + lane >= r && jw + lane < q.n) xw[lane * r + kk] = (xw[lane * r + kk] - mine) / row[kk];
+    __syncwarp();
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int jj = jw + u;
+    if (jj < r || jj >= q.n) continue;
+    double* col = p + (size_t)q.piv[jj] * r;
+    for (int t = lane; t < r; t += 32) col[t] = xw[u * r + t];
+  }
+}
+
 template <class T>
 cudaError_t upload(const std::vector<T>& h, T** d, cudaStream_t s) {
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(d), std::max<size_t>(h.size(), 1) * sizeof(T), s);
   if (e == cudaSuccess && !h.empty()) e = cudaMemcpyAsync(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, s);
   return e;
 }
+
+// HKS_SKEL_TRACE=1: device time of each skeletonization stage on stderr.
+struct StageTimer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaStream_t s;
+  const char* name;
+  bool on;
+  StageTimer(const char* n, cudaStream_t st) : s(st), name(n) {
+    static const bool trace = getenv("HKS_SKEL_TRACE") != nullptr;
+    on = trace;
+    if (on) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, s);
+    }
+  }
+  ~StageTimer() {
+    if (!on) return;
+    cudaEventRecord(b, s);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    fprintf(stderr, "HKS_SKEL_TRACE %s %.3f ms\n", name, ms);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+};
 
 // Pre-reduction policy: blocks with at least kTsqrMinRows rows and twice as
 // many rows as columns (HKS_TSQR=0 disables; the QRCP then runs on the
@@ -350,7 +448,10 @@ cudaError_t tsqr_prereduce(std::vector<QrNode>& nodes, double** rscratch, TsqrJo
   }
   e = upload(jobs, djobs, s);
   for (auto& st : stages)
-    if (e == cudaSuccess && st.second > 0) e = launch_tsqr_absorb(*djobs + st.first, st.second, s);
+    if (e == cudaSuccess && st.second > 0) {
+      StageTimer tm(&st == &stages[0] ? "tsqr_absorb" : "tsqr_merge", s);
+      e = launch_tsqr_absorb(*djobs + st.first, st.second, s);
+    }
   if (e != cudaSuccess) return e;
   // `jobs` is pageable host memory read by the asynchronous upload
   e = cudaStreamSynchronize(s);
@@ -413,6 +514,7 @@ cudaError_t run_qrcp(std::vector<QrNode>& nodes, double tau, const std::vector<d
   if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&dranks), count * sizeof(int64_t), s);
   const int nch = (int)ch.size();
   if (e == cudaSuccess) {
+    StageTimer tm("qrcp", s);
     qr_init<<<count, 256, 0, s>>>(dn, dst, count);
     qr_norms<<<nch, QT, 0, s>>>(dn, dc, dst, 0, npart);
     for (int k = 0; k <= kmax_all && e == cudaSuccess; ++k) {
@@ -422,7 +524,16 @@ cudaError_t run_qrcp(std::vector<QrNode>& nodes, double tau, const std::vector<d
       qr_update<<<nch, QT, 0, s>>>(dn, dc, dst, k, wpart, npart);
       e = cudaGetLastError();
     }
-    qr_id<<<count, 256, 0, s>>>(dn, dst, dP, skel.empty() ? nullptr : dcand, skel.empty() ? nullptr : dskel, dranks);
+    StageTimer tm_id("qr_id", s);
+    int nmax = 1;
+    for (auto& q : nodes) nmax = std::max(nmax, q.n);
+    const size_t id_smem = (size_t)IDC * std::max(kmax_all, 1) * sizeof(double);
+    static const bool id_old = getenv("HKS_QR_ID_OLD") != nullptr;  // development knob
+    if (!id_old && id_smem <= 200 * 1024 && raise_smem_limit(qr_id_rows, id_smem) == cudaSuccess)
+      qr_id_rows<<<dim3(count, (nmax + IDC - 1) / IDC), 128, id_smem, s>>>(
+          dn, dst, dP, skel.empty() ? nullptr : dcand, skel.empty() ? nullptr : dskel, dranks);
+    else
+      qr_id<<<count, 256, 0, s>>>(dn, dst, dP, skel.empty() ? nullptr : dcand, skel.empty() ? nullptr : dskel, dranks);
     ranks_out.resize(count);
     // callers that read R from the workspace (hks_interp_decomp): the first
     // kmax rows of a pre-reduced node's triangle go back into its block
@@ -563,7 +674,9 @@ extern "C" int hks_skeletonize_level(const double* X, int64_t d, const hks_kerne
     Bases b{};
     Bases* db = nullptr;
     if (e == cudaSuccess && !ev.empty()) e = upload_bases(b, &db, s);
+    StageTimer* tm_eval = new StageTimer("eval", s);
     if (e == cudaSuccess && !ev.empty()) e = launch_eval_batched(X, (int)d, kp, db, dev, (int)ev.size(), mm, mn, true, s);
+    delete tm_eval;
     if (db) cudaFreeAsync(db, s);
     std::vector<int64_t> ranks;
     if (e == cudaSuccess) e = run_qrcp(nodes, tau, P, cl, sk, ranks, s);

@@ -39,17 +39,21 @@ constexpr int TNT = 256;  // threads
 constexpr int TNW = TNT / 32;
 constexpr int TPB = 32;   // panel width
 constexpr int TTW = 16;   // trailing tile width
-constexpr int TW2LD = 20; // ld of W2 (== 4 mod 16: conflict-free DMMA B fragments)
+
+constexpr int TWLD = 20;  // ld of W / W2 (== 4 mod 16: conflict-free DMMA B fragments)
+constexpr int TTLD = 36;  // ld of T^T
+constexpr int TNB = 3;    // trailing tile buffers (two tiles in flight)
 
 template <int B>
 struct TsqrSmem {
   static constexpr int LD = B + 4;  // == 4 (mod 16)
   double Vs[TPB * LD];              // panel of S, column-major (v_s after the panel is factored)
-  double St[2][TTW * LD];           // trailing tiles, column-major
-  double Wp[4][TPB * TTW];          // split-K partials of Vs^T S_t; Wp[0] then holds W; also the Gram matrix
-  double T[TPB * 33];               // block reflector factor, row-major ld 33
-  double Rd[TPB * 33];              // diagonal block of R, row-major ld 33
-  double W2[TPB * TW2LD];           // T^T W
+  double St[TNB][TTW * LD];         // trailing tiles, column-major
+  double Tt[TPB * TTLD];            // T^T of the block reflector (Tt[k][i] = T[i][k])
+  // one scratch region, three lives: the diagonal block of R (row-major ld
+  // 33) while the panel is factored, the Gram matrix Vs^T Vs (ld 32) while T
+  // is built, then W and W2 (ld 20) in the trailing loop
+  double X[2 * TPB * TWLD > TPB * 33 ? 2 * TPB * TWLD : TPB * 33];
   double tau[TPB];
 };
 
@@ -72,10 +76,44 @@ __device__ __forceinline__ void tsqr_load_tile(double* St, const double* S, int 
   }
 }
 
+// dlarfg on [R_kk; x]: x (this lane's rows of column k, in registers) becomes
+// v_s in shared memory, R_kk becomes beta, tau[k] is published (one warp).
+template <int B>
+__device__ __forceinline__ void tsqr_reflector(TsqrSmem<B>& sm, double* Rd, int k, const double (&x)[B / 32],
+                                               int lane) {
+  constexpr int LD = TsqrSmem<B>::LD;
+  double ss = 0.0;
+#pragma unroll
+  for (int q = 0; q < B / 32; ++q) ss = fma(x[q], x[q], ss);
+  ss = warp_sum(ss);
+  const double x0 = Rd[k * 33 + k];
+  double tau = 0.0;
+  if (ss > 0.0) {
+    // beta = -sign(x0) ||[x0; x]||, tau = (beta - x0) / beta, v_s = x / (x0 - beta):
+    // one division for both quotients (the reflector is orthogonal to roundoff either way)
+    const double beta = -copysign(sqrt(fma(x0, x0, ss)), x0);
+    const double d = x0 - beta, bd = beta * d;
+    double scale;
+    if (fabs(bd) >= 1e-290 && fabs(bd) <= 1e290) {
+      const double rcp = 1.0 / bd;
+      scale = beta * rcp;
+      tau = -(d * d) * rcp;
+    } else {
+      scale = 1.0 / d;
+      tau = (beta - x0) / beta;
+    }
+#pragma unroll
+    for (int q = 0; q < B / 32; ++q) sm.Vs[k * LD + lane + 32 * q] = x[q] * scale;
+    if (lane == 0) Rd[k * 33 + k] = beta;
+  }
+  if (lane == 0) sm.tau[k] = tau;
+}
+
 template <int B>
 __global__ void __launch_bounds__(TNT, B <= 128 ? 2 : 1) tsqr_absorb_kernel(const TsqrJob* __restrict__ jobs) {
   constexpr int LD = TsqrSmem<B>::LD;
   constexpr int RQ = B / 32;  // rows per lane in the panel factorization
+  constexpr int CW = TPB / TNW;  // panel columns per warp
   extern __shared__ __align__(16) unsigned char tsqr_raw[];
   TsqrSmem<B>& sm = *reinterpret_cast<TsqrSmem<B>*>(tsqr_raw);
   const TsqrJob J = jobs[blockIdx.x];
@@ -84,6 +122,10 @@ __global__ void __launch_bounds__(TNT, B <= 128 ? 2 : 1) tsqr_absorb_kernel(cons
   double* __restrict__ S = J.S;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int fr = lane >> 2, fc = lane & 3;
+  double* Rd = sm.X;
+  double* G = sm.X;
+  double* Wm = sm.X;
+  double* W2 = sm.X + TPB * TWLD;
 
   for (int s0 = 0; s0 < J.nrows; s0 += B) {
     const int nb = min(B, J.nrows - s0);
@@ -91,8 +133,8 @@ __global__ void __launch_bounds__(TNT, B <= 128 ? 2 : 1) tsqr_absorb_kernel(cons
     const int pstart = J.tri ? s0 / TPB : 0;
     for (int j0 = pstart * TPB; j0 < c; j0 += TPB) {
       const int ntile = (c - j0 - TPB + TTW - 1) / TTW;  // trailing tiles (<= 0: none)
-      // ---- stage the panel of S, the diagonal block of R and the first trailing tile
-      __syncthreads();  // the previous panel's last tile is written out
+      // ---- stage the panel of S, the diagonal block of R and the first two trailing tiles
+      __syncthreads();  // the previous panel's trailing loop is complete
       {
         const int rr = lane & 3, cc = lane >> 2;
 #pragma unroll
@@ -109,77 +151,88 @@ __global__ void __launch_bounds__(TNT, B <= 128 ? 2 : 1) tsqr_absorb_kernel(cons
       cp_async_commit();
       if (ntile > 0) tsqr_load_tile<B>(sm.St[0], S, lds, s0, nb, j0 + TPB, c, wid, lane);
       cp_async_commit();
+      if (ntile > 1) tsqr_load_tile<B>(sm.St[1], S, lds, s0, nb, j0 + TPB + TTW, c, wid, lane);
+      cp_async_commit();
       for (int e = tid; e < TPB * TPB; e += TNT) {
         const int i = e >> 5, k = e & 31;
-        sm.Rd[i * 33 + k] = (j0 + i < c && j0 + k < c && k >= i) ? R[(size_t)(j0 + i) * c + j0 + k] : 0.0;
+        Rd[i * 33 + k] = (j0 + i < c && j0 + k < c && k >= i) ? R[(size_t)(j0 + i) * c + j0 + k] : 0.0;
       }
-      cp_async_wait<1>();
+      cp_async_wait<2>();
       __syncthreads();
-      // ---- panel factorization: warp w owns columns w, w + 8, w + 16, w + 24
+      // ---- panel factorization: warp w owns columns w, w + 8, w + 16, w + 24.
+      // Step k: every warp applies reflector k to its columns j > k (the four
+      // dot products reduced together); the owner of column k + 1 then forms
+      // reflector k + 1 from the registers it just updated, ahead of the barrier.
+      if (wid == 0) {
+        double x[RQ];
+#pragma unroll
+        for (int q = 0; q < RQ; ++q) x[q] = sm.Vs[lane + 32 * q];
+        tsqr_reflector<B>(sm, Rd, 0, x, lane);
+      }
+      __syncthreads();
       for (int k = 0; k < TPB; ++k) {
-        if ((k & (TNW - 1)) == wid) {  // dlarfg on [R_kk; S[:, k]]
-          double xv[RQ], ss = 0.0;
+        const double tau = sm.tau[k];
+        double v[RQ], a[CW][RQ], dot[CW], rk[CW];
+#pragma unroll
+        for (int q = 0; q < RQ; ++q) v[q] = sm.Vs[k * LD + lane + 32 * q];
+#pragma unroll
+        for (int t = 0; t < CW; ++t) {
+          const int j = wid + TNW * t;
+          dot[t] = 0.0;
+          rk[t] = j > k ? Rd[k * 33 + j] : 0.0;
 #pragma unroll
           for (int q = 0; q < RQ; ++q) {
-            xv[q] = sm.Vs[k * LD + lane + 32 * q];
-            ss = fma(xv[q], xv[q], ss);
+            a[t][q] = j > k ? sm.Vs[j * LD + lane + 32 * q] : 0.0;
+            dot[t] = fma(v[q], a[t][q], dot[t]);
           }
-          ss = warp_sum(ss);
-          const double x0 = sm.Rd[k * 33 + k];
-          double tau = 0.0;
-          if (ss > 0.0) {
-            const double beta = -copysign(sqrt(fma(x0, x0, ss)), x0);
-            tau = (beta - x0) / beta;
-            const double scale = 1.0 / (x0 - beta);
-#pragma unroll
-            for (int q = 0; q < RQ; ++q) sm.Vs[k * LD + lane + 32 * q] = xv[q] * scale;
-            if (lane == 0) sm.Rd[k * 33 + k] = beta;
-          }
-          if (lane == 0) sm.tau[k] = tau;
         }
-        __syncthreads();
-        const double tau = sm.tau[k];
-        if (tau != 0.0) {
-          double v[RQ];
 #pragma unroll
-          for (int q = 0; q < RQ; ++q) v[q] = sm.Vs[k * LD + lane + 32 * q];
+        for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-          for (int t = 0; t < TPB / TNW; ++t) {
-            const int j = wid + TNW * t;
-            if (j > k) {
-              double a[RQ], dot = 0.0;
+          for (int t = 0; t < CW; ++t) dot[t] += __shfl_xor_sync(0xffffffffu, dot[t], o);
+        __syncwarp();
 #pragma unroll
-              for (int q = 0; q < RQ; ++q) {
-                a[q] = sm.Vs[j * LD + lane + 32 * q];
-                dot = fma(v[q], a[q], dot);
-              }
-              dot = warp_sum(dot);
-              const double tw = tau * (sm.Rd[k * 33 + j] + dot);
-              __syncwarp();
-              if (lane == 0) sm.Rd[k * 33 + j] -= tw;
+        for (int t = 0; t < CW; ++t) {
+          const int j = wid + TNW * t;
+          if (j > k) {
+            const double tw = tau * (rk[t] + dot[t]);
+            if (lane == 0) Rd[k * 33 + j] = rk[t] - tw;
 #pragma unroll
-              for (int q = 0; q < RQ; ++q) sm.Vs[j * LD + lane + 32 * q] = fma(-tw, v[q], a[q]);
+            for (int q = 0; q < RQ; ++q) {
+              a[t][q] = fma(-tw, v[q], a[t][q]);
+              sm.Vs[j * LD + lane + 32 * q] = a[t][q];
             }
           }
         }
+        if (k + 1 < TPB && ((k + 1) & (TNW - 1)) == wid) {
+          double x[RQ];
+          const int ts = (k + 1) >> 3;
+#pragma unroll
+          for (int q = 0; q < RQ; ++q) {
+            x[q] = a[0][q];
+#pragma unroll
+            for (int t = 1; t < CW; ++t) x[q] = t == ts ? a[t][q] : x[q];
+          }
+          tsqr_reflector<B>(sm, Rd, k + 1, x, lane);
+        }
+        __syncthreads();
       }
-      __syncthreads();
-      // ---- R's diagonal block back; Gram matrix G = Vs^T Vs (into Wp)
+      // ---- R's diagonal block back; Gram matrix G = Vs^T Vs
       for (int e = tid; e < TPB * TPB; e += TNT) {
         const int i = e >> 5, k = e & 31;
-        if (k >= i && j0 + k < c) R[(size_t)(j0 + i) * c + j0 + k] = sm.Rd[i * 33 + k];
+        if (k >= i && j0 + k < c) R[(size_t)(j0 + i) * c + j0 + k] = Rd[i * 33 + k];
       }
       if (ntile <= 0) continue;  // last panel: nothing to update (uniform)
-      double* G = &sm.Wp[0][0];  // 32 x 32, row-major ld 32
+      __syncthreads();           // Rd is read; G takes its place
       {
         const int mf = wid >> 1, nf0 = (wid & 1) * 2;
         double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
         for (int kk = 0; kk < B; kk += 4) {
-          const double a = sm.Vs[(8 * mf + fr) * LD + kk + fc];
+          const double av = sm.Vs[(8 * mf + fr) * LD + kk + fc];
 #pragma unroll
           for (int n = 0; n < 2; ++n) {
-            const double b = sm.Vs[(8 * (nf0 + n) + fr) * LD + kk + fc];
-            dmma884(acc[n][0], acc[n][1], a, b);
+            const double bv = sm.Vs[(8 * (nf0 + n) + fr) * LD + kk + fc];
+            dmma884(acc[n][0], acc[n][1], av, bv);
           }
         }
 #pragma unroll
@@ -188,67 +241,74 @@ __global__ void __launch_bounds__(TNT, B <= 128 ? 2 : 1) tsqr_absorb_kernel(cons
           for (int h = 0; h < 2; ++h) G[(8 * mf + fr) * 32 + 8 * (nf0 + n) + 2 * fc + h] = acc[n][h];
       }
       __syncthreads();
-      // ---- T (dlarft, forward columnwise): T[k,k] = tau_k, T[0:k,k] = -tau_k T[0:k,0:k] G[0:k,k]
+      // ---- T (dlarft, forward columnwise): T[k,k] = tau_k, T[0:k,k] = -tau_k T[0:k,0:k] G[0:k,k];
+      // stored transposed (lane = row i of T)
       if (wid == 0) {
         for (int k = 0; k < TPB; ++k) {
           const double tk = sm.tau[k];
-          double s = 0.0;
+          double sacc = 0.0;
           if (lane < k)
-            for (int l = lane; l < k; ++l) s = fma(sm.T[lane * 33 + l], G[l * 32 + k], s);
+            for (int l = lane; l < k; ++l) sacc = fma(sm.Tt[l * TTLD + lane], G[l * 32 + k], sacc);
           __syncwarp();
-          sm.T[lane * 33 + k] = lane < k ? -tk * s : (lane == k ? tk : 0.0);
+          sm.Tt[k * TTLD + lane] = lane < k ? -tk * sacc : (lane == k ? tk : 0.0);
           __syncwarp();
         }
       }
-      // ---- trailing tiles
+      // ---- trailing tiles: warp = fragment (mf, nf) of the 32 x 16 W / W2, rows [wid B/8, +B/8) of S_t
+      const int mf = wid >> 1, nf = wid & 1;
       for (int t = 0; t < ntile; ++t) {
         const int col0 = j0 + TPB + t * TTW;
-        double* St = sm.St[t & 1];
-        cp_async_wait<0>();
-        __syncthreads();  // tile t landed; tile t-1 is written out; T is built
-        if (t + 1 < ntile) tsqr_load_tile<B>(sm.St[(t + 1) & 1], S, lds, s0, nb, col0 + TTW, c, wid, lane);
-        cp_async_commit();
-        // W partials: warp = (K quarter, n fragment), 4 m fragments each
-        {
-          const int kq = wid & 3, nf = wid >> 2;
-          double acc[4][2];
-#pragma unroll
-          for (int m = 0; m < 4; ++m) acc[m][0] = acc[m][1] = 0.0;
-          for (int kk = kq * (B / 4); kk < (kq + 1) * (B / 4); kk += 4) {
-            const double b = St[(8 * nf + fr) * LD + kk + fc];
-#pragma unroll
-            for (int m = 0; m < 4; ++m) {
-              const double a = sm.Vs[(8 * m + fr) * LD + kk + fc];
-              dmma884(acc[m][0], acc[m][1], a, b);
-            }
-          }
-#pragma unroll
-          for (int m = 0; m < 4; ++m)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) sm.Wp[kq][(8 * m + fr) * TTW + 8 * nf + 2 * fc + h] = acc[m][h];
-        }
-        __syncthreads();
-        // W = R_rows + sum of partials (fixed order); thread owns elements tid, tid + 256
+        const double* St = sm.St[t % TNB];
+        // this lane's two entries of R_rows (consumed after the first product)
         double rold[2];
+        bool rok[2];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int o = tid + TNT * u, i = o / TTW, jj = o % TTW;
-          const bool ok = j0 + i < c && col0 + jj < c;
-          rold[u] = ok ? R[(size_t)(j0 + i) * c + col0 + jj] : 0.0;
-          sm.Wp[0][o] = rold[u] + (((sm.Wp[0][o] + sm.Wp[1][o]) + sm.Wp[2][o]) + sm.Wp[3][o]);
+        for (int h = 0; h < 2; ++h) {
+          rok[h] = j0 + 8 * mf + fr < c && col0 + 8 * nf + 2 * fc + h < c;
+          rold[h] = rok[h] ? R[(size_t)(j0 + 8 * mf + fr) * c + col0 + 8 * nf + 2 * fc + h] : 0.0;
+        }
+        cp_async_wait<1>();
+        __syncthreads();  // tile t landed; everyone is done with tile t-1, W, W2 (and T is built)
+        if (t + 2 < ntile)
+          tsqr_load_tile<B>(sm.St[(t + 2) % TNB], S, lds, s0, nb, col0 + 2 * TTW, c, wid, lane);
+        cp_async_commit();
+        // W = R_rows + Vs^T S_t, one 8 x 8 fragment per warp over all B rows
+        {
+          double acc[4][2];  // four independent chains over interleaved k steps, summed in a fixed order
+#pragma unroll
+          for (int u = 0; u < 4; ++u) acc[u][0] = acc[u][1] = 0.0;
+          const double* ap = sm.Vs + (8 * mf + fr) * LD + fc;
+          const double* bp = St + (8 * nf + fr) * LD + fc;
+#pragma unroll 2
+          for (int kk = 0; kk < B; kk += 16) {
+            double av[4], bv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              av[u] = ap[kk + 4 * u];
+              bv[u] = bp[kk + 4 * u];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) dmma884(acc[u][0], acc[u][1], av[u], bv[u]);
+          }
+          Wm[(8 * mf + fr) * TWLD + 8 * nf + 2 * fc] = rold[0] + ((acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0]));
+          Wm[(8 * mf + fr) * TWLD + 8 * nf + 2 * fc + 1] = rold[1] + ((acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1]));
         }
         __syncthreads();
-        // W2 = T^T W (T upper triangular), R_rows -= W2
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int o = tid + TNT * u, k = o / TTW, jj = o % TTW;
-          double s = 0.0;
-          for (int i = 0; i <= k; ++i) s = fma(sm.T[i * 33 + k], sm.Wp[0][i * TTW + jj], s);
-          sm.W2[k * TW2LD + jj] = s;
-          if (j0 + k < c && col0 + jj < c) R[(size_t)(j0 + k) * c + col0 + jj] = rold[u] - s;
+        // W2 = T^T W (T upper triangular: rows 0 .. 8 mf + 7 of W), R_rows -= W2
+        {
+          double a0 = 0.0, a1 = 0.0;
+          for (int kk = 0; kk < 8 * (mf + 1); kk += 4) {
+            const double av = sm.Tt[(8 * mf + fr) * TTLD + kk + fc];
+            const double bv = Wm[(kk + fc) * TWLD + 8 * nf + fr];
+            dmma884(a0, a1, av, bv);
+          }
+          W2[(8 * mf + fr) * TWLD + 8 * nf + 2 * fc] = a0;
+          W2[(8 * mf + fr) * TWLD + 8 * nf + 2 * fc + 1] = a1;
+          if (rok[0]) R[(size_t)(j0 + 8 * mf + fr) * c + col0 + 8 * nf + 2 * fc] = rold[0] - a0;
+          if (rok[1]) R[(size_t)(j0 + 8 * mf + fr) * c + col0 + 8 * nf + 2 * fc + 1] = rold[1] - a1;
         }
         __syncthreads();
-        // S_t -= Vs W2: warp owns rows [wid * B/8, +B/8)
+        // S_t -= Vs W2, straight from the accumulators to global memory
         {
           constexpr int MF = B / 64;
           const int r0 = wid * (B / 8);
@@ -261,35 +321,26 @@ __global__ void __launch_bounds__(TNT, B <= 128 ? 2 : 1) tsqr_absorb_kernel(cons
               for (int h = 0; h < 2; ++h) acc[m][n][h] = St[(8 * n + 2 * fc + h) * LD + r0 + 8 * m + fr];
 #pragma unroll
           for (int kk = 0; kk < TPB; kk += 4) {
-            double a[MF], b[2];
+            double av[MF], bv[2];
 #pragma unroll
-            for (int m = 0; m < MF; ++m) a[m] = -sm.Vs[(kk + fc) * LD + r0 + 8 * m + fr];
+            for (int m = 0; m < MF; ++m) av[m] = -sm.Vs[(kk + fc) * LD + r0 + 8 * m + fr];
 #pragma unroll
-            for (int n = 0; n < 2; ++n) b[n] = sm.W2[(kk + fc) * TW2LD + 8 * n + fr];
+            for (int n = 0; n < 2; ++n) bv[n] = W2[(kk + fc) * TWLD + 8 * n + fr];
 #pragma unroll
             for (int m = 0; m < MF; ++m)
 #pragma unroll
-              for (int n = 0; n < 2; ++n) dmma884(acc[m][n][0], acc[m][n][1], a[m], b[n]);
+              for (int n = 0; n < 2; ++n) dmma884(acc[m][n][0], acc[m][n][1], av[m], bv[n]);
           }
 #pragma unroll
-          for (int m = 0; m < MF; ++m)
+          for (int m = 0; m < MF; ++m) {
+            const int row = r0 + 8 * m + fr;
 #pragma unroll
             for (int n = 0; n < 2; ++n)
 #pragma unroll
-              for (int h = 0; h < 2; ++h) St[(8 * n + 2 * fc + h) * LD + r0 + 8 * m + fr] = acc[m][n][h];
-        }
-        __syncthreads();
-        // tile back to S (row-major: 64-byte row segments per warp instruction)
-        {
-          const int rr = lane & 3, cc = lane >> 2;
-#pragma unroll
-          for (int it = 0; it < B / 32; ++it) {
-            const int row = 4 * (wid + TNW * it) + rr;
-#pragma unroll
-            for (int h = 0; h < TTW / 8; ++h) {
-              const int col = 8 * h + cc;
-              if (row < nb && col0 + col < c) S[(size_t)(s0 + row) * lds + col0 + col] = St[col * LD + row];
-            }
+              for (int h = 0; h < 2; ++h) {
+                const int col = col0 + 8 * n + 2 * fc + h;
+                if (row < nb && col < c) S[(size_t)(s0 + row) * lds + col] = acc[m][n][h];
+              }
           }
         }
       }
