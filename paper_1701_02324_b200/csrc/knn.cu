@@ -8,6 +8,7 @@
 // j-th best), inserting with a ballot when a candidate beats the k-th.
 #include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 #include <vector>
 
 #include "hks_internal.h"
@@ -174,6 +175,214 @@ __global__ void __launch_bounds__(KT) knn_kernel(const double* __restrict__ X, c
   }
 }
 
+// Exact kNN for d <= 32 (the whole feature vector in one staged slab).  Same
+// distances, same (d^2, index) order as knn_kernel, restructured so that the
+// common case -- no candidate of a tile beats any query's k-th best -- costs
+// the DMMA products and one register-level test:
+//   * a warp owns 16 queries and ALL 64 candidates of the tile (2 x 8
+//     fragments), so a query's candidates never leave its warp: no distance
+//     tile in shared memory, no barrier between the products and the merge;
+//   * every lane keeps the k-th best (value, index) of its two query rows in
+//     registers and tests its 32 accumulators against them; only when some
+//     lane has a hit does the warp insert, into (d^2, index)-sorted lists in
+//     shared memory (lane j = j-th best, ballot for the position);
+//   * candidate tiles (points and their squared norms) are double-buffered
+//     with cp.async behind the previous tile's products: one barrier a tile.
+// The sum x.y of a pair runs over k in the same DMMA order wherever the pair
+// sits in a tile, so the lists equal knn_kernel's bit for bit.
+constexpr int SQB = 64, SCB = 64, SKT = 128;
+
+// Row stride of the staged points: the smallest value >= dpad that keeps the
+// DMMA fragment loads conflict-free (stride == 4 or 12 mod 16).
+__host__ __device__ inline int knn_stream_stride(int d) {
+  int v = (d + 3) & ~3;
+  while ((v & 15) != 4 && (v & 15) != 12) v += 4;
+  return v;
+}
+inline size_t knn_stream_smem(int d) {
+  return (size_t)(3 * SQB * knn_stream_stride(d) + 2 * SCB + SQB * 32) * sizeof(double) + SQB * 32 * sizeof(int);
+}
+
+struct KnnStreamSmem {  // carved from dynamic shared memory (SDS is a run-time stride)
+  double* Qs;
+  double* Cs[2];
+  double* sqc[2];
+  double* Lv;
+  int* Li;
+};
+
+__global__ void __launch_bounds__(SKT) knn_stream_kernel(const double* __restrict__ X, const double* __restrict__ sq,
+                                                        int n, int d, int kk, int qlo, int qhi,
+                                                        int64_t* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char knn_raw[];
+  const int SDS = knn_stream_stride(d);
+  KnnStreamSmem sm;
+  {
+    double* base = reinterpret_cast<double*>(knn_raw);
+    sm.Qs = base;
+    sm.Cs[0] = base + SQB * SDS;
+    sm.Cs[1] = base + 2 * SQB * SDS;
+    sm.sqc[0] = base + 3 * SQB * SDS;
+    sm.sqc[1] = sm.sqc[0] + SCB;
+    sm.Lv = sm.sqc[1] + SCB;
+    sm.Li = reinterpret_cast<int*>(sm.Lv + SQB * 32);
+  }
+  const int q0 = qlo + blockIdx.x * SQB;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int fr = lane >> 2, fc = lane & 3;
+  const int dpad = (d + 3) & ~3;
+  const bool vec16 = (d & 1) == 0;  // rows of X start 16-byte aligned
+  auto stage = [&](double* S, int base) {  // 64 points x dpad, zero-filled past n and past d
+    if (vec16) {
+      const int pr = dpad / 2;  // 16-byte pairs per row (d even: a pair never straddles d)
+      for (int e = tid; e < 64 * pr; e += SKT) {
+        const int r = e / pr, k = 2 * (e % pr);
+        const int pt = base + r;
+        if (pt < n && k < d) cp_async16(S + r * SDS + k, X + (size_t)pt * d + k);
+        else S[r * SDS + k] = S[r * SDS + k + 1] = 0.0;
+      }
+    } else {
+      for (int e = tid; e < 64 * dpad; e += SKT) {
+        const int r = e / dpad, k = e % dpad;
+        const int pt = base + r;
+        const bool ok = pt < n && k < d;
+        cp_async8(S + r * SDS + k, ok ? X + (size_t)pt * d + k : X, ok);
+      }
+    }
+  };
+  auto stage_sq = [&](double* S, int base) {
+    if (tid < SCB) {
+      const bool ok = base + tid < n;
+      cp_async8(S + tid, ok ? sq + base + tid : sq, ok);
+    }
+  };
+  stage(sm.Qs, q0);
+  {
+    const int ntile0 = (n + SCB - 1) / SCB;
+    const int c_first = min(q0 / SCB, ntile0 - 1) * SCB;
+    stage(sm.Cs[0], c_first);
+    stage_sq(sm.sqc[0], c_first);
+  }
+  cp_async_commit();
+  for (int e = tid; e < SQB * 32; e += SKT) {
+    sm.Lv[e] = DBL_MAX;
+    sm.Li[e] = 0x7fffffff;
+  }
+  // this lane's two query rows: 16 wid + fr and + 8
+  int qrow[2], qid[2];
+  double sqq[2], tv[2];
+  int ti[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    qrow[i] = wid * 16 + 8 * i + fr;
+    qid[i] = q0 + qrow[i];
+    sqq[i] = qid[i] < n ? sq[qid[i]] : 0.0;
+    tv[i] = DBL_MAX;
+    ti[i] = 0x7fffffff;
+  }
+  // Tiles are visited outwards from the queries' own position: the points
+  // are in tree order, so the first tiles hold the spatially nearest
+  // candidates, the k-th best distances are tight from the start and almost
+  // every later tile takes the no-insertion path.  (The result does not
+  // depend on the order: it is the k smallest (d^2, index) pairs.)
+  const int ntile = (n + SCB - 1) / SCB;
+  const int own = min(q0 / SCB, ntile - 1);
+  auto tile_at = [&](int sidx) {  // offsets 0, +1, -1, +2, -2, ... modulo ntile
+    const int off = (sidx & 1) ? (sidx + 1) / 2 : ntile - sidx / 2;
+    return (own + off) % ntile;
+  };
+  for (int t = 0; t < ntile; ++t) {
+    const int c0 = tile_at(t) * SCB;
+    const double* Cs = sm.Cs[t & 1];
+    const double* sqc = sm.sqc[t & 1];
+    cp_async_wait<0>();
+    __syncthreads();  // tile t landed; everyone is done reading tile t - 1's buffer
+    if (t + 1 < ntile) {
+      const int c1 = tile_at(t + 1) * SCB;
+      stage(sm.Cs[(t + 1) & 1], c1);
+      stage_sq(sm.sqc[(t + 1) & 1], c1);
+    }
+    cp_async_commit();
+    double acc[2][8][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int k4 = 0; k4 < dpad; k4 += 4) {
+      double a[2], b[8];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) a[i] = sm.Qs[qrow[i] * SDS + k4 + fc];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) b[j] = Cs[(8 * j + fr) * SDS + k4 + fc];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+    // d^2 = (|x|^2 + |y|^2) - 2 x.y (tree.py:179), tested against the rows' k-th best
+    bool hit = false;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = 8 * j + 2 * fc + h, ci = c0 + c;
+        const double sc = sqc[c];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const double dv = (sqq[i] + sc) - 2.0 * acc[i][j][h];
+          acc[i][j][h] = dv;
+          hit |= ci < n && ci != qid[i] && qid[i] < qhi && lex_less(dv, ci, tv[i], ti[i]);
+        }
+      }
+    if (!__any_sync(0xffffffffu, hit)) continue;
+    // insertion path: slot by slot (static registers), lanes with a hit one at a time
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int ci = c0 + 8 * j + 2 * fc + h;
+          const double dv = acc[i][j][h];
+          const bool ok = ci < n && ci != qid[i] && qid[i] < qhi && lex_less(dv, ci, tv[i], ti[i]);
+          unsigned m = __ballot_sync(0xffffffffu, ok);
+          while (m) {
+            const int src = __ffs(m) - 1;
+            m &= m - 1;
+            const double v = __shfl_sync(0xffffffffu, dv, src);
+            const int vi = __shfl_sync(0xffffffffu, ci, src);
+            const int row = wid * 16 + 8 * i + (src >> 2);
+            const double lv = sm.Lv[row * 32 + lane];
+            const int li = sm.Li[row * 32 + lane];
+            const unsigned gm = __ballot_sync(0xffffffffu, lane < kk && lex_less(v, vi, lv, li));
+            if (gm == 0) continue;  // the row's k-th moved since the test
+            const int pos = __ffs(gm) - 1;
+            const double up_v = __shfl_up_sync(0xffffffffu, lv, 1);
+            const int up_i = __shfl_up_sync(0xffffffffu, li, 1);
+            if (lane == pos) {
+              sm.Lv[row * 32 + lane] = v;
+              sm.Li[row * 32 + lane] = vi;
+            } else if (lane > pos && lane < kk) {
+              sm.Lv[row * 32 + lane] = up_v;
+              sm.Li[row * 32 + lane] = up_i;
+            }
+            __syncwarp();
+          }
+        }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      tv[i] = sm.Lv[qrow[i] * 32 + kk - 1];
+      ti[i] = sm.Li[qrow[i] * 32 + kk - 1];
+    }
+  }
+  __syncwarp();
+  for (int r = 0; r < 16; ++r) {
+    const int row = wid * 16 + r, q = q0 + row;
+    if (q < qhi && lane < kk) out[(size_t)(q - qlo) * kk + lane] = sm.Li[row * 32 + lane];
+  }
+}
+
 }  // namespace
 }  // namespace hks
 
@@ -192,10 +401,17 @@ extern "C" int hks_knn_rows(const double* X, int64_t n, int64_t d, int64_t k, in
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&sq), n * sizeof(double), s);
   if (e == cudaSuccess) {
     sqnorm_kernel<<<592, 256, 0, s>>>(X, n, (int)d, sq);
-    const size_t sm = (size_t)(2 * QB * DS + QB * (CB + 1)) * sizeof(double);
-    raise_smem_limit(knn_kernel<false>, sm);
-    knn_kernel<false><<<(unsigned)((nq + QB - 1) / QB), KT, sm, s>>>(X, sq, (int)n, (int)d, (int)k, (int)q0,
-                                                                    (int)(q0 + nq), out, nullptr, nullptr, nullptr);
+    static const bool stream_off = getenv("HKS_KNN_STREAM") != nullptr && atoi(getenv("HKS_KNN_STREAM")) == 0;
+    if (d <= 32 && !stream_off) {
+      raise_smem_limit(knn_stream_kernel, knn_stream_smem((int)d));
+      knn_stream_kernel<<<(unsigned)((nq + SQB - 1) / SQB), SKT, knn_stream_smem((int)d), s>>>(
+          X, sq, (int)n, (int)d, (int)k, (int)q0, (int)(q0 + nq), out);
+    } else {
+      const size_t sm = (size_t)(2 * QB * DS + QB * (CB + 1)) * sizeof(double);
+      raise_smem_limit(knn_kernel<false>, sm);
+      knn_kernel<false><<<(unsigned)((nq + QB - 1) / QB), KT, sm, s>>>(X, sq, (int)n, (int)d, (int)k, (int)q0,
+                                                                      (int)(q0 + nq), out, nullptr, nullptr, nullptr);
+    }
     e = cudaGetLastError();
     cudaFreeAsync(sq, s);
   }
