@@ -604,7 +604,10 @@ void add_lu_program(StepList& sl, const std::vector<LuJob>& jobs, bool with_norm
     const char* e = getenv("HKS_LU_GATHER");
     return e ? atoi(e) : -1;
   }();
-  const bool use_perm = track && (gather_env >= 0 ? gather_env != 0 : jobs.size() <= 64);
+  // (round 2, after the staged narrow-batch gathers: gathers also win on the
+  // wide levels -- C3 124.7 -> 121.8 ms, C2 14.88 -> 14.77 ms -- so they are
+  // the default whenever the permutations are recorded)
+  const bool use_perm = track && (gather_env >= 0 ? gather_env != 0 : true);
   // The group-end interchanges (trailing columns and right-hand sides, the
   // wide ones) always gather by the group permutation when it is recorded:
   // one coalesced pass whatever the number of interchanges.  Sequential
@@ -629,7 +632,9 @@ void add_lu_program(StepList& sl, const std::vector<LuJob>& jobs, bool with_norm
   };
   static const bool look_ahead = [] {
     const char* e = getenv("HKS_LOOKAHEAD");
-    return e ? atoi(e) != 0 : false;  // measured neutral: the leaf panels fill the SMs' register files
+    // round 1 measured it neutral; with the gathers above it hides the tail of
+    // each trailing update behind the next group's panels (C3 -1.6 ms, C2 -0.3 ms)
+    return e ? atoi(e) != 0 : true;
   }();
   bool side_pending = false;
   for (int g0 = 0; g0 < nmax; g0 += kGroup) {

@@ -20,7 +20,7 @@ for lev in range(depth, -1, -1):
     ids = range(2 ** lev - 1, 2 ** (lev + 1) - 1)
     r = np.array([rank.get(i, 0) for i in ids])
     R = np.array([rank.get(2 * i + 1, 0) + rank.get(2 * i + 2, 0) for i in ids]) if lev < depth else np.zeros(1)
-    print(f"level {lev:2d} nodes {len(ids):5d} r mean {r.mean():6.1f} max {r.max():4d}  R mean {R.mean():6.1f} max {R.max():4d}")
+    print(f"level {lev:2d} nodes {len(ids):5d} r mean {r.mean():6.1f} max {int(r.max()):4d}  R mean {R.mean():6.1f} max {int(R.max()):4d}")
 for cond in (False, True):
     for _ in range(3):
         f = hk.factorize(op, w.lam, with_cond=cond)
