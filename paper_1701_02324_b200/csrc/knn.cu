@@ -200,7 +200,36 @@ __host__ __device__ inline int knn_stream_stride(int d) {
   return v;
 }
 inline size_t knn_stream_smem(int d) {
-  return (size_t)(3 * SQB * knn_stream_stride(d) + 2 * SCB + SQB * 32) * sizeof(double) + SQB * 32 * sizeof(int);
+  return (size_t)(3 * SQB * knn_stream_stride(d) + 2 * SCB + SQB * 32) * sizeof(double) + SQB * 32 * sizeof(int) +
+         4 * sizeof(uint64_t);  // + the bulk-copy mbarriers
+}
+
+// TMA bulk copies (cp.async.bulk, SASS UBLKCP) completing on an mbarrier: a
+// candidate tile of 64 points is one contiguous 64 d doubles in X, so when
+// the staged stride equals d (d = 28: C3) one elected thread moves the whole
+// tile with one instruction instead of 7 LDGSTS per thread.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  unsigned ok;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
 }
 
 struct KnnStreamSmem {  // carved from dynamic shared memory (SDS is a run-time stride)
@@ -211,6 +240,7 @@ struct KnnStreamSmem {  // carved from dynamic shared memory (SDS is a run-time 
   int* Li;
 };
 
+template <bool BULK>
 __global__ void __launch_bounds__(SKT) knn_stream_kernel(const double* __restrict__ X, const double* __restrict__ sq,
                                                         int n, int d, int kk, int qlo, int qhi,
                                                         int64_t* __restrict__ out) {
@@ -227,6 +257,9 @@ __global__ void __launch_bounds__(SKT) knn_stream_kernel(const double* __restric
     sm.Lv = sm.sqc[1] + SCB;
     sm.Li = reinterpret_cast<int*>(sm.Lv + SQB * 32);
   }
+  // BULK: bars[0], bars[1] = tile buffers full, bars[2] = queries
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm.Li + SQB * 32);
+  const unsigned tile_bytes = (unsigned)(SCB * d * sizeof(double)), sq_bytes = (unsigned)(SCB * sizeof(double));
   const int q0 = qlo + blockIdx.x * SQB;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int fr = lane >> 2, fc = lane & 3;
@@ -250,20 +283,43 @@ __global__ void __launch_bounds__(SKT) knn_stream_kernel(const double* __restric
       }
     }
   };
+  // BULK: 64 points are one dense block of X and of the staged layout
+  // (stride == d): one copy by one thread.  (One copy per row for padded
+  // strides was measured 2x slower than the LDGSTS path at d = 18.)
+  auto bulk_tile = [&](double* S, int base, uint64_t* bar) {
+    if (tid == 0) bulk_g2s(S, X + (size_t)base * d, tile_bytes, bar);
+  };
   auto stage_sq = [&](double* S, int base) {
     if (tid < SCB) {
       const bool ok = base + tid < n;
       cp_async8(S + tid, ok ? sq + base + tid : sq, ok);
     }
   };
-  stage(sm.Qs, q0);
   {
     const int ntile0 = (n + SCB - 1) / SCB;
     const int c_first = min(q0 / SCB, ntile0 - 1) * SCB;
-    stage(sm.Cs[0], c_first);
-    stage_sq(sm.sqc[0], c_first);
+    if (BULK) {
+      if (tid == 0) {
+        mbar_init(bars + 0, 1);
+        mbar_init(bars + 1, 1);
+        mbar_init(bars + 2, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      }
+      __syncthreads();
+      if (tid == 0) {
+        mbar_expect_tx(bars + 2, tile_bytes);
+        mbar_expect_tx(bars + 0, tile_bytes + sq_bytes);
+        bulk_g2s(sm.sqc[0], sq + c_first, sq_bytes, bars + 0);
+      }
+      bulk_tile(sm.Qs, q0, bars + 2);
+      bulk_tile(sm.Cs[0], c_first, bars + 0);
+    } else {
+      stage(sm.Qs, q0);
+      stage(sm.Cs[0], c_first);
+      stage_sq(sm.sqc[0], c_first);
+      cp_async_commit();
+    }
   }
-  cp_async_commit();
   for (int e = tid; e < SQB * 32; e += SKT) {
     sm.Lv[e] = DBL_MAX;
     sm.Li[e] = 0x7fffffff;
@@ -295,14 +351,28 @@ __global__ void __launch_bounds__(SKT) knn_stream_kernel(const double* __restric
     const int c0 = tile_at(t) * SCB;
     const double* Cs = sm.Cs[t & 1];
     const double* sqc = sm.sqc[t & 1];
-    cp_async_wait<0>();
+    if (BULK) {
+      if (t == 0) mbar_wait(bars + 2, 0);
+      mbar_wait(bars + (t & 1), (t >> 1) & 1);
+    } else {
+      cp_async_wait<0>();
+    }
     __syncthreads();  // tile t landed; everyone is done reading tile t - 1's buffer
     if (t + 1 < ntile) {
       const int c1 = tile_at(t + 1) * SCB;
-      stage(sm.Cs[(t + 1) & 1], c1);
-      stage_sq(sm.sqc[(t + 1) & 1], c1);
+      if (BULK) {
+        uint64_t* bar = bars + ((t + 1) & 1);
+        if (tid == 0) {
+          mbar_expect_tx(bar, tile_bytes + sq_bytes);
+          bulk_g2s(sm.sqc[(t + 1) & 1], sq + c1, sq_bytes, bar);
+        }
+        bulk_tile(sm.Cs[(t + 1) & 1], c1, bar);
+      } else {
+        stage(sm.Cs[(t + 1) & 1], c1);
+        stage_sq(sm.sqc[(t + 1) & 1], c1);
+      }
     }
-    cp_async_commit();
+    if (!BULK) cp_async_commit();
     double acc[2][8][2];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
@@ -403,9 +473,22 @@ extern "C" int hks_knn_rows(const double* X, int64_t n, int64_t d, int64_t k, in
     sqnorm_kernel<<<592, 256, 0, s>>>(X, n, (int)d, sq);
     static const bool stream_off = getenv("HKS_KNN_STREAM") != nullptr && atoi(getenv("HKS_KNN_STREAM")) == 0;
     if (d <= 32 && !stream_off) {
-      raise_smem_limit(knn_stream_kernel, knn_stream_smem((int)d));
-      knn_stream_kernel<<<(unsigned)((nq + SQB - 1) / SQB), SKT, knn_stream_smem((int)d), s>>>(
-          X, sq, (int)n, (int)d, (int)k, (int)q0, (int)(q0 + nq), out);
+      // whole tiles as TMA bulk copies when a tile is one dense block of the
+      // staged layout: stride == d, every tile and query block full, 16-byte
+      // aligned rows (d even)
+      static const bool bulk_off = getenv("HKS_KNN_BULK") != nullptr && atoi(getenv("HKS_KNN_BULK")) == 0;
+      const bool bulk = !bulk_off && knn_stream_stride((int)d) == d && d % 2 == 0 && n % SCB == 0 &&
+                        q0 % SQB == 0 && (q0 + nq) % SQB == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+      const unsigned grid = (unsigned)((nq + SQB - 1) / SQB);
+      if (bulk) {
+        raise_smem_limit(knn_stream_kernel<true>, knn_stream_smem((int)d));
+        knn_stream_kernel<true><<<grid, SKT, knn_stream_smem((int)d), s>>>(X, sq, (int)n, (int)d, (int)k, (int)q0,
+                                                                           (int)(q0 + nq), out);
+      } else {
+        raise_smem_limit(knn_stream_kernel<false>, knn_stream_smem((int)d));
+        knn_stream_kernel<false><<<grid, SKT, knn_stream_smem((int)d), s>>>(X, sq, (int)n, (int)d, (int)k, (int)q0,
+                                                                            (int)(q0 + nq), out);
+      }
     } else {
       const size_t sm = (size_t)(2 * QB * DS + QB * (CB + 1)) * sizeof(double);
       raise_smem_limit(knn_kernel<false>, sm);
