@@ -875,8 +875,11 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl,
   {
     Copies early;
     for (int64_t i = 0; i < L.first(early_levels); ++i) {
-      const int R = c.r(2 * i + 1) + c.r(2 * i + 2);
-      early.fill(c.z_lu(i), R, R, R, true);
+      const int rl = c.r(2 * i + 1), R = rl + c.r(2 * i + 2);
+      // only Z's diagonal blocks: the coupling products below write the
+      // off-diagonal ones (beta = 0), so they are neither zeroed nor re-read
+      early.fill(c.z_lu(i), R, rl, rl, true);
+      early.fill(adv(c.z_lu(i), (int64_t)rl * R + rl), R, R - rl, R - rl, true);
     }
     if (!early.v.empty()) {
       sl.fork();
@@ -941,9 +944,12 @@ void build_factorize(const hks_plan& P, bool with_cond, StepList& sl,
       const int rl = c.r(a), rr = c.r(b), R = rl + rr, r = c.r(i);
       maxR = std::max(maxR, R);
       const Ref Z = c.z_lu(i), C = c.coup(i);
-      if (!early_node(i)) c_id.fill(Z, R, R, R, true);  // else Z = I from the early branch
-      g_z.add(c.theta(a), rl, 0, C, rl, 0, adv(Z, (int64_t)rl * R), R, rl, rr, rl, 1.0, 1.0);
-      g_z.add(c.theta(b), rr, 0, C, rl, 1, adv(Z, rl), R, rr, rl, rr, 1.0, 1.0);
+      if (!early_node(i)) {  // else the diagonal blocks come from the early branch
+        c_id.fill(Z, R, rl, rl, true);
+        c_id.fill(adv(Z, (int64_t)rl * R + rl), R, rr, rr, true);
+      }
+      g_z.add(c.theta(a), rl, 0, C, rl, 0, adv(Z, (int64_t)rl * R), R, rl, rr, rl, 1.0, 0.0);
+      g_z.add(c.theta(b), rr, 0, C, rl, 1, adv(Z, rl), R, rr, rl, rr, 1.0, 0.0);
       lu.push_back(LuDesc{Z, c.z_piv(i), c.info(i), c.anorm(i), with_cond ? c.rcond(i) : kNull, R, R});
       if (!L.has_up(i)) {
         jobs.push_back(LuJob{Z, R, R, c.z_piv(i), c.info(i), c.anorm(i), kNull, 0, R, c.z_ws(i), (int)L.ccap[i]});
