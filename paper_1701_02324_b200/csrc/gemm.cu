@@ -84,26 +84,26 @@ __device__ __forceinline__ void stage_pairs(double* sm, const double* base, int 
 
 // Stage the A (TBM x TBK) and B (TBK x 64) tiles of k-block k0 into shared
 // memory (layouts above); out-of-range elements are zero-filled.
-template <int TBM, int TBK>
+template <int TBM, int TBK, int TBN>
 __device__ __forceinline__ void load_stage(const GemmOp& g, int m0, int n0, int k0, double* As, double* Bs, bool va,
                                            bool vb) {
-  constexpr int T = 2 * TBM, KST = TBK + 4;  // threads, [row][k] stride
-  constexpr int AMS = TBM + 4, BNS = BN + 4;  // [k][row] strides
+  constexpr int T = TBM * TBN / 32, KST = TBK + 4;  // threads (one warp per 32 x 32 block), [row][k] stride
+  constexpr int AMS = TBM + 4, BNS = TBN + 4;        // [k][row] strides
   if (!g.transA)  // A column-major: m contiguous -> As[k][m]
     stage_pairs<TBM, TBK, AMS, T>(As, g.A, g.lda, m0, g.m, k0, g.k, va);
   else  // A^T stored: k contiguous -> As[m][k]
     stage_pairs<TBK, TBM, KST, T>(As, g.A, g.lda, k0, g.k, m0, g.m, va);
   if (!g.transB)  // B column-major: k contiguous -> Bs[n][k]
-    stage_pairs<TBK, BN, KST, T>(Bs, g.B, g.ldb, k0, g.k, n0, g.n, vb);
+    stage_pairs<TBK, TBN, KST, T>(Bs, g.B, g.ldb, k0, g.k, n0, g.n, vb);
   else  // B^T stored: n contiguous -> Bs[k][n]
-    stage_pairs<BN, TBK, BNS, T>(Bs, g.B, g.ldb, n0, g.n, k0, g.k, vb);
+    stage_pairs<TBN, TBK, BNS, T>(Bs, g.B, g.ldb, n0, g.n, k0, g.k, vb);
 }
 
-template <int TBM, int TBK = BK>
-__global__ void __launch_bounds__(2 * TBM) gemm_batched_kernel(const Bases* __restrict__ bases_ptr,
-                                                                const GemmDesc* __restrict__ descs,
-                                                                int tiles_n, bool g_vec16) {
-  constexpr int BM = TBM, BK = TBK, KS = TBK + 4;
+template <int TBM, int TBK = BK, int TBN = 64>
+__global__ void __launch_bounds__(TBM * TBN / 32) gemm_batched_kernel(const Bases* __restrict__ bases_ptr,
+                                                                       const GemmDesc* __restrict__ descs,
+                                                                       int tiles_n, bool g_vec16) {
+  constexpr int BM = TBM, BK = TBK, KS = TBK + 4, BN = TBN, NT = TBM * TBN / 32, WN = TBN / 32;
   const Bases& bases = *bases_ptr;
   const GemmDesc gd = descs[blockIdx.y];
   const GemmOp g{at<const double>(bases, gd.A), at<const double>(bases, gd.B), at<double>(bases, gd.C),
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(2 * TBM) gemm_batched_kernel(const Bases* __re
   double* Bs = gsm + STAGES * AE;         // STAGES x BE
 
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int wm = (wid >> 1) * 32, wn = (wid & 1) * 32;
+  const int wm = (wid / WN) * 32, wn = (wid % WN) * 32;
   const int fr = lane >> 2, fc = lane & 3;
   // fragment offsets in either layout: element (row, k) at row * rs + k * ks
   const int ars = g.transA ? KS : 1, aks = g.transA ? 1 : BM + 4;
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(2 * TBM) gemm_batched_kernel(const Bases* __re
   // start (no registers held, no stall at the first DMMA), so the
   // epilogue's loads hit L2 after the k loop.
   if (g.beta != 0.0) {  // one 64-byte line per (column, 8-row group) of the tile
-    for (int e = threadIdx.x; e < BN * (BM / 8); e += 2 * TBM) {
+    for (int e = threadIdx.x; e < BN * (BM / 8); e += NT) {
       const int c = n0 + e / (BM / 8), r = m0 + (e % (BM / 8)) * 8;
       if (c < g.n && r < g.m) asm volatile("prefetch.global.L2 [%0];" ::"l"(g.C + r + (size_t)c * g.ldc));
     }
@@ -149,14 +149,15 @@ __global__ void __launch_bounds__(2 * TBM) gemm_batched_kernel(const Bases* __re
   const bool vb = g_vec16 && ((reinterpret_cast<uintptr_t>(g.B) & 15) == 0) && (g.ldb % 2 == 0);
 #pragma unroll
   for (int st = 0; st < STAGES - 1; ++st) {
-    if (st < nk) load_stage<TBM, TBK>(g, m0, n0, st * BK, As + st * AE, Bs + st * BE, va, vb);
+    if (st < nk) load_stage<TBM, TBK, TBN>(g, m0, n0, st * BK, As + st * AE, Bs + st * BE, va, vb);
     cp_async_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     const int pf = kt + STAGES - 1;
-    if (pf < nk) load_stage<TBM, TBK>(g, m0, n0, pf * BK, As + (pf % STAGES) * AE, Bs + (pf % STAGES) * BE, va, vb);
+    if (pf < nk)
+      load_stage<TBM, TBK, TBN>(g, m0, n0, pf * BK, As + (pf % STAGES) * AE, Bs + (pf % STAGES) * BE, va, vb);
     cp_async_commit();
     const double* as = As + (kt % STAGES) * AE;
     const double* bs = Bs + (kt % STAGES) * BE;
@@ -407,6 +408,21 @@ cudaError_t launch_gemm_batched(const Bases* bases, const GemmDesc* d_descs, int
     for (int first = 0; first < count; first += 65535) {
       const int cnt = count - first < 65535 ? count - first : 65535;
       gemm_skinny_kernel<<<dim3((max_m + SBM - 1) / SBM, cnt), 128, sm, stream>>>(bases, d_descs + first);
+    }
+    return cudaGetLastError();
+  }
+  // narrow products (n <= 32: the LU program's in-group panel updates):
+  // 128 x 32 tiles, four warps stacked along m -- a 64 x 64 tile would
+  // compute and stage a half-empty B operand
+  static const bool narrow_ok = getenv("HKS_GEMM_NARROW") == nullptr || atoi(getenv("HKS_GEMM_NARROW")) != 0;
+  if (narrow_ok && max_n <= 32 && max_m >= 96) {
+    static const bool vec16n = getenv("HKS_GEMM_VEC16") == nullptr || atoi(getenv("HKS_GEMM_VEC16")) != 0;
+    const int tmn = (max_m + 127) / 128;
+    const size_t smn = (size_t)STAGES * (OperandLayout<128>::kElems + OperandLayout<32>::kElems) * sizeof(double);
+    raise_smem_limit(gemm_batched_kernel<128, BK, 32>, smn);
+    for (int first = 0; first < count; first += 65535) {
+      const int cnt = count - first < 65535 ? count - first : 65535;
+      gemm_batched_kernel<128, BK, 32><<<dim3(tmn, cnt), 128, smn, stream>>>(bases, d_descs + first, 1, vec16n);
     }
     return cudaGetLastError();
   }
