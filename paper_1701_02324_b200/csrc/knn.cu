@@ -240,6 +240,71 @@ struct KnnStreamSmem {  // carved from dynamic shared memory (SDS is a run-time 
   int* Li;
 };
 
+// Epilogue of one candidate tile for a warp's 16 queries x 64 candidates:
+// accumulators -> distances, register test against the rows' k-th best, and
+// the (rare) insertion into the sorted lists in shared memory.
+__device__ __forceinline__ void knn_tile_merge(double (&acc)[2][8][2], const double (&sqq)[2], const double* sqc,
+                                               int c0, int n, const int (&qid)[2], const int (&qrow)[2], int qhi,
+                                               double (&tv)[2], int (&ti)[2], double* Lv, int* Li, int kk, int wid,
+                                               int lane, int fc) {
+    // d^2 = (|x|^2 + |y|^2) - 2 x.y (tree.py:179), tested against the rows' k-th best
+    bool hit = false;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = 8 * j + 2 * fc + h, ci = c0 + c;
+        const double sc = sqc[c];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const double dv = (sqq[i] + sc) - 2.0 * acc[i][j][h];
+          acc[i][j][h] = dv;
+          hit |= ci < n && ci != qid[i] && qid[i] < qhi && lex_less(dv, ci, tv[i], ti[i]);
+        }
+      }
+    if (!__any_sync(0xffffffffu, hit)) return;
+    // insertion path: slot by slot (static registers), lanes with a hit one at a time
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int ci = c0 + 8 * j + 2 * fc + h;
+          const double dv = acc[i][j][h];
+          const bool ok = ci < n && ci != qid[i] && qid[i] < qhi && lex_less(dv, ci, tv[i], ti[i]);
+          unsigned m = __ballot_sync(0xffffffffu, ok);
+          while (m) {
+            const int src = __ffs(m) - 1;
+            m &= m - 1;
+            const double v = __shfl_sync(0xffffffffu, dv, src);
+            const int vi = __shfl_sync(0xffffffffu, ci, src);
+            const int row = wid * 16 + 8 * i + (src >> 2);
+            const double lv = Lv[row * 32 + lane];
+            const int li = Li[row * 32 + lane];
+            const unsigned gm = __ballot_sync(0xffffffffu, lane < kk && lex_less(v, vi, lv, li));
+            if (gm == 0) continue;  // the row's k-th moved since the test
+            const int pos = __ffs(gm) - 1;
+            const double up_v = __shfl_up_sync(0xffffffffu, lv, 1);
+            const int up_i = __shfl_up_sync(0xffffffffu, li, 1);
+            if (lane == pos) {
+              Lv[row * 32 + lane] = v;
+              Li[row * 32 + lane] = vi;
+            } else if (lane > pos && lane < kk) {
+              Lv[row * 32 + lane] = up_v;
+              Li[row * 32 + lane] = up_i;
+            }
+            __syncwarp();
+          }
+        }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      tv[i] = Lv[qrow[i] * 32 + kk - 1];
+      ti[i] = Li[qrow[i] * 32 + kk - 1];
+    }
+  }
+
 template <bool BULK>
 __global__ void __launch_bounds__(SKT) knn_stream_kernel(const double* __restrict__ X, const double* __restrict__ sq,
                                                         int n, int d, int kk, int qlo, int qhi,
@@ -389,62 +454,127 @@ __global__ void __launch_bounds__(SKT) knn_stream_kernel(const double* __restric
 #pragma unroll
         for (int j = 0; j < 8; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
-    // d^2 = (|x|^2 + |y|^2) - 2 x.y (tree.py:179), tested against the rows' k-th best
-    bool hit = false;
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int c = 8 * j + 2 * fc + h, ci = c0 + c;
-        const double sc = sqc[c];
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const double dv = (sqq[i] + sc) - 2.0 * acc[i][j][h];
-          acc[i][j][h] = dv;
-          hit |= ci < n && ci != qid[i] && qid[i] < qhi && lex_less(dv, ci, tv[i], ti[i]);
-        }
+    knn_tile_merge(acc, sqq, sqc, c0, n, qid, qrow, qhi, tv, ti, sm.Lv, sm.Li, kk, wid, lane, fc);
+  }
+  __syncwarp();
+  for (int r = 0; r < 16; ++r) {
+    const int row = wid * 16 + r, q = q0 + row;
+    if (q < qhi && lane < kk) out[(size_t)(q - qlo) * kk + lane] = sm.Li[row * 32 + lane];
+  }
+}
+
+// d > 32 (C5: d = 784): the same warp-owned merge, with the feature
+// dimension walked in 32-wide chunks.  Every (candidate tile, chunk) step
+// stages the chunk of the 64 queries and of the 64 candidates (cp.async,
+// double-buffered: the next step's 32 KB land behind this step's 512 DMMA),
+// the accumulators live across a tile's chunks, and the epilogue runs once
+// per tile.  knn_kernel staged each chunk synchronously between two
+// barriers and merged through a distance tile in shared memory.
+constexpr int CDS = 36;  // staged row stride of a 32-wide chunk
+struct KnnChunkSmem {
+  double Qs[2][SQB * CDS];
+  double Cs[2][SCB * CDS];
+  double sqc[2][SCB];
+  double Lv[SQB * 32];
+  int Li[SQB * 32];
+};
+
+__global__ void __launch_bounds__(SKT) knn_chunk_kernel(const double* __restrict__ X, const double* __restrict__ sq,
+                                                       int n, int d, int kk, int qlo, int qhi,
+                                                       int64_t* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char knn_raw[];
+  KnnChunkSmem& sm = *reinterpret_cast<KnnChunkSmem*>(knn_raw);
+  const int q0 = qlo + blockIdx.x * SQB;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int fr = lane >> 2, fc = lane & 3;
+  const bool vec16 = (d & 1) == 0;  // rows and 32-wide chunks start 16-byte aligned
+  const int nch = (d + 31) / 32;
+  // 64 points x 32 features [k0, k0 + 32) (zero past n and past d)
+  auto stage = [&](double* S, int base, int k0) {
+    if (vec16) {
+      for (int e = tid; e < 64 * 16; e += SKT) {
+        const int r = e >> 4, k = 2 * (e & 15);
+        const int pt = base + r;
+        if (pt < n && k0 + k < d) cp_async16(S + r * CDS + k, X + (size_t)pt * d + k0 + k);
+        else S[r * CDS + k] = S[r * CDS + k + 1] = 0.0;
       }
-    if (!__any_sync(0xffffffffu, hit)) continue;
-    // insertion path: slot by slot (static registers), lanes with a hit one at a time
+    } else {
+      for (int e = tid; e < 64 * 32; e += SKT) {
+        const int r = e >> 5, k = e & 31;
+        const int pt = base + r;
+        const bool ok = pt < n && k0 + k < d;
+        cp_async8(S + r * CDS + k, ok ? X + (size_t)pt * d + k0 + k : X, ok);
+      }
+    }
+  };
+  auto stage_sq = [&](double* S, int base) {
+    if (tid < SCB) {
+      const bool ok = base + tid < n;
+      cp_async8(S + tid, ok ? sq + base + tid : sq, ok);
+    }
+  };
+  const int ntile = (n + SCB - 1) / SCB;
+  const int own = min(q0 / SCB, ntile - 1);
+  auto tile_at = [&](int sidx) {  // outwards from the queries' own tree position (see knn_stream_kernel)
+    const int off = (sidx & 1) ? (sidx + 1) / 2 : ntile - sidx / 2;
+    return (own + off) % ntile;
+  };
+  stage(sm.Qs[0], q0, 0);
+  stage(sm.Cs[0], tile_at(0) * SCB, 0);
+  stage_sq(sm.sqc[0], tile_at(0) * SCB);
+  cp_async_commit();
+  for (int e = tid; e < SQB * 32; e += SKT) {
+    sm.Lv[e] = DBL_MAX;
+    sm.Li[e] = 0x7fffffff;
+  }
+  int qrow[2], qid[2];
+  double sqq[2], tv[2];
+  int ti[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    qrow[i] = wid * 16 + 8 * i + fr;
+    qid[i] = q0 + qrow[i];
+    sqq[i] = qid[i] < n ? sq[qid[i]] : 0.0;
+    tv[i] = DBL_MAX;
+    ti[i] = 0x7fffffff;
+  }
+  int step = 0;
+  for (int t = 0; t < ntile; ++t) {
+    const int c0 = tile_at(t) * SCB;
+    double acc[2][8][2];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int ci = c0 + 8 * j + 2 * fc + h;
-          const double dv = acc[i][j][h];
-          const bool ok = ci < n && ci != qid[i] && qid[i] < qhi && lex_less(dv, ci, tv[i], ti[i]);
-          unsigned m = __ballot_sync(0xffffffffu, ok);
-          while (m) {
-            const int src = __ffs(m) - 1;
-            m &= m - 1;
-            const double v = __shfl_sync(0xffffffffu, dv, src);
-            const int vi = __shfl_sync(0xffffffffu, ci, src);
-            const int row = wid * 16 + 8 * i + (src >> 2);
-            const double lv = sm.Lv[row * 32 + lane];
-            const int li = sm.Li[row * 32 + lane];
-            const unsigned gm = __ballot_sync(0xffffffffu, lane < kk && lex_less(v, vi, lv, li));
-            if (gm == 0) continue;  // the row's k-th moved since the test
-            const int pos = __ffs(gm) - 1;
-            const double up_v = __shfl_up_sync(0xffffffffu, lv, 1);
-            const int up_i = __shfl_up_sync(0xffffffffu, li, 1);
-            if (lane == pos) {
-              sm.Lv[row * 32 + lane] = v;
-              sm.Li[row * 32 + lane] = vi;
-            } else if (lane > pos && lane < kk) {
-              sm.Lv[row * 32 + lane] = up_v;
-              sm.Li[row * 32 + lane] = up_i;
-            }
-            __syncwarp();
-          }
+      for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int ch = 0; ch < nch; ++ch, ++step) {
+      const double* Qs = sm.Qs[step & 1];
+      const double* Cs = sm.Cs[step & 1];
+      cp_async_wait<0>();
+      __syncthreads();  // this step's chunks landed; everyone is done with the other buffers
+      {                 // next step: next chunk of this tile, or chunk 0 of the next tile
+        const int nt = ch + 1 < nch ? t : t + 1, nc = ch + 1 < nch ? ch + 1 : 0;
+        if (nt < ntile) {
+          const int c1 = tile_at(nt) * SCB;
+          stage(sm.Qs[(step + 1) & 1], q0, nc * 32);
+          stage(sm.Cs[(step + 1) & 1], c1, nc * 32);
+          if (nc == 0) stage_sq(sm.sqc[nt & 1], c1);
         }
-    __syncwarp();
+      }
+      cp_async_commit();
+      const int dc = min(32, d - ch * 32);
+      for (int k4 = 0; k4 < dc; k4 += 4) {
+        double a[2], b[8];
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      tv[i] = sm.Lv[qrow[i] * 32 + kk - 1];
-      ti[i] = sm.Li[qrow[i] * 32 + kk - 1];
+        for (int i = 0; i < 2; ++i) a[i] = Qs[qrow[i] * CDS + k4 + fc];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) b[j] = Cs[(8 * j + fr) * CDS + k4 + fc];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+      }
     }
+    knn_tile_merge(acc, sqq, sm.sqc[t & 1], c0, n, qid, qrow, qhi, tv, ti, sm.Lv, sm.Li, kk, wid, lane, fc);
   }
   __syncwarp();
   for (int r = 0; r < 16; ++r) {
@@ -489,6 +619,10 @@ extern "C" int hks_knn_rows(const double* X, int64_t n, int64_t d, int64_t k, in
         knn_stream_kernel<false><<<grid, SKT, knn_stream_smem((int)d), s>>>(X, sq, (int)n, (int)d, (int)k, (int)q0,
                                                                             (int)(q0 + nq), out);
       }
+    } else if (!stream_off) {
+      raise_smem_limit(knn_chunk_kernel, sizeof(KnnChunkSmem));
+      knn_chunk_kernel<<<(unsigned)((nq + SQB - 1) / SQB), SKT, sizeof(KnnChunkSmem), s>>>(
+          X, sq, (int)n, (int)d, (int)k, (int)q0, (int)(q0 + nq), out);
     } else {
       const size_t sm = (size_t)(2 * QB * DS + QB * (CB + 1)) * sizeof(double);
       raise_smem_limit(knn_kernel<false>, sm);
