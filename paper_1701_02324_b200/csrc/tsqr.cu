@@ -186,10 +186,26 @@ __global__ void __launch_bounds__(TNT, B <= 128 ? 2 : 1) tsqr_absorb_kernel(cons
             dot[t] = fma(v[q], a[t][q], dot[t]);
           }
         }
+        {
+          // four sums over the warp in 6 + 4 shuffles instead of 20: the first
+          // two butterfly rounds also hand each lane ONE of the four columns
+          // (lanes 16..31 keep columns 2, 3; odd 8-lane groups keep the odd
+          // one), three rounds finish it inside the 8-lane group, and the
+          // totals are broadcast from lanes 0, 8, 16, 24.  Fixed order.
+          static_assert(CW == 4, "butterfly reduction is written for four columns per warp");
+          const bool b4 = (lane & 16) != 0, b3 = (lane & 8) != 0;
+          const double s0 = b4 ? dot[0] : dot[2], s1 = b4 ? dot[1] : dot[3];
+          double k0 = b4 ? dot[2] : dot[0], k1 = b4 ? dot[3] : dot[1];
+          k0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+          k1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+          double kq = b3 ? k1 : k0;
+          kq += __shfl_xor_sync(0xffffffffu, b3 ? k0 : k1, 8);
+          kq += __shfl_xor_sync(0xffffffffu, kq, 4);
+          kq += __shfl_xor_sync(0xffffffffu, kq, 2);
+          kq += __shfl_xor_sync(0xffffffffu, kq, 1);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-          for (int t = 0; t < CW; ++t) dot[t] += __shfl_xor_sync(0xffffffffu, dot[t], o);
+          for (int t = 0; t < CW; ++t) dot[t] = __shfl_sync(0xffffffffu, kq, 8 * t);
+        }
         __syncwarp();
 #pragma unroll
         for (int t = 0; t < CW; ++t) {
