@@ -186,6 +186,26 @@ def knn(coords, k, chunk=256):
     return out
 
 
+def knn_rows(coords, k, rows, chunk=256):
+    """The lists of knn() for the query rows `rows` only (same formula, same
+    (d^2, index) order; tree.py:163-188): full-size spot checks where the
+    whole table would take hours of CPU."""
+    n = coords.shape[0]
+    rows = np.asarray(rows, dtype=np.int64)
+    sq = np.einsum("ij,ij->i", coords, coords)
+    out = np.empty((rows.size, k), dtype=np.int64)
+    for lo in range(0, rows.size, chunk):
+        q = rows[lo:lo + chunk]
+        d2 = sq[q, None] + sq[None, :] - 2.0 * (coords[q] @ coords.T)
+        d2[np.arange(q.size), q] = np.inf
+        kth = np.partition(d2, k - 1, axis=1)[:, k - 1]
+        for r in range(q.size):
+            cand = np.flatnonzero(d2[r] <= kth[r])
+            cand = cand[np.lexsort((cand, d2[r, cand]))]
+            out[lo + r] = cand[:k]
+    return out
+
+
 # ----------------------------------------------------------------------------
 # column-pivoted QR and interpolative decomposition  (linalg.py:43-136)
 # ----------------------------------------------------------------------------
