@@ -45,3 +45,30 @@ def test_full_size_perm_and_knn(name):
         rows = np.asarray(g["knn_sample_rows"], dtype=np.int64)
         assert knn[rows[:8]].tolist() == g["knn_sample_head"]
         assert _sha(knn[rows]) == g["knn_sample_sha256"]
+
+
+SKEL_CASES = sorted(p.stem[len("full_"):-len("_skeletons")] for p in GOLDEN.glob("full_*_skeletons.json"))
+
+
+@pytest.mark.parametrize("name", SKEL_CASES)
+def test_full_size_skeleton_subtree(name):
+    """Skeleton index sets of one depth-2 subtree at the configuration's full
+    N (tools/make_full_skeleton_digest.py: the oracle's skeleton.py:84-182 /
+    linalg.py:43-136 on the sampled blocks themselves) against the GPU path,
+    whose blocks of 3.3 k - 9 k rows go through the tall-skinny QR
+    pre-reduction (csrc/tsqr.cu) before the pivoting: same row counts, same
+    ranks, same pivot order."""
+    import paper_1701_02324_b200 as hk
+    from paper_1701_02324_b200 import workloads as W
+    g = json.loads((GOLDEN / f"full_{name}_skeletons.json").read_text())
+    w = W.CONFIGS[g["workload"]]
+    x = W.points(w, 0)
+    kern = hk.KernelSpec("gaussian", h=w.h, regularization=w.lam)
+    tree = hk.build_tree(hk.PointSet(x), w.leaf_size, seed=0)
+    knn = hk.knn_bruteforce(tree.points, w.kappa)
+    cfg = hk.SkeletonConfig(tau=w.tau, max_rank=w.max_rank, samples=w.samples, sample_mode="knn_augmented", seed=0)
+    sk = hk.build_skeletons(tree, kern, cfg, knn=knn)
+    for node, ref in g["nodes"].items():
+        i = int(node)
+        assert int(sk.rows_count[i]) == ref["rows"], node
+        assert np.array_equal(np.asarray(sk[i].indices), np.asarray(ref["indices"], dtype=np.int64)), node
