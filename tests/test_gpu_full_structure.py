@@ -72,3 +72,31 @@ def test_full_size_skeleton_subtree(name):
         i = int(node)
         assert int(sk.rows_count[i]) == ref["rows"], node
         assert np.array_equal(np.asarray(sk[i].indices), np.asarray(ref["indices"], dtype=np.int64)), node
+    # the subtree's factorization against the oracle's (solver.py:111-186 on
+    # the same seven nodes; it depends on nothing outside the subtree):
+    # theta of every node and push of the internal ones by norm, the subtree
+    # root's theta / push by 8 Gaussian sketches, to the tolerance of the
+    # reduced-N parity tests (1e-8, scaled by the node's z_cond where the
+    # reduced system amplifies roundoff), and LAPACK's condition estimate
+    fx = GOLDEN / f"full_{name}_factor.npz"
+    if not fx.exists():
+        return
+    z = np.load(fx)
+    op = hk.build_operator(tree, sk, kern)
+    f = hk.factorize(op, float(z["lam"]))
+    root = int(g["subtree_root"])
+    for node in g["nodes"]:
+        i = int(node)
+        nf = f.factors[i]
+        tol = 1e-8 * max(1.0, float(z[f"z_cond_{i}"]) / 1e4) if f"z_cond_{i}" in z else 1e-8
+        ref = float(z[f"theta_norm_{i}"])
+        assert abs(np.linalg.norm(nf.theta) - ref) <= tol * ref, node
+        if f"z_cond_{i}" in z:
+            pref = float(z[f"push_norm_{i}"])
+            assert abs(np.linalg.norm(nf.child_push) - pref) <= tol * pref, node
+            assert abs(nf.z_cond - float(z[f"z_cond_{i}"])) <= 1e-3 * float(z[f"z_cond_{i}"]), node
+    nf = f.factors[root]
+    gs = np.random.default_rng([29, root]).standard_normal((nf.theta.shape[1], 8))
+    tol = 1e-8 * max(1.0, float(z[f"z_cond_{root}"]) / 1e4)
+    for got, key in ((nf.theta @ gs, "theta_root_sketch"), (nf.child_push @ gs, "push_root_sketch")):
+        assert np.linalg.norm(got - z[key]) <= tol * np.linalg.norm(z[key]), key

@@ -45,17 +45,54 @@ def main(key, which):
     depth = tree.depth
     g = (1 << (depth - 2)) - 1 + which  # a node two levels above the leaves
     order = [4 * g + 3, 4 * g + 4, 4 * g + 5, 4 * g + 6, 2 * g + 1, 2 * g + 2, g]
-    skel, out = {}, {}
+    skel, interp, out = {}, {}, {}
     for i in order:
         b, e = int(tree.begin[i]), int(tree.end[i])
         rows = O.sample_rows(tree.n, b, e, i, w.samples, "knn_augmented", 0, knn)
         cands = np.arange(b, e) if tree.is_leaf(i) else np.concatenate([skel[2 * i + 1], skel[2 * i + 2]])
         blk = O.kernel_block("gaussian", tree.coords[rows], tree.coords[cands], h=w.h)
         tau = w.tau if w.tau else 1e-300
-        cols, _p = O.interp_decomp(blk, tau, w.max_rank)
+        cols, p_i = O.interp_decomp(blk, tau, w.max_rank)
         skel[i] = cands[cols]
+        interp[i] = p_i
         out[str(i)] = {"rows": int(rows.size), "indices": skel[i].tolist()}
         print(i, "rows", rows.size, "rank", cols.size, f"{time.time() - t0:.0f} s", flush=True)
+    # the subtree's factorization (solver.py:111-186 restated in the oracle):
+    # theta of every node, push / z_cond of the internal ones -- the subtree
+    # depends on nothing outside it
+    lam = w.lam
+    fac, facts = {}, {}
+    for i in order:
+        if tree.is_leaf(i):
+            b, e = int(tree.begin[i]), int(tree.end[i])
+            a = O.kernel_block("gaussian", tree.coords[b:e], tree.coords[b:e], h=w.h) + lam * np.eye(e - b)
+            phi = O.lu_solve(O.lu(a), interp[i].T)
+            fac[i] = {"theta": interp[i] @ phi}
+        else:
+            tl, tr = fac[2 * i + 1]["theta"], fac[2 * i + 2]["theta"]
+            rl, rr = tl.shape[0], tr.shape[0]
+            c = O.kernel_block("gaussian", tree.coords[skel[2 * i + 1]], tree.coords[skel[2 * i + 2]], h=w.h)
+            z = np.eye(rl + rr)
+            z[:rl, rl:] += tl @ c
+            z[rl:, :rl] += tr @ c.T
+            zf, cond = O.factor_z(z, i, tree.level_of(i))
+            th = np.zeros((rl + rr, rl + rr))
+            th[:rl, :rl] = tl
+            th[rl:, rl:] = tr
+            folded = O._couple(c, O.lu_solve(zf, th))
+            fac[i] = {"theta": interp[i] @ (th - th @ folded) @ interp[i].T, "push": interp[i].T - folded @ interp[i].T,
+                      "z_cond": cond}
+        facts[f"theta_norm_{i}"] = np.linalg.norm(fac[i]["theta"])
+        if "z_cond" in fac[i]:
+            facts[f"z_cond_{i}"] = fac[i]["z_cond"]
+            facts[f"push_norm_{i}"] = np.linalg.norm(fac[i]["push"])
+    # the subtree root's theta and push as 8 seeded Gaussian sketches (the test regenerates G)
+    gs = np.random.default_rng([29, int(g)]).standard_normal((fac[g]["theta"].shape[1], 8))
+    facts["theta_root_sketch"] = fac[g]["theta"] @ gs
+    facts["push_root_sketch"] = fac[g]["push"] @ gs
+    facts["lam"] = lam
+    np.savez_compressed(ROOT / "tests" / "golden" / f"full_{key.lower()}_factor.npz", **facts)
+    print("factor fixtures", f"{time.time() - t0:.0f} s", {k: float(v) for k, v in facts.items() if np.ndim(v) == 0})
     res = {"workload": key, "n": w.n, "subtree_root": int(g), "nodes": out,
            "seconds": round(time.time() - t0, 1)}
     (ROOT / "tests" / "golden" / f"full_{key.lower()}_skeletons.json").write_text(json.dumps(res) + "\n")
