@@ -163,3 +163,14 @@ def test_oracle_tree_knn_vs_ladder_fixture(name):
     assert np.array_equal(tree.perm, z["perm"].astype(np.int64))
     nl = O.knn(tree.coords, w.kappa)
     assert hashlib.sha256(np.ascontiguousarray(nl, dtype=np.int64).tobytes()).hexdigest() == str(z["knn_sha256"])
+
+
+def test_knn_rows_equals_knn_table():
+    """oracle.knn_rows (full-size spot checks, tools/make_full_digests.py) is
+    the row-restricted oracle.knn: same lists on the reference-pinned table."""
+    from oracle import hks_oracle as O
+    rng = np.random.default_rng(4)
+    x = rng.random((3000, 5))
+    full = O.knn(x, 9)
+    rows = np.sort(rng.choice(3000, size=400, replace=False))
+    assert np.array_equal(O.knn_rows(x, 9, rows, chunk=64), full[rows])
