@@ -95,6 +95,12 @@ def test_full_size_skeleton_subtree(name):
             pref = float(z[f"push_norm_{i}"])
             assert abs(np.linalg.norm(nf.child_push) - pref) <= tol * pref, node
             assert abs(nf.z_cond - float(z[f"z_cond_{i}"])) <= 1e-3 * float(z[f"z_cond_{i}"]), node
+    if "upward_root" in z:  # treecode upward pass of a weight vector supported on the subtree
+        b0, e0 = int(tree._begin[root]), int(tree._end[root])
+        wv = np.zeros(w.n)
+        wv[b0:e0] = np.random.default_rng([31, root]).standard_normal(e0 - b0)
+        up = hk.upward_pass(op, wv)[root]
+        assert np.linalg.norm(up - z["upward_root"]) <= 1e-8 * np.linalg.norm(z["upward_root"])
     nf = f.factors[root]
     gs = np.random.default_rng([29, root]).standard_normal((nf.theta.shape[1], 8))
     tol = 1e-8 * max(1.0, float(z[f"z_cond_{root}"]) / 1e4)

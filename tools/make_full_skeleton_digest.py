@@ -90,6 +90,17 @@ def main(key, which):
     gs = np.random.default_rng([29, int(g)]).standard_normal((fac[g]["theta"].shape[1], 8))
     facts["theta_root_sketch"] = fac[g]["theta"] @ gs
     facts["push_root_sketch"] = fac[g]["push"] @ gs
+    # upward pass of a seeded weight vector supported on the subtree
+    # (treecode.py:65-89): the subtree root's skeleton weights
+    b0, e0 = int(tree.begin[g]), int(tree.end[g])
+    wv = np.random.default_rng([31, int(g)]).standard_normal(e0 - b0)
+    up = {}
+    for i in order:
+        if tree.is_leaf(i):
+            up[i] = interp[i] @ wv[int(tree.begin[i]) - b0: int(tree.end[i]) - b0]
+        else:
+            up[i] = interp[i] @ np.concatenate([up[2 * i + 1], up[2 * i + 2]])
+    facts["upward_root"] = up[g]
     facts["lam"] = lam
     np.savez_compressed(ROOT / "tests" / "golden" / f"full_{key.lower()}_factor.npz", **facts)
     print("factor fixtures", f"{time.time() - t0:.0f} s", {k: float(v) for k, v in facts.items() if np.ndim(v) == 0})
