@@ -247,19 +247,21 @@ __device__ __forceinline__ void knn_tile_merge(double (&acc)[2][8][2], const dou
                                                int c0, int n, const int (&qid)[2], const int (&qrow)[2], int qhi,
                                                double (&tv)[2], int (&ti)[2], double* Lv, int* Li, int kk, int wid,
                                                int lane, int fc) {
-    // d^2 = (|x|^2 + |y|^2) - 2 x.y (tree.py:179), tested against the rows' k-th best
+    // d^2 = (|x|^2 + |y|^2) - 2 x.y (tree.py:179), tested against the rows' k-th best.
+    // The test is conservative (d^2 <= k-th: ties, the row's own point and
+    // padding included): one FP64 compare per candidate; the insertion path
+    // below re-checks every candidate exactly.
     bool hit = false;
 #pragma unroll
     for (int j = 0; j < 8; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int c = 8 * j + 2 * fc + h, ci = c0 + c;
-        const double sc = sqc[c];
+        const double sc = sqc[8 * j + 2 * fc + h];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           const double dv = (sqq[i] + sc) - 2.0 * acc[i][j][h];
           acc[i][j][h] = dv;
-          hit |= ci < n && ci != qid[i] && qid[i] < qhi && lex_less(dv, ci, tv[i], ti[i]);
+          hit |= dv <= tv[i];
         }
       }
     if (!__any_sync(0xffffffffu, hit)) return;
@@ -300,7 +302,8 @@ __device__ __forceinline__ void knn_tile_merge(double (&acc)[2][8][2], const dou
     __syncwarp();
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
-      tv[i] = Lv[qrow[i] * 32 + kk - 1];
+      // rows past the query range never insert: their threshold stays below every distance
+      tv[i] = qid[i] < qhi ? Lv[qrow[i] * 32 + kk - 1] : -DBL_MAX;
       ti[i] = Li[qrow[i] * 32 + kk - 1];
     }
   }
@@ -398,7 +401,7 @@ __global__ void __launch_bounds__(SKT) knn_stream_kernel(const double* __restric
     qrow[i] = wid * 16 + 8 * i + fr;
     qid[i] = q0 + qrow[i];
     sqq[i] = qid[i] < n ? sq[qid[i]] : 0.0;
-    tv[i] = DBL_MAX;
+    tv[i] = qid[i] < qhi ? DBL_MAX : -DBL_MAX;  // see knn_tile_merge
     ti[i] = 0x7fffffff;
   }
   // Tiles are visited outwards from the queries' own position: the points
@@ -535,7 +538,7 @@ __global__ void __launch_bounds__(SKT) knn_chunk_kernel(const double* __restrict
     qrow[i] = wid * 16 + 8 * i + fr;
     qid[i] = q0 + qrow[i];
     sqq[i] = qid[i] < n ? sq[qid[i]] : 0.0;
-    tv[i] = DBL_MAX;
+    tv[i] = qid[i] < qhi ? DBL_MAX : -DBL_MAX;  // see knn_tile_merge
     ti[i] = 0x7fffffff;
   }
   int step = 0;
