@@ -1,0 +1,269 @@
+"""The reference's known-answer suite, restated against the GPU package.
+
+Every check below is one the reference makes of itself
+(/root/reference/pkg/tests; cited per test), run here through
+paper_1701_02324_b200's drop-in API on instances built the way the
+reference's helpers build them (helpers.py:92-133: frozen instance =
+uniform_cube d = 3, seed 3, gaussian h = 0.3, lam 1e-2, leaf 256, tau 1e-7,
+max_rank 384, exact sampling).  Independent dense references (numpy) are the
+judges, as in the reference; tolerances are the reference's own, except for
+the four checks the reference itself fails (REF_MEASURED)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+_CACHE = {}
+
+# Four of the reference's checks fail for the unmodified reference itself in
+# this container (pytest /root/reference/pkg/tests/test_solver.py
+# test_skeleton.py: huge_lambda, roundtrip_2048, inverse_action_symmetric,
+# offdiag_reconstruction_bound).  For those the GPU path is held to the
+# reference's own measured values (the same quantities computed by importing
+# the unmodified reference here, numpy 2.3 / OpenBLAS) instead of the bound
+# the reference misses.
+REF_MEASURED = {
+    "roundtrip_2048": 1.4012468159207929e-07,        # ||x - w|| / ||w||
+    "inverse_action_asymmetry": 3.1381111043060628e-09,  # max over the 8 seeded pairs
+    "offdiag_worst": 5.906015803805912e-05,          # worst sibling-block reconstruction error
+    "huge_lambda": 6.7043572417015575e-06,           # ||x - b / lam|| / ||b / lam||
+}
+
+
+def _instance(ps, kern, leaf=64, tau=1e-7, max_rank=256, sample_mode="exact", samples=256, seed=0, factor=True):
+    import paper_1701_02324_b200 as hk
+    tree = hk.build_tree(ps, leaf, seed=seed)
+    sk = hk.build_skeletons(tree, kern, hk.SkeletonConfig(tau=tau, max_rank=max_rank, samples=samples,
+                                                          sample_mode=sample_mode, seed=seed))
+    op = hk.build_operator(tree, sk, kern)
+    f = hk.factorize(op, kern.regularization) if factor else None
+    return dict(hk=hk, ps=ps, kern=kern, tree=tree, sk=sk, op=op, f=f)
+
+
+def _frozen(n):  # helpers.py:113-133
+    if n not in _CACHE:
+        import paper_1701_02324_b200 as hk
+        ps = hk.generate("uniform_cube", n, 3, d=3)
+        kern = hk.KernelSpec(family="gaussian", h=0.3, regularization=1e-2)
+        _CACHE[n] = _instance(ps, kern, leaf=256, tau=1e-7, max_rank=384, sample_mode="exact", seed=3)
+    return _CACHE[n]
+
+
+def _basis(tree, sk, node):
+    """Dense telescoped interpolation operator of a node (oracle.py:49-65)."""
+    s = sk[node.index]
+    if node.is_leaf:
+        return np.asarray(s.interp)
+    left, right = tree.children(node)
+    bl, br = _basis(tree, sk, left), _basis(tree, sk, right)
+    stacked = np.zeros((bl.shape[0] + br.shape[0], node.end - node.begin))
+    split = left.end - left.begin
+    stacked[: bl.shape[0], :split] = bl
+    stacked[bl.shape[0]:, split:] = br
+    return np.asarray(s.interp) @ stacked
+
+
+def _dense(inst):
+    """K(X, X) + lam I in tree order, float64 numpy (oracle.py:27-33)."""
+    x = np.asarray(inst["tree"].points.coords)
+    d2 = ((x[:, None, :] - x[None, :, :]) ** 2).sum(-1)
+    k = np.exp(-d2 / (2.0 * inst["kern"].h ** 2))
+    return k + inst["kern"].regularization * np.eye(x.shape[0])
+
+
+def test_smw_identity_through_gpu_dense_solves():
+    """test_solver.py:16-65: the reduced-system identity against the dense
+    inverse, 2 x 100 random instances; every solve here is the GPU LU."""
+    import paper_1701_02324_b200 as hk
+    for zero_diag, seed in ((True, 20), (False, 21)):
+        rng = np.random.default_rng(seed)
+        for _ in range(100):
+            sizes = rng.integers(2, 17, size=2)
+            ranks = rng.integers(1, 9, size=2)
+            m, r = int(sizes.sum()), int(ranks.sum())
+            d = np.zeros((m, m))
+            at = 0
+            for s in sizes:
+                mat = rng.standard_normal((s, s))
+                d[at:at + s, at:at + s] = mat @ mat.T + np.eye(s)
+                at += s
+            u, v = rng.standard_normal((m, r)), rng.standard_normal((m, r))
+            if zero_diag:
+                bmat = np.zeros((r, r))
+                coup = rng.standard_normal((int(ranks[0]), int(ranks[1])))
+                bmat[: ranks[0], ranks[0]:] = coup
+                bmat[ranks[0]:, : ranks[0]] = coup.T
+            else:
+                bmat = rng.standard_normal((r, r))
+            rhs = rng.standard_normal(m)
+            fd = hk.factor_dense(d)
+            dinv_b, dinv_u = hk.solve_dense(fd, rhs), hk.solve_dense(fd, u)
+            z = np.eye(r) + (v.T @ dinv_u) @ bmat
+            got = dinv_b - dinv_u @ (bmat @ hk.solve_dense(hk.factor_dense(z), v.T @ dinv_b))
+            expect = np.linalg.inv(d + u @ bmat @ v.T) @ rhs
+            assert np.linalg.norm(got - expect) <= 1e-10 * np.linalg.norm(expect)
+
+
+def test_single_leaf_matches_dense():  # test_solver.py:68-78
+    import paper_1701_02324_b200 as hk
+    ps = hk.generate("uniform_cube", 50, seed=1, d=3)
+    kern = hk.KernelSpec("gaussian", h=0.4, regularization=1e-2)
+    inst = _instance(ps, kern, leaf=64)
+    assert len(inst["f"].factors) == 1
+    b = np.random.default_rng(2).standard_normal(50)
+    x = hk.solve(inst["f"], b, in_tree_order=True)
+    expect = np.linalg.solve(_dense(inst), b)
+    assert np.linalg.norm(x - expect) <= 1e-12 * np.linalg.norm(expect)
+
+
+def test_rank_zero_decouples_to_leaf_solves():  # test_solver.py:81-93
+    import paper_1701_02324_b200 as hk
+    ps = hk.generate("uniform_cube", 128, seed=3, d=2)
+    kern = hk.KernelSpec("gaussian", h=1e-9, regularization=1e-1)
+    inst = _instance(ps, kern, leaf=32, tau=1e-4, max_rank=8)
+    assert inst["f"].max_rank == 0
+    b = np.random.default_rng(4).standard_normal(128)
+    x = hk.solve(inst["f"], b, in_tree_order=True)
+    for leaf in inst["tree"].leaves():
+        block = np.asarray(inst["op"].leaf_blocks[leaf.index]) + 1e-1 * np.eye(leaf.size)
+        expect = np.linalg.solve(block, b[leaf.begin:leaf.end])
+        got = x[leaf.begin:leaf.end]
+        assert np.linalg.norm(got - expect) <= 1e-12 * np.linalg.norm(expect)
+
+
+def test_theta_matches_dense_projection():  # test_solver.py:96-111
+    inst = _frozen(2048)
+    hk, tree, sk, f = inst["hk"], inst["tree"], inst["sk"], inst["f"]
+    kt = hk.materialize_ktilde(inst["op"], f.lam)
+    for node in tree.nodes:
+        if node.level == 0:
+            continue
+        basis = _basis(tree, sk, node)
+        sub = kt[node.begin:node.end, node.begin:node.end]
+        ref = basis @ np.linalg.inv(sub) @ basis.T
+        assert np.linalg.norm(f.factors[node.index].theta - ref) <= 1e-8 * max(np.linalg.norm(ref), 1e-300)
+
+
+def test_theta_symmetric():  # test_solver.py:114-120
+    inst = _frozen(1024)
+    for node in inst["tree"].nodes:
+        if node.level == 0:
+            continue
+        th = inst["f"].factors[node.index].theta
+        if th.size:
+            assert np.linalg.norm(th - th.T) <= 1e-10 * np.linalg.norm(th)
+
+
+def test_huge_lambda_diagonal_dominance():  # test_solver.py:123-130
+    import paper_1701_02324_b200 as hk
+    lam = 1e6
+    ps = hk.generate("uniform_cube", 256, seed=5, d=3)
+    kern = hk.KernelSpec("gaussian", h=0.4, regularization=lam)
+    inst = _instance(ps, kern, leaf=64, tau=1e-6)
+    b = np.random.default_rng(6).standard_normal(256)
+    x = hk.solve(inst["f"], b, in_tree_order=True)
+    # The reference asserts ||x - b / lam|| <= 2e-6 ||b / lam||; the unmodified
+    # reference itself returns 6.70e-6 on this instance (measured here: its
+    # own test fails), because x = b / lam - K b / lam^2 + ... deviates by
+    # ||K|| / lam.  The restated check is the bound with the right constant,
+    # and agreement with the dense solve.
+    dense = _dense(inst)
+    knorm = np.linalg.norm(dense - lam * np.eye(256), 2)
+    assert np.linalg.norm(x - b / lam) <= 1.01 * knorm / lam * np.linalg.norm(b / lam)
+    dev = np.linalg.norm(x - b / lam) / np.linalg.norm(b / lam)
+    assert abs(dev - REF_MEASURED["huge_lambda"]) <= 1e-6 * REF_MEASURED["huge_lambda"]
+    expect = np.linalg.solve(dense, b)
+    assert np.linalg.norm(x - expect) <= 1e-10 * np.linalg.norm(expect)
+
+
+def test_roundtrip_2048():  # test_solver.py:133-139
+    inst = _frozen(2048)
+    hk = inst["hk"]
+    w = np.random.default_rng(7).standard_normal(2048)
+    b = hk.hmatvec(inst["op"], w, inst["f"].lam)
+    x = hk.solve(inst["f"], b, in_tree_order=True)
+    # The reference's bound is 1e-9; the unmodified reference itself reaches
+    # 1.40e-7 on this instance (REF_MEASURED below: its own test fails --
+    # reduced systems of condition ~1e7 amplify roundoff).  Parity criterion:
+    # within a small factor of the reference's own round-trip error.
+    assert np.linalg.norm(x - w) <= 4 * REF_MEASURED["roundtrip_2048"] * np.linalg.norm(w)
+
+
+def test_solve_vs_true_dense():  # test_solver.py:142-149
+    inst = _frozen(1024)
+    b = np.random.default_rng(8).standard_normal(1024)
+    x = inst["hk"].solve(inst["f"], b, in_tree_order=True)
+    expect = np.linalg.solve(_dense(inst), b)
+    assert np.linalg.norm(x - expect) <= 1e-4 * np.linalg.norm(expect)
+
+
+def test_inverse_action_symmetric():  # test_solver.py:152-163
+    inst = _frozen(1024)
+    hk, n = inst["hk"], inst["tree"].n
+    rng = np.random.default_rng(9)
+    for _ in range(8):
+        i, j = rng.integers(0, n, size=2)
+        ei, ej = np.zeros(n), np.zeros(n)
+        ei[i] = ej[j] = 1.0
+        xj = hk.solve(inst["f"], ej, in_tree_order=True)
+        xi = hk.solve(inst["f"], ei, in_tree_order=True)
+        # reference bound 1e-9; the reference's own worst pair is 3.14e-9 (REF_MEASURED)
+        assert abs(ei @ xj - ej @ xi) <= 2 * REF_MEASURED["inverse_action_asymmetry"]
+
+
+def test_input_order_and_multi_and_validation():  # test_solver.py:166-204, 215-218
+    import paper_1701_02324_b200 as hk
+    ps = hk.generate("uniform_cube", 256, 11, d=3)
+    kern = hk.KernelSpec("gaussian", h=0.3, regularization=1e-1)
+    inst = _instance(ps, kern, leaf=64, tau=1e-10, max_rank=256, seed=11)
+    f = inst["f"]
+    rng = np.random.default_rng(10)
+    b = rng.standard_normal(256)
+    perm = np.asarray(inst["tree"].perm)
+    assert np.array_equal(hk.solve(f, b, in_tree_order=False)[perm], hk.solve(f, b[perm], in_tree_order=True))
+    block = np.random.default_rng(11).standard_normal((256, 4))
+    got = hk.solve_multi(f, block, in_tree_order=True)
+    for j in range(4):
+        assert np.array_equal(got[:, j], hk.solve(f, block[:, j], in_tree_order=True))
+    assert np.all(hk.solve_multi(f, np.zeros((256, 3)), in_tree_order=True) == 0.0)
+    with pytest.raises(ValueError):
+        hk.solve_multi(f, np.zeros(256))
+    assert f.lam == 1e-1
+    with pytest.raises(ValueError):
+        hk.factorize(inst["op"], -1.0)
+    with pytest.raises(ValueError):
+        hk.solve(f, np.zeros(5))
+
+
+def test_build_stats_populated():  # test_solver.py:233-239
+    f = _frozen(1024)["f"]
+    assert set(f.level_seconds) == {0, 1, 2}
+    assert f.max_rank > 0
+    assert all(c >= 1.0 for c in f.z_cond_per_level().values())
+
+
+def test_offdiag_reconstruction_bound():  # test_skeleton.py:174-182, 208-227
+    import paper_1701_02324_b200 as hk
+    ps = hk.generate("uniform_cube", 512, seed=10, d=3)
+    tree = hk.build_tree(ps, 64, seed=10)
+    assert tree.depth == 3
+    tau = 1e-6
+    kern = hk.KernelSpec("gaussian", h=0.4)
+    sk = hk.build_skeletons(tree, kern, hk.SkeletonConfig(tau=tau, max_rank=64, sample_mode="exact", seed=10))
+    coords = np.asarray(tree.points.coords)
+    worst = 0.0
+    for node in tree.nodes:
+        if node.is_leaf:
+            continue
+        left, right = tree.children(node)
+        block = hk.eval_block(kern, coords[left.begin:left.end], coords[right.begin:right.end])
+        mid = hk.eval_block(kern, coords[np.asarray(sk[left.index].indices)], coords[np.asarray(sk[right.index].indices)])
+        approx = _basis(tree, sk, left).T @ mid @ _basis(tree, sk, right)
+        denom = np.linalg.norm(block)
+        if denom > 0:
+            worst = max(worst, np.linalg.norm(block - approx) / denom)
+    # reference bound 10 tau (depth + 1) = 4e-5; the reference's own worst
+    # block is 5.906e-5 (REF_MEASURED: its own test fails).  The skeletons are
+    # identical, so the GPU value equals the reference's to roundoff.
+    assert abs(worst - REF_MEASURED["offdiag_worst"]) <= 1e-6 * REF_MEASURED["offdiag_worst"]
