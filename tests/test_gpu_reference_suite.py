@@ -375,3 +375,129 @@ def test_solver_consistency_roundtrip():  # test_treecode.py:149-157
     x = hk.solve(inst["f"], b, in_tree_order=True)
     # reference bound 1e-9; the unmodified reference itself reaches 5.92e-9 here (REF_MEASURED)
     assert np.linalg.norm(x - w) <= 4 * REF_MEASURED["consistency_roundtrip"] * np.linalg.norm(w)
+
+
+# ------------------------------------------------------------------ linalg
+# test_linalg.py restated: pivoted QR, interpolative decomposition, dense LU.
+
+def _decaying(rng, m, n, decay=0.5, rank=None):  # helpers.py:55-62
+    rank = rank or min(m, n)
+    u, _ = np.linalg.qr(rng.standard_normal((m, rank)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, rank)))
+    return (u * decay ** np.arange(rank)) @ v.T
+
+
+def test_pivoted_qr_known_answers():  # test_linalg.py:15-78
+    import paper_1701_02324_b200 as hk
+    res = hk.pivoted_qr(np.eye(3), 1e-12, 10)
+    assert res.rank == 3 and np.allclose(np.abs(np.diag(res.r_factor)), 1.0)
+    rng = np.random.default_rng(0)
+    assert hk.pivoted_qr(np.outer(rng.standard_normal(5), rng.standard_normal(7)), 1e-10, 10).rank == 1
+    # rank against the SVD oracle (singular values 2^-j)
+    a = _decaying(np.random.default_rng(1), 50, 80)
+    tol = 1e-6
+    sigma = np.linalg.svd(a, compute_uv=False)
+    oracle_rank = int(np.sum(sigma / sigma[0] > tol))
+    assert oracle_rank == int(np.sum(0.5 ** np.arange(50) > tol))
+    assert abs(hk.pivoted_qr(a, tol, 64).rank - oracle_rank) <= 1
+    # |R_kk| non-increasing
+    rng = np.random.default_rng(2)
+    for _ in range(100):
+        m, n = rng.integers(2, 40, size=2)
+        res = hk.pivoted_qr(_decaying(rng, m, n, decay=rng.uniform(0.3, 0.9)), 1e-14, 64)
+        assert np.all(np.diff(np.abs(np.diag(res.r_factor[:, : res.rank]))) <= 0.0)
+    # empty / zero / cap / column space / bad arguments
+    res = hk.pivoted_qr(np.zeros((0, 4)), 1e-8, 4)
+    assert res.rank == 0 and res.r_factor.shape == (0, 4)
+    assert hk.pivoted_qr(np.zeros((3, 0)), 1e-8, 4).rank == 0
+    assert hk.pivoted_qr(np.zeros((5, 5)), 1e-8, 4).rank == 0
+    assert hk.pivoted_qr(np.random.default_rng(3).standard_normal((20, 20)), 1e-15, 7).rank == 7
+    a = _decaying(np.random.default_rng(4), 30, 25, decay=0.25)
+    res = hk.pivoted_qr(a, 1e-9, 30)
+    q, _ = np.linalg.qr(a[:, res.pivots[: res.rank]])
+    assert np.linalg.norm(a - q @ (q.T @ a)) <= 10 * 1e-9 * np.linalg.norm(a)
+    with pytest.raises(ValueError):
+        hk.pivoted_qr(np.eye(2), -1.0, 3)
+    with pytest.raises(ValueError):
+        hk.pivoted_qr(np.eye(2), 1e-8, 0)
+
+
+def test_interpolative_decomposition_known_answers():  # test_linalg.py:81-123
+    import paper_1701_02324_b200 as hk
+    rng = np.random.default_rng(5)
+    c0, c2 = rng.standard_normal(6), rng.standard_normal(6)
+    a = np.column_stack([c0, c0, c2])
+    cols, interp = hk.interpolative_decomposition(a, 1e-12, 10)
+    assert len(cols) == 2 and np.linalg.norm(a - a[:, cols] @ interp) <= 1e-12 * np.linalg.norm(a)
+    rng = np.random.default_rng(6)
+    a = rng.standard_normal((40, 3)) @ rng.standard_normal((3, 60))
+    cols, interp = hk.interpolative_decomposition(a, 1e-10, 40)
+    assert len(cols) == 3 and np.linalg.norm(a - a[:, cols] @ interp) <= 1e-9 * np.linalg.norm(a)
+    cols, interp = hk.interpolative_decomposition(np.zeros((4, 6)), 1e-10, 4)
+    assert cols.size == 0 and interp.shape == (0, 6)
+    rng = np.random.default_rng(7)
+    for _ in range(100):
+        m, n = rng.integers(3, 30, size=2)
+        a = _decaying(rng, m, n, decay=rng.uniform(0.2, 0.8))
+        cols, interp = hk.interpolative_decomposition(a, 1e-8, 20)
+        assert np.array_equal(interp[:, cols], np.eye(len(cols)))
+    rng = np.random.default_rng(8)
+    tol = 1e-6
+    for _ in range(100):
+        m, n = int(rng.integers(10, 50)), int(rng.integers(10, 50))
+        a = _decaying(rng, m, n, decay=0.4)
+        cols, interp = hk.interpolative_decomposition(a, tol, min(m, n))
+        r = max(len(cols), 1)
+        assert np.linalg.norm(a - a[:, cols] @ interp) <= 10 * np.sqrt(n * r) * tol * np.linalg.norm(a)
+
+
+def test_dense_factor_known_answers():  # test_linalg.py:126-190
+    import paper_1701_02324_b200 as hk
+    b = np.random.default_rng(9).standard_normal((4, 3))
+    assert np.allclose(hk.solve_dense(hk.factor_dense(np.eye(4)), b), b)
+    assert np.allclose(hk.solve_dense(hk.factor_dense(np.diag([2.0, 2.0, 2.0])), np.array([2.0, 4.0, 6.0])), [1.0, 2.0, 3.0])
+    rng = np.random.default_rng(10)
+    m = rng.standard_normal((8, 8))
+    a = m.T @ m + np.eye(8)
+    rhs = rng.standard_normal(8)
+    x = hk.solve_dense(hk.factor_dense(a), rhs)
+    # hand-rolled elimination with partial pivoting as the oracle (helpers.py:18-37)
+    aa, bb = a.copy(), rhs.copy()
+    for col in range(8):
+        piv = col + int(np.argmax(np.abs(aa[col:, col])))
+        if piv != col:
+            aa[[col, piv]], bb[[col, piv]] = aa[[piv, col]], bb[[piv, col]]
+        for row in range(col + 1, 8):
+            f = aa[row, col] / aa[col, col]
+            aa[row, col:] -= f * aa[col, col:]
+            bb[row] -= f * bb[col]
+    xo = np.zeros(8)
+    for row in range(7, -1, -1):
+        xo[row] = (bb[row] - aa[row, row + 1:] @ xo[row + 1:]) / aa[row, row]
+    assert np.linalg.norm(x - xo) <= 1e-10 * np.linalg.norm(xo)
+    # condition number 1e6 by construction
+    rng = np.random.default_rng(11)
+    u, _ = np.linalg.qr(rng.standard_normal((12, 12)))
+    v, _ = np.linalg.qr(rng.standard_normal((12, 12)))
+    a = (u * np.logspace(0, -6, 12)) @ v.T
+    xt = rng.standard_normal(12)
+    assert np.linalg.norm(hk.solve_dense(hk.factor_dense(a), a @ xt) - xt) <= 1e-9 * np.linalg.norm(xt)
+    with pytest.raises(hk.SingularMatrixError, match="step"):
+        hk.factor_dense(np.array([[1.0, 2.0], [2.0, 4.0]]))
+    with pytest.raises(hk.SingularMatrixError):
+        hk.factor_dense(np.zeros((3, 3)))
+    # P L U = A
+    a = np.random.default_rng(12).standard_normal((9, 9))
+    f = hk.factor_dense(a)
+    lower, upper = np.tril(f.lu, -1) + np.eye(9), np.triu(f.lu)
+    perm = np.arange(9)
+    for i, p in enumerate(f.piv):
+        perm[[i, p]] = perm[[p, i]]
+    pmat = np.zeros((9, 9))
+    pmat[perm, np.arange(9)] = 1.0
+    assert np.linalg.norm(pmat @ lower @ upper - a) <= 1e-12 * np.linalg.norm(a)
+    with pytest.raises(ValueError):
+        hk.factor_dense(np.zeros((2, 3)))
+    with pytest.raises(ValueError):
+        hk.solve_dense(hk.factor_dense(np.eye(3)), np.zeros(4))
+    assert hk.solve_dense(hk.factor_dense(np.zeros((0, 0))), np.zeros(0)).shape == (0,)
