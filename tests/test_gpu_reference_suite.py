@@ -501,3 +501,195 @@ def test_dense_factor_known_answers():  # test_linalg.py:126-190
     with pytest.raises(ValueError):
         hk.solve_dense(hk.factor_dense(np.eye(3)), np.zeros(4))
     assert hk.solve_dense(hk.factor_dense(np.zeros((0, 0))), np.zeros(0)).shape == (0,)
+
+
+# -------------------------------------------------------------- tree / kNN
+# test_tree.py restated.
+
+def _check_structure(hk, tree, n, m):  # test_tree.py:11-30
+    perm = np.asarray(tree.perm)
+    assert sorted(perm) == list(range(n))
+    assert np.array_equal(perm[np.asarray(tree.inv_perm)], np.arange(n))
+    for node in tree.nodes:
+        assert node.size >= 1
+        if not node.is_leaf:
+            left, right = tree.children(node)
+            assert (left.begin, right.end) == (node.begin, node.end)
+            assert left.end == right.begin
+            assert abs(left.size - right.size) <= 1
+    for leaf in tree.leaves():
+        assert leaf.size <= m
+        if n >= m:
+            assert leaf.size >= -(m // -2)
+    for level_nodes in hk.levels(tree, bottom_up=False):
+        spans = [(nd.begin, nd.end) for nd in level_nodes]
+        assert spans[0][0] == 0 and spans[-1][1] == n
+        for (b0, e0), (b1, e1) in zip(spans, spans[1:]):
+            assert e0 == b1
+
+
+def test_tree_known_answers():  # test_tree.py:33-100
+    import paper_1701_02324_b200 as hk
+    t = np.linspace(0, 1, 8)
+    tree = hk.build_tree(hk.PointSet(np.column_stack([t, 2 * t])), 2, seed=0)
+    assert len(tree.leaves()) == 4 and all(leaf.size == 2 for leaf in tree.leaves())
+    tree = hk.build_tree(hk.generate("uniform_cube", 5, seed=1, d=2), 8, seed=0)
+    assert tree.depth == 0 and len(tree.nodes) == 1
+    _check_structure(hk, tree, 5, 8)
+    rng = np.random.default_rng(3)
+    coords = np.vstack([rng.normal(0.0, 0.1, (16, 2)), rng.normal(50.0, 0.1, (16, 2))])
+    labels = np.array([0] * 16 + [1] * 16)
+    tree = hk.build_tree(hk.PointSet(coords), 8, seed=2)
+    left, right = tree.children(tree.nodes[0])
+    perm = np.asarray(tree.perm)
+    gl, gr = labels[perm[left.begin:left.end]], labels[perm[right.begin:right.end]]
+    assert len(set(gl)) == 1 and len(set(gr)) == 1 and set(gl) != set(gr)
+    for n, m, seed in [(17, 4, 0), (64, 8, 1), (100, 7, 2), (1000, 32, 3), (3, 2, 4), (257, 16, 5)]:
+        ps = hk.generate("uniform_cube", n, seed=seed, d=3)
+        tree = hk.build_tree(ps, m, seed=seed)
+        _check_structure(hk, tree, n, m)
+        assert np.array_equal(np.asarray(tree.points.coords), ps.coords[np.asarray(tree.perm)])
+    tree = hk.build_tree(hk.generate("uniform_cube", 64, seed=6, d=2), 16, seed=0)
+    assert [len(lv) for lv in hk.levels(tree, bottom_up=True)] == [4, 2, 1]
+    assert [len(lv) for lv in hk.levels(tree, bottom_up=False)] == [1, 2, 4]
+    ps = hk.generate("uniform_cube", 200, seed=7, d=3)
+    t1, t2 = hk.build_tree(ps, 16, seed=9), hk.build_tree(ps, 16, seed=9)
+    assert np.array_equal(np.asarray(t1.perm), np.asarray(t2.perm))
+    with pytest.raises(ValueError):
+        hk.build_tree(hk.generate("uniform_cube", 10, seed=0, d=2), 1)
+
+
+def test_knn_known_answers():  # test_tree.py:103-137
+    import paper_1701_02324_b200 as hk
+    nb = np.asarray(hk.knn_bruteforce(hk.PointSet(np.array([[0.0], [1.0], [2.0]])), 1))
+    assert nb[0, 0] == 1 and nb[2, 0] == 1
+    nb = np.asarray(hk.knn_bruteforce(hk.generate("uniform_cube", 9, seed=8, d=2), 8))
+    for i in range(9):
+        assert sorted(nb[i]) == sorted(set(range(9)) - {i})
+    ps = hk.generate("uniform_cube", 200, seed=12, d=3)
+    got = np.asarray(hk.knn_bruteforce(ps, 5))
+    expect = np.empty((200, 5), dtype=np.int64)  # per-point scan with explicit (distance, index) sorting
+    for i in range(200):
+        pairs = sorted((float((ps.coords[i] - ps.coords[j]) @ (ps.coords[i] - ps.coords[j])), j)
+                       for j in range(200) if j != i)
+        expect[i] = [j for _, j in pairs[:5]]
+    assert np.array_equal(got, expect)
+    nb = np.asarray(hk.knn_bruteforce(hk.PointSet(np.array([[0.0, 0.0], [1.0, 0.0], [0.0, 1.0], [1.0, 1.0]])), 2))
+    assert list(nb[3]) == [1, 2] and list(nb[0]) == [1, 2]
+    ps = hk.generate("uniform_cube", 10, seed=0, d=2)
+    with pytest.raises(ValueError):
+        hk.knn_bruteforce(ps, 0)
+    with pytest.raises(ValueError):
+        hk.knn_bruteforce(ps, 10)
+
+
+# --------------------------------------------------------------- skeletons
+# test_skeleton.py restated (structure; the bound is above).
+
+def test_skeleton_structure_known_answers():  # test_skeleton.py:95-161
+    import paper_1701_02324_b200 as hk
+    ps = hk.generate("uniform_cube", 64, seed=3, d=3)
+    diameter = np.linalg.norm(ps.coords.max(0) - ps.coords.min(0))
+    tree = hk.build_tree(ps, 16, seed=0)
+    sk = hk.build_skeletons(tree, hk.KernelSpec("gaussian", h=1e6 * diameter),
+                            hk.SkeletonConfig(tau=1e-8, max_rank=32, sample_mode="exact", seed=0))
+    assert all(sk[i].rank == 1 for i in range(1, len(tree.nodes)))
+    tree = hk.build_tree(hk.generate("uniform_cube", 32, seed=5, d=2), 8, seed=0)
+    sk = hk.build_skeletons(tree, hk.KernelSpec("gaussian", h=1e-9),
+                            hk.SkeletonConfig(tau=1e-4, max_rank=8, sample_mode="exact", seed=0))
+    assert all(sk[i].rank == 0 for i in range(1, len(tree.nodes)))
+    tree = hk.build_tree(hk.generate("uniform_cube", 6, seed=0, d=2), 8, seed=0)
+    assert len(hk.build_skeletons(tree, hk.KernelSpec("gaussian"), hk.SkeletonConfig(sample_mode="exact"))) == 0
+    tree = hk.build_tree(hk.generate("uniform_cube", 64, seed=1, d=2), 16, seed=0)
+    assert tree.depth == 2
+    assert len(hk.build_skeletons(tree, hk.KernelSpec("gaussian", h=0.4), hk.SkeletonConfig(sample_mode="exact"))) == 6
+    # nestedness and the exact identity block
+    # (the reference draws generate("gaussian_mixture", 300, seed=2, d=2) here, which never
+    # returns in the unmodified reference -- four centres 12 sigma apart do not fit its 2-D box and
+    # the rejection loop is unbounded; the package raises ValueError instead.  Same check on a cube.)
+    with pytest.raises(ValueError, match="mixture"):
+        hk.generate("gaussian_mixture", 300, seed=2, d=2)
+    ps = hk.generate("uniform_cube", 300, seed=2, d=2)
+    tree = hk.build_tree(ps, 32, seed=1)
+    sk = hk.build_skeletons(tree, hk.KernelSpec("gaussian", h=1.0),
+                            hk.SkeletonConfig(tau=1e-6, max_rank=24, samples=64, sample_mode="uniform", seed=7))
+    for node in tree.nodes:
+        if node.level == 0:
+            continue
+        s = sk[node.index]
+        if node.is_leaf:
+            cands = np.arange(node.begin, node.end)
+        else:
+            left, right = tree.children(node)
+            cands = np.concatenate([np.asarray(sk[left.index].indices), np.asarray(sk[right.index].indices)])
+            assert set(np.asarray(s.indices)) <= set(cands)
+        pos = [int(np.flatnonzero(cands == q)[0]) for q in np.asarray(s.indices)]
+        assert np.array_equal(np.asarray(s.interp)[:, pos], np.eye(s.rank))
+        assert s.rank <= min(len(cands), 24)
+    # accuracy monotone in tau
+    ps = hk.generate("uniform_cube", 256, seed=9, d=3)
+    tree = hk.build_tree(ps, 64, seed=9)
+    kern = hk.KernelSpec("gaussian", h=0.4)
+    coords = np.asarray(tree.points.coords)
+    errs = []
+    for tau in (1e-2, 1e-4, 1e-6):
+        sk = hk.build_skeletons(tree, kern, hk.SkeletonConfig(tau=tau, max_rank=64, sample_mode="exact", seed=9))
+        worst = 0.0
+        for node in tree.nodes:
+            if node.is_leaf:
+                continue
+            left, right = tree.children(node)
+            block = hk.eval_block(kern, coords[left.begin:left.end], coords[right.begin:right.end])
+            mid = hk.eval_block(kern, coords[np.asarray(sk[left.index].indices)], coords[np.asarray(sk[right.index].indices)])
+            approx = _basis(tree, sk, left).T @ mid @ _basis(tree, sk, right)
+            worst = max(worst, np.linalg.norm(block - approx) / np.linalg.norm(block))
+        errs.append(worst)
+    assert errs[0] >= errs[1] >= errs[2]
+
+
+# ------------------------------------------------------------------ krylov
+# test_krylov.py restated (the golden baseline run is tests/test_gpu_dense.py).
+
+def test_gmres_known_answers():  # test_krylov.py:18-95
+    import paper_1701_02324_b200 as hk
+    b = np.random.default_rng(0).standard_normal(32)
+    x, rep = hk.gmres(lambda v: v, lambda v: v, b, tol=1e-12)
+    assert rep.iterations == 1 and rep.converged and np.allclose(x, b, atol=1e-12)
+    rng = np.random.default_rng(1)
+    m = rng.standard_normal((64, 64))
+    a = m @ m.T + 64 * np.eye(64)
+    a_inv = np.linalg.inv(a)
+    b = rng.standard_normal(64)
+    x, rep = hk.gmres(lambda v: a @ v, lambda v: a_inv @ v, b, tol=1e-12)
+    assert rep.iterations == 1 and rep.final_residual <= 1e-12
+    rng = np.random.default_rng(2)
+    m = rng.standard_normal((80, 80))
+    a = m @ m.T + 10 * np.eye(80)
+    b = rng.standard_normal(80)
+    x, rep = hk.gmres(lambda v: a @ v, lambda v: v, b, tol=1e-10, restart=30)
+    assert abs(rep.final_residual - np.linalg.norm(b - a @ x) / np.linalg.norm(b)) <= 1e-12
+    assert rep.residuals[-1] == rep.final_residual
+    rng = np.random.default_rng(3)
+    m = rng.standard_normal((120, 120))
+    a = m @ m.T + 5 * np.eye(120)
+    b = rng.standard_normal(120)
+    x, rep = hk.gmres(lambda v: a @ v, lambda v: v, b, tol=1e-10, restart=25)
+    for i in range(1, len(rep.residuals)):
+        if i % 25:
+            assert rep.residuals[i] <= rep.residuals[i - 1] * (1.0 + 1e-9)
+    x, rep = hk.gmres(lambda v: v, lambda v: v, np.zeros(5))
+    assert rep.converged and rep.iterations == 0 and np.all(x == 0.0)
+    with pytest.raises(ValueError, match="shape"):
+        hk.gmres(lambda v: v[:2], lambda v: v, np.ones(4))
+    rng = np.random.default_rng(4)
+    m = rng.standard_normal((60, 60))
+    a = m @ m.T + 30 * np.eye(60)
+    b = rng.standard_normal(60)
+    x, rep = hk.gmres(lambda v: a @ v, lambda v: v, b, tol=1e-9, restart=5, max_iter=400)
+    assert rep.converged and rep.restarts > 0 and np.linalg.norm(b - a @ x) <= 1e-9 * np.linalg.norm(b)
+    rng = np.random.default_rng(5)
+    m = rng.standard_normal((50, 50))
+    a = m @ m.T + 1e-8 * np.eye(50)
+    b = rng.standard_normal(50)
+    x, rep = hk.gmres(lambda v: a @ v, lambda v: v, b, tol=1e-14, restart=10, max_iter=20)
+    assert rep.iterations <= 20 and (not rep.converged or rep.final_residual <= 1e-14)
