@@ -693,3 +693,50 @@ def test_gmres_known_answers():  # test_krylov.py:18-95
     b = rng.standard_normal(50)
     x, rep = hk.gmres(lambda v: a @ v, lambda v: v, b, tol=1e-14, restart=10, max_iter=20)
     assert rep.iterations <= 20 and (not rep.converged or rep.final_residual <= 1e-14)
+
+
+# ----------------------------------------------------------------- kernels
+# test_kernels.py restated (closed forms, conventions, validation, symmetry).
+
+def test_kernel_known_answers():  # test_kernels.py:7-92
+    import paper_1701_02324_b200 as hk
+    x = np.array([[0.3, -0.2, 1.0]])
+    assert hk.eval_block(hk.KernelSpec("gaussian", h=0.7), x, x)[0, 0] == 1.0
+    val = hk.eval_block(hk.KernelSpec("gaussian", h=1.0), np.array([[0.0, 0.0]]), np.array([[1.0, 1.0]]))[0, 0]
+    assert abs(val - 0.3678794412) < 1e-9
+    lap = hk.KernelSpec("laplace3d")
+    o, e1 = np.array([[0.0, 0.0, 0.0]]), np.array([[1.0, 0.0, 0.0]])
+    assert abs(hk.eval_block(lap, o, e1)[0, 0] - 0.0795774715) < 1e-9
+    assert hk.eval_block(lap, o, o)[0, 0] == 0.0  # self-interaction convention
+    poly = hk.KernelSpec("polynomial", degree=3, shift=1.0)
+    assert abs(hk.eval_block(poly, np.array([[1.0, 2.0]]), np.array([[0.5, 0.25]]))[0, 0] - 2.0 ** 3) < 1e-12
+    k = hk.KernelSpec("gaussian", h=0.5, regularization=0.25)
+    x = np.random.default_rng(0).random((4, 2))
+    assert np.all(np.diag(hk.eval_block(k, x, x)) == 1.0)  # lambda is not added
+    assert hk.eval_system_diag_shift(hk.KernelSpec("gaussian", regularization=0.0)) == 0.0
+    assert hk.eval_system_diag_shift(hk.KernelSpec("gaussian", regularization=1e-2)) == 1e-2
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        hk.eval_block(hk.KernelSpec("gaussian"), np.zeros((2, 3)), np.zeros((2, 2)))
+    with pytest.raises(ValueError, match="3-d"):
+        hk.eval_block(hk.KernelSpec("laplace3d"), np.zeros((2, 2)), np.zeros((2, 2)))
+    for spec in (dict(family="gaussian", h=0.0), dict(family="gaussian", h=-1.0), dict(family="polynomial", degree=0),
+                 dict(family="polynomial", shift=-0.5), dict(family="gaussian", regularization=-1e-3),
+                 dict(family="matern")):
+        with pytest.raises(ValueError):
+            hk.KernelSpec(**spec)
+    rng = np.random.default_rng(13)
+    xt, xs = rng.random((37, 3)), rng.random((21, 3))
+    for family, kw in (("gaussian", dict(h=0.4)), ("laplace3d", {}), ("polynomial", dict(degree=2, shift=0.3))):
+        kk = hk.KernelSpec(family, **kw)
+        assert np.array_equal(hk.eval_block(kk, xt, xs), hk.eval_block(kk, xs, xt).T)
+    x = np.random.default_rng(14).random((30, 3))
+    g = hk.eval_block(hk.KernelSpec("gaussian", h=0.2), x, x)
+    assert np.all(g > 0.0) and np.all(g <= 1.0)
+    assert np.all(hk.eval_block(lap, x, x)[~np.eye(30, dtype=bool)] > 0.0)
+    # entries do not depend on how the rows are split over launches
+    rng = np.random.default_rng(15)
+    xt, xs = rng.random((700, 3)), rng.random((11, 3))
+    k = hk.KernelSpec("gaussian", h=0.3)
+    full = hk.eval_block(k, xt, xs)
+    parts = np.vstack([hk.eval_block(k, xt[i:i + 64], xs) for i in range(0, 700, 64)])
+    assert np.array_equal(full, parts)
