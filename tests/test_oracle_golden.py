@@ -174,3 +174,36 @@ def test_knn_rows_equals_knn_table():
     full = O.knn(x, 9)
     rows = np.sort(rng.choice(3000, size=400, replace=False))
     assert np.array_equal(O.knn_rows(x, 9, rows, chunk=64), full[rows])
+
+
+def test_full_size_fixtures_well_formed():
+    """The full-size fixtures of tests/test_gpu_full_structure.py (made by
+    tools/make_full_digests.py / make_full_skeleton_digest.py from the
+    oracle): consistent sizes, skeleton indices inside their candidates'
+    ranges, nested parents, finite factor quantities."""
+    import json
+    from oracle import hks_oracle as O
+    from paper_1701_02324_b200 import workloads as W
+    golden = Path(__file__).resolve().parent / "golden"
+    for key in ("c2", "c3"):
+        d = json.loads((golden / f"full_{key}_digest.json").read_text())
+        s = json.loads((golden / f"full_{key}_skeletons.json").read_text())
+        w = W.CONFIGS[d["workload"]]
+        assert d["n"] == s["n"] == w.n and len(d["perm_head"]) == 64
+        depth = O.tree_depth(w.n, w.leaf_size)
+        begin, end = O.node_ranges(w.n, depth)
+        first_leaf = (1 << depth) - 1
+        g = s["subtree_root"]
+        assert sorted(int(k) for k in s["nodes"]) == sorted([g, 2 * g + 1, 2 * g + 2] + [4 * g + 3 + j for j in range(4)])
+        for node, rec in s["nodes"].items():
+            i = int(node)
+            idx = np.asarray(rec["indices"])
+            assert 0 < idx.size <= w.max_rank and np.unique(idx).size == idx.size
+            assert idx.min() >= begin[i] and idx.max() < end[i] and rec["rows"] >= w.samples
+            if i < first_leaf:
+                kids = set(s["nodes"][str(2 * i + 1)]["indices"]) | set(s["nodes"][str(2 * i + 2)]["indices"])
+                assert set(rec["indices"]) <= kids
+        z = np.load(golden / f"full_{key}_factor.npz")
+        assert float(z["lam"]) == w.lam
+        assert all(np.all(np.isfinite(z[k])) for k in z.files)
+        assert z["theta_root_sketch"].shape[1] == 8 and z["upward_root"].shape == (len(s["nodes"][str(g)]["indices"]),)
