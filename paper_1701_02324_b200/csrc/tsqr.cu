@@ -18,9 +18,13 @@
 // diagonal block of R are factored in shared memory (dlarfg reflectors,
 // v = [e_k; v_s]), the block reflector I - V T V^T is formed (dlarft; the
 // top of V is the identity so V^T V = I + Vs^T Vs), and the trailing columns
-// are updated 16 at a time, double-buffered through shared memory, with two
-// DMMA products per tile: W = R_rows + Vs^T S_t, W2 = T^T W, R_rows -= W2,
-// S_t -= Vs W2.  2 c^2 flops per absorbed row, the cost of an unpivoted QR.
+// are updated 16 at a time, streamed through three cp.async buffers in shared
+// memory (two tiles in flight), with DMMA products per tile: W = R_rows +
+// Vs^T S_t, W2 = T^T W, R_rows -= W2, S_t -= Vs W2 (stored straight from the
+// accumulators; a panel's own columns of S are dead once factored and are
+// never written back).  "One pass over A" above means one read and one
+// write of the slab's trailing columns per 32-column panel; 2 c^2 flops per
+// absorbed row, the cost of an unpivoted QR.
 // One CTA per (node, row chunk) job; the chunks' triangles are merged
 // pairwise by the same kernel (a triangular source skips its zero panels).
 // Every reduction has a fixed order: results are deterministic.
