@@ -63,7 +63,7 @@ def test_full_size_skeleton_subtree(name):
     from paper_1701_02324_b200 import workloads as W
     g = json.loads((GOLDEN / f"full_{name}_skeletons.json").read_text())
     w = W.CONFIGS[g["workload"]]
-    if w.n > (1 << 21) and not os.environ.get("HKS_TEST_FULL_LARGE"):
+    if (w.n > (1 << 21) or w.d > 64) and not os.environ.get("HKS_TEST_FULL_LARGE"):
         pytest.skip("minutes of setup at this size: set HKS_TEST_FULL_LARGE=1 (result recorded under profiles/)")
     x = W.points(w, 0)
     kern = hk.KernelSpec("gaussian", h=w.h, regularization=w.lam)
